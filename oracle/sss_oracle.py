@@ -1,0 +1,723 @@
+"""CPU oracle for the relight / material-edit hot path — TEST INFRASTRUCTURE ONLY.
+
+This module is the checker, never the product: only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / ``--impl
+reference`` leg may import it. The product (``paper_2203_12339_b200``) never
+imports it and has no CPU fallback.
+
+It restates, in numpy float64, the reference's algorithm for the path named by
+BASELINE.json's north star (reference = ``sssrelight`` under
+/root/reference/pkg). Each function cites the reference file:line it follows.
+Where BASELINE asks for something the reference does not have (L-level
+Haar, a Haar w1 transform, SH light transfer, geometry images, the exact
+per-pair PCA projection) the restatement is composed from the reference's own
+primitives and says so.
+
+Parity pin: ``tests/golden/make_golden.py`` imports the real reference in the
+build container and writes small fixtures under ``tests/golden/``;
+``tests/test_oracle_golden.py`` checks this module against them bit-for-bit
+(full-pyramid Haar / 9/7, top-n, energy select, transfer rows, CSC apply, the
+full two-step precompute at levels=full + w1=9/7, and the frame).
+
+Floating-point conventions follow the reference numpy twin
+(``_kernels_np.py``): no fused multiply-add, element-wise expression order
+kept exactly so results are bitwise reproducible.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+# ---------------------------------------------------------------------------
+# constants — _kernels_np.py:18-26
+# ---------------------------------------------------------------------------
+CDF97_ALPHA = -1.586134342059924
+CDF97_BETA = -0.05298011857296141
+_T = 1.0 + 2.0 * CDF97_BETA * (1.0 + 2.0 * CDF97_ALPHA)
+CDF97_GAMMA = -(1.0 + 2.0 * CDF97_ALPHA) / (2.0 * _T)
+CDF97_DELTA = 0.4435068520511142
+CDF97_ZETA = math.sqrt(2.0) / _T
+CDF97_INV_ZETA = 1.0 / CDF97_ZETA
+ISQRT2 = 1.0 / math.sqrt(2.0)
+
+
+def full_levels(side: int) -> int:
+    return int(side).bit_length() - 1
+
+
+# ---------------------------------------------------------------------------
+# Haar — _kernels_np.py:33-74, restated with a level limit (SURVEY §8c "L-level
+# Haar"): identical arithmetic and Mallat layout, stop after L levels.
+# L = log2(side) reproduces haar2d_fwd_batch / haar2d_inv_batch bitwise.
+# ---------------------------------------------------------------------------
+
+def _haar_axis_fwd(a):  # _kernels_np.py:33-41
+    h = a.shape[-1] // 2
+    ev = a[..., 0::2]
+    od = a[..., 1::2]
+    lo = (ev + od) * ISQRT2
+    hi = (ev - od) * ISQRT2
+    a[..., :h] = lo
+    a[..., h:] = hi
+
+
+def _haar_axis_inv(a):  # _kernels_np.py:44-50
+    h = a.shape[-1] // 2
+    lo = a[..., :h].copy()
+    hi = a[..., h:].copy()
+    a[..., 0::2] = (lo + hi) * ISQRT2
+    a[..., 1::2] = (lo - hi) * ISQRT2
+
+
+def _levels_or_full(side, levels):
+    full = full_levels(side)
+    if levels is None:
+        return full
+    if not 0 <= levels <= full:
+        raise ValueError(f"levels must lie in [0, {full}]")
+    return levels
+
+
+def haar2d_fwd(blocks, levels=None):
+    """(B, s, s) forward Haar, L levels (default: full pyramid).
+
+    Follows haar2d_fwd_batch (_kernels_np.py:53-62): per level rows, then
+    columns, on the shrinking top-left s x s sub-block.
+    """
+    out = np.array(blocks, dtype=np.float64, copy=True)
+    s = out.shape[-1]
+    for _ in range(_levels_or_full(s, levels)):
+        sub = out[..., :s, :s]
+        _haar_axis_fwd(sub)
+        _haar_axis_fwd(sub.swapaxes(-1, -2))
+        s //= 2
+    return out
+
+
+def haar2d_inv(blocks, levels=None):
+    """Exact adjoint of haar2d_fwd (haar2d_inv_batch, _kernels_np.py:65-74)."""
+    out = np.array(blocks, dtype=np.float64, copy=True)
+    full = out.shape[-1]
+    lv = _levels_or_full(full, levels)
+    s = full >> (lv - 1) if lv else full * 2
+    while s <= full and lv:
+        sub = out[..., :s, :s]
+        _haar_axis_inv(sub.swapaxes(-1, -2))
+        _haar_axis_inv(sub)
+        s *= 2
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CDF 9/7 — _kernels_np.py:81-135 (kept for reference-container parity mode)
+# ---------------------------------------------------------------------------
+
+def _cdf97_axis_fwd(a):  # _kernels_np.py:81-97
+    s = a.shape[-1]
+    h = s // 2
+    a[..., 1:s - 2:2] += CDF97_ALPHA * (a[..., 0:s - 3:2] + a[..., 2:s - 1:2])
+    a[..., s - 1] += 2.0 * CDF97_ALPHA * a[..., s - 2]
+    a[..., 2::2] += CDF97_BETA * (a[..., 1:s - 2:2] + a[..., 3::2])
+    a[..., 0] += 2.0 * CDF97_BETA * a[..., 1]
+    a[..., 1:s - 2:2] += CDF97_GAMMA * (a[..., 0:s - 3:2] + a[..., 2:s - 1:2])
+    a[..., s - 1] += 2.0 * CDF97_GAMMA * a[..., s - 2]
+    a[..., 2::2] += CDF97_DELTA * (a[..., 1:s - 2:2] + a[..., 3::2])
+    a[..., 0] += 2.0 * CDF97_DELTA * a[..., 1]
+    ev = a[..., 0::2] * CDF97_ZETA
+    od = a[..., 1::2] * CDF97_INV_ZETA
+    a[..., :h] = ev
+    a[..., h:] = od
+
+
+def _cdf97_axis_inv(a):  # _kernels_np.py:100-111
+    s = a.shape[-1]
+    ev = a[..., : s // 2] * CDF97_INV_ZETA
+    od = a[..., s // 2:] * CDF97_ZETA
+    a[..., 0::2] = ev
+    a[..., 1::2] = od
+    a[..., 0] -= 2.0 * CDF97_DELTA * a[..., 1]
+    a[..., 2::2] -= CDF97_DELTA * (a[..., 1:s - 2:2] + a[..., 3::2])
+    a[..., s - 1] -= 2.0 * CDF97_GAMMA * a[..., s - 2]
+    a[..., 1:s - 2:2] -= CDF97_GAMMA * (a[..., 0:s - 3:2] + a[..., 2:s - 1:2])
+    a[..., 0] -= 2.0 * CDF97_BETA * a[..., 1]
+    a[..., 2::2] -= CDF97_BETA * (a[..., 1:s - 2:2] + a[..., 3::2])
+    a[..., s - 1] -= 2.0 * CDF97_ALPHA * a[..., s - 2]
+    a[..., 1:s - 2:2] -= CDF97_ALPHA * (a[..., 0:s - 3:2] + a[..., 2:s - 1:2])
+
+
+def cdf97_fwd(blocks, levels=None):  # cdf97_fwd_batch, _kernels_np.py:114-123
+    out = np.array(blocks, dtype=np.float64, copy=True)
+    s = out.shape[-1]
+    for _ in range(_levels_or_full(s, levels)):
+        sub = out[..., :s, :s]
+        _cdf97_axis_fwd(sub)
+        _cdf97_axis_fwd(sub.swapaxes(-1, -2))
+        s //= 2
+    return out
+
+
+def cdf97_inv(blocks, levels=None):  # cdf97_inv_batch, _kernels_np.py:126-135
+    out = np.array(blocks, dtype=np.float64, copy=True)
+    full = out.shape[-1]
+    lv = _levels_or_full(full, levels)
+    s = full >> (lv - 1) if lv else full * 2
+    while s <= full and lv:
+        sub = out[..., :s, :s]
+        _cdf97_axis_inv(sub.swapaxes(-1, -2))
+        _cdf97_axis_inv(sub)
+        s *= 2
+    return out
+
+
+def w_fwd(kind, blocks, levels):
+    return (haar2d_fwd if kind == "haar" else cdf97_fwd)(blocks, levels)
+
+
+def w_inv(kind, blocks, levels):
+    return (haar2d_inv if kind == "haar" else cdf97_inv)(blocks, levels)
+
+
+# ---------------------------------------------------------------------------
+# truncation — wavelets.py:108-153
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Spectrum:
+    indices: np.ndarray  # uint32 sorted
+    values: np.ndarray  # float64
+    size: int
+    total_energy: float
+    kept_energy: float
+
+    @property
+    def count(self):
+        return int(self.indices.size)
+
+    def to_dense(self):
+        d = np.zeros(self.size)
+        d[self.indices] = self.values
+        return d
+
+
+def _make_spectrum(flat, order, kept):  # wavelets.py:116-125
+    idx = np.sort(order[:kept]).astype(np.uint32)
+    vals = flat[idx]
+    total = float(np.sum(flat * flat))
+    kept_e = min(float(np.sum(vals * vals)), total)
+    return Spectrum(idx, vals, flat.size, total, kept_e)
+
+
+def compress_top_n(spectrum, n: int) -> Spectrum:
+    """wavelets.py:128-136: n largest |c|, stable tie -> lower flat index."""
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    flat = np.asarray(spectrum, dtype=np.float64).reshape(-1)
+    n = min(n, flat.size)
+    order = np.argsort(-np.abs(flat), kind="stable")
+    return _make_spectrum(flat, order, n)
+
+
+def compress_energy(spectrum, fraction: float) -> Spectrum:
+    """wavelets.py:139-153: shortest |c|-ordered prefix reaching the fraction."""
+    if not 0.0 <= fraction <= 1.0:
+        raise ValueError("fraction must be in [0, 1]")
+    flat = np.asarray(spectrum, dtype=np.float64).reshape(-1)
+    order = np.argsort(-np.abs(flat), kind="stable")
+    sq = flat[order] ** 2
+    cum = np.cumsum(sq)
+    total = cum[-1] if cum.size else 0.0
+    if fraction == 0.0 or total == 0.0:
+        kept = 0
+    else:
+        kept = int(np.searchsorted(cum, fraction * total, side="left")) + 1
+        kept = min(kept, int(np.count_nonzero(flat)))
+    return _make_spectrum(flat, order, kept)
+
+
+def energy_select_margin(spectrum, fraction: float) -> float:
+    """Near-tie audit for compress_energy: relative distance between
+    fraction*total and the two cumulative sums that bracket the cut. A value
+    below ~1e-12 means a different (but equally valid) summation order could
+    move the cut by one entry."""
+    flat = np.asarray(spectrum, dtype=np.float64).reshape(-1)
+    order = np.argsort(-np.abs(flat), kind="stable")
+    cum = np.cumsum(flat[order] ** 2)
+    if not cum.size or cum[-1] == 0.0:
+        return np.inf
+    target = fraction * cum[-1]
+    pos = int(np.searchsorted(cum, target, side="left"))
+    cand = [abs(cum[pos] - target)] if pos < cum.size else []
+    if pos > 0:
+        cand.append(abs(target - cum[pos - 1]))
+    return min(cand) / cum[-1] if cand else np.inf
+
+
+# ---------------------------------------------------------------------------
+# dipole — dipole.py:85-152
+# ---------------------------------------------------------------------------
+
+def fdr(eta):  # dipole.py:85-89
+    return -1.440 / (eta * eta) + 0.710 / eta + 0.668 + 0.0636 * eta
+
+
+@dataclass(frozen=True)
+class Dipole:
+    sigma_t_prime: float
+    alpha_prime: float
+    sigma_tr: float
+    z_r: float
+    z_v: float
+
+
+def derive_dipole_raw(sp, sa, eta) -> Dipole:  # dipole.py:100-116
+    st = sp + sa
+    ap = sp / st
+    f = fdr(eta)
+    a_boundary = (1.0 + f) / (1.0 - f)
+    z_r = 1.0 / st
+    return Dipole(st, ap, float(np.sqrt(3.0 * sa * st)), z_r,
+                  z_r * (1.0 + 4.0 * a_boundary / 3.0))
+
+
+def eval_rd(d: Dipole, r):  # dipole.py:119-132
+    r = np.asarray(r, dtype=np.float64)
+    d_r = np.sqrt(r * r + d.z_r * d.z_r)
+    d_v = np.sqrt(r * r + d.z_v * d.z_v)
+    s = d.sigma_tr
+    term_r = d.z_r * (s + 1.0 / d_r) * np.exp(-s * d_r) / (d_r * d_r)
+    term_v = d.z_v * (s + 1.0 / d_v) * np.exp(-s * d_v) / (d_v * d_v)
+    return d.alpha_prime / (4.0 * np.pi) * (term_r + term_v)
+
+
+def fresnel_transmittance(eta, cos_theta):  # dipole.py:135-152
+    ci = np.clip(np.asarray(cos_theta, dtype=np.float64), 0.0, 1.0)
+    if eta == 1.0:
+        return np.ones_like(ci)
+    sin2_t = (1.0 - ci * ci) / (eta * eta)
+    tir = sin2_t >= 1.0
+    ct = np.sqrt(np.maximum(1.0 - sin2_t, 0.0))
+    rs = (ci - eta * ct) / (ci + eta * ct + 1e-300)
+    rp = (eta * ci - ct) / (eta * ci + ct + 1e-300)
+    ft = 1.0 - 0.5 * (rs * rs + rp * rp)
+    return np.where(tir, 0.0, np.clip(ft, 0.0, 1.0))
+
+
+# ---------------------------------------------------------------------------
+# PCA basis — basisgen.py:90-191
+# ---------------------------------------------------------------------------
+
+def trapezoid_weights(nodes):  # basisgen.py:90-95
+    w = np.empty_like(nodes)
+    w[0] = (nodes[1] - nodes[0]) / 2.0
+    w[-1] = (nodes[-1] - nodes[-2]) / 2.0
+    w[1:-1] = (nodes[2:] - nodes[:-2]) / 2.0
+    return w
+
+
+def find_r_max(d: Dipole, ratio=1e-9):  # basisgen.py:98-112
+    rd0 = float(eval_rd(d, 0.0))
+    lo, hi = 0.0, 1.0
+    while float(eval_rd(d, hi)) >= ratio * rd0:
+        hi *= 2.0
+    for _ in range(128):
+        mid = 0.5 * (lo + hi)
+        if float(eval_rd(d, mid)) < ratio * rd0:
+            hi = mid
+        else:
+            lo = mid
+    return hi
+
+
+def r_nodes_for_box(sigma_box, eta, n_r=512):  # basisgen.py:115-129
+    corner = derive_dipole_raw(sigma_box[0], sigma_box[2], eta)
+    r_max = find_r_max(corner)
+    return np.concatenate([[0.0], np.geomspace(1e-3, r_max, n_r - 1)])
+
+
+def sigma_lattice(sigma_box, n_sp, n_sa):
+    """Training materials: an n_sp x n_sa log-log lattice (basisgen.py:125-127
+    uses lattice x lattice; BASELINE's 16/32/64 materials need 4x4, 8x4, 8x8 —
+    SURVEY Appendix A)."""
+    sp = np.geomspace(sigma_box[0], sigma_box[1], n_sp)
+    sa = np.geomspace(sigma_box[2], sigma_box[3], n_sa)
+    return np.stack(np.meshgrid(sp, sa, indexing="ij"), axis=-1).reshape(-1, 2)
+
+
+def assemble_matrix(r_nodes, sigma_nodes, eta):  # basisgen.py:137-142
+    sqrt_w = np.sqrt(trapezoid_weights(r_nodes))
+    rows = np.empty((sigma_nodes.shape[0], r_nodes.shape[0]))
+    for i, (sp, sa) in enumerate(sigma_nodes):
+        rows[i] = eval_rd(derive_dipole_raw(sp, sa, eta), r_nodes) * sqrt_w
+    return rows
+
+
+def decompose(values, r_nodes, K):  # basisgen.py:145-169
+    """Returns (bases (K, Nr) unweighted, singular values, U (M, K))."""
+    u, s, vh = np.linalg.svd(values, full_matrices=False)
+    weighted = vh[:K].copy()
+    flip = np.ones(K)
+    for i, row in enumerate(weighted):
+        nz = np.flatnonzero(np.abs(row) > 1e-12 * np.abs(row).max())
+        if nz.size and row[nz[0]] < 0.0:
+            row *= -1.0
+            flip[i] = -1.0
+    return weighted / np.sqrt(trapezoid_weights(r_nodes)), s, u[:, :K] * flip
+
+
+def project_row(bases, r_nodes, sp, sa, eta):  # basisgen.py:172-176
+    w = trapezoid_weights(r_nodes)
+    rd = eval_rd(derive_dipole_raw(sp, sa, eta), r_nodes)
+    return (bases * w) @ rd
+
+
+def project_material(bases, r_nodes, sigma_s_prime, sigma_a, eta):
+    """basisgen.py:178-191 -> s (3, K)."""
+    return np.stack([project_row(bases, r_nodes, float(sigma_s_prime[c]),
+                                 float(sigma_a[c]), eta) for c in range(3)])
+
+
+def basis_slopes(bases, r_nodes):  # transfer.py:155-156
+    return (bases[:, 1:] - bases[:, :-1]) / np.diff(r_nodes)
+
+
+# ---------------------------------------------------------------------------
+# scattering-transfer rows — _kernels_np.py:142-158 (lerp mode) and the
+# exact per-pair projection (SURVEY §8c "Exact per-pair projection")
+# ---------------------------------------------------------------------------
+
+def transfer_block(block_pos, positions, areas, r_nodes, bases, slopes):
+    """(B, K, N): out[b,k,i] = (bases[k,j] + slopes[k,j]*(d - r_j)) * A_i."""
+    nr = r_nodes.shape[0]
+    diff = block_pos[:, None, :] - positions[None, :, :]
+    d2 = (diff[..., 0] * diff[..., 0] + diff[..., 1] * diff[..., 1]) + diff[..., 2] * diff[..., 2]
+    d = np.sqrt(d2)
+    j = np.searchsorted(r_nodes, d, side="right") - 1
+    np.clip(j, 0, nr - 2, out=j)
+    frac = d - r_nodes[j]
+    inside = d <= r_nodes[nr - 1]
+    out = (bases[:, j] + slopes[:, j] * frac) * (areas * inside)
+    return np.ascontiguousarray(out.swapaxes(0, 1))
+
+
+def exact_projection_coeffs(U, singular_values, r_nodes, K):
+    """P (K, M) with b_k(r) = sum_m P[k,m] R_d(r; sigma_m) on the nodes.
+
+    decompose (basisgen.py:151-169) keeps V^T and discards U; since
+    M = U S V^T with rows sqrt(w) R_d, V^T[k] = U[:,k]^T M / S_k, i.e. the
+    unweighted basis b_k(r) = sum_m U[m,k]/S_k R_d(r; sigma_m).
+    """
+    return (U[:, :K] / singular_values[None, :K]).T.copy()
+
+
+def transfer_block_exact(block_pos, positions, areas, r_max, sigma_nodes, eta, P):
+    """(B, K, N) exact mode: b_k(d) = sum_m P[k,m] R_d(d; sigma_m), masked
+    d <= r_max, times A_i (what the lerp in transfer_block approximates)."""
+    diff = block_pos[:, None, :] - positions[None, :, :]
+    d = np.sqrt((diff[..., 0] ** 2 + diff[..., 1] ** 2) + diff[..., 2] ** 2)
+    rd = np.stack([eval_rd(derive_dipole_raw(sp, sa, eta), d)
+                   for sp, sa in sigma_nodes])  # (M, B, N)
+    out = np.einsum("km,mbn->bkn", P, rd)
+    return out * (areas * (d <= r_max))[:, None, :]
+
+
+# ---------------------------------------------------------------------------
+# two-step compression — transfer.py:185-361, restated for a geometry image
+# (identity atlas: part_count = 1, cell_of = arange) with the
+# w0 / w1 transforms parameterised: (levels=full, w1="cdf97") is the
+# reference exactly; (levels=L, w1="haar") is BASELINE's restatement.
+# ---------------------------------------------------------------------------
+
+TRANSFER_BLOCK = 64  # transfer.py:36
+
+
+@dataclass
+class Operator:
+    cols: np.ndarray  # uint32 sorted w0 ids
+    colptr: np.ndarray  # int64
+    rowidx: np.ndarray  # uint32 w1 ids
+    vals: np.ndarray  # float64
+    kept_energy: float
+    total_energy: float
+    step1_entries: int
+
+    @property
+    def nnz(self):
+        return int(self.rowidx.size)
+
+
+def row_spectra_blocks(positions, areas, side, r_nodes, bases, levels, rows=None):
+    """Yield (ids, (B, K, N) w0 spectra) — transfer.py:201-213."""
+    n = positions.shape[0]
+    slopes = basis_slopes(bases, r_nodes)
+    ids_all = np.arange(n) if rows is None else np.asarray(rows)
+    for lo in range(0, ids_all.size, TRANSFER_BLOCK):
+        ids = ids_all[lo:lo + TRANSFER_BLOCK]
+        block = transfer_block(positions[ids], positions, areas, r_nodes, bases, slopes)
+        nb, K = len(ids), bases.shape[0]
+        coeffs = haar2d_fwd(block.reshape(nb * K, side, side), levels)
+        yield ids, coeffs.reshape(nb, K, n)
+
+
+def step1(positions, areas, side, r_nodes, bases, keep, levels):
+    """run_step1 + step1_unions (transfer.py:216-246) without the spill file.
+
+    Returns (n, masks (K, N) bool, step1_entries per k, per-row sets dict
+    when requested)."""
+    n_dom = side * side
+    n = max(int(round(keep * n_dom)), 1)
+    K = bases.shape[0]
+    masks = np.zeros((K, n_dom), bool)
+    entries = [0] * K
+    for ids, coeffs in row_spectra_blocks(positions, areas, side, r_nodes, bases, levels):
+        for b in range(len(ids)):
+            for k in range(K):
+                spec = compress_top_n(coeffs[b, k], n)
+                masks[k, spec.indices.astype(np.int64)] = True
+                entries[k] += spec.count
+    return n, masks, entries
+
+
+def step2(positions, areas, side, r_nodes, bases, masks, entries, fraction,
+          levels, w1="haar"):
+    """compress_step2 + _threshold_columns (transfer.py:249-333)."""
+    n_dom = side * side
+    K = bases.shape[0]
+    col_ids = [np.flatnonzero(masks[k]).astype(np.int64) for k in range(K)]
+    columns = [np.zeros((c.size, n_dom), np.float32) for c in col_ids]
+    for ids, coeffs in row_spectra_blocks(positions, areas, side, r_nodes, bases, levels):
+        for k in range(K):
+            columns[k][:, ids] = coeffs[:, k, col_ids[k]].T
+    ops = []
+    for k in range(K):
+        ops.append(threshold_columns(columns[k], col_ids[k], side, fraction,
+                                     entries[k], levels, w1))
+    return ops
+
+
+def threshold_columns(column_values, cols, side, fraction, step1_entries,
+                      levels, w1="haar"):  # transfer.py:303-333
+    n_dom = side * side
+    specs = []
+    for c0 in range(0, cols.size, 256):
+        c1 = min(c0 + 256, cols.size)
+        batch = column_values[c0:c1].astype(np.float64).reshape(-1, side, side)
+        spectral = w_fwd(w1, batch, levels).reshape(c1 - c0, n_dom)
+        for ci in range(c1 - c0):
+            specs.append(compress_energy(spectral[ci], fraction))
+    colptr = np.zeros(cols.size + 1, np.int64)
+    for ci, sp in enumerate(specs):
+        colptr[ci + 1] = colptr[ci] + sp.count
+    rowidx = np.concatenate([s.indices for s in specs]) if specs else np.empty(0, np.uint32)
+    vals = np.concatenate([s.values for s in specs]) if specs else np.empty(0)
+    return Operator(cols.astype(np.uint32), colptr, rowidx.astype(np.uint32),
+                    vals.astype(np.float64),
+                    float(sum(s.kept_energy for s in specs)),
+                    float(sum(s.total_energy for s in specs)), step1_entries)
+
+
+def precompute_compressed(positions, areas, side, r_nodes, bases, step1_keep,
+                          step2_fraction, levels=None, w1="haar"):
+    """precompute_compressed (transfer.py:350-361) on a geometry image."""
+    _, masks, entries = step1(positions, areas, side, r_nodes, bases, step1_keep, levels)
+    return step2(positions, areas, side, r_nodes, bases, masks, entries,
+                 step2_fraction, levels, w1)
+
+
+def round_trip_f32(op: Operator) -> Operator:
+    """PRTS1 stores vals as f32 (container.py:88, 103); the parity reference
+    runs on the same rounded values."""
+    return Operator(op.cols, op.colptr, op.rowidx,
+                    op.vals.astype(np.float32).astype(np.float64),
+                    op.kept_energy, op.total_energy, op.step1_entries)
+
+
+# ---------------------------------------------------------------------------
+# sparse apply — _kernels_np.py:239-257 / _kernels_nb.py:301-313
+# ---------------------------------------------------------------------------
+
+def csc_apply(cols, colptr, rowidx, vals, x_idx, x_val, out_len):
+    """Serial reference order (_kernels_nb.py:301-313)."""
+    out = np.zeros(out_len, np.float64)
+    pos = np.searchsorted(cols, x_idx)
+    ok = pos < cols.shape[0]
+    ok &= cols[np.minimum(pos, cols.shape[0] - 1)] == x_idx
+    pos = pos[ok]
+    xv = np.asarray(x_val, np.float64)[ok]
+    if pos.size == 0:
+        return out
+    starts = colptr[pos].astype(np.int64)
+    counts = (colptr[pos + 1] - colptr[pos]).astype(np.int64)
+    total = int(counts.sum())
+    if total == 0:
+        return out
+    offs = np.repeat(np.cumsum(counts) - counts, counts)
+    sel = np.arange(total, dtype=np.int64) - offs + np.repeat(starts, counts)
+    # bincount accumulates sequentially in input order == the serial loop
+    out += np.bincount(rowidx[sel].astype(np.int64),
+                       weights=vals[sel] * np.repeat(xv, counts), minlength=out_len)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# light projection (a) — lighting.py:293-336, envmap.py:45-66
+# ---------------------------------------------------------------------------
+
+def face_directions(side):  # envmap.py:45-58
+    t = (np.arange(side) + 0.5) / side * 2.0 - 1.0
+    v, u = np.meshgrid(t, t, indexing="ij")
+    one = np.ones_like(u)
+    raw = np.stack([
+        np.stack([one, -v, -u], axis=-1),
+        np.stack([-one, -v, u], axis=-1),
+        np.stack([u, one, v], axis=-1),
+        np.stack([u, -one, -v], axis=-1),
+        np.stack([u, -v, one], axis=-1),
+        np.stack([-u, -v, -one], axis=-1),
+    ])
+    return raw / np.linalg.norm(raw, axis=-1, keepdims=True)
+
+
+def face_solid_angles(side):  # envmap.py:61-66
+    t = (np.arange(side) + 0.5) / side * 2.0 - 1.0
+    v, u = np.meshgrid(t, t, indexing="ij")
+    w = 4.0 / (side * side) / np.power(u * u + v * v + 1.0, 1.5)
+    return np.tile(w, (6, 1, 1))
+
+
+def visibility_weights(normals, side, eta=1.0, visibility=None):
+    """lighting.py:318-329: W = V * F_t(eta, cos+) * cos+ * d_omega.
+
+    BASELINE's light transfer is unshadowed (V = 1) with eta_light = 1
+    (F_t == 1, dipole.py:142-144) — SURVEY Appendix A."""
+    dirs = face_directions(side).reshape(-1, 3)
+    dom = face_solid_angles(side).reshape(-1)
+    cosp = np.clip(normals @ dirs.T, 0.0, 1.0)
+    vis = 1.0 if visibility is None else visibility
+    return vis * fresnel_transmittance(eta, cosp) * cosp * dom[None, :]
+
+
+def env_transfer_w2(normals, side):
+    """W in the w2 (per-face full Haar) domain, as fold_visibility builds it
+    (transfer.py:407-411), stored as float32 (BASELINE: fp32 transfer)."""
+    w = visibility_weights(normals, side)
+    n = normals.shape[0]
+    w2 = haar2d_fwd(w.reshape(n * 6, side, side)).reshape(n, 6 * side * side)
+    return w2.astype(np.float32)
+
+
+def project_environment(faces, n_keep=128):
+    """lighting.py:293-305: faces (6, s, s, 3) -> 3 Spectrum (top n_keep)."""
+    out = []
+    for c in range(3):
+        coeffs = haar2d_fwd(np.ascontiguousarray(faces[..., c], dtype=np.float64))
+        out.append(compress_top_n(coeffs.reshape(-1), n_keep))
+    return out
+
+
+def env_irradiance(w2_t32, spectra):
+    """E[:, c] = sum over the (sorted) union of the three channels' kept w2
+    ids of W^{w2}[:, l] * L_c[l] (L_c[l] = 0 where channel c dropped l);
+    fp64 accumulate in ascending l order. Equals
+    ambient_irradiance_dense(W, reconstruct_environment(spectra)) by Parseval
+    (lighting.py:308-336)."""
+    n = w2_t32.shape[0]
+    union = np.unique(np.concatenate([s.indices for s in spectra])).astype(np.int64)
+    lc = np.zeros((3, union.size))
+    for c in range(3):
+        pos = np.searchsorted(union, spectra[c].indices.astype(np.int64))
+        lc[c, pos] = spectra[c].values
+    E = np.zeros((n, 3))
+    for q, l in enumerate(union):
+        col = w2_t32[:, l].astype(np.float64)
+        for c in range(3):
+            if lc[c, q] != 0.0:
+                E[:, c] = E[:, c] + col * lc[c, q]
+    return E
+
+
+def sh_irradiance(T32, Lsh):
+    """E[:, c] = sum_l T[:, l] * L[l, c], fp64 accumulate in l order
+    (the SH analogue of ambient_irradiance_dense, lighting.py:332-336)."""
+    E = np.zeros((T32.shape[0], 3))
+    for l in range(T32.shape[1]):
+        col = T32[:, l].astype(np.float64)
+        for c in range(3):
+            E[:, c] = E[:, c] + col * float(Lsh[l, c])
+    return E
+
+
+# ---------------------------------------------------------------------------
+# the frame — runtime.py:109-216 (Scene.relight / set_material / _finish)
+# ---------------------------------------------------------------------------
+
+def select_irradiance(E, side, levels, e_keep):
+    """_stage1_irradiance (runtime.py:109-118): per channel w0 Haar, top-n."""
+    n_dom = side * side
+    keep = max(1, int(round(e_keep * n_dom)))
+    spectra = []
+    for c in range(3):
+        coeffs = haar2d_fwd(E[:, c].reshape(1, side, side), levels).reshape(-1)
+        spectra.append(compress_top_n(coeffs, keep))
+    return spectra
+
+
+def transfer_stage(ops, spectra, n_dom):
+    """_stage2_transfer (runtime.py:138-150) -> vk (K, 3, n_dom)."""
+    vk = np.zeros((len(ops), 3, n_dom))
+    for k, op in enumerate(ops):
+        for c in range(3):
+            vk[k, c] = csc_apply(op.cols, op.colptr, op.rowidx, op.vals,
+                                 spectra[c].indices, spectra[c].values, n_dom)
+    return vk
+
+
+def finish(vk, weights, side, levels, w1, normals, positions, cam_pos, eta):
+    """_finish + _stage5_reconstruct + _shade (runtime.py:155-168, 202-216)."""
+    summed = np.einsum("ck,kcd->cd", weights, vk)
+    scatter = np.empty((side * side, 3))
+    for c in range(3):
+        scatter[:, c] = w_inv(w1, summed[c].reshape(1, side, side), levels).reshape(-1)
+    view = cam_pos[None, :] - positions
+    view = view / np.linalg.norm(view, axis=1, keepdims=True)
+    cos = np.clip(np.einsum("ij,ij->i", normals, view), 0.0, 1.0)
+    ft = fresnel_transmittance(eta, cos)
+    unclamped = scatter * (ft / np.pi)[:, None]
+    return np.maximum(unclamped, 0.0), unclamped, scatter
+
+
+def relight(E, ops, bases, r_nodes, material, side, levels, w1, e_keep,
+            normals, positions, cam_pos):
+    """Full frame: returns dict(radiance, radiance_unclamped, scatter, vk,
+    spectra, weights)."""
+    sp, sa, eta = material
+    spectra = select_irradiance(E, side, levels, e_keep)
+    vk = transfer_stage(ops, spectra, side * side)
+    weights = project_material(bases, r_nodes, sp, sa, eta)
+    rad, unc, scatter = finish(vk, weights, side, levels, w1, normals, positions,
+                               cam_pos, eta)
+    return dict(radiance=rad, radiance_unclamped=unc, scatter=scatter, vk=vk,
+                spectra=spectra, weights=weights)
+
+
+def parity_error(got, ref, tau=1e-3):
+    """max_i |got-ref| / max(|ref_i|, tau * max|ref|)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    floor = tau * np.abs(ref).max()
+    if floor == 0.0:
+        return float(np.abs(got).max())
+    return float((np.abs(got - ref) / np.maximum(np.abs(ref), floor)).max())
+
+
+def coeff_tile(r, c, side, levels):
+    """Spatial 2^L x 2^L tile that coefficient (r, c) of an L-level Mallat
+    layout belongs to (the L-level transform is tile-local)."""
+    for lvl in range(1, levels + 1):
+        half = side >> lvl
+        if r >= half or c >= half:
+            sh = levels - lvl
+            return ((r % half) >> sh, (c % half) >> sh)
+    return (r, c)
