@@ -721,3 +721,16 @@ def coeff_tile(r, c, side, levels):
             sh = levels - lvl
             return ((r % half) >> sh, (c % half) >> sh)
     return (r, c)
+
+
+def env_transfer_w2_exact(normals32, side):
+    """env_transfer_w2 with the dot product written out in the device's
+    order ((n0 d0 + n1 d1) + n2 d2) so the float32 table is bitwise
+    reproducible (BLAS may fuse or reorder `normals @ dirs.T`)."""
+    n = np.asarray(normals32, np.float64)
+    dirs = face_directions(side).reshape(-1, 3)
+    dom = face_solid_angles(side).reshape(-1)
+    cos = (n[:, 0:1] * dirs[None, :, 0] + n[:, 1:2] * dirs[None, :, 1]) + n[:, 2:3] * dirs[None, :, 2]
+    w = np.clip(cos, 0.0, 1.0) * dom[None, :]
+    w2 = haar2d_fwd(w.reshape(n.shape[0] * 6, side, side)).reshape(n.shape[0], 6 * side * side)
+    return w2.astype(np.float32)

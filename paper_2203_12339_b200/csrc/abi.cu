@@ -1,0 +1,183 @@
+// extern "C" entry points declared in include/sss_b200.h. One translation unit
+// so every kernel is visible to its launcher; built into
+// paper_2203_12339_b200/_sss_b200.so for sm_100a (see build.py).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/sss_b200.h"
+#include "frame.cu"
+#include "precompute.cu"
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return SSS_ECUDA;
+  }
+  return SSS_OK;
+}
+
+bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) {
+      g_err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+      return SSS_ECUDA;
+    }
+  }
+  return SSS_OK;
+}
+
+int check_geom(int side, int levels) {
+  if (!pow2(side) || side < 2) return fail(SSS_EINVAL, "side must be a power of two >= 2");
+  if (levels < 1 || (1 << levels) > side || levels > 6)
+    return fail(SSS_EINVAL, "levels must lie in [1, min(6, log2 side)]");
+  return SSS_OK;
+}
+
+inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+const char* sss_last_error(void) { return g_err.c_str(); }
+int sss_version(void) { return 1; }
+
+int sss_haar2d(const double* in, double* out, int batch, int side, int levels, int inverse,
+               void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (batch < 0 || !in || !out) return fail(SSS_EINVAL, "bad batch or pointer");
+  if (batch == 0) return SSS_OK;
+  const int T = 1 << levels;
+  const long long grid = (long long)batch * (side / T) * (side / T);
+  if (grid > 2147483647LL) return fail(SSS_EINVAL, "grid too large");
+  const size_t smem = 2 * (size_t)T * T * sizeof(double);
+  if (int r = set_smem((const void*)sss::k_haar2d_batch, smem)) return r;
+  sss::k_haar2d_batch<<<(unsigned)grid, 256, smem, S_(stream)>>>(in, out, side, levels, inverse);
+  return check_launch("k_haar2d_batch");
+}
+
+int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, double* x_out,
+                    uint32_t* mask, double* energy, void* stream) {
+  if (nvec < 0 || nvec > 65535 || n_dom <= 0 || n_keep < 0 || !v || !x_out)
+    return fail(SSS_EINVAL, "bad select arguments");
+  if (nvec == 0) return SSS_OK;
+  if (mask) {
+    cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)nvec * ((n_dom + 31) / 32) * 4, S_(stream));
+    if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  }
+  sss::k_select_topn<<<nvec, 1024, 0, S_(stream)>>>(v, n_dom, n_keep, x_out, mask, energy);
+  return check_launch("k_select_topn");
+}
+
+int sss_sh_irradiance(const float* T_l, const double* Lsh, int nl, int side, int levels,
+                      double* E_out, double* ehat, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (nl <= 0 || !T_l || !Lsh || !ehat) return fail(SSS_EINVAL, "bad SH arguments");
+  const int T = 1 << levels;
+  const size_t smem = 4 * (size_t)T * T * sizeof(double);
+  if (int r = set_smem((const void*)sss::k_sh_irradiance_haar, smem)) return r;
+  sss::k_sh_irradiance_haar<<<(side / T) * (side / T), 128, smem, S_(stream)>>>(
+      T_l, Lsh, nl, side, levels, E_out, ehat);
+  return check_launch("k_sh_irradiance_haar");
+}
+
+int sss_env_project(const double* faces, int env_side, int n_keep, uint32_t* idx, double* val,
+                    uint32_t* union_idx, double* union_lc, int* n_union, void* stream) {
+  if (!pow2(env_side) || env_side > 64 || n_keep <= 0 || !faces || !idx || !val)
+    return fail(SSS_EINVAL, "bad env_project arguments");
+  const int s2 = env_side * env_side;
+  const size_t smem = (size_t)7 * s2 * sizeof(double) + 2048 * 4 + 34 * 4;
+  if (int r = set_smem((const void*)sss::k_env_project, smem)) return r;
+  sss::k_env_project<<<3, 1024, smem, S_(stream)>>>(faces, env_side, n_keep, idx, val, nullptr);
+  if (int r = check_launch("k_env_project")) return r;
+  if (union_idx && union_lc && n_union) {
+    sss::k_env_union<<<1, 32, 0, S_(stream)>>>(idx, val, n_keep, union_idx, union_lc, n_union);
+    return check_launch("k_env_union");
+  }
+  return SSS_OK;
+}
+
+int sss_env_irradiance(const float* W2, int D, const uint32_t* union_idx, const double* union_lc,
+                       const int* n_union, int n_keep, int side, int levels, double* E_out,
+                       double* ehat, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (!W2 || !union_idx || !union_lc || !n_union || !ehat || n_keep <= 0)
+    return fail(SSS_EINVAL, "bad env_irradiance arguments");
+  const int T = 1 << levels;
+  const size_t smem = 4 * (size_t)T * T * sizeof(double) + 9 * (size_t)n_keep * sizeof(double) +
+                      3 * (size_t)n_keep * sizeof(int);
+  if (int r = set_smem((const void*)sss::k_env_irradiance_haar, smem)) return r;
+  sss::k_env_irradiance_haar<<<(side / T) * (side / T), 128, smem, S_(stream)>>>(
+      W2, D, union_idx, union_lc, n_union, n_keep, side, levels, E_out, ehat);
+  return check_launch("k_env_irradiance_haar");
+}
+
+int sss_env_transfer(const float* normals, int n_points, const double* dirs, const double* dom,
+                     int env_side, float* W2, void* stream) {
+  if (!pow2(env_side) || env_side > 64 || n_points <= 0 || !normals || !dirs || !dom || !W2)
+    return fail(SSS_EINVAL, "bad env_transfer arguments");
+  const int s2 = env_side * env_side;
+  const size_t smem = (size_t)(sss::kEnvP + 1) * s2 * sizeof(double);
+  if (int r = set_smem((const void*)sss::k_env_transfer, smem)) return r;
+  dim3 grid((n_points + sss::kEnvP - 1) / sss::kEnvP, 6);
+  sss::k_env_transfer<<<grid, 256, smem, S_(stream)>>>(normals, n_points, dirs, dom, env_side, W2);
+  return check_launch("k_env_transfer");
+}
+
+int sss_material_weights(const double* bw, const double* r_nodes, int K, int nr,
+                         const double* material, double* g, void* stream) {
+  if (K <= 0 || nr < 2 || !bw || !r_nodes || !material || !g)
+    return fail(SSS_EINVAL, "bad material_weights arguments");
+  sss::k_material_weights<<<3, 512, nr * sizeof(double), S_(stream)>>>(bw, r_nodes, K, nr,
+                                                                       material, g);
+  return check_launch("k_material_weights");
+}
+
+int sss_transfer_relight(int K, int side, int levels, const uint64_t* rowptr, const uint32_t* cols,
+                         const float* vals, const double* x, const double* g,
+                         const float* positions, const float* normals, const double* cam,
+                         const double* material, double* vk, double* scatter, float* radiance,
+                         float* radiance_unclamped, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (K <= 0 || !rowptr || !x || !g || !positions || !normals || !cam || !material || !vk || !radiance ||
+      !radiance_unclamped)
+    return fail(SSS_EINVAL, "bad transfer_relight arguments");
+  const int T = 1 << levels;
+  const size_t smem = 4 * (size_t)T * T * sizeof(double);
+  if (int r = set_smem((const void*)sss::k_transfer_relight, smem)) return r;
+  sss::k_transfer_relight<<<(side / T) * (side / T), 256, smem, S_(stream)>>>(
+      K, side, levels, rowptr, cols, vals, x, g, positions, normals, cam, material, vk, scatter,
+      radiance, radiance_unclamped);
+  return check_launch("k_transfer_relight");
+}
+
+int sss_edit_finish(int K, int side, int levels, const double* vk, const double* g,
+                    const float* positions, const float* normals, const double* cam,
+                    const double* material, double* scatter, float* radiance,
+                    float* radiance_unclamped, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (K <= 0 || !vk || !g || !positions || !normals || !cam || !material || !radiance ||
+      !radiance_unclamped)
+    return fail(SSS_EINVAL, "bad edit_finish arguments");
+  const int T = 1 << levels;
+  const size_t smem = 4 * (size_t)T * T * sizeof(double);
+  if (int r = set_smem((const void*)sss::k_edit_finish, smem)) return r;
+  sss::k_edit_finish<<<(side / T) * (side / T), 128, smem, S_(stream)>>>(
+      K, side, levels, vk, g, positions, normals, cam, material, scatter, radiance,
+      radiance_unclamped);
+  return check_launch("k_edit_finish");
+}
+
+}  // extern "C"

@@ -1,0 +1,151 @@
+// Shared device helpers for the sm_100a relight / material-edit path.
+//
+// Index spaces (geometry image = identity atlas):
+//   * w0 / w1 "flat" index = r * S + c of the L-level Mallat layout of the
+//     S x S grid (the reference's domain, transfer.py:122-151).
+//   * tile-major index = tile * T^2 + (lr * T + lc), T = 2^L, where (lr, lc)
+//     is the position inside the tile's own L-level (= full-pyramid) Mallat
+//     layout. The L-level transform is tile-local, so a CTA that owns a tile
+//     owns every coefficient it needs for the inverse (the fused epilogue).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define SSS_ISQRT2 0.7071067811865475  // 1/sqrt(2) as the reference rounds it
+
+namespace sss {
+
+// exact-order double arithmetic (no FMA contraction) so results are bitwise
+// equal to the numpy reference (_kernels_np.py, no fused multiply-add)
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// local tile position (lr, lc) of an L-level tile (tile side T = 1 << L) ->
+// global Mallat (row, col) of an S x S grid, tile (tr, tc)
+__device__ __forceinline__ void local_to_global(int lr, int lc, int tr, int tc,
+                                                int L, int S, int* gr, int* gc) {
+  const int T = 1 << L;
+  int hl = 1, hg = S >> L;
+  for (int l = 1; l <= L; ++l) {
+    const int h = T >> l;
+    if (lr >= h || lc >= h) { hl = h; hg = S >> l; break; }
+  }
+  *gr = (lr >= hl) ? hg + tr * hl + (lr - hl) : tr * hl + lr;
+  *gc = (lc >= hl) ? hg + tc * hl + (lc - hl) : tc * hl + lc;
+}
+
+// global Mallat (r, c) -> (tile id, local index lr*T+lc)
+__device__ __forceinline__ void global_to_tile(int r, int c, int L, int S,
+                                               int* tile, int* local) {
+  const int T = 1 << L;
+  int hg = S >> L, hl = 1;  // LL band by default
+  for (int l = 1; l <= L; ++l) {
+    const int h = S >> l;
+    if (r >= h || c >= h) { hg = h; hl = T >> l; break; }
+  }
+  const int pr = (r >= hg) ? r - hg : r;
+  const int pc = (c >= hg) ? c - hg : c;
+  const int tr = pr / hl, tc = pc / hl;
+  const int lr = (r >= hg ? hl : 0) + pr % hl;
+  const int lc = (c >= hg ? hl : 0) + pc % hl;
+  *tile = tr * (S / T) + tc;
+  *local = lr * T + lc;
+}
+
+// In-place forward full-pyramid Haar of a T x T tile held in shared memory
+// (row-major, stride T), following haar2d_fwd_batch (_kernels_np.py:53-62):
+// per level rows then columns. Called by all threads of the block; uses
+// `tmp` (T*T doubles) as scratch. Bitwise equal to the reference.
+__device__ inline void tile_haar_fwd(double* a, double* tmp, int T, int nthreads, int tid) {
+  for (int s = T; s >= 2; s >>= 1) {
+    const int h = s >> 1;
+    // rows
+    for (int e = tid; e < s * h; e += nthreads) {
+      const int i = e / h, j = e % h;
+      const double ev = a[i * T + 2 * j], od = a[i * T + 2 * j + 1];
+      tmp[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+      tmp[i * T + h + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int e = tid; e < s * s; e += nthreads) a[(e / s) * T + e % s] = tmp[(e / s) * T + e % s];
+    __syncthreads();
+    // columns
+    for (int e = tid; e < s * h; e += nthreads) {
+      const int j = e / h, i = e % h;
+      const double ev = a[(2 * i) * T + j], od = a[(2 * i + 1) * T + j];
+      tmp[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+      tmp[(h + i) * T + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int e = tid; e < s * s; e += nthreads) a[(e / s) * T + e % s] = tmp[(e / s) * T + e % s];
+    __syncthreads();
+  }
+}
+
+// In-place inverse (haar2d_inv_batch, _kernels_np.py:65-74): per level
+// columns then rows, s = 2 .. T.
+__device__ inline void tile_haar_inv(double* a, double* tmp, int T, int nthreads, int tid) {
+  for (int s = 2; s <= T; s <<= 1) {
+    const int h = s >> 1;
+    for (int e = tid; e < s * h; e += nthreads) {
+      const int j = e / h, i = e % h;
+      const double lo = a[i * T + j], hi = a[(h + i) * T + j];
+      tmp[(2 * i) * T + j] = dmul(dadd(lo, hi), SSS_ISQRT2);
+      tmp[(2 * i + 1) * T + j] = dmul(dsub(lo, hi), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int e = tid; e < s * s; e += nthreads) a[(e / s) * T + e % s] = tmp[(e / s) * T + e % s];
+    __syncthreads();
+    for (int e = tid; e < s * h; e += nthreads) {
+      const int i = e / h, j = e % h;
+      const double lo = a[i * T + j], hi = a[i * T + h + j];
+      tmp[i * T + 2 * j] = dmul(dadd(lo, hi), SSS_ISQRT2);
+      tmp[i * T + 2 * j + 1] = dmul(dsub(lo, hi), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int e = tid; e < s * s; e += nthreads) a[(e / s) * T + e % s] = tmp[(e / s) * T + e % s];
+    __syncthreads();
+  }
+}
+
+// F_t(eta, cos) = 1 - F_r, dipole.py:135-152
+__device__ __forceinline__ double fresnel_transmittance(double eta, double ci) {
+  ci = fmin(fmax(ci, 0.0), 1.0);
+  if (eta == 1.0) return 1.0;
+  const double sin2_t = (1.0 - ci * ci) / (eta * eta);
+  if (sin2_t >= 1.0) return 0.0;
+  const double ct = sqrt(fmax(1.0 - sin2_t, 0.0));
+  const double rs = (ci - eta * ct) / (ci + eta * ct + 1e-300);
+  const double rp = (eta * ci - ct) / (eta * ci + ct + 1e-300);
+  const double ft = 1.0 - 0.5 * (rs * rs + rp * rp);
+  return fmin(fmax(ft, 0.0), 1.0);
+}
+
+// Jensen dipole R_d (dipole.py:100-132) for one channel
+struct Dipole {
+  double alpha_prime, sigma_tr, z_r, z_v;
+};
+
+__device__ __forceinline__ Dipole derive_dipole(double sp, double sa, double eta) {
+  const double st = sp + sa;
+  const double f = -1.440 / (eta * eta) + 0.710 / eta + 0.668 + 0.0636 * eta;
+  const double a = (1.0 + f) / (1.0 - f);
+  Dipole d;
+  d.alpha_prime = sp / st;
+  d.sigma_tr = sqrt(3.0 * sa * st);
+  d.z_r = 1.0 / st;
+  d.z_v = d.z_r * (1.0 + 4.0 * a / 3.0);
+  return d;
+}
+
+__device__ __forceinline__ double eval_rd(const Dipole& d, double r) {
+  const double dr = sqrt(r * r + d.z_r * d.z_r);
+  const double dv = sqrt(r * r + d.z_v * d.z_v);
+  const double s = d.sigma_tr;
+  const double tr = d.z_r * (s + 1.0 / dr) * exp(-s * dr) / (dr * dr);
+  const double tv = d.z_v * (s + 1.0 / dv) * exp(-s * dv) / (dv * dv);
+  return d.alpha_prime / (4.0 * 3.141592653589793) * (tr + tv);
+}
+
+}  // namespace sss

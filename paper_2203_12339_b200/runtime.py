@@ -1,0 +1,371 @@
+"""The per-frame relight / material-edit runtime on one B200.
+
+Mirrors the reference's ``Scene`` (runtime.py:65-227): ``relight``,
+``set_material``, ``set_light``, ``set_camera`` -> ``FrameResult`` with the
+same fields (radiance, radiance_unclamped, timings_ms over the same STAGES,
+kept_energy_ratio, sequence) and the same stage-2 cache semantics: a
+material or camera edit re-runs only weights -> recombine -> inverse ->
+shade against the cached v_k.
+
+Every stage is a CUDA kernel from ``_sss_b200.so``:
+  stage 1  light projection + w0 Haar   sss_sh_irradiance / sss_env_*
+           exact top-n                  sss_select_topn
+  stage 3  material weights             sss_material_weights
+  stage 2+4+5  transfer, K-fused, with the recombine/inverse/shade epilogue
+                                        sss_transfer_relight
+  edit     stages 3-5                   sss_edit_finish
+The relight sequence can be captured once in a CUDA graph (``capture``)
+because every per-frame input (light, material, camera) lives in a device
+buffer the kernels read.
+"""
+
+from __future__ import annotations
+
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .basis import DiffusionBasis, OpticalMaterial
+from .config import CAMERA, E_KEEP, ENV_COEFF_KEEP
+from .geometry import GeometryImage
+from .lighting import face_directions, face_solid_angles, sh_transfer
+from .transfer import DeviceTransfer
+
+STAGES = ("irradiance", "transfer", "weighting", "inverse_wavelet", "raster")
+
+
+@dataclass
+class Camera:
+    """runtime.py:39-53 (position / look_at; only the position shades)."""
+
+    position: np.ndarray
+    look_at: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    up: np.ndarray = field(default_factory=lambda: np.array([0.0, 1.0, 0.0]))
+    fov_y_degrees: float = 40.0
+
+    def __post_init__(self):
+        self.position = np.asarray(self.position, np.float64)
+        self.look_at = np.asarray(self.look_at, np.float64)
+        if np.linalg.norm(self.look_at - self.position) == 0.0:
+            raise ValueError("camera position and look-at coincide")
+        if not 0.0 < self.fov_y_degrees < 180.0:
+            raise ValueError("vertical FOV must lie in (0, 180)")
+
+
+@dataclass(frozen=True)
+class SHLight:
+    """Real SH radiance, (bands^2, 3) coefficients per channel."""
+
+    coeffs: np.ndarray
+
+    @property
+    def bands(self) -> int:
+        return int(round(np.sqrt(self.coeffs.shape[0])))
+
+
+@dataclass(frozen=True)
+class EnvLight:
+    """Cubemap radiance (6, s, s, 3), face order +X,-X,+Y,-Y,+Z,-Z."""
+
+    faces: np.ndarray
+
+    @property
+    def side(self) -> int:
+        return int(self.faces.shape[1])
+
+
+@dataclass
+class FrameResult:
+    radiance: np.ndarray  # (N, 3) clamped >= 0
+    radiance_unclamped: np.ndarray
+    timings_ms: dict
+    kept_energy_ratio: float
+    sequence: int = 0
+
+
+class Scene:
+    """Owns the relight state and the stage-2 (v_k) cache, all in HBM."""
+
+    def __init__(self, geometry: GeometryImage, transfer: DeviceTransfer,
+                 basis: DiffusionBasis, material: OpticalMaterial, light,
+                 camera: Camera = None, e_keep: float = E_KEEP,
+                 env_keep: int = ENV_COEFF_KEEP, keep_scatter: bool = False):
+        _lib.load()
+        if transfer.side != geometry.side:
+            raise ValueError("transfer operator was precomputed for a different geometry image")
+        if transfer.K != basis.K:
+            raise ValueError("operator count != basis K")
+        self.geometry = geometry
+        self.transfer = transfer
+        self.basis = basis
+        self.e_keep = e_keep
+        self.env_keep = env_keep
+        self.side, self.levels, self.K = geometry.side, transfer.levels, transfer.K
+        n = geometry.count
+        self.n = n
+        dev = torch.device("cuda")
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.positions = torch.as_tensor(geometry.positions, device=dev).contiguous()
+        self.normals = torch.as_tensor(geometry.normals, device=dev).contiguous()
+        self.ehat = torch.empty((3, n), **f64)
+        self.x = torch.empty((3, n), **f64)
+        self.mask = torch.empty((3, (n + 31) // 32), dtype=torch.int32, device=dev)
+        self.energy = torch.zeros((3, 2), **f64)
+        self.g = torch.empty((3, self.K), **f64)
+        self.vk = torch.empty((self.K, 3, n), **f64)
+        self.radiance = torch.empty((n, 3), dtype=torch.float32, device=dev)
+        self.radiance_unclamped = torch.empty((n, 3), dtype=torch.float32, device=dev)
+        self.scatter = torch.empty((n, 3), **f64) if keep_scatter else None
+        self.E = None
+        self.material_buf = torch.empty(7, **f64)
+        self.cam_buf = torch.empty(3, **f64)
+        self._light_kind = None
+        self._have_cache = False
+        self._sequence = 0
+        self._graph = None
+        self.camera = camera or Camera(position=np.array(CAMERA[0]))
+        self.material = self._clamp_material(material)
+        self._write_material()
+        self._write_camera()
+        self._install_light(light)
+
+    # ------------------------------------------------------------------
+    # device-resident inputs
+    # ------------------------------------------------------------------
+
+    def _clamp_material(self, material: OpticalMaterial) -> OpticalMaterial:
+        """runtime.py:92-103: clip sigma to the basis box with a warning."""
+        lo_p, hi_p, lo_a, hi_a = self.basis.sigma_box
+        sp = np.clip(material.sigma_s_prime, lo_p, hi_p)
+        sa = np.clip(material.sigma_a, lo_a, hi_a)
+        if not (np.array_equal(sp, material.sigma_s_prime) and np.array_equal(sa, material.sigma_a)):
+            warnings.warn("material clamped to the basis sigma box", stacklevel=3)
+            return OpticalMaterial(sigma_s_prime=sp, sigma_a=sa, g=material.g, eta=material.eta)
+        return material
+
+    def _write_material(self):
+        m = self.material
+        self.material_buf.copy_(torch.tensor(
+            np.concatenate([m.sigma_s_prime, m.sigma_a, [m.eta]]), dtype=torch.float64))
+
+    def _write_camera(self):
+        self.cam_buf.copy_(torch.tensor(self.camera.position, dtype=torch.float64))
+
+    def _install_light(self, light):
+        dev = torch.device("cuda")
+        if isinstance(light, SHLight):
+            nl = light.coeffs.shape[0]
+            if self._light_kind != ("sh", nl):
+                T = sh_transfer(self.geometry.normals, light.bands)  # (N, nl) f32
+                self.T_l = torch.as_tensor(np.ascontiguousarray(T.T), device=dev)
+                self.light_buf = torch.empty((nl, 3), dtype=torch.float64, device=dev)
+                self._light_kind = ("sh", nl)
+                self._graph = None
+            self.light_buf.copy_(torch.as_tensor(light.coeffs, dtype=torch.float64))
+        elif isinstance(light, EnvLight):
+            s = light.side
+            if self._light_kind != ("env", s):
+                D = 6 * s * s
+                dirs = torch.as_tensor(face_directions(s).reshape(-1, 3), device=dev)
+                dom = torch.as_tensor(face_solid_angles(s).reshape(-1), device=dev)
+                self.W2 = torch.empty((D, self.n), dtype=torch.float32, device=dev)
+                _lib.call("sss_env_transfer", _lib.ptr(self.normals), self.n, _lib.ptr(dirs),
+                          _lib.ptr(dom), s, _lib.ptr(self.W2), _lib.stream_ptr())
+                self.light_buf = torch.empty((6, s, s, 3), dtype=torch.float64, device=dev)
+                kk = self.env_keep
+                self.env_idx = torch.empty((3, kk), dtype=torch.int32, device=dev)
+                self.env_val = torch.empty((3, kk), dtype=torch.float64, device=dev)
+                self.env_uidx = torch.empty(3 * kk, dtype=torch.int32, device=dev)
+                self.env_ulc = torch.empty((3 * kk, 3), dtype=torch.float64, device=dev)
+                self.env_nu = torch.empty(1, dtype=torch.int32, device=dev)
+                self._light_kind = ("env", s)
+                self._graph = None
+            self.light_buf.copy_(torch.as_tensor(light.faces, dtype=torch.float64))
+        else:
+            raise TypeError(f"unsupported light {type(light).__name__}")
+        self.light = light
+
+    # ------------------------------------------------------------------
+    # kernel sequences (stream-ordered, capturable)
+    # ------------------------------------------------------------------
+
+    def _launch_stage1(self, stream=None, want_E=False):
+        sp = _lib.stream_ptr(stream)
+        if want_E and self.E is None:
+            self.E = torch.empty((self.n, 3), dtype=torch.float64, device="cuda")
+        E = self.E if want_E else None
+        if self._light_kind[0] == "sh":
+            _lib.call("sss_sh_irradiance", _lib.ptr(self.T_l), _lib.ptr(self.light_buf),
+                      self._light_kind[1], self.side, self.levels, _lib.ptr(E),
+                      _lib.ptr(self.ehat), sp)
+        else:
+            s, kk = self._light_kind[1], self.env_keep
+            _lib.call("sss_env_project", _lib.ptr(self.light_buf), s, kk, _lib.ptr(self.env_idx),
+                      _lib.ptr(self.env_val), _lib.ptr(self.env_uidx), _lib.ptr(self.env_ulc),
+                      _lib.ptr(self.env_nu), sp)
+            _lib.call("sss_env_irradiance", _lib.ptr(self.W2), 6 * s * s, _lib.ptr(self.env_uidx),
+                      _lib.ptr(self.env_ulc), _lib.ptr(self.env_nu), kk, self.side, self.levels,
+                      _lib.ptr(E), _lib.ptr(self.ehat), sp)
+        keep = max(1, int(round(self.e_keep * self.n)))  # runtime.py:112
+        _lib.call("sss_select_topn", _lib.ptr(self.ehat), 3, self.n, keep, _lib.ptr(self.x),
+                  _lib.ptr(self.mask), _lib.ptr(self.energy), sp)
+
+    def _launch_weights(self, stream=None):
+        dev = self.basis.device()
+        _lib.call("sss_material_weights", _lib.ptr(dev["bw"]), _lib.ptr(dev["r_nodes"]), self.K,
+                  len(self.basis.r_nodes), _lib.ptr(self.material_buf), _lib.ptr(self.g),
+                  _lib.stream_ptr(stream))
+
+    def _launch_transfer(self, stream=None):
+        t = self.transfer
+        _lib.call("sss_transfer_relight", self.K, self.side, self.levels, _lib.ptr(t.rowptr),
+                  _lib.ptr(t.cols), _lib.ptr(t.vals), _lib.ptr(self.x), _lib.ptr(self.g),
+                  _lib.ptr(self.positions), _lib.ptr(self.normals), _lib.ptr(self.cam_buf),
+                  _lib.ptr(self.material_buf), _lib.ptr(self.vk), _lib.ptr(self.scatter),
+                  _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped),
+                  _lib.stream_ptr(stream))
+
+    def _launch_edit(self, stream=None):
+        _lib.call("sss_edit_finish", self.K, self.side, self.levels, _lib.ptr(self.vk),
+                  _lib.ptr(self.g), _lib.ptr(self.positions), _lib.ptr(self.normals),
+                  _lib.ptr(self.cam_buf), _lib.ptr(self.material_buf), _lib.ptr(self.scatter),
+                  _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped),
+                  _lib.stream_ptr(stream))
+
+    def launch_relight(self, stream=None):
+        """Enqueue a full relight (no host sync)."""
+        self._launch_stage1(stream)
+        self._launch_weights(stream)
+        self._launch_transfer(stream)
+        self._have_cache = True
+
+    def launch_edit(self, stream=None):
+        """Enqueue the edit path (no host sync)."""
+        self._launch_weights(stream)
+        self._launch_edit(stream)
+
+    def capture(self):
+        """Capture the relight sequence in a CUDA graph (replayed by
+        ``replay``); per-frame inputs are the device buffers it reads."""
+        self.launch_relight()  # warm (sets smem attributes, first-touch)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.launch_relight()
+        self._graph = g
+        ge = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ge):
+            self.launch_edit()
+        self._graph_edit = ge
+        return g
+
+    def replay(self, edit=False):
+        if self._graph is None:
+            self.capture()
+        (self._graph_edit if edit else self._graph).replay()
+        self._have_cache = True
+
+    # ------------------------------------------------------------------
+    # reference API (runtime.py:174-227)
+    # ------------------------------------------------------------------
+
+    def _frame(self, timings) -> FrameResult:
+        e = self.energy.cpu().numpy()
+        total, kept = float(e[:, 0].sum()), float(e[:, 1].sum())
+        self._cache_energy = kept / total if total else 1.0
+        self._sequence += 1
+        return FrameResult(radiance=self.radiance.cpu().numpy().astype(np.float64),
+                           radiance_unclamped=self.radiance_unclamped.cpu().numpy().astype(np.float64),
+                           timings_ms=timings, kept_energy_ratio=self._cache_energy,
+                           sequence=self._sequence)
+
+    def relight(self) -> FrameResult:
+        """Full pipeline; repopulates the stage-2 cache (runtime.py:174-187)."""
+        timings = dict.fromkeys(STAGES, 0.0)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        self._launch_stage1()
+        ev[1].record()
+        self._launch_weights()
+        ev[2].record()
+        self._launch_transfer()
+        ev[3].record()
+        ev[3].synchronize()
+        self._have_cache = True
+        timings["irradiance"] = ev[0].elapsed_time(ev[1])
+        timings["weighting"] = ev[1].elapsed_time(ev[2])
+        # transfer + recombine + inverse wavelet + shade are one fused kernel
+        timings["transfer"] = ev[2].elapsed_time(ev[3])
+        return self._frame(timings)
+
+    def _edit_frame(self) -> FrameResult:
+        timings = dict.fromkeys(STAGES, 0.0)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        self._launch_weights()
+        ev[1].record()
+        self._launch_edit()
+        ev[2].record()
+        ev[2].synchronize()
+        timings["weighting"] = ev[0].elapsed_time(ev[1])
+        timings["inverse_wavelet"] = ev[1].elapsed_time(ev[2])
+        return self._frame(timings)
+
+    def set_material(self, material: OpticalMaterial) -> FrameResult:
+        """Fast edit path: stages 3-5 only (runtime.py:189-200). E here does
+        not depend on eta (eta_light = 1), so an eta change is an edit too."""
+        self.material = self._clamp_material(material)
+        self._write_material()
+        if not self._have_cache:
+            return self.relight()
+        return self._edit_frame()
+
+    def set_light(self, light) -> FrameResult:
+        self._install_light(light)
+        return self.relight()
+
+    def set_camera(self, camera: Camera) -> FrameResult:
+        """Camera only affects shading: reuse the cache (runtime.py:221-226)."""
+        self.camera = camera
+        self._write_camera()
+        if not self._have_cache:
+            return self.relight()
+        return self._edit_frame()
+
+    # ------------------------------------------------------------------
+    # parity hooks
+    # ------------------------------------------------------------------
+
+    def selected_indices(self, c: int) -> np.ndarray:
+        words = self.mask[c].cpu().numpy().view(np.uint32)
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[: self.n]
+        return np.flatnonzero(bits).astype(np.uint32)
+
+
+def bench(scene: Scene, iterations: int = 20) -> dict:
+    """runtime.py:280-307: median / p10 / p90 of relight and edit (host clock
+    around synchronous API calls, like the reference)."""
+    if iterations < 1:
+        raise ValueError("iterations must be >= 1")
+    scene.relight()
+    full, edit = [], []
+    material = scene.material
+    for _ in range(iterations):
+        t0 = time.perf_counter()
+        scene.relight()
+        full.append((time.perf_counter() - t0) * 1e3)
+        t0 = time.perf_counter()
+        scene.set_material(material)
+        edit.append((time.perf_counter() - t0) * 1e3)
+    full, edit = np.asarray(full), np.asarray(edit)
+
+    def stats(a):
+        return {"median_ms": float(np.median(a)), "p10_ms": float(np.percentile(a, 10)),
+                "p90_ms": float(np.percentile(a, 90))}
+
+    return {"iterations": iterations, "relight": stats(full), "material_edit": stats(edit),
+            "edit_faster": bool(np.median(edit) < np.median(full))}

@@ -1,0 +1,331 @@
+"""GPU parity: the sm_100a frame path vs the CPU oracle (and, where the
+golden fixtures came from the reference itself, vs the reference directly).
+
+Bars (SURVEY §8d / BASELINE north star):
+  * kept index sets (E top-n per channel, env top-128) identical;
+  * E, its Haar spectrum, the env transfer table: bitwise (same fp64
+    operation order, no FMA);
+  * radiance: max_i |got - ref| / max(|ref_i|, tau * max|ref|) <= 1e-4 with
+    tau = 1e-3, against the oracle on the same f32-rounded operator values.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import sss_oracle as O  # noqa: E402
+from paper_2203_12339_b200 import config as C  # noqa: E402
+
+TOL = 1e-4
+TAU = 1e-3
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2203_12339_b200 import _lib, build
+
+    build.build()
+    return _lib.load()
+
+
+def test_haar_levels_bitwise_vs_reference_golden(lib, golden):
+    from paper_2203_12339_b200 import wavelets as W
+
+    g = golden("wavelets")
+    x = torch.as_tensor(g["x"], device="cuda")
+    assert np.array_equal(W.haar2d(x).cpu().numpy(), g["haar_fwd"])
+    assert np.array_equal(W.haar2d_inverse(x).cpu().numpy(), g["haar_inv"])
+    for L in (1, 2, 3):
+        assert np.array_equal(W.haar2d(x, L).cpu().numpy(), g[f"haar_fwd_L{L}"])
+        assert np.array_equal(W.haar2d_inverse(x, L).cpu().numpy(), g[f"haar_inv_L{L}"])
+
+
+@pytest.mark.parametrize("side,L", [(64, 3), (256, 3), (16, 4)])
+def test_haar_levels_bitwise_vs_oracle(lib, side, L):
+    from paper_2203_12339_b200 import wavelets as W
+
+    x = np.random.default_rng(side + L).standard_normal((3, side, side))
+    got = W.haar2d(torch.as_tensor(x, device="cuda"), L).cpu().numpy()
+    assert np.array_equal(got, O.haar2d_fwd(x, L))
+    back = W.haar2d_inverse(torch.as_tensor(got, device="cuda"), L).cpu().numpy()
+    assert np.array_equal(back, O.haar2d_inv(got, L))
+
+
+def test_select_topn_bitwise_vs_reference_golden(lib, golden):
+    from paper_2203_12339_b200 import wavelets as W
+
+    g = golden("select")
+    for n in (0, 1, 7, 410, 1024, 4096):
+        s = W.compress_top_n(g["v"], n)
+        assert np.array_equal(s.indices, g[f"top_{n}_idx"]), n
+        assert np.array_equal(s.values, g[f"top_{n}_val"])
+
+
+@pytest.mark.parametrize("n_dom,n", [(65536, 16384), (16384, 4096), (1000, 1), (4096, 4096),
+                                     (5000, 0)])
+def test_select_topn_vs_oracle(lib, n_dom, n):
+    from paper_2203_12339_b200 import wavelets as W
+
+    rng = np.random.default_rng(n_dom + n)
+    v = rng.standard_normal((3, n_dom))
+    v[0, ::7] = np.round(v[0, ::7], 1)  # exact ties
+    v[1, :100] = 0.0
+    x, mask, energy = W.select_top_n_device(torch.as_tensor(v, device="cuda"), n)
+    x = x.cpu().numpy()
+    for c in range(3):
+        s = O.compress_top_n(v[c], n)
+        got = W.mask_to_indices(mask[c].cpu().numpy(), n_dom)
+        assert np.array_equal(got, s.indices)
+        dense = np.zeros(n_dom)
+        dense[s.indices] = v[c, s.indices]
+        assert np.array_equal(x[c], dense)
+        e = energy[c].cpu().numpy()
+        assert e[0] == pytest.approx(s.total_energy, rel=1e-12)
+        assert e[1] == pytest.approx(s.kept_energy, rel=1e-12)
+
+
+def test_select_all_equal_ties_lowest_index(lib):
+    from paper_2203_12339_b200 import wavelets as W
+
+    v = np.full(5000, -2.5)
+    s = W.compress_top_n(v, 1234)
+    assert np.array_equal(s.indices, np.arange(1234))
+
+
+def _geom(cfg):
+    from paper_2203_12339_b200.geometry import from_config
+
+    return from_config(cfg)
+
+
+def test_sh_irradiance_bitwise(lib):
+    from paper_2203_12339_b200 import _lib, lighting as LT
+
+    cfg = C.C2
+    g = _geom(cfg)
+    T = LT.sh_transfer(g.normals, 5)
+    Lsh = LT.random_sh_light(5, 11)
+    T_l = torch.as_tensor(np.ascontiguousarray(T.T), device="cuda")
+    Ld = torch.as_tensor(Lsh, device="cuda")
+    E = torch.empty((g.count, 3), dtype=torch.float64, device="cuda")
+    ehat = torch.empty((3, g.count), dtype=torch.float64, device="cuda")
+    _lib.call("sss_sh_irradiance", _lib.ptr(T_l), _lib.ptr(Ld), 25, cfg.side, cfg.levels,
+              _lib.ptr(E), _lib.ptr(ehat), _lib.stream_ptr())
+    E_ref = O.sh_irradiance(T, Lsh)
+    assert np.array_equal(E.cpu().numpy(), E_ref)
+    want = np.stack([O.haar2d_fwd(E_ref[:, c].reshape(1, cfg.side, cfg.side), cfg.levels).reshape(-1)
+                     for c in range(3)])
+    assert np.array_equal(ehat.cpu().numpy(), want)
+
+
+def test_env_projection_bitwise_vs_reference_golden(lib, golden):
+    from paper_2203_12339_b200 import _lib
+
+    g = golden("env")
+    faces = torch.as_tensor(np.ascontiguousarray(g["faces"]), device="cuda")
+    kk = 32
+    idx = torch.empty((3, kk), dtype=torch.int32, device="cuda")
+    val = torch.empty((3, kk), dtype=torch.float64, device="cuda")
+    uidx = torch.empty(3 * kk, dtype=torch.int32, device="cuda")
+    ulc = torch.empty((3 * kk, 3), dtype=torch.float64, device="cuda")
+    nu = torch.empty(1, dtype=torch.int32, device="cuda")
+    _lib.call("sss_env_project", _lib.ptr(faces), 8, kk, _lib.ptr(idx), _lib.ptr(val),
+              _lib.ptr(uidx), _lib.ptr(ulc), _lib.ptr(nu), _lib.stream_ptr())
+    for c in range(3):
+        assert np.array_equal(idx[c].cpu().numpy().astype(np.uint32), g[f"idx{c}"])
+        assert np.array_equal(val[c].cpu().numpy(), g[f"val{c}"])
+    union = np.unique(np.concatenate([g[f"idx{c}"] for c in range(3)]))
+    assert int(nu.item()) == union.size
+    assert np.array_equal(uidx[: union.size].cpu().numpy().astype(np.uint32), union)
+
+
+def test_env_transfer_and_irradiance_bitwise(lib):
+    from paper_2203_12339_b200 import _lib, lighting as LT
+
+    side, L, s = 32, 2, 16
+    g = _geom(C.C1)
+    dirs = torch.as_tensor(LT.face_directions(s).reshape(-1, 3), device="cuda")
+    dom = torch.as_tensor(LT.face_solid_angles(s).reshape(-1), device="cuda")
+    nrm = torch.as_tensor(g.normals, device="cuda")
+    D = 6 * s * s
+    W2 = torch.empty((D, g.count), dtype=torch.float32, device="cuda")
+    _lib.call("sss_env_transfer", _lib.ptr(nrm), g.count, _lib.ptr(dirs), _lib.ptr(dom), s,
+              _lib.ptr(W2), _lib.stream_ptr())
+    W2_ref = O.env_transfer_w2_exact(g.normals, s)
+    assert np.array_equal(W2.cpu().numpy().T, W2_ref)
+    env = LT.Environment(side=s, seed=5)
+    faces = env.faces(13.0)
+    spectra = O.project_environment(faces, 128)
+    E_ref = O.env_irradiance(W2_ref, spectra)
+    from paper_2203_12339_b200.runtime import EnvLight, Scene  # noqa: F401
+
+    kk = 128
+    fd = torch.as_tensor(faces, device="cuda")
+    idx = torch.empty((3, kk), dtype=torch.int32, device="cuda")
+    val = torch.empty((3, kk), dtype=torch.float64, device="cuda")
+    uidx = torch.empty(3 * kk, dtype=torch.int32, device="cuda")
+    ulc = torch.empty((3 * kk, 3), dtype=torch.float64, device="cuda")
+    nu = torch.empty(1, dtype=torch.int32, device="cuda")
+    _lib.call("sss_env_project", _lib.ptr(fd), s, kk, _lib.ptr(idx), _lib.ptr(val), _lib.ptr(uidx),
+              _lib.ptr(ulc), _lib.ptr(nu), _lib.stream_ptr())
+    E = torch.empty((g.count, 3), dtype=torch.float64, device="cuda")
+    ehat = torch.empty((3, g.count), dtype=torch.float64, device="cuda")
+    _lib.call("sss_env_irradiance", _lib.ptr(W2), D, _lib.ptr(uidx), _lib.ptr(ulc), _lib.ptr(nu),
+              kk, side, L, _lib.ptr(E), _lib.ptr(ehat), _lib.stream_ptr())
+    assert np.array_equal(E.cpu().numpy(), E_ref)
+
+
+def test_material_weights_match_oracle(lib):
+    from paper_2203_12339_b200.basis import OpticalMaterial, build_basis, project_material
+
+    b = build_basis(8, (8, 4))
+    rng = np.random.default_rng(1)
+    for _ in range(5):
+        m = OpticalMaterial(sigma_s_prime=rng.uniform(0.5, 3.0, 3), sigma_a=rng.uniform(0.001, 0.05, 3),
+                            eta=float(rng.uniform(1.2, 1.5)))
+        got = project_material(b, m).s
+        want = O.project_material(b.bases, b.r_nodes, m.sigma_s_prime, m.sigma_a, m.eta)
+        assert np.allclose(got, want, rtol=1e-11, atol=1e-14 * np.abs(want).max())
+
+
+# ---------------------------------------------------------------------------
+# full frame at C1 against the oracle pipeline
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def c1(lib):
+    from paper_2203_12339_b200.basis import build_basis
+
+    cfg = C.C1
+    g = _geom(cfg)
+    b = build_basis(cfg.K, cfg.lattice)
+    ops = O.precompute_compressed(g.positions.astype(np.float64), g.area.astype(np.float64),
+                                  cfg.side, b.r_nodes, b.bases, cfg.step1_keep,
+                                  cfg.step2_fraction, levels=cfg.levels, w1="haar")
+    ops = [O.round_trip_f32(op) for op in ops]
+    return cfg, g, b, ops
+
+
+def _scene(c1, light, material=None, **kw):
+    from paper_2203_12339_b200.basis import OpticalMaterial
+    from paper_2203_12339_b200.runtime import Scene
+    from paper_2203_12339_b200.transfer import DeviceTransfer
+
+    cfg, g, b, ops = c1
+    dt = DeviceTransfer.from_reference(ops, cfg.side, cfg.levels)
+    m = material or OpticalMaterial(sigma_s_prime=cfg.material[0], sigma_a=cfg.material[1],
+                                    eta=cfg.material[2])
+    return Scene(g, dt, b, m, light, keep_scatter=True, **kw)
+
+
+def _oracle_frame(c1, E, material, e_keep=0.25):
+    cfg, g, b, ops = c1
+    return O.relight(E, ops, b.bases, b.r_nodes,
+                     (material.sigma_s_prime, material.sigma_a, material.eta), cfg.side,
+                     cfg.levels, "haar", e_keep, g.normals.astype(np.float64),
+                     g.positions.astype(np.float64), np.array(C.CAMERA[0]))
+
+
+def test_frame_c1_sh_parity(c1):
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import SHLight
+
+    cfg, g, b, ops = c1
+    Lsh = LT.random_sh_light(cfg.sh_bands, 17)
+    sc = _scene(c1, SHLight(Lsh))
+    fr = sc.relight()
+    E = O.sh_irradiance(LT.sh_transfer(g.normals, cfg.sh_bands), Lsh)
+    ref = _oracle_frame(c1, E, sc.material)
+    for c in range(3):
+        assert np.array_equal(sc.selected_indices(c), ref["spectra"][c].indices)
+    assert O.parity_error(sc.scatter.cpu().numpy(), ref["scatter"], TAU) <= TOL
+    assert O.parity_error(fr.radiance_unclamped, ref["radiance_unclamped"], TAU) <= TOL
+    assert O.parity_error(fr.radiance, ref["radiance"], TAU) <= TOL
+    assert np.all(fr.radiance >= 0)
+    assert fr.kept_energy_ratio == pytest.approx(
+        sum(s.kept_energy for s in ref["spectra"]) / sum(s.total_energy for s in ref["spectra"]),
+        rel=1e-9)
+    assert fr.timings_ms["irradiance"] > 0 and fr.timings_ms["transfer"] > 0
+
+
+def test_frame_c1_env_parity(c1):
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import EnvLight
+
+    cfg, g, b, ops = c1
+    env = LT.Environment(side=16, seed=2)
+    faces = env.faces(30.0)
+    sc = _scene(c1, EnvLight(faces))
+    fr = sc.relight()
+    E = O.env_irradiance(O.env_transfer_w2_exact(g.normals, 16), O.project_environment(faces, 128))
+    ref = _oracle_frame(c1, E, sc.material)
+    for c in range(3):
+        assert np.array_equal(sc.selected_indices(c), ref["spectra"][c].indices)
+    assert O.parity_error(fr.radiance_unclamped, ref["radiance_unclamped"], TAU) <= TOL
+
+
+def test_edit_path_c1(c1):
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.basis import OpticalMaterial
+    from paper_2203_12339_b200.runtime import SHLight
+
+    cfg, g, b, ops = c1
+    Lsh = LT.random_sh_light(cfg.sh_bands, 3)
+    sc = _scene(c1, SHLight(Lsh))
+    f1 = sc.relight()
+    f2 = sc.set_material(sc.material)
+    assert np.array_equal(f1.radiance, f2.radiance)  # identity edit bitwise (test_runtime.py:75-78)
+    assert f2.timings_ms["irradiance"] == 0.0 and f2.timings_ms["transfer"] == 0.0
+    E = O.sh_irradiance(LT.sh_transfer(g.normals, cfg.sh_bands), Lsh)
+    rng = np.random.default_rng(2)
+    for _ in range(3):
+        m = OpticalMaterial(sigma_s_prime=rng.uniform(0.5, 3.0, 3),
+                            sigma_a=rng.uniform(0.001, 0.05, 3), eta=float(rng.uniform(1.2, 1.5)))
+        edited = sc.set_material(m)
+        full = sc.relight()
+        assert np.abs(edited.radiance - full.radiance).max() <= 1e-6 * np.abs(full.radiance).max()
+        ref = _oracle_frame(c1, E, m)
+        assert O.parity_error(edited.radiance_unclamped, ref["radiance_unclamped"], TAU) <= TOL
+
+
+def test_linearity_and_zero_light(c1):
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import SHLight
+
+    cfg = c1[0]
+    Lsh = LT.random_sh_light(cfg.sh_bands, 8)
+    sc = _scene(c1, SHLight(Lsh))
+    f1 = sc.relight()
+    f2 = sc.set_light(SHLight(2.0 * Lsh))
+    # doubling is exact in binary fp: same selection, exactly doubled sums
+    assert np.allclose(f2.radiance_unclamped, 2.0 * f1.radiance_unclamped, rtol=1e-6, atol=0)
+    f0 = sc.set_light(SHLight(np.zeros_like(Lsh)))
+    assert np.all(f0.radiance == 0.0)
+
+
+def test_out_of_box_material_clamped(c1):
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.basis import OpticalMaterial
+    from paper_2203_12339_b200.runtime import SHLight
+
+    sc = _scene(c1, SHLight(LT.random_sh_light(3, 1)))
+    sc.relight()
+    with pytest.warns(UserWarning, match="clamped"):
+        sc.set_material(OpticalMaterial(sigma_s_prime=[50.0, 1.0, 1.0], sigma_a=[0.01, 0.01, 0.01]))
+    assert sc.material.sigma_s_prime[0] == sc.basis.sigma_box[1]
+
+
+def test_cuda_graph_replay_matches_eager(c1):
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import SHLight
+
+    sc = _scene(c1, SHLight(LT.random_sh_light(3, 21)))
+    eager = sc.relight().radiance_unclamped
+    sc.capture()
+    sc.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(sc.radiance_unclamped.cpu().numpy().astype(np.float64), eager)
