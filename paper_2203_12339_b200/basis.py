@@ -193,16 +193,18 @@ def basis_for(cfg) -> DiffusionBasis:
 
 def material_weights_device(basis: DiffusionBasis, material: OpticalMaterial, out=None,
                             sigma_dev=None, stream=None):
-    """s (3, K) fp64 on the device; sigma_dev: optional preallocated (6,) buffer."""
+    """s (3, K) fp64 on the device; sigma_dev: optional preallocated (7,)
+    buffer {sp[3], sa[3], eta}."""
     dev = basis.device()
     if sigma_dev is None:
-        sigma_dev = torch.tensor(np.concatenate([material.sigma_s_prime, material.sigma_a]),
+        sigma_dev = torch.tensor(np.concatenate([material.sigma_s_prime, material.sigma_a,
+                                                 [material.eta]]),
                                  dtype=torch.float64, device="cuda")
     if out is None:
         out = torch.empty((3, basis.K), dtype=torch.float64, device="cuda")
     _lib.call("sss_material_weights", _lib.ptr(dev["bw"]), _lib.ptr(dev["r_nodes"]),
-              basis.K, len(basis.r_nodes), _lib.ptr(sigma_dev), float(material.eta),
-              _lib.ptr(out), _lib.stream_ptr(stream))
+              basis.K, len(basis.r_nodes), _lib.ptr(sigma_dev), _lib.ptr(out),
+              _lib.stream_ptr(stream))
     return out
 
 
