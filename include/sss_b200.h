@@ -104,6 +104,52 @@ int sss_edit_finish(int K, int side, int levels, const double* vk, const double*
                     const double* material, double* scatter, float* radiance,
                     float* radiance_unclamped, void* stream);
 
+/* ================= precompute (path d): pair pass + two-step compression ====
+ * replaces precompute_compressed (transfer.py:350-361) for a geometry image
+ * with L-level Haar (L <= 3) on w0 and w1. N = side^2; "tm" = tile-major.  */
+
+/* Pair block pass for PCA term k (transfer_block, _kernels_nb.py:179-205):
+ *   exact = 0: lerp of the tabulated bases, fp64, bitwise the reference's;
+ *   exact = 1: R_d evaluated per pair for each of n_mat training materials in
+ *              fp32, projected with Pkm (K, n_mat) = U/S (mat (n_mat, 4):
+ *              sigma_tr, z_r, z_v, alpha'/(4 pi)), masked at r_max.
+ * Writes D (N, N) fp64 = w0 Haar of each receiver row (tm rows, tm columns)
+ * and/or Mout (N, N) fp64 = w1 Haar of f32(D) along receivers, column-major
+ * (column c_tm contiguous). Either may be NULL. */
+int sss_pair_block(int levels, int exact, int side, const float* pos, const float* area,
+                   const double* r_nodes, const double* bases, const double* slopes, int nr, int k,
+                   const float* Pkm, const float* mat, int n_mat, float r_max, double* D,
+                   double* Mout, void* stream);
+
+/* Step 1 (run_step1 + step1_unions, transfer.py:216-246): per row of D keep
+ * the n_keep largest |v| (flat-index tie-break) and OR the kept flat column
+ * ids into union_bits (N/32 words, caller-zeroed). */
+int sss_step1_select(const double* D, int n_dom, int n_rows, int n_keep, const uint32_t* tm2flat,
+                     uint32_t* union_bits, void* stream);
+
+/* Step 2 (_threshold_columns, transfer.py:303-333 with compress_energy): for
+ * each union column, the energy-fraction cut. Per tm column: threshold key
+ * col_t (~0 = column dropped), tie bound col_fmax (flat row), kept count,
+ * energy (kept, total). */
+int sss_step2_select(const double* M, int n_dom, double fraction, const uint32_t* flat2tm,
+                     const uint32_t* tm2flat, const uint32_t* union_bits, uint64_t* col_t,
+                     uint32_t* col_fmax, uint32_t* col_cnt, double* col_energy, void* stream);
+
+/* Emission into the frame layout (tile-major CSR). pass 0: counts
+ * (N rows x nchunks); pass 1: write cols (flat w0 ids) / vals (f32) at offs
+ * (exclusive scan of counts, relative to this k's arrays). */
+int sss_emit(int pass, const double* M, int n_dom, int tile_rows, int chunk, const uint64_t* col_t,
+             const uint32_t* col_fmax, const uint32_t* tm2flat, uint32_t* counts,
+             const uint64_t* offs, uint32_t* cols, float* vals, void* stream);
+
+/* exclusive scan u32 -> u64 (block_sums: ceil(n/1024) scratch; total out) */
+int sss_scan_u32(const uint32_t* in, uint64_t* out, size_t n, uint64_t* block_sums,
+                 uint64_t* total, void* stream);
+
+/* rowptr[r] = base + offs[r * nchunks], rowptr[n_rows] = base + *total */
+int sss_rowptr(const uint64_t* offs, int nchunks, int n_rows, uint64_t base, const uint64_t* total,
+               uint64_t* rowptr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

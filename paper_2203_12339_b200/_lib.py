@@ -29,6 +29,12 @@ _SIGS = {
     "sss_material_weights": [_P, _P, _I, _I, _P, _P, _P],
     "sss_transfer_relight": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_edit_finish": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_pair_block": [_I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _I, C.c_float, _P, _P, _P],
+    "sss_step1_select": [_P, _I, _I, _I, _P, _P, _P],
+    "sss_step2_select": [_P, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_emit": [_I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_scan_u32": [_P, _P, C.c_size_t, _P, _P, _P],
+    "sss_rowptr": [_P, _I, _I, C.c_uint64, _P, _P, _P],
 }
 
 

@@ -180,4 +180,106 @@ int sss_edit_finish(int K, int side, int levels, const double* vk, const double*
   return check_launch("k_edit_finish");
 }
 
+// ---------------------------------------------------------------------------
+// precompute (path d)
+// ---------------------------------------------------------------------------
+
+int sss_pair_block(int levels, int exact, int side, const float* pos, const float* area,
+                   const double* r_nodes, const double* bases, const double* slopes, int nr, int k,
+                   const float* Pkm, const float* mat, int n_mat, float r_max, double* D,
+                   double* Mout, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (levels > 3) return fail(SSS_EINVAL, "pair pass supports levels <= 3");
+  if (!pos || !area || (!D && !Mout)) return fail(SSS_EINVAL, "bad pair_block pointers");
+  if (!exact && (!r_nodes || !bases || !slopes || nr < 2))
+    return fail(SSS_EINVAL, "lerp mode needs r_nodes / bases / slopes");
+  if (exact && (!Pkm || !mat || n_mat <= 0)) return fail(SSS_EINVAL, "exact mode needs Pkm / mat");
+  sss::PairParams p{pos, area, r_nodes, bases, slopes, nr, k, side, Pkm, mat, n_mat, r_max};
+  const int T = 1 << levels, T2 = T * T;
+  const int tiles = (side / T) * (side / T);
+  dim3 grid(tiles, tiles);
+  const size_t smem = ((size_t)T2 * (T2 + 1) + (exact ? 0 : 3 * (size_t)nr)) * sizeof(double);
+  const void* fn = nullptr;
+#define SSS_PAIR_CASE(LV)                                                                     \
+  case LV:                                                                                    \
+    fn = exact ? (const void*)sss::k_pair_block<LV, true> : (const void*)sss::k_pair_block<LV, false>; \
+    if (int r = set_smem(fn, smem)) return r;                                                 \
+    if (exact) sss::k_pair_block<LV, true><<<grid, 128, smem, S_(stream)>>>(p, D, Mout);      \
+    else sss::k_pair_block<LV, false><<<grid, 128, smem, S_(stream)>>>(p, D, Mout);           \
+    break;
+  switch (levels) {
+    SSS_PAIR_CASE(1)
+    SSS_PAIR_CASE(2)
+    SSS_PAIR_CASE(3)
+    default: return fail(SSS_EINVAL, "levels");
+  }
+#undef SSS_PAIR_CASE
+  return check_launch("k_pair_block");
+}
+
+int sss_step1_select(const double* D, int n_dom, int n_rows, int n_keep, const uint32_t* tm2flat,
+                     uint32_t* union_bits, void* stream) {
+  if (!D || !tm2flat || !union_bits || n_dom <= 0 || n_rows < 0 || n_keep < 1)
+    return fail(SSS_EINVAL, "bad step1 arguments");
+  if (n_rows == 0) return SSS_OK;
+  const size_t smem = sizeof(sss::SelShared) + 2 * (size_t)((n_dom + 31) / 32) * 4;
+  if (int r = set_smem((const void*)sss::k_step1_select, smem)) return r;
+  sss::k_step1_select<<<n_rows, sss::kSelThreads, smem, S_(stream)>>>(D, n_dom, n_keep, tm2flat,
+                                                                      union_bits);
+  return check_launch("k_step1_select");
+}
+
+int sss_step2_select(const double* M, int n_dom, double fraction, const uint32_t* flat2tm,
+                     const uint32_t* tm2flat, const uint32_t* union_bits, uint64_t* col_t,
+                     uint32_t* col_fmax, uint32_t* col_cnt, double* col_energy, void* stream) {
+  if (!M || !flat2tm || !tm2flat || !union_bits || !col_t || !col_fmax || !col_cnt || !col_energy ||
+      n_dom <= 0 || !(fraction >= 0.0 && fraction <= 1.0))
+    return fail(SSS_EINVAL, "bad step2 arguments");
+  const size_t smem = sizeof(sss::SelShared) + (size_t)((n_dom + 31) / 32) * 4;
+  if (int r = set_smem((const void*)sss::k_step2_select, smem)) return r;
+  sss::k_step2_select<<<n_dom, sss::kSelThreads, smem, S_(stream)>>>(
+      M, n_dom, fraction, flat2tm, tm2flat, union_bits, col_t, col_fmax, col_cnt, col_energy);
+  return check_launch("k_step2_select");
+}
+
+int sss_emit(int pass, const double* M, int n_dom, int tile_rows, int chunk, const uint64_t* col_t,
+             const uint32_t* col_fmax, const uint32_t* tm2flat, uint32_t* counts,
+             const uint64_t* offs, uint32_t* cols, float* vals, void* stream) {
+  if (!M || !col_t || !col_fmax || !tm2flat || tile_rows <= 0 || tile_rows > 1024 || chunk <= 0 ||
+      n_dom % tile_rows)
+    return fail(SSS_EINVAL, "bad emit arguments");
+  dim3 grid((n_dom + chunk - 1) / chunk, n_dom / tile_rows);
+  const int thr = ((tile_rows + 31) / 32) * 32;
+  if (pass == 0) {
+    if (!counts) return fail(SSS_EINVAL, "emit count needs counts");
+    sss::k_emit_count<<<grid, thr, 0, S_(stream)>>>(M, n_dom, tile_rows, chunk, col_t, col_fmax,
+                                                   tm2flat, counts);
+    return check_launch("k_emit_count");
+  }
+  if (!offs || !cols || !vals) return fail(SSS_EINVAL, "emit write needs offs / cols / vals");
+  sss::k_emit_write<<<grid, thr, 0, S_(stream)>>>(M, n_dom, tile_rows, chunk, col_t, col_fmax,
+                                                 tm2flat, offs, 0, cols, vals);
+  return check_launch("k_emit_write");
+}
+
+int sss_scan_u32(const uint32_t* in, uint64_t* out, size_t n, uint64_t* block_sums,
+                 uint64_t* total, void* stream) {
+  if (!in || !out || !block_sums || !total) return fail(SSS_EINVAL, "bad scan arguments");
+  const int nb = (int)((n + 1023) / 1024);
+  if (nb == 0) return cudaMemsetAsync(total, 0, 8, S_(stream)) == cudaSuccess ? SSS_OK : SSS_ECUDA;
+  sss::k_scan_blocks<<<nb, 1024, 0, S_(stream)>>>(in, out, n, block_sums);
+  sss::k_scan_sums<<<1, 1, 0, S_(stream)>>>(block_sums, nb, total);
+  sss::k_scan_add<<<nb, 1024, 0, S_(stream)>>>(out, n, block_sums);
+  return check_launch("k_scan");
+}
+
+int sss_rowptr(const uint64_t* offs, int nchunks, int n_rows, uint64_t base, const uint64_t* total,
+               uint64_t* rowptr, void* stream) {
+  if (!offs || !total || !rowptr || nchunks <= 0 || n_rows <= 0)
+    return fail(SSS_EINVAL, "bad rowptr arguments");
+  sss::k_rowptr<<<(n_rows + 1 + 255) / 256, 256, 0, S_(stream)>>>(offs, nchunks, n_rows, base,
+                                                                   total, rowptr);
+  return check_launch("k_rowptr");
+}
+
 }  // extern "C"
