@@ -1,0 +1,399 @@
+"""Headline benchmark: the 256x256 environment-lit relight + material-edit
+frame (BASELINE.json configs[2], "C3") on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one frame of the C3 sequence: the cubemap rotates 1 deg about +y
+(relight: env projection -> E -> w0 Haar -> top-n -> K-fused transfer +
+recombine + inverse Haar + shade), and every 10th frame also applies a
+material edit (edit path). ``value`` = shaded points/s with inputs resident
+in HBM (CUDA graphs, device timing); ``e2e`` = the same through the public
+Scene API with host cubemaps in and host radiance out. Under torchrun every
+rank renders its own independent object (weak scaling, no data-path
+collective); timing is the max over ranks.
+
+``--impl reference`` times the CPU oracle port of the same frame on the host
+cores (rank 0 only), on a bounded sample (stage 2 on a subset of operator
+rows, scaled), using an operator built by the GPU precompute in setup.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "shaded points/sec & ms per relight+material-edit frame; % of HBM roofline"
+UNIT = "shaded points/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="env_large_256")
+    ap.add_argument("--cpu-sample-rows", type=int, default=32, help="1/x of tiles in the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--side", type=int, default=None, help="override the geometry-image side (testing)")
+    return ap.parse_args()
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = Path("/tmp") / f"sss_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def setup_scene(cfg, rank, torch, stats):
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.basis import OpticalMaterial, build_basis
+    from paper_2203_12339_b200.geometry import make_geometry_image
+    from paper_2203_12339_b200.precompute import precompute_compressed
+    from paper_2203_12339_b200.runtime import EnvLight, Scene
+
+    g = make_geometry_image(cfg.side, cfg.radius, cfg.bump_amp, cfg.bump_terms, cfg.seed + rank)
+    b = build_basis(cfg.K, cfg.lattice)
+    t0 = time.perf_counter()
+    dt = precompute_compressed(g, b, cfg.levels, cfg.step1_keep, cfg.step2_fraction, stats=stats)
+    torch.cuda.synchronize()
+    stats["precompute_s"] = time.perf_counter() - t0
+    env = LT.Environment(side=cfg.env_side, seed=7 + rank)
+    m0 = OpticalMaterial(sigma_s_prime=cfg.material[0], sigma_a=cfg.material[1], eta=cfg.material[2])
+    scene = Scene(g, dt, b, m0, EnvLight(env.faces(0.0)), e_keep=cfg.e_keep)
+    return g, b, dt, env, scene
+
+
+def frame_inputs(cfg, env, n_frames, seed):
+    """Host inputs of the C3 sequence: rotated cubemaps and edit materials."""
+    from paper_2203_12339_b200.basis import OpticalMaterial
+    from paper_2203_12339_b200.config import SIGMA_BOX
+
+    rng = np.random.default_rng(seed)
+    faces = [env.faces(cfg.extra.get("rotate_deg", 1.0) * f) for f in range(n_frames)]
+    mats = {}
+    every = cfg.extra.get("edit_every", 10)
+    for f in range(n_frames):
+        if f % every == every - 1:
+            sp = np.exp(rng.uniform(np.log(SIGMA_BOX[0]), np.log(SIGMA_BOX[1]), 3))
+            sa = np.exp(rng.uniform(np.log(SIGMA_BOX[2]), np.log(SIGMA_BOX[3]), 3))
+            mats[f] = OpticalMaterial(sigma_s_prime=sp, sigma_a=sa, eta=cfg.material[2])
+    return faces, mats
+
+
+def run_ours(a, cfg):
+    import torch
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    from paper_2203_12339_b200 import _lib
+
+    _lib.load()
+    stats = {}
+    g, b, dt, env, scene = setup_scene(cfg, rank, torch, stats)
+    n = g.count
+    total = a.warmup + a.steps
+    faces, mats = frame_inputs(cfg, env, total, 100 + rank)
+    dev_faces = torch.stack([torch.as_tensor(f) for f in faces]).cuda()
+    dev_mats = {f: torch.tensor(np.concatenate([m.sigma_s_prime, m.sigma_a, [m.eta]]),
+                                dtype=torch.float64).cuda() for f, m in mats.items()}
+    scene.capture()
+    stream = torch.cuda.current_stream()
+
+    def step(f):
+        scene.light_buf.copy_(dev_faces[f], non_blocking=True)
+        scene.replay(edit=False)
+        if f in dev_mats:
+            scene.material_buf.copy_(dev_mats[f], non_blocking=True)
+            scene.replay(edit=True)
+
+    for f in range(a.warmup):
+        step(f)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for f in range(a.warmup, total):
+        step(f)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    n_edit = sum(1 for f in range(a.warmup, total) if f in dev_mats)
+    ms_per_step = ms / a.steps
+    value = ws * n * a.steps / (ms / 1e3)
+
+    # ---- dominant kernel: the K-fused transfer, timed alone on its stream
+    kt = []
+    for f in range(min(a.steps, 20)):
+        ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ka.record(stream)
+        scene._launch_transfer()
+        kb.record(stream)
+        kt.append((ka, kb))
+    torch.cuda.synchronize()
+    k_ms = float(np.mean([x.elapsed_time(y) for x, y in kt]))
+    # algorithmic bytes of one transfer launch (SURVEY §8d B_T + B_c), with the
+    # selection of the current frame: entries whose w0 column is kept by any
+    # channel (8 B each: u32 col + f32 val) + row pointers + v_k cache write +
+    # radiance writes + geometry reads
+    sel = (scene.x != 0).any(dim=0)
+    touched = int(sel[dt.cols.long()].sum().item())
+    K = dt.K
+    alg_bytes = 8 * touched + 8 * K * (n + 1) + 24 * K * n + 24 * n + 24 * n
+    all_bytes = 8 * dt.nnz + 8 * K * (n + 1) + 24 * K * n + 24 * n + 24 * n
+    peak, peak_kind = _peaks()
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9
+    traffic_path = ROOT / "profiles" / "r01_transfer_dram_bytes.json"
+    traffic = None
+    if traffic_path.exists():
+        try:
+            traffic = json.loads(traffic_path.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: public API, host cubemap in, host radiance out
+    from paper_2203_12339_b200.runtime import EnvLight
+
+    n_e2e = min(a.steps, 30)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for i in range(n_e2e):
+        f = a.warmup + i
+        fr = scene.set_light(EnvLight(faces[f]))
+        if f in mats:
+            fr = scene.set_material(mats[f])
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    n_edit_e2e = sum(1 for i in range(n_e2e) if a.warmup + i in mats)
+    h2d = faces[0].nbytes + (56 * n_edit_e2e) / n_e2e
+    d2h = (2 * n * 3 * 4 + 48) * (1 + n_edit_e2e / n_e2e)
+    e2e = {"value": ws * n * n_e2e / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s / n_e2e,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_e2e,
+           "path": "Scene.set_light(EnvLight(host cubemap)) / set_material -> FrameResult (numpy)"}
+
+    # ---- edit-path latency alone (launch-bound; reported separately)
+    ee = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ee[0].record(stream)
+    for _ in range(50):
+        scene.replay(edit=True)
+    ee[1].record(stream)
+    torch.cuda.synchronize()
+    edit_ms = ee[0].elapsed_time(ee[1]) / 50
+    relight_only = []
+    rr = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    rr[0].record(stream)
+    for _ in range(20):
+        scene.replay(edit=False)
+    rr[1].record(stream)
+    torch.cuda.synchronize()
+    relight_ms = rr[0].elapsed_time(rr[1]) / 20
+
+    cpu = None
+    if rank == 0 and ws == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, scene, dt, g, b, faces, mats, a.cpu_sample_rows, steps=2, warmup=0)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded geometry image + log-normal/lobe cubemap; BASELINE C3 shapes)",
+            "config": {
+                "workload": f"{cfg.name} (BASELINE configs[2], C3): relight per frame, edit every "
+                            f"{cfg.extra.get('edit_every', 10)}",
+                "side": cfg.side, "points": n, "K": cfg.K, "training_materials": cfg.n_materials,
+                "levels": cfg.levels, "step1_keep": cfg.step1_keep,
+                "step2_fraction": cfg.step2_fraction, "e_keep": cfg.e_keep,
+                "env": f"6x{cfg.env_side}x{cfg.env_side} cubemap, top-128 per channel, "
+                       f"{cfg.extra.get('rotate_deg', 1.0)} deg/frame about +y",
+                "operator_nnz": dt.nnz, "operator_bytes": dt.nbytes,
+                "l2": f"inputs larger than L2 (operator {dt.nbytes / 1e9:.2f} GB > 126 MB)",
+                "parallelism": f"{ws} independent objects (1 per GPU)" if ws > 1 else "1 GPU",
+                "precompute_s": stats.get("precompute_s"), "precompute_pairs": stats.get("pairs"),
+            },
+            "roofline": {"bound": "hbm", "kernel": "k_transfer_relight", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg_bytes, "stored_bytes_per_launch": all_bytes,
+                         "touched_nnz": touched, "kernel_ms": k_ms},
+            "e2e": e2e,
+            "gpu_launches": 6 * a.steps + 2 * n_edit,
+            "clocks": clk,
+            "relight_ms": relight_ms, "edit_ms": edit_ms,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(cfg, scene, dt, g, b, faces, mats, sample, steps=2, warmup=0):
+    """Oracle port of the C3 frame on the host (numpy, 1 thread of BLAS-free
+    code): stage 1 in full, stage 2 on every `sample`-th tile's rows (scaled),
+    stages 3-5 in full. Returns the cpu_baseline object."""
+    import torch
+
+    from oracle import sss_oracle as O
+
+    n, side, L, K = g.count, g.side, cfg.levels, dt.K
+    T2 = (1 << L) ** 2
+    rp = dt.rowptr.cpu().numpy()
+    cols = dt.cols.cpu().numpy().view(np.uint32)
+    vals = dt.vals.cpu().numpy()
+    W2 = scene.W2.cpu().numpy().T  # (N, D) float32 table (precompute output)
+    tiles = np.arange(0, n // T2, sample)
+    rows = (tiles[:, None] * T2 + np.arange(T2)[None, :]).reshape(-1)
+    cam = np.array(scene.camera.position)
+    times = []
+    for i in range(warmup + steps):
+        f = i
+        t0 = time.perf_counter()
+        spectra = O.project_environment(faces[f], 128)
+        E = O.env_irradiance(W2, spectra)
+        sel = O.select_irradiance(E, side, L, cfg.e_keep)
+        x = np.zeros((3, n))
+        for c in range(3):
+            x[c, sel[c].indices] = sel[c].values
+        t1 = time.perf_counter()
+        for k in range(K):
+            O.csr_rows_apply(rp[k], cols, vals, rows, x)
+        t2 = time.perf_counter()
+        m = scene.material
+        w = O.project_material(b.bases, b.r_nodes, m.sigma_s_prime, m.sigma_a, m.eta)
+        vk = np.zeros((K, 3, n))
+        O.finish(vk, w, side, L, "haar", g.normals.astype(np.float64),
+                 g.positions.astype(np.float64), cam, m.eta)
+        t3 = time.perf_counter()
+        if i >= warmup:
+            times.append((t1 - t0) + (t2 - t1) * (n / rows.size) + (t3 - t2))
+    per_frame = float(np.mean(times))
+    return {"value": n / per_frame, "unit": UNIT, "cores": 1, "kind": "port",
+            "ms_per_step": per_frame * 1e3,
+            "sample": f"C3 frame, oracle (numpy) port: stage 1 + stages 3-5 in full, stage 2 on "
+                      f"1/{sample} of the tiles ({rows.size} of {n} rows, scaled linearly), "
+                      f"{steps} frames, operator from the GPU precompute"}
+
+
+def run_reference(a, cfg):
+    ws, rank, local = _dist()
+    if rank != 0:
+        return
+    import torch
+
+    torch.cuda.set_device(local)
+    stats = {}
+    g, b, dt, env, scene = setup_scene(cfg, 0, torch, stats)
+    faces, mats = frame_inputs(cfg, env, a.warmup + a.steps, 100)
+    cpu = cpu_baseline(cfg, scene, dt, g, b, faces, mats, a.cpu_sample_rows, steps=a.steps,
+                       warmup=a.warmup)
+    line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": cpu["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic (BASELINE C3 shapes)",
+            "config": {"workload": f"{cfg.name} (BASELINE configs[2], C3)", "side": cfg.side,
+                       "points": g.count, "K": cfg.K, "operator_nnz": dt.nnz},
+            "cpu_baseline": cpu,
+            "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    a = _args()
+    from paper_2203_12339_b200.config import CONFIGS
+
+    cfg = CONFIGS[a.config]
+    if a.side:
+        cfg = cfg.with_(side=a.side)
+    if a.impl == "reference":
+        run_reference(a, cfg)
+    else:
+        run_ours(a, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -734,3 +734,25 @@ def env_transfer_w2_exact(normals32, side):
     w = np.clip(cos, 0.0, 1.0) * dom[None, :]
     w2 = haar2d_fwd(w.reshape(n.shape[0] * 6, side, side)).reshape(n.shape[0], 6 * side * side)
     return w2.astype(np.float32)
+
+
+def csr_rows_apply(rowptr, cols, vals, rows, x):
+    """CPU port of the transfer apply for a subset of operator rows stored in
+    the device's tile-major CSR layout: out[q, c] = sum_p vals[p] x[c, cols[p]]
+    over row rows[q] (the same products csc_apply accumulates column by
+    column, _kernels_nb.py:301-313). x: (3, N) masked E spectrum."""
+    rows = np.asarray(rows, np.int64)
+    starts = rowptr[rows].astype(np.int64)
+    counts = (rowptr[rows + 1] - rowptr[rows]).astype(np.int64)
+    total = int(counts.sum())
+    out = np.zeros((rows.size, x.shape[0]))
+    if total == 0:
+        return out
+    offs = np.repeat(np.cumsum(counts) - counts, counts)
+    sel = np.arange(total, dtype=np.int64) - offs + np.repeat(starts, counts)
+    seg = np.repeat(np.arange(rows.size), counts)
+    c = cols[sel].astype(np.int64)
+    v = vals[sel].astype(np.float64)
+    for ch in range(x.shape[0]):
+        out[:, ch] = np.bincount(seg, weights=v * x[ch, c], minlength=rows.size)
+    return out
