@@ -325,6 +325,9 @@ def cpu_baseline(cfg, scene, dt, g, b, faces, mats, sample, steps=2, warmup=0):
     cols = dt.cols.cpu().numpy().view(np.uint32)
     vals = dt.vals.cpu().numpy()
     W2 = scene.W2.cpu().numpy().T  # (N, D) float32 table (precompute output)
+    from paper_2203_12339_b200.transfer import tile_major_to_flat
+
+    tm2flat = tile_major_to_flat(side, L)
     tiles = np.arange(0, n // T2, sample)
     rows = (tiles[:, None] * T2 + np.arange(T2)[None, :]).reshape(-1)
     cam = np.array(scene.camera.position)
@@ -338,6 +341,7 @@ def cpu_baseline(cfg, scene, dt, g, b, faces, mats, sample, steps=2, warmup=0):
         x = np.zeros((3, n))
         for c in range(3):
             x[c, sel[c].indices] = sel[c].values
+        x = x[:, tm2flat]  # the operator's columns are tile-major ids
         t1 = time.perf_counter()
         for k in range(K):
             O.csr_rows_apply(rp[k], cols, vals, rows, x)

@@ -44,9 +44,10 @@ int sss_haar2d(const double* in, double* out, int batch, int side, int levels,
  *      for each of `nvec` vectors of length n_dom, keep the n_keep largest |v|
  *      (ties -> lower index). x_out = v where kept else 0; mask (nvec x
  *      ceil(n_dom/32) words, zeroed by the callee) marks kept ids; energy
- *      (nvec x 2: total, kept) may be NULL. nvec <= 65535. */
-int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, double* x_out,
-                    uint32_t* mask, double* energy, void* stream);
+ *      (nvec x 2: total, kept) may be NULL. nvec <= 65535. f2t (may be NULL)
+ *      permutes x_out into the operator's tile-major column space. */
+int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, const uint32_t* f2t,
+                    double* x_out, uint32_t* mask, double* energy, void* stream);
 
 /* ---- (a) light projection. SH: E = T L (ambient_irradiance_dense analogue,
  *      lighting.py:332-336) fused with the w0 Haar (transfer.w0_forward,
@@ -87,15 +88,26 @@ int sss_material_weights(const double* bw, const double* r_nodes, int K, int nr,
 /* ---- (b)+(c) relight: K-fused transfer (TransferOperator.apply x K x 3,
  *      transfer.py:66-71 / csc_apply _kernels_nb.py:301-313) with the
  *      recombine + inverse-Haar + Fresnel shade epilogue (runtime.py:155-216).
- *      Operator: tile-major CSR per k: rowptr (K, N+1) u64 absolute offsets
- *      into cols (u32 flat w0 ids) / vals (f32). x (3, N) = masked E spectrum.
- *      g (3, K). vk (K, 3, N) tile-major cache out. scatter (N, 3) may be NULL.
- *      radiance / radiance_unclamped (N, 3) float32. cam (3). */
-int sss_transfer_relight(int K, int side, int levels, const uint64_t* rowptr,
-                         const uint32_t* cols, const float* vals, const double* x,
-                         const double* g, const float* positions, const float* normals,
-                         const double* cam, const double* material, double* vk, double* scatter,
-                         float* radiance, float* radiance_unclamped, void* stream);
+ *      Frame layout: per k a tile-major CSR (rowptr (K, N+1) u64 absolute
+ *      offsets; cols = TILE-MAJOR w0 ids, ascending within a row; vals f32),
+ *      split into column bands of band_width ids (bandoff (K, N, n_bands+1)
+ *      u32 offsets relative to the row start). A CTA owns unit_tiles tiles
+ *      (unit_tiles * 4^levels rows, a multiple of 32, <= 256) visited in
+ *      rowperm order (N global row ids, unit-major). x (3, N) = masked E
+ *      spectrum in tile-major column order; g (3, K) material weights; vk
+ *      (K, 3, N) tile-major cache out; scatter (N, 3) may be NULL;
+ *      radiance / radiance_unclamped (N, 3) float32; cam (3); material
+ *      {sp[3], sa[3], eta}. K <= 16. */
+int sss_transfer_relight(int K, int side, int levels, int unit_tiles, const uint64_t* rowptr,
+                         const uint32_t* bandoff, int band_width, int n_bands, const int* rowperm,
+                         const uint32_t* cols, const float* vals, const double* x, const double* g,
+                         const float* positions, const float* normals, const double* cam,
+                         const double* material, double* vk, double* scatter, float* radiance,
+                         float* radiance_unclamped, void* stream);
+
+/* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
+int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
+                     int band_width, int n_bands, uint32_t* bandoff, void* stream);
 
 /* ---- edit path: stages 3-5 against the cached vk (Scene.set_material,
  *      runtime.py:189-216). */

@@ -21,13 +21,14 @@ _D = C.c_double
 
 _SIGS = {
     "sss_haar2d": [_P, _P, _I, _I, _I, _I, _P],
-    "sss_select_topn": [_P, _I, _I, _I, _P, _P, _P, _P],
+    "sss_select_topn": [_P, _I, _I, _I, _P, _P, _P, _P, _P],
     "sss_sh_irradiance": [_P, _P, _I, _I, _I, _P, _P, _P],
     "sss_env_project": [_P, _I, _I, _P, _P, _P, _P, _P, _P],
     "sss_env_irradiance": [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P, _P],
     "sss_env_transfer": [_P, _I, _P, _P, _I, _P, _P],
     "sss_material_weights": [_P, _P, _I, _I, _P, _P, _P],
-    "sss_transfer_relight": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_transfer_relight": [_I, _I, _I, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_band_offsets": [_P, _P, _I, _I, _I, _I, _P, _P],
     "sss_edit_finish": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_pair_block": [_I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _I, C.c_float, _P, _P, _P],
     "sss_step1_select": [_P, _I, _I, _I, _P, _P, _P],

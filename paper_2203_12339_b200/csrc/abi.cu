@@ -68,8 +68,8 @@ int sss_haar2d(const double* in, double* out, int batch, int side, int levels, i
   return check_launch("k_haar2d_batch");
 }
 
-int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, double* x_out,
-                    uint32_t* mask, double* energy, void* stream) {
+int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, const uint32_t* f2t,
+                    double* x_out, uint32_t* mask, double* energy, void* stream) {
   if (nvec < 0 || nvec > 65535 || n_dom <= 0 || n_keep < 0 || !v || !x_out)
     return fail(SSS_EINVAL, "bad select arguments");
   if (nvec == 0) return SSS_OK;
@@ -77,7 +77,9 @@ int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, double* x_
     cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)nvec * ((n_dom + 31) / 32) * 4, S_(stream));
     if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
   }
-  sss::k_select_topn<<<nvec, 1024, 0, S_(stream)>>>(v, n_dom, n_keep, x_out, mask, energy);
+  const size_t smem = sizeof(sss::SelShared);
+  if (int r = set_smem((const void*)sss::k_select_topn, smem)) return r;
+  sss::k_select_topn<<<nvec, 1024, smem, S_(stream)>>>(v, n_dom, n_keep, f2t, x_out, mask, energy);
   return check_launch("k_select_topn");
 }
 
@@ -145,22 +147,48 @@ int sss_material_weights(const double* bw, const double* r_nodes, int K, int nr,
   return check_launch("k_material_weights");
 }
 
-int sss_transfer_relight(int K, int side, int levels, const uint64_t* rowptr, const uint32_t* cols,
-                         const float* vals, const double* x, const double* g,
+int sss_transfer_relight(int K, int side, int levels, int unit_tiles, const uint64_t* rowptr,
+                         const uint32_t* bandoff, int band_width, int n_bands, const int* rowperm,
+                         const uint32_t* cols, const float* vals, const double* x, const double* g,
                          const float* positions, const float* normals, const double* cam,
                          const double* material, double* vk, double* scatter, float* radiance,
                          float* radiance_unclamped, void* stream) {
   if (int r = check_geom(side, levels)) return r;
-  if (K <= 0 || !rowptr || !x || !g || !positions || !normals || !cam || !material || !vk || !radiance ||
-      !radiance_unclamped)
+  if (K <= 0 || K > 16 || !rowptr || !bandoff || !rowperm || !x || !g || !positions || !normals ||
+      !cam || !material || !vk || !radiance || !radiance_unclamped)
     return fail(SSS_EINVAL, "bad transfer_relight arguments");
-  const int T = 1 << levels;
-  const size_t smem = 4 * (size_t)T * T * sizeof(double);
-  if (int r = set_smem((const void*)sss::k_transfer_relight, smem)) return r;
-  sss::k_transfer_relight<<<(side / T) * (side / T), 256, smem, S_(stream)>>>(
-      K, side, levels, rowptr, cols, vals, x, g, positions, normals, cam, material, vk, scatter,
-      radiance, radiance_unclamped);
-  return check_launch("k_transfer_relight");
+  const int T = 1 << levels, T2 = T * T;
+  const int tiles = (side / T) * (side / T);
+  if (unit_tiles <= 0 || tiles % unit_tiles || unit_tiles * T2 > 256 || (unit_tiles * T2) % 32)
+    return fail(SSS_EINVAL, "unit_tiles * 4^levels must be a multiple of 32 and <= 256");
+  if (band_width <= 0 || n_bands != (side * side + band_width - 1) / band_width)
+    return fail(SSS_EINVAL, "band_width / n_bands mismatch");
+  const int R = unit_tiles * T2;
+  const size_t smem = (3 * (size_t)band_width + 3 * (size_t)R + T2) * sizeof(double);
+  const unsigned grid = tiles / unit_tiles;
+#define SSS_TB(KM)                                                                              \
+  {                                                                                             \
+    if (int r = set_smem((const void*)sss::k_transfer_banded<KM>, smem)) return r;              \
+    sss::k_transfer_banded<KM><<<grid, R, smem, S_(stream)>>>(                                  \
+        K, side, levels, unit_tiles, rowptr, bandoff, band_width, n_bands, rowperm, cols, vals, \
+        x, g, positions, normals, cam, material, vk, scatter, radiance, radiance_unclamped);    \
+  }
+  if (K <= 4) SSS_TB(4)
+  else if (K <= 8) SSS_TB(8)
+  else if (K <= 12) SSS_TB(12)
+  else SSS_TB(16)
+#undef SSS_TB
+  return check_launch("k_transfer_banded");
+}
+
+int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
+                     int band_width, int n_bands, uint32_t* bandoff, void* stream) {
+  if (!rowptr || !bandoff || K <= 0 || n_rows <= 0 || band_width <= 0 || n_bands <= 0)
+    return fail(SSS_EINVAL, "bad band_offsets arguments");
+  const long long n = (long long)K * n_rows;
+  sss::k_band_offsets<<<(unsigned)((n + 255) / 256), 256, 0, S_(stream)>>>(rowptr, cols, K, n_rows,
+                                                                          band_width, n_bands, bandoff);
+  return check_launch("k_band_offsets");
 }
 
 int sss_edit_finish(int K, int side, int levels, const double* vk, const double* g,

@@ -11,7 +11,7 @@
 // operation order (no FMA), so kept index sets are bit-identical to the CPU
 // reference; transfer sums accumulate fp64 over f32 operator values
 // (fp64 accumulation is what makes the 1e-4 criterion hold).
-#include "sss_common.cuh"
+#include "select.cuh"
 
 namespace sss {
 
@@ -252,12 +252,22 @@ __global__ void k_env_irradiance_haar(const float* __restrict__ W2, int D,
   for (int e = threadIdx.x; e < T2; e += blockDim.x) {
     const int i = (tr * T + e / T) * S + tc * T + e % T;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    for (int q = 0; q < m; ++q) {
-      const double w = (double)__ldg(&W2[(size_t)ul[q] * N + i]);
-      const double l0 = lc[q * 3], l1 = lc[q * 3 + 1], l2 = lc[q * 3 + 2];
-      if (l0 != 0.0) acc0 = dadd(acc0, dmul(w, l0));
-      if (l1 != 0.0) acc1 = dadd(acc1, dmul(w, l1));
-      if (l2 != 0.0) acc2 = dadd(acc2, dmul(w, l2));
+    constexpr int kPf = 8;  // independent loads in flight; the adds stay in l order
+    for (int q0 = 0; q0 < m; q0 += kPf) {
+      float wv[kPf];
+#pragma unroll
+      for (int u = 0; u < kPf; ++u)
+        wv[u] = (q0 + u < m) ? __ldg(&W2[(size_t)ul[q0 + u] * N + i]) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) {
+        if (q0 + u >= m) break;
+        const int q = q0 + u;
+        const double w = (double)wv[u];
+        const double l0 = lc[q * 3], l1 = lc[q * 3 + 1], l2 = lc[q * 3 + 2];
+        if (l0 != 0.0) acc0 = dadd(acc0, dmul(w, l0));
+        if (l1 != 0.0) acc1 = dadd(acc1, dmul(w, l1));
+        if (l2 != 0.0) acc2 = dadd(acc2, dmul(w, l2));
+      }
     }
     a[e] = acc0; a[T2 + e] = acc1; a[2 * T2 + e] = acc2;
     if (E_out) { E_out[i * 3 + 0] = acc0; E_out[i * 3 + 1] = acc1; E_out[i * 3 + 2] = acc2; }
@@ -277,43 +287,40 @@ __global__ void k_env_irradiance_haar(const float* __restrict__ W2, int D,
 // grid: 3 CTAs x 1024 threads. x = ehat where kept, else 0.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_select_topn(const double* __restrict__ ehat, int n_dom, int n_keep,
+                                                      const uint32_t* __restrict__ f2t,
                                                       double* __restrict__ x, uint32_t* __restrict__ mask,
                                                       double* __restrict__ energy) {
-  __shared__ unsigned hist[2048];
-  __shared__ int scal[2 + 32];
-  __shared__ double red[2][32];
+  extern __shared__ __align__(16) unsigned char dsm[];
+  SelShared& sh = *reinterpret_cast<SelShared*>(dsm);
   const int c = blockIdx.x;
   const double* v = ehat + (size_t)c * n_dom;
   const int n = min(n_keep, n_dom);
   SelectResult sel;
+  sel.key = ~0ULL;
+  sel.take_eq = 0;
   if (n > 0) {
-    sel = block_radix_select(v, n_dom, n, hist, scal);
-  } else {
-    sel.key = ~0ULL; sel.take_eq = 0;
+    uint64_t t;
+    long long take, tiecnt;
+    radix_cut<false>(v, n_dom, n, 0.0, sh, &t, &take, &tiecnt);
+    sel.key = t;
+    sel.take_eq = (int)take;
   }
   double tot = 0.0, kept = 0.0;
   double* xo = x + (size_t)c * n_dom;
   uint32_t* mo = mask ? mask + (size_t)c * ((n_dom + 31) / 32) : nullptr;
-  block_apply_selection(v, n_dom, sel, scal + 2, [&](int i, bool k) {
+  // x is written in the operator's column space: tile-major when f2t is given
+  block_apply_selection(v, n_dom, sel, reinterpret_cast<int*>(sh.wsum), [&](int i, bool k) {
     const double e = v[i];
     tot += e * e;
     if (k) kept += e * e;
-    xo[i] = k ? e : 0.0;
+    xo[f2t ? f2t[i] : i] = k ? e : 0.0;
     if (mo && k) atomicOr(&mo[i >> 5], 1u << (i & 31));
   });
-  // block reduce energies
-  for (int o = 16; o > 0; o >>= 1) {
-    tot += __shfl_down_sync(0xffffffffu, tot, o);
-    kept += __shfl_down_sync(0xffffffffu, kept, o);
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) { red[0][wid] = tot; red[1][wid] = kept; }
-  __syncthreads();
+  tot = block_sum_d(tot, sh.red);
+  kept = block_sum_d(kept, sh.red);
   if (threadIdx.x == 0 && energy) {
-    double t = 0.0, k = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += red[0][w]; k += red[1][w]; }
-    energy[c * 2 + 0] = t;
-    energy[c * 2 + 1] = fmin(k, t);
+    energy[c * 2 + 0] = tot;
+    energy[c * 2 + 1] = fmin(kept, tot);
   }
 }
 
@@ -538,6 +545,97 @@ __global__ void k_env_transfer(const float* __restrict__ normals, int n_points,
   for (int e = threadIdx.x; e < kEnvP * s2; e += blockDim.x) {
     const int t = e / kEnvP, p = e % kEnvP, i = i0 + p;
     if (i < n_points) W2[(size_t)(f * s2 + t) * N + i] = (float)a[p * s2 + t];
+  }
+}
+
+}  // namespace sss
+
+namespace sss {
+
+// ---------------------------------------------------------------------------
+// (b)+(c) fused transfer, frame layout v2 ("banded"): a CTA owns a unit of
+// G tiles (R = G * 4^L rows, one thread per row, rows visited longest-first
+// so a warp's rows have similar lengths); the masked E spectrum x is staged
+// in shared memory one column band at a time (band_width tile-major w0 ids,
+// fp64, 3 channels) and every row's entries inside the band are streamed
+// with register accumulation for all K terms (no atomics, no shuffles, no
+// L2 gathers). Epilogue: v_k cache write, sum_k g_k v_k, per-tile inverse
+// Haar + Fresnel shade.
+// ---------------------------------------------------------------------------
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_transfer_banded(
+    int K, int S, int L, int G, const uint64_t* __restrict__ rowptr,
+    const uint32_t* __restrict__ bandoff, int band_width, int NB,
+    const int* __restrict__ rowperm, const uint32_t* __restrict__ cols,
+    const float* __restrict__ vals, const double* __restrict__ x, const double* __restrict__ g,
+    const float* __restrict__ positions, const float* __restrict__ normals,
+    const double* __restrict__ cam, const double* __restrict__ material,
+    double* __restrict__ vk, double* __restrict__ scatter, float* __restrict__ radiance,
+    float* __restrict__ radiance_unclamped) {
+  extern __shared__ double sm[];
+  const int T = 1 << L, T2 = T * T, N = S * S;
+  const int R = G * T2;
+  double* xs = sm;                          // 3 * band_width
+  double* summed = xs + 3 * band_width;     // G * 3 * T2
+  double* tmp = summed + 3 * R;             // T2
+  const int unit = blockIdx.x;
+  const int t = threadIdx.x;
+  const int row = rowperm[unit * R + t];
+  const int lr = row - unit * R;
+  double acc[KMAX][3];
+  uint64_t base[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
+    base[k] = k < K ? rowptr[(size_t)k * (N + 1) + row] : 0;
+  }
+  for (int b = 0; b < NB; ++b) {
+    const int c0 = b * band_width;
+    const int bw = min(band_width, N - c0);
+    __syncthreads();
+    for (int j = t; j < bw; j += blockDim.x) {
+      xs[j] = x[c0 + j];
+      xs[band_width + j] = x[N + c0 + j];
+      xs[2 * band_width + j] = x[2 * N + c0 + j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k >= K) break;
+      const uint32_t* bo = bandoff + ((size_t)k * N + row) * (NB + 1) + b;
+      const uint64_t p0 = base[k] + bo[0], p1 = base[k] + bo[1];
+      double a0 = acc[k][0], a1 = acc[k][1], a2 = acc[k][2];
+#pragma unroll 4
+      for (uint64_t p = p0; p < p1; ++p) {
+        const int col = (int)__ldg(&cols[p]) - c0;
+        const double v = (double)__ldg(&vals[p]);
+        a0 = fma(v, xs[col], a0);
+        a1 = fma(v, xs[band_width + col], a1);
+        a2 = fma(v, xs[2 * band_width + col], a2);
+      }
+      acc[k][0] = a0; acc[k][1] = a1; acc[k][2] = a2;
+    }
+  }
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    if (k >= K) break;
+    double* vo = vk + (size_t)k * 3 * N;
+    vo[row] = acc[k][0]; vo[N + row] = acc[k][1]; vo[2 * N + row] = acc[k][2];
+    s0 += g[k] * acc[k][0];
+    s1 += g[K + k] * acc[k][1];
+    s2 += g[2 * K + k] * acc[k][2];
+  }
+  const int tj = lr / T2, e = lr % T2;
+  summed[(tj * 3 + 0) * T2 + e] = s0;
+  summed[(tj * 3 + 1) * T2 + e] = s1;
+  summed[(tj * 3 + 2) * T2 + e] = s2;
+  __syncthreads();
+  const int tiles_per_row = S / T;
+  for (int j = 0; j < G; ++j) {
+    const int tile = unit * G + j;
+    tile_epilogue(summed + j * 3 * T2, tmp, T, tile / tiles_per_row, tile % tiles_per_row, S,
+                  positions, normals, cam, material, scatter, radiance, radiance_unclamped);
   }
 }
 

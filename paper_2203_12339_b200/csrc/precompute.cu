@@ -21,16 +21,11 @@
 // Lerp mode reproduces transfer_block bit for bit (fp64, reference operation
 // order, no FMA); exact mode evaluates R_d per pair for every training
 // material in fp32 and projects on the PCA bases.
-#include "sss_common.cuh"
+#include "select.cuh"
 
 namespace sss {
 
 constexpr int kSelThreads = 1024;
-constexpr int kCandCap = 4096;
-
-__device__ __forceinline__ uint64_t mkey(double v) {
-  return (uint64_t)__double_as_longlong(v) & 0x7fffffffffffffffULL;
-}
 
 // sequential full-pyramid Haar of a T x T tile held at base[(a*T+b)*stride]
 // (one thread), reference order: per level rows then columns
@@ -174,192 +169,6 @@ __global__ void __launch_bounds__(128) k_pair_block(PairParams p, double* __rest
   }
 }
 
-// ---------------------------------------------------------------------------
-// exact radix selection over a row / column of N doubles in global memory
-// (tile-major order; tm2flat maps positions to the flat index that breaks
-// ties). ENERGY=false: keep the n largest |v| (compress_top_n).
-// ENERGY=true: keep the shortest |v|-ordered prefix reaching `fraction` of
-// the energy (compress_energy), in 2^62 fixed point.
-// ---------------------------------------------------------------------------
-
-struct SelShared {
-  unsigned hist[2048];
-  unsigned elo[2048];
-  unsigned ehi[2048];
-  uint64_t cand_key[kCandCap];
-  uint32_t cand_pos[kCandCap];
-  int ncand_store;
-  int scal_b;
-  long long scal_need;
-  long long scal_cnt;
-  double red[32];
-  long long redi[32];
-  unsigned wsum[32];
-};
-
-__device__ __forceinline__ double block_sum_d(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x < 32) {
-    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) red[0] = s;
-  }
-  __syncthreads();
-  s = red[0];
-  __syncthreads();
-  return s;
-}
-
-__device__ __forceinline__ long long block_sum_i(long long v, long long* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    long long s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) red[0] = s;
-  }
-  __syncthreads();
-  const long long s = red[0];
-  __syncthreads();
-  return s;
-}
-
-__device__ __forceinline__ uint64_t fixq(double v, double scale) {
-  return (uint64_t)(v * v * scale);
-}
-
-// Returns threshold key t and `take` (# of elements with key == t to keep,
-// lowest flat index first). For ENERGY, need_q is the fixed-point target.
-template <bool ENERGY>
-__device__ void radix_cut(const double* __restrict__ v, int N, long long need_init, double scale,
-                          SelShared& sh, uint64_t* t_out, long long* take_out, long long* tiecnt) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int digits[6] = {53, 42, 31, 20, 9, 0};
-  const int widths[6] = {11, 11, 11, 11, 11, 9};
-  uint64_t prefix = 0, pmask = 0;
-  long long need = need_init;  // count (top-n) or fixed-point energy (energy)
-  long long ncand = N;
-  bool in_smem = false;
-  for (int p = 0; p < 6; ++p) {
-    const int shf = digits[p], nb = 1 << widths[p];
-    for (int b = tid; b < nb; b += nt) { sh.hist[b] = 0; if (ENERGY) { sh.elo[b] = 0; sh.ehi[b] = 0; } }
-    const bool gather = !in_smem && ncand <= kCandCap;
-    if (tid == 0 && gather) sh.ncand_store = 0;
-    __syncthreads();
-    if (!in_smem) {
-      for (int i = tid; i < N; i += nt) {
-        const double x = v[i];
-        const uint64_t k = mkey(x);
-        if ((k & pmask) != prefix) continue;
-        const int b = (int)((k >> shf) & (nb - 1));
-        atomicAdd(&sh.hist[b], 1u);
-        if (ENERGY) {
-          const uint64_t q = fixq(x, scale);
-          const unsigned lo = (unsigned)q;
-          const unsigned old = atomicAdd(&sh.elo[b], lo);
-          atomicAdd(&sh.ehi[b], (unsigned)(q >> 32) + ((unsigned)(old + lo) < old ? 1u : 0u));
-        }
-        if (gather) {
-          const int s = atomicAdd(&sh.ncand_store, 1);
-          sh.cand_key[s] = k;
-          sh.cand_pos[s] = (uint32_t)i;
-        }
-      }
-    } else {
-      const int nc = sh.ncand_store;
-      for (int s = tid; s < nc; s += nt) {
-        const uint64_t k = sh.cand_key[s];
-        if ((k & pmask) != prefix) continue;
-        const int b = (int)((k >> shf) & (nb - 1));
-        atomicAdd(&sh.hist[b], 1u);
-        if (ENERGY) {
-          const uint64_t q = fixq(__longlong_as_double((long long)k), scale);
-          const unsigned lo = (unsigned)q;
-          const unsigned old = atomicAdd(&sh.elo[b], lo);
-          atomicAdd(&sh.ehi[b], (unsigned)(q >> 32) + ((unsigned)(old + lo) < old ? 1u : 0u));
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      long long acc = 0;
-      int b = nb - 1;
-      for (; b > 0; --b) {
-        const long long w = ENERGY ? (long long)(((uint64_t)sh.ehi[b] << 32) | sh.elo[b])
-                                   : (long long)sh.hist[b];
-        if (acc + w >= need) break;
-        acc += w;
-      }
-      sh.scal_b = b;
-      sh.scal_need = need - acc;
-      sh.scal_cnt = sh.hist[b];
-    }
-    __syncthreads();
-    const int b = sh.scal_b;
-    need = sh.scal_need;
-    ncand = sh.scal_cnt;
-    prefix |= (uint64_t)b << shf;
-    pmask |= (uint64_t)(nb - 1) << shf;
-    if (gather) in_smem = true;
-    __syncthreads();
-  }
-  *t_out = prefix;
-  *tiecnt = ncand;
-  if (ENERGY) {
-    const uint64_t qt = fixq(__longlong_as_double((long long)prefix), scale);
-    long long take = qt == 0 ? ncand : (long long)((need + (long long)qt - 1) / (long long)qt);
-    if (need <= 0) take = 0;
-    *take_out = take < ncand ? take : ncand;
-  } else {
-    *take_out = need;
-  }
-}
-
-// flat index of the `take`-th (1-based) set bit of a block-shared bitmap
-__device__ int kth_set_bit(const uint32_t* bits, int nwords, long long take, unsigned* wsum) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int per = (nwords + nt - 1) / nt;
-  const int w0 = min(tid * per, nwords), w1 = min(w0 + per, nwords);
-  unsigned cnt = 0;
-  for (int w = w0; w < w1; ++w) cnt += __popc(bits[w]);
-  const int lane = tid & 31, wid = tid >> 5;
-  unsigned incl = cnt;
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) wsum[wid] = incl;
-  __syncthreads();
-  if (tid == 0) {
-    unsigned a = 0;
-    for (int w = 0; w < (nt >> 5); ++w) { const unsigned t = wsum[w]; wsum[w] = a; a += t; }
-  }
-  __syncthreads();
-  __shared__ int result;
-  if (tid == 0) result = -1;
-  __syncthreads();
-  long long before = wsum[wid] + incl - cnt;
-  if (take > before && take <= before + cnt) {
-    long long r = take - before;
-    for (int w = w0; w < w1; ++w) {
-      uint32_t x = bits[w];
-      const int pc = __popc(x);
-      if (r > pc) { r -= pc; continue; }
-      for (int b = 0; b < 32; ++b)
-        if ((x >> b) & 1u) { if (--r == 0) { result = w * 32 + b; break; } }
-      break;
-    }
-  }
-  __syncthreads();
-  return result;
-}
-
 // step 1: one CTA per receiver row of D (tile-major), top-n with flat-index
 // tie-break, OR the kept flat column ids into the per-k union bitmap
 __global__ void __launch_bounds__(kSelThreads) k_step1_select(const double* __restrict__ D, int N,
@@ -384,7 +193,7 @@ __global__ void __launch_bounds__(kSelThreads) k_step1_select(const double* __re
   }
   __syncthreads();
   int fmax = N;  // all ties kept
-  if (take < tiecnt) fmax = kth_set_bit(tie, nw, take, sh.wsum);
+  if (take < tiecnt) fmax = kth_set_bit(tie, nw, take, sh);
   for (int w = threadIdx.x; w < nw; w += blockDim.x) {
     uint32_t tb = tie[w];
     if (fmax < N) {
@@ -443,7 +252,7 @@ __global__ void __launch_bounds__(kSelThreads) k_step2_select(
   __syncthreads();
   long long kept = above + take;
   int fmax = -1;
-  if (take > 0) fmax = (take < tiecnt) ? kth_set_bit(tie, nw, take, sh.wsum) : N;
+  if (take > 0) fmax = (take < tiecnt) ? kth_set_bit(tie, nw, take, sh) : N;
   if (kept > nz) {  // never keep zeros (wavelets.py:151)
     kept = nz;
     t = 0;
@@ -507,7 +316,7 @@ __global__ void k_emit_write(const double* __restrict__ M, int N, int T2, int ch
     if (t == ~0ULL) continue;
     const double x = M[(size_t)c * N + rtm];
     if (kept_entry(mkey(x), t, __ldg(&col_fmax[c]), fr)) {
-      cols[o] = tm2flat[c];
+      cols[o] = (uint32_t)c;  // tile-major w0 id (frame layout)
       vals[o] = (float)x;
       ++o;
     }
@@ -562,4 +371,26 @@ __global__ void k_rowptr(const uint64_t* __restrict__ offs, int nchunks, int N, 
   if (r == N) rowptr[N] = base + *total;
 }
 
+}  // namespace sss
+
+namespace sss {
+// per (k, row): offsets (relative to the row start) of the first entry whose
+// tile-major column is >= b * band_width, b = 0..NB (frame layout v2)
+__global__ void k_band_offsets(const uint64_t* __restrict__ rowptr, const uint32_t* __restrict__ cols,
+                               int K, int N, int band_width, int NB, uint32_t* __restrict__ bandoff) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)K * N) return;
+  const int k = (int)(i / N), r = (int)(i % N);
+  const uint64_t s = rowptr[(size_t)k * (N + 1) + r], e = rowptr[(size_t)k * (N + 1) + r + 1];
+  uint32_t* out = bandoff + (size_t)i * (NB + 1);
+  for (int b = 0; b <= NB; ++b) {
+    const uint32_t lim = (uint32_t)b * (uint32_t)band_width;
+    uint64_t lo = s, hi = e;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (cols[mid] < lim) lo = mid + 1; else hi = mid;
+    }
+    out[b] = (uint32_t)(lo - s);
+  }
+}
 }  // namespace sss

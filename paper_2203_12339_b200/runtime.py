@@ -33,7 +33,7 @@ from .basis import DiffusionBasis, OpticalMaterial
 from .config import CAMERA, E_KEEP, ENV_COEFF_KEEP
 from .geometry import GeometryImage
 from .lighting import face_directions, face_solid_angles, sh_transfer
-from .transfer import DeviceTransfer
+from .transfer import DeviceTransfer, flat_to_tile_major
 
 STAGES = ("irradiance", "transfer", "weighting", "inverse_wavelet", "raster")
 
@@ -112,7 +112,9 @@ class Scene:
         self.positions = torch.as_tensor(geometry.positions, device=dev).contiguous()
         self.normals = torch.as_tensor(geometry.normals, device=dev).contiguous()
         self.ehat = torch.empty((3, n), **f64)
-        self.x = torch.empty((3, n), **f64)
+        self.x = torch.empty((3, n), **f64)  # masked spectrum, tile-major column order
+        self.f2t = torch.as_tensor(
+            flat_to_tile_major(np.arange(n), self.side, self.levels).astype(np.int32), device=dev)
         self.mask = torch.empty((3, (n + 31) // 32), dtype=torch.int32, device=dev)
         self.energy = torch.zeros((3, 2), **f64)
         self.g = torch.empty((3, self.K), **f64)
@@ -211,8 +213,8 @@ class Scene:
                       _lib.ptr(self.env_ulc), _lib.ptr(self.env_nu), kk, self.side, self.levels,
                       _lib.ptr(E), _lib.ptr(self.ehat), sp)
         keep = max(1, int(round(self.e_keep * self.n)))  # runtime.py:112
-        _lib.call("sss_select_topn", _lib.ptr(self.ehat), 3, self.n, keep, _lib.ptr(self.x),
-                  _lib.ptr(self.mask), _lib.ptr(self.energy), sp)
+        _lib.call("sss_select_topn", _lib.ptr(self.ehat), 3, self.n, keep, _lib.ptr(self.f2t),
+                  _lib.ptr(self.x), _lib.ptr(self.mask), _lib.ptr(self.energy), sp)
 
     def _launch_weights(self, stream=None):
         dev = self.basis.device()
@@ -222,8 +224,10 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
-        _lib.call("sss_transfer_relight", self.K, self.side, self.levels, _lib.ptr(t.rowptr),
-                  _lib.ptr(t.cols), _lib.ptr(t.vals), _lib.ptr(self.x), _lib.ptr(self.g),
+        _lib.call("sss_transfer_relight", self.K, self.side, self.levels, t.unit_tiles,
+                  _lib.ptr(t.rowptr), _lib.ptr(t.bandoff), t.band_width, t.n_bands,
+                  _lib.ptr(t.rowperm), _lib.ptr(t.cols), _lib.ptr(t.vals), _lib.ptr(self.x),
+                  _lib.ptr(self.g),
                   _lib.ptr(self.positions), _lib.ptr(self.normals), _lib.ptr(self.cam_buf),
                   _lib.ptr(self.material_buf), _lib.ptr(self.vk), _lib.ptr(self.scatter),
                   _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped),

@@ -4,11 +4,16 @@ Reference data model (transfer.py:50-93): per PCA term k a
 ``TransferOperator`` in CSC over retained w0 columns (cols, colptr, rowidx
 into the w1 flat domain, vals), grouped in a ``CompressedTransfer``.
 
-Device layout (this framework): one tile-major CSR per k so a CTA that owns
-a 2^L x 2^L spatial tile owns the 4^L w1 rows its inverse Haar needs
-(SURVEY §7 hard part 4/5): ``rowptr`` (K, N+1) u64 absolute offsets,
-``cols`` u32 w0 flat ids (sorted within a row), ``vals`` f32. 8 bytes per
-stored coefficient, the reference container's width (container.py:87-88).
+Device layout (this framework, "frame layout v2"): one tile-major CSR per k
+so a CTA that owns 2^L x 2^L spatial tiles owns the 4^L w1 rows their
+inverse Haar needs (SURVEY §7 hard parts 4/5): ``rowptr`` (K, N+1) u64
+absolute offsets, ``cols`` u32 TILE-MAJOR w0 ids ascending within a row,
+``vals`` f32 — 8 bytes per stored coefficient, the reference container's
+width (container.py:87-88). Each row is split into column bands of
+``band_width`` ids (``bandoff`` (K, N, n_bands+1) u32 offsets relative to
+the row start) so the transfer kernel can stage one band of the E spectrum
+in shared memory at a time; ``rowperm`` orders each CTA unit's rows
+longest-first so a warp's rows have similar lengths.
 
 ``DeviceTransfer.from_reference`` is the bridge from reference-format
 operators (e.g. a PRTS1 container) to the device layout;
@@ -71,15 +76,19 @@ def tile_major_to_flat(side: int, levels: int) -> np.ndarray:
     return perm
 
 
+BAND_WIDTH = 4096  # w0 ids per shared-memory band (3 x 4096 doubles = 96 KB)
+UNIT_ROWS = 256  # rows per CTA of the transfer kernel
+
+
 @dataclass
 class DeviceTransfer:
-    """K operators resident in HBM in the tile-major CSR frame layout."""
+    """K operators resident in HBM in the banded tile-major CSR frame layout."""
 
     K: int
     side: int
     levels: int
     rowptr: torch.Tensor  # int64 (K, N+1), absolute offsets
-    cols: torch.Tensor  # int32 (nnz,) w0 flat ids (u32 on the device)
+    cols: torch.Tensor  # int32 (nnz,) tile-major w0 ids (u32 on the device)
     vals: torch.Tensor  # float32 (nnz,)
     nnz_per_k: list
     step1_keep: float = 0.0
@@ -87,6 +96,48 @@ class DeviceTransfer:
     kept_energy: list = None
     total_energy: list = None
     step1_entries: list = None
+    band_width: int = 0
+    n_bands: int = 0
+    bandoff: torch.Tensor = None  # int32 (K, N, n_bands+1)
+    rowperm: torch.Tensor = None  # int32 (N,)
+    unit_tiles: int = 0
+
+    def __post_init__(self):
+        if self.bandoff is None:
+            self._finalize()
+
+    def _finalize(self):
+        n, K = self.n, self.K
+        T2 = (1 << self.levels) ** 2
+        self.band_width = min(BAND_WIDTH, n)
+        self.n_bands = (n + self.band_width - 1) // self.band_width
+        rows = min(UNIT_ROWS, n)
+        self.unit_tiles = max(1, rows // T2)
+        rp = self.rowptr.cpu().numpy()
+        if self.rowptr.is_cuda:
+            from . import _lib
+
+            self.bandoff = torch.empty((K, n, self.n_bands + 1), dtype=torch.int32,
+                                       device=self.rowptr.device)
+            _lib.call("sss_band_offsets", _lib.ptr(self.rowptr), _lib.ptr(self.cols), K, n,
+                      self.band_width, self.n_bands, _lib.ptr(self.bandoff), _lib.stream_ptr())
+        else:
+            cols = self.cols.numpy().view(np.uint32).astype(np.int64)
+            bo = np.zeros((K, n, self.n_bands + 1), np.int64)
+            for k in range(K):
+                counts = np.diff(rp[k])
+                rid = np.repeat(np.arange(n), counts)
+                band = cols[rp[k, 0]:rp[k, -1]] // self.band_width
+                h = np.bincount(rid * self.n_bands + band, minlength=n * self.n_bands)
+                bo[k, :, 1:] = np.cumsum(h.reshape(n, self.n_bands), axis=1)
+            self.bandoff = torch.as_tensor(bo.astype(np.int32))
+        lengths = (rp[:, 1:] - rp[:, :-1]).sum(axis=0)
+        R = self.unit_tiles * T2
+        perm = np.empty(n, np.int64)
+        for u in range(n // R):
+            seg = lengths[u * R:(u + 1) * R]
+            perm[u * R:(u + 1) * R] = u * R + np.argsort(-seg, kind="stable")
+        self.rowperm = torch.as_tensor(perm.astype(np.int32), device=self.rowptr.device)
 
     @property
     def n(self) -> int:
@@ -102,18 +153,22 @@ class DeviceTransfer:
 
     @property
     def nbytes(self) -> int:
-        return self.nnz * 8 + self.rowptr.numel() * 8
+        """Stored bytes of the operator the frame streams (8 B / coefficient
+        + row pointers + band offsets)."""
+        return self.nnz * 8 + self.rowptr.numel() * 8 + self.bandoff.numel() * 4
 
     @classmethod
     def from_reference(cls, operators, side: int, levels: int, device="cuda",
                        step1_keep=0.0, step2_fraction=0.0) -> "DeviceTransfer":
-        """CSC (reference TransferOperator list, w1 flat rows) -> tile-major CSR."""
+        """CSC (reference TransferOperator list, flat w0 cols / w1 rows) ->
+        banded tile-major CSR (the PRTS1 bridge direction reference -> B200)."""
         n = side * side
+        f2t = flat_to_tile_major(np.arange(n), side, levels)
         rowptrs, cols_all, vals_all, nnz = [], [], [], []
         base = 0
         for op in operators:
             counts = np.diff(np.asarray(op.colptr, np.int64))
-            ecol = np.repeat(np.asarray(op.cols, np.int64), counts)
+            ecol = f2t[np.repeat(np.asarray(op.cols, np.int64), counts)]
             erow = flat_to_tile_major(np.asarray(op.rowidx, np.int64), side, levels)
             order = np.lexsort((ecol, erow))
             rc = np.bincount(erow, minlength=n)
@@ -138,11 +193,11 @@ class DeviceTransfer:
         )
 
     def to_reference(self):
-        """Device layout -> reference CSC operators (vals f32 -> f64), for the
-        PRTS1 bridge and parity checks."""
+        """Device layout -> reference CSC operators (flat ids, vals f32 -> f64),
+        for the PRTS1 bridge and parity checks."""
         perm = tile_major_to_flat(self.side, self.levels)
         rp = self.rowptr.cpu().numpy()
-        cols = self.cols.cpu().numpy().view(np.uint32).astype(np.int64)
+        cols = perm[self.cols.cpu().numpy().view(np.uint32).astype(np.int64)]
         vals = self.vals.cpu().numpy()
         ops = []
         n = self.n

@@ -78,7 +78,7 @@ def select_top_n_device(v: torch.Tensor, n: int):
     x = torch.empty_like(v)
     mask = torch.empty((B, (n_dom + 31) // 32), dtype=torch.int32, device=v.device)
     energy = torch.empty((B, 2), dtype=torch.float64, device=v.device)
-    _lib.call("sss_select_topn", _lib.ptr(v), B, n_dom, int(n), _lib.ptr(x), _lib.ptr(mask),
+    _lib.call("sss_select_topn", _lib.ptr(v), B, n_dom, int(n), None, _lib.ptr(x), _lib.ptr(mask),
               _lib.ptr(energy), _lib.stream_ptr())
     return x, mask, energy
 

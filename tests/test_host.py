@@ -67,16 +67,29 @@ def test_operator_layout_round_trip():
     # dense product equivalence (the frame layout computes the same thing)
     x = rng.standard_normal(n)
     perm = tile_major_to_flat(side, L)
+    x_tm = x[perm]  # operator columns are tile-major ids
     rp = dt.rowptr.numpy()
     cols = dt.cols.numpy().view(np.uint32)
     vals = dt.vals.numpy().astype(np.float64)
+    bo = dt.bandoff.numpy()
     for k, op in enumerate(ops):
         want = O.csc_apply(op.cols, op.colptr, op.rowidx, op.vals, np.arange(n, dtype=np.uint32), x, n)
         got = np.zeros(n)
         for r in range(n):
             sl = slice(rp[k, r], rp[k, r + 1])
-            got[perm[r]] = np.dot(vals[sl], x[cols[sl]])
+            assert np.all(np.diff(cols[sl].astype(np.int64)) > 0)  # ascending within a row
+            got[perm[r]] = np.dot(vals[sl], x_tm[cols[sl]])
+            # band offsets partition the row by column band
+            for b in range(dt.n_bands):
+                seg = cols[rp[k, r] + bo[k, r, b]: rp[k, r] + bo[k, r, b + 1]]
+                assert np.all(seg // dt.band_width == b)
+            assert bo[k, r, dt.n_bands] == rp[k, r + 1] - rp[k, r]
         assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+    # rowperm: a permutation within each unit, longest rows first
+    R = dt.unit_tiles * (1 << L) ** 2
+    pr = dt.rowperm.numpy()
+    assert np.array_equal(np.sort(pr), np.arange(n))
+    assert np.all(pr // R == np.arange(n) // R)
 
 
 def test_library_exports_every_header_symbol():
@@ -98,7 +111,7 @@ def test_library_rejects_bad_arguments_without_gpu():
     lib = _lib.load(require_cuda=False)
     rc = lib.sss_haar2d(None, None, 1, 12, 2, 0, None)  # side not a power of two
     assert rc == -1 and b"power of two" in lib.sss_last_error()
-    rc = lib.sss_select_topn(None, 1, 16, 4, None, None, None, None)
+    rc = lib.sss_select_topn(None, 1, 16, 4, None, None, None, None, None)
     assert rc == -1
 
 
