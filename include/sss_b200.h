@@ -105,6 +105,28 @@ int sss_transfer_relight(int K, int side, int levels, int unit_tiles, const uint
                          const double* material, double* vk, double* scatter, float* radiance,
                          float* radiance_unclamped, void* stream);
 
+/* ---- frame layout v3 ("stream"): each CTA unit's entries as one contiguous
+ *      TMA-streamable range, item = (band, k), rows in rowperm order inside
+ *      an item, entry = {u32 band-local column, f32 value}, items padded to
+ *      even length. pass 0: item_len (units*n_bands*K) + exclusive scan
+ *      item_off (+ total entries); pass 1: rowoff (items x (unit_rows+1))
+ *      and the entries (8 B each, 16-byte aligned buffer). */
+int sss_stream_build(int pass, const uint64_t* rowptr, const uint32_t* cols, const float* vals,
+                     const uint32_t* bandoff, const int* rowperm, int K, int n_rows, int n_bands,
+                     int unit_rows, int band_width, uint32_t* item_len, uint64_t* item_off,
+                     uint64_t* block_sums, uint64_t* total, uint32_t* rowoff, void* entries,
+                     void* stream);
+
+/* ---- relight on the stream layout: cp.async.bulk + mbarrier double-buffered
+ *      pipeline into shared memory; otherwise identical contract to
+ *      sss_transfer_relight. */
+int sss_transfer_stream(int K, int side, int levels, int unit_tiles, int band_width, int n_bands,
+                        const uint64_t* item_off, const uint32_t* item_len, const uint32_t* rowoff,
+                        const void* entries, const int* rowperm, const double* x, const double* g,
+                        const float* positions, const float* normals, const double* cam,
+                        const double* material, double* vk, double* scatter, float* radiance,
+                        float* radiance_unclamped, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

@@ -8,6 +8,7 @@
 #include "../../include/sss_b200.h"
 #include "frame.cu"
 #include "precompute.cu"
+#include "stream.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -179,6 +180,65 @@ int sss_transfer_relight(int K, int side, int levels, int unit_tiles, const uint
   else SSS_TB(16)
 #undef SSS_TB
   return check_launch("k_transfer_banded");
+}
+
+int sss_stream_build(int pass, const uint64_t* rowptr, const uint32_t* cols, const float* vals,
+                     const uint32_t* bandoff, const int* rowperm, int K, int n_rows, int n_bands,
+                     int unit_rows, int band_width, uint32_t* item_len, uint64_t* item_off,
+                     uint64_t* block_sums, uint64_t* total, uint32_t* rowoff, void* entries,
+                     void* stream) {
+  if (!bandoff || !rowperm || !item_len || !item_off || K <= 0 || n_rows <= 0 || n_bands <= 0 ||
+      unit_rows <= 0 || unit_rows > 1024 || unit_rows % 32 || n_rows % unit_rows)
+    return fail(SSS_EINVAL, "bad stream_build arguments");
+  const long long nitems = (long long)(n_rows / unit_rows) * n_bands * K;
+  if (nitems > 2147483647LL) return fail(SSS_EINVAL, "too many items");
+  if (pass == 0) {
+    if (!block_sums || !total) return fail(SSS_EINVAL, "stream_build pass 0 needs scan scratch");
+    sss::k_stream_sizes<<<(unsigned)nitems, unit_rows, 0, S_(stream)>>>(bandoff, rowperm, K, n_rows,
+                                                                        n_bands, unit_rows, item_len);
+    if (int r = check_launch("k_stream_sizes")) return r;
+    return sss_scan_u32(item_len, item_off, (size_t)nitems, block_sums, total, stream);
+  }
+  if (!rowptr || !cols || !vals || !rowoff || !entries) return fail(SSS_EINVAL, "stream_build fill");
+  sss::k_stream_fill<<<(unsigned)nitems, unit_rows, 0, S_(stream)>>>(
+      rowptr, cols, vals, bandoff, rowperm, K, n_rows, n_bands, unit_rows, band_width, item_off,
+      rowoff, reinterpret_cast<uint2*>(entries));
+  return check_launch("k_stream_fill");
+}
+
+int sss_transfer_stream(int K, int side, int levels, int unit_tiles, int band_width, int n_bands,
+                        const uint64_t* item_off, const uint32_t* item_len, const uint32_t* rowoff,
+                        const void* entries, const int* rowperm, const double* x, const double* g,
+                        const float* positions, const float* normals, const double* cam,
+                        const double* material, double* vk, double* scatter, float* radiance,
+                        float* radiance_unclamped, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (K <= 0 || K > 16 || !item_off || !item_len || !rowoff || !entries || !rowperm || !x || !g ||
+      !positions || !normals || !cam || !material || !vk || !radiance || !radiance_unclamped)
+    return fail(SSS_EINVAL, "bad transfer_stream arguments");
+  if (reinterpret_cast<uintptr_t>(entries) % 16) return fail(SSS_EINVAL, "entries not 16B aligned");
+  const int T = 1 << levels, T2 = T * T;
+  const int tiles = (side / T) * (side / T);
+  if (unit_tiles <= 0 || tiles % unit_tiles || unit_tiles * T2 > 256 || (unit_tiles * T2) % 32)
+    return fail(SSS_EINVAL, "unit_tiles * 4^levels must be a multiple of 32 and <= 256");
+  const int R = unit_tiles * T2;
+  const size_t smem = 2 * sss::kStreamCap * sizeof(uint2) + 2 * sizeof(uint64_t) +
+                      (3 * (size_t)band_width + 3 * (size_t)R + T2) * sizeof(double);
+  const unsigned grid = tiles / unit_tiles;
+#define SSS_TS(KM)                                                                                \
+  {                                                                                               \
+    if (int r = set_smem((const void*)sss::k_transfer_stream<KM>, smem)) return r;                \
+    sss::k_transfer_stream<KM><<<grid, R, smem, S_(stream)>>>(                                    \
+        K, side, levels, unit_tiles, band_width, n_bands, item_off, item_len, rowoff,             \
+        reinterpret_cast<const uint2*>(entries), rowperm, x, g, positions, normals, cam, material, \
+        vk, scatter, radiance, radiance_unclamped);                                               \
+  }
+  if (K <= 4) SSS_TS(4)
+  else if (K <= 8) SSS_TS(8)
+  else if (K <= 12) SSS_TS(12)
+  else SSS_TS(16)
+#undef SSS_TS
+  return check_launch("k_transfer_stream");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

@@ -126,6 +126,7 @@ class Scene:
         self.material_buf = torch.empty(7, **f64)
         self.cam_buf = torch.empty(3, **f64)
         self._light_kind = None
+        self.transfer_kernel = "stream"  # "stream" (TMA pipeline) | "banded"
         self._have_cache = False
         self._sequence = 0
         self._graph = None
@@ -224,6 +225,15 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
+        if self.transfer_kernel == "stream" and t.entries is not None:
+            _lib.call("sss_transfer_stream", self.K, self.side, self.levels, t.unit_tiles,
+                      t.band_width, t.n_bands, _lib.ptr(t.item_off), _lib.ptr(t.item_len),
+                      _lib.ptr(t.rowoff), _lib.ptr(t.entries), _lib.ptr(t.rowperm),
+                      _lib.ptr(self.x), _lib.ptr(self.g), _lib.ptr(self.positions),
+                      _lib.ptr(self.normals), _lib.ptr(self.cam_buf), _lib.ptr(self.material_buf),
+                      _lib.ptr(self.vk), _lib.ptr(self.scatter), _lib.ptr(self.radiance),
+                      _lib.ptr(self.radiance_unclamped), _lib.stream_ptr(stream))
+            return
         _lib.call("sss_transfer_relight", self.K, self.side, self.levels, t.unit_tiles,
                   _lib.ptr(t.rowptr), _lib.ptr(t.bandoff), t.band_width, t.n_bands,
                   _lib.ptr(t.rowperm), _lib.ptr(t.cols), _lib.ptr(t.vals), _lib.ptr(self.x),

@@ -76,7 +76,7 @@ def tile_major_to_flat(side: int, levels: int) -> np.ndarray:
     return perm
 
 
-BAND_WIDTH = 4096  # w0 ids per shared-memory band (3 x 4096 doubles = 96 KB)
+BAND_WIDTH = 2048  # w0 ids per shared-memory band (3 x 2048 doubles = 48 KB)
 UNIT_ROWS = 256  # rows per CTA of the transfer kernel
 
 
@@ -101,6 +101,12 @@ class DeviceTransfer:
     bandoff: torch.Tensor = None  # int32 (K, N, n_bands+1)
     rowperm: torch.Tensor = None  # int32 (N,)
     unit_tiles: int = 0
+    # stream layout (v3), built on CUDA devices
+    item_len: torch.Tensor = None
+    item_off: torch.Tensor = None
+    rowoff: torch.Tensor = None
+    entries: torch.Tensor = None
+    stream_entries: int = 0
 
     def __post_init__(self):
         if self.bandoff is None:
@@ -138,6 +144,31 @@ class DeviceTransfer:
             seg = lengths[u * R:(u + 1) * R]
             perm[u * R:(u + 1) * R] = u * R + np.argsort(-seg, kind="stable")
         self.rowperm = torch.as_tensor(perm.astype(np.int32), device=self.rowptr.device)
+        if self.rowptr.is_cuda and R % 32 == 0:
+            self._build_stream(R)
+
+    def _build_stream(self, R):
+        """Frame layout v3: per-unit contiguous (band, k) items for the TMA
+        pipeline (csrc/stream.cu)."""
+        from . import _lib
+
+        n, K, dev = self.n, self.K, self.rowptr.device
+        nitems = (n // R) * self.n_bands * K
+        self.item_len = torch.empty(nitems, dtype=torch.int32, device=dev)
+        self.item_off = torch.empty(nitems, dtype=torch.int64, device=dev)
+        bs = torch.empty((nitems + 1023) // 1024 + 1, dtype=torch.int64, device=dev)
+        total = torch.empty(1, dtype=torch.int64, device=dev)
+        sp = _lib.stream_ptr()
+        args = (_lib.ptr(self.rowptr), _lib.ptr(self.cols), _lib.ptr(self.vals),
+                _lib.ptr(self.bandoff), _lib.ptr(self.rowperm), K, n, self.n_bands, R,
+                self.band_width, _lib.ptr(self.item_len), _lib.ptr(self.item_off))
+        _lib.call("sss_stream_build", 0, *args, _lib.ptr(bs), _lib.ptr(total), None, None, sp)
+        ne = int(total.item())
+        self.rowoff = torch.empty(nitems * (R + 1), dtype=torch.int32, device=dev)
+        self.entries = torch.empty(max(ne, 2), dtype=torch.int64, device=dev)  # 8 B each
+        _lib.call("sss_stream_build", 1, *args, _lib.ptr(bs), _lib.ptr(total),
+                  _lib.ptr(self.rowoff), _lib.ptr(self.entries), sp)
+        self.stream_entries = ne
 
     @property
     def n(self) -> int:

@@ -319,6 +319,23 @@ def test_out_of_box_material_clamped(c1):
     assert sc.material.sigma_s_prime[0] == sc.basis.sigma_box[1]
 
 
+def test_stream_and_banded_kernels_agree(c1):
+    """The TMA-pipelined stream layout and the banded layout compute the same
+    frame (different fp64 summation order only)."""
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import SHLight
+
+    sc = _scene(c1, SHLight(LT.random_sh_light(3, 23)))
+    assert sc.transfer.entries is not None
+    sc.transfer_kernel = "stream"
+    a = sc.relight()
+    vk_a = sc.vk.clone()
+    sc.transfer_kernel = "banded"
+    b = sc.relight()
+    assert np.abs(sc.vk - vk_a).max().item() <= 1e-12 * np.abs(vk_a.cpu().numpy()).max()
+    assert O.parity_error(a.radiance_unclamped, b.radiance_unclamped, TAU) <= 1e-9
+
+
 def test_cuda_graph_replay_matches_eager(c1):
     from paper_2203_12339_b200 import lighting as LT
     from paper_2203_12339_b200.runtime import SHLight
