@@ -127,6 +127,22 @@ int sss_transfer_stream(int K, int side, int levels, int unit_tiles, int band_wi
                         const double* material, double* vk, double* scatter, float* radiance,
                         float* radiance_unclamped, void* stream);
 
+/* ---- relight on frame layout v4 (persistent, warp-specialized): one CTA per
+ *      unit (a contiguous tile range, ~one per SM); a producer warp streams
+ *      self-describing (band, k) items {u16 warp bases, u8 per-thread counts,
+ *      entries} into a 4-slot ring with cp.async.bulk and the x bands into a
+ *      double buffer; 16 consumer warps (512 virtual threads, long rows split
+ *      over several) accumulate in fp64 registers; mbarrier full/empty
+ *      hand-off only. Layout built by paper_2203_12339_b200/stream4.py;
+ *      contract otherwise as sss_transfer_relight. */
+int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes, int units,
+                    const int* unit_tile0, const int* unit_ntiles, const int* unit_item0,
+                    const int* unit_nitems, const void* items, const void* stream_bytes,
+                    const void* vrow_first, const double* x, const double* g,
+                    const float* positions, const float* normals, const double* cam,
+                    const double* material, double* vk, double* scatter, float* radiance,
+                    float* radiance_unclamped, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

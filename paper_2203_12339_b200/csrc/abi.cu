@@ -9,6 +9,8 @@
 #include "frame.cu"
 #include "precompute.cu"
 #include "stream.cu"
+#include "select_cluster.cu"
+#include "stream4.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -78,6 +80,15 @@ int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, const uint
     cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)nvec * ((n_dom + 31) / 32) * 4, S_(stream));
     if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
   }
+  const int chunk = (((n_dom + sss::kSelCluster - 1) / sss::kSelCluster) + 31) / 32 * 32;
+  if (chunk <= 16384 && n_dom >= 32 * sss::kSelCluster) {
+    // one 8-CTA cluster per vector, slices resident in shared memory
+    const size_t smem = ((sizeof(sss::ClusterSelShared) + 15) & ~size_t(15)) + chunk * sizeof(double);
+    if (int r = set_smem((const void*)sss::k_select_cluster, smem)) return r;
+    sss::k_select_cluster<<<nvec * sss::kSelCluster, 1024, smem, S_(stream)>>>(
+        v, n_dom, n_keep, chunk, f2t, x_out, mask, energy);
+    return check_launch("k_select_cluster");
+  }
   const size_t smem = sizeof(sss::SelShared);
   if (int r = set_smem((const void*)sss::k_select_topn, smem)) return r;
   sss::k_select_topn<<<nvec, 1024, smem, S_(stream)>>>(v, n_dom, n_keep, f2t, x_out, mask, energy);
@@ -98,15 +109,16 @@ int sss_sh_irradiance(const float* T_l, const double* Lsh, int nl, int side, int
 
 int sss_env_project(const double* faces, int env_side, int n_keep, uint32_t* idx, double* val,
                     uint32_t* union_idx, double* union_lc, int* n_union, void* stream) {
-  if (!pow2(env_side) || env_side > 64 || n_keep <= 0 || !faces || !idx || !val)
-    return fail(SSS_EINVAL, "bad env_project arguments");
+  if (!pow2(env_side) || env_side > 32 || n_keep <= 0 || !faces || !idx || !val)
+    return fail(SSS_EINVAL, "bad env_project arguments (env_side must be a power of two <= 32)");
   const int s2 = env_side * env_side;
-  const size_t smem = (size_t)7 * s2 * sizeof(double) + 2048 * 4 + 34 * 4;
+  const size_t smem = (size_t)7 * s2 * sizeof(double) + sizeof(sss::SelShared);
   if (int r = set_smem((const void*)sss::k_env_project, smem)) return r;
   sss::k_env_project<<<3, 1024, smem, S_(stream)>>>(faces, env_side, n_keep, idx, val, nullptr);
   if (int r = check_launch("k_env_project")) return r;
   if (union_idx && union_lc && n_union) {
-    sss::k_env_union<<<1, 32, 0, S_(stream)>>>(idx, val, n_keep, union_idx, union_lc, n_union);
+    sss::k_env_union<<<1, 1024, 0, S_(stream)>>>(idx, val, n_keep, 6 * s2, union_idx, union_lc,
+                                                n_union);
     return check_launch("k_env_union");
   }
   return SSS_OK;
@@ -239,6 +251,45 @@ int sss_transfer_stream(int K, int side, int levels, int unit_tiles, int band_wi
   else SSS_TS(16)
 #undef SSS_TS
   return check_launch("k_transfer_stream");
+}
+
+int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes, int units,
+                    const int* unit_tile0, const int* unit_ntiles, const int* unit_item0,
+                    const int* unit_nitems, const void* items, const void* stream_bytes,
+                    const void* vrow_first, const double* x, const double* g,
+                    const float* positions, const float* normals, const double* cam,
+                    const double* material, double* vk, double* scatter, float* radiance,
+                    float* radiance_unclamped, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (K <= 0 || K > 16 || units <= 0 || !unit_tile0 || !unit_ntiles || !unit_item0 ||
+      !unit_nitems || !items || !stream_bytes || !vrow_first || !x || !g || !positions ||
+      !normals || !cam || !material || !vk || !radiance || !radiance_unclamped)
+    return fail(SSS_EINVAL, "bad transfer_v4 arguments");
+  if (slot_bytes % 16 || reinterpret_cast<uintptr_t>(stream_bytes) % 16 ||
+      (band_width * 8) % 16)
+    return fail(SSS_EINVAL, "transfer_v4: 16-byte alignment violated");
+  const int T = 1 << levels, T2 = T * T;
+  const size_t pipe = (size_t)sss::kV4Slots * slot_bytes + 6 * (size_t)band_width * 8 + 12 * 8;
+  const size_t epi = (size_t)sss::kV4TPU * K * 3 * 8 + (size_t)(sss::kV4TPU / T2 + 1) * 3 * T2 * 8 +
+                     (size_t)T2 * 8;
+  const size_t smem = pipe > epi ? pipe : epi;
+  if (smem > 227 * 1024) return fail(SSS_EINVAL, "transfer_v4: shared memory budget exceeded");
+#define SSS_T4(KM)                                                                               \
+  {                                                                                              \
+    if (int r = set_smem((const void*)sss::k_transfer_v4<KM>, smem)) return r;                   \
+    sss::k_transfer_v4<KM><<<units, sss::kV4Threads, smem, S_(stream)>>>(                        \
+        K, side, levels, band_width, slot_bytes, unit_tile0, unit_ntiles, unit_item0,            \
+        unit_nitems, reinterpret_cast<const sss::V4Item*>(items),                                \
+        reinterpret_cast<const unsigned char*>(stream_bytes),                                    \
+        reinterpret_cast<const unsigned short*>(vrow_first), x, g, positions, normals, cam,      \
+        material, vk, scatter, radiance, radiance_unclamped);                                    \
+  }
+  if (K <= 4) SSS_T4(4)
+  else if (K <= 8) SSS_T4(8)
+  else if (K <= 12) SSS_T4(12)
+  else SSS_T4(16)
+#undef SSS_T4
+  return check_launch("k_transfer_v4");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

@@ -154,19 +154,25 @@ __global__ void k_sh_irradiance_haar(const float* __restrict__ T_l, const double
 __global__ void k_env_project(const double* __restrict__ faces, int s, int n_keep,
                               uint32_t* __restrict__ idx_out, double* __restrict__ val_out,
                               double* __restrict__ energy) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   const int c = blockIdx.x, s2 = s * s, D = 6 * s2;
   double* a = sm;             // D
   double* tmp = sm + D;       // s2
-  unsigned* hist = (unsigned*)(tmp + s2);  // 2048
-  int* scal = (int*)(hist + 2048);         // 2 + 32
+  SelShared& sh = *reinterpret_cast<SelShared*>(tmp + s2);
   for (int e = threadIdx.x; e < D; e += blockDim.x) a[e] = faces[(size_t)e * 3 + c];
   __syncthreads();
   for (int f = 0; f < 6; ++f) tile_haar_fwd(a + f * s2, tmp, s, blockDim.x, threadIdx.x);
   const int n = min(n_keep, D);
-  SelectResult sel = block_radix_select(a, D, n, hist, scal);
+  SelectResult sel;
+  {
+    uint64_t t;
+    long long take, tiecnt;
+    radix_cut<false>(a, D, n, 0.0, sh, &t, &take, &tiecnt);
+    sel.key = t;
+    sel.take_eq = (int)take;
+  }
   // compaction in index order: rank via a second scan
-  int* wsum = scal + 2;
+  int* wsum = reinterpret_cast<int*>(sh.wsum);
   // mark kept into tmp-as-flags then compact with a block scan
   unsigned char* keep = (unsigned char*)tmp;  // reuse (s2 doubles >= D bytes)
   block_apply_selection(a, D, sel, wsum, [&](int i, bool k) { keep[i] = k; });
@@ -203,25 +209,55 @@ __global__ void k_env_project(const double* __restrict__ faces, int s, int n_kee
 
 // one thread: ascending union of the three channels' kept w2 ids with the
 // per-channel value (0 where the channel dropped the id)
-__global__ void k_env_union(const uint32_t* __restrict__ idx, const double* __restrict__ val,
-                            int n_keep, uint32_t* __restrict__ union_idx,
-                            double* __restrict__ union_lc, int* __restrict__ n_union) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int p[3] = {0, 0, 0}, m = 0;
-  while (true) {
-    uint32_t best = 0xffffffffu;
-    for (int c = 0; c < 3; ++c)
-      if (p[c] < n_keep && idx[c * n_keep + p[c]] < best) best = idx[c * n_keep + p[c]];
-    if (best == 0xffffffffu) break;
-    union_idx[m] = best;
-    for (int c = 0; c < 3; ++c) {
-      double v = 0.0;
-      if (p[c] < n_keep && idx[c * n_keep + p[c]] == best) { v = val[c * n_keep + p[c]]; ++p[c]; }
-      union_lc[m * 3 + c] = v;
+__global__ void __launch_bounds__(1024) k_env_union(const uint32_t* __restrict__ idx,
+                                                    const double* __restrict__ val, int n_keep, int D,
+                                                    uint32_t* __restrict__ union_idx,
+                                                    double* __restrict__ union_lc,
+                                                    int* __restrict__ n_union) {
+  // parallel: mark the kept ids of every channel in a D-long flag array, then
+  // an index-order block scan compacts the ascending union (D <= 6144)
+  __shared__ unsigned char flag[6144];
+  __shared__ unsigned short pos[3][6144];
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < D; i += nt) flag[i] = 0;
+  __syncthreads();
+  for (int e = tid; e < 3 * n_keep; e += nt) {
+    const int c = e / n_keep, q = e % n_keep;
+    const uint32_t id = idx[e];
+    if (id < (uint32_t)D) {
+      atomicOr(reinterpret_cast<unsigned*>(flag) + (id >> 2), 1u << (8 * (id & 3) + c));
+      pos[c][id] = (unsigned short)q;
     }
+  }
+  __syncthreads();
+  const int chunk = (D + nt - 1) / nt;
+  const int lo = min(tid * chunk, D), hi = min(lo + chunk, D);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i) cnt += flag[i] != 0;
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (tid == 0) {
+    int a = 0;
+    for (int w = 0; w < nw; ++w) { const int t = wsum[w]; wsum[w] = a; a += t; }
+    *n_union = a;
+  }
+  __syncthreads();
+  int m = wsum[wid] + incl - cnt;
+  for (int i = lo; i < hi; ++i) {
+    const unsigned f = flag[i];
+    if (!f) continue;
+    union_idx[m] = (uint32_t)i;
+    for (int c = 0; c < 3; ++c)
+      union_lc[m * 3 + c] = ((f >> c) & 1u) ? val[c * n_keep + pos[c][i]] : 0.0;
     ++m;
   }
-  *n_union = m;
 }
 
 // grid: one CTA per tile. W2: (D, N) float32 l-major (w2 coefficient major).

@@ -1,0 +1,208 @@
+// Frame layout v4: persistent, warp-specialized transfer kernel.
+//
+// One CTA per unit (a contiguous range of G tiles, ~one unit per SM). The
+// unit's operator entries are pre-arranged (host build, stream4.py) into
+// self-describing items, item = (column band, PCA term k[, split]):
+//
+//   item = [u16 warp_base[NW+1]][u8 count[TPU]] (padded to 16 B)
+//          [entries: {u32 band-local w0 col, f32 val} x n (padded to 16 B)]
+//
+// The unit's rows are split into TPU "virtual threads" proportional to their
+// length (long LL rows get several threads) so every consumer thread streams
+// a similar number of entries. Thread t of warp w reads its `count[t]` entries
+// starting at warp_base[w] + (exclusive warp-scan of counts).
+//
+// Warp roles: NW consumer warps + 1 producer warp. The producer streams items
+// into an NS-slot ring with cp.async.bulk (mbarrier full/empty per slot) and
+// the column bands of x into a double buffer (3 bulk copies per band). The
+// consumers never use a CTA-wide barrier in the main loop: each warp releases
+// a slot (or a band buffer) by one mbarrier arrive when it is done with it.
+// Accumulation: fp64 registers acc[k][3] per thread; epilogue reduces the
+// virtual threads of each row, writes v_k, recombines with g, inverse-Haars
+// each tile and shades.
+#include "sss_common.cuh"
+
+namespace sss {
+
+constexpr int kV4Warps = 16;              // consumer warps
+constexpr int kV4TPU = kV4Warps * 32;     // consumer threads (virtual rows)
+constexpr int kV4Slots = 4;
+constexpr int kV4Threads = kV4TPU + 32;   // + producer warp
+
+struct V4Item {
+  unsigned long long off;  // byte offset of the item in the stream
+  unsigned bytes;          // item size (header + entries), multiple of 16
+  unsigned short band;     // column band
+  unsigned char k;         // PCA term
+  unsigned char pad;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
+    int K, int S, int L, int band_width, int slot_bytes,
+    const int* __restrict__ unit_tile0, const int* __restrict__ unit_ntiles,
+    const int* __restrict__ unit_item0, const int* __restrict__ unit_nitems,
+    const V4Item* __restrict__ items, const unsigned char* __restrict__ stream,
+    const unsigned short* __restrict__ vrow_first,  // per unit: R+1 first virtual thread per row
+    const double* __restrict__ x, const double* __restrict__ g,
+    const float* __restrict__ positions, const float* __restrict__ normals,
+    const double* __restrict__ cam, const double* __restrict__ material,
+    double* __restrict__ vk, double* __restrict__ scatter, float* __restrict__ radiance,
+    float* __restrict__ radiance_unclamped) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int T = 1 << L, T2 = T * T, N = S * S;
+  const int unit = blockIdx.x;
+  const int tile0 = unit_tile0[unit], ntiles = unit_ntiles[unit];
+  const int R = ntiles * T2;
+  const int row0 = tile0 * T2;
+  const int nitems = unit_nitems[unit];
+  const V4Item* uitems = items + unit_item0[unit];
+
+  // shared memory carve-up
+  unsigned char* ring = smraw;                                     // kV4Slots * slot_bytes
+  double* xsb = reinterpret_cast<double*>(ring + kV4Slots * slot_bytes);  // 2 x 3 x band_width
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xsb + 6 * band_width);
+  uint64_t* full = bars;                  // kV4Slots
+  uint64_t* empty = bars + kV4Slots;      // kV4Slots
+  uint64_t* xfull = bars + 2 * kV4Slots;  // 2
+  uint64_t* xempty = xfull + 2;           // 2
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  double acc[KMAX][3];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
+
+  if (tid == 0) {
+    for (int s = 0; s < kV4Slots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kV4Warps); }
+    for (int j = 0; j < 2; ++j) { mbar_init(&xfull[j], 1); mbar_init(&xempty[j], kV4Warps); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (wid == kV4Warps) {
+    // ------------------------------ producer warp ------------------------------
+    if (lane == 0) {
+      int last_band = -1, bs = -1;
+      for (int i = 0; i < nitems; ++i) {
+        const V4Item it = uitems[i];
+        if (it.band != last_band) {
+          ++bs;
+          // x band for this bandseq: buffer bs & 1, use number bs >> 1
+          const int j = bs & 1, use = bs >> 1;
+          if (use >= 1) mbar_wait(&xempty[j], (use - 1) & 1);
+          const int c0 = it.band * band_width;
+          const int bw = min(band_width, N - c0);
+          const unsigned bytes = (unsigned)bw * 8u;
+          mbar_expect_tx(&xfull[j], 3u * bytes);
+          for (int c = 0; c < 3; ++c)
+            bulk_g2s(xsb + (j * 3 + c) * band_width, x + (size_t)c * N + c0, bytes, &xfull[j]);
+          last_band = it.band;
+        }
+        const int s = i % kV4Slots, use = i / kV4Slots;
+        if (use >= 1) mbar_wait(&empty[s], (use - 1) & 1);
+        mbar_expect_tx(&full[s], it.bytes);
+        bulk_g2s(ring + (size_t)s * slot_bytes, stream + it.off, it.bytes, &full[s]);
+      }
+    }
+  } else {
+    // ------------------------------ consumer warps -----------------------------
+    const int hdr_bytes = ((2 * (kV4Warps + 1) + kV4TPU) + 15) & ~15;
+    int cur_bs = -1, cur_band = -1;
+    const double* xs = xsb;
+    for (int i = 0; i < nitems; ++i) {
+      const V4Item it = uitems[i];
+      if (it.band != cur_band) {
+        if (cur_bs >= 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xempty[cur_bs & 1]);
+        }
+        ++cur_bs;
+        cur_band = it.band;
+        mbar_wait(&xfull[cur_bs & 1], (cur_bs >> 1) & 1);
+        xs = xsb + (cur_bs & 1) * 3 * band_width;
+      }
+      const int s = i % kV4Slots;
+      mbar_wait(&full[s], (i / kV4Slots) & 1);
+      const unsigned char* item = ring + (size_t)s * slot_bytes;
+      const unsigned short* wbase = reinterpret_cast<const unsigned short*>(item);
+      const unsigned cnt = item[2 * (kV4Warps + 1) + tid];
+      unsigned incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned start = (unsigned)wbase[wid] + incl - cnt;
+      const uint2* ent = reinterpret_cast<const uint2*>(item + hdr_bytes) + start;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll 4
+      for (unsigned p = 0; p < cnt; ++p) {
+        const uint2 e = ent[p];
+        const double v = (double)__uint_as_float(e.y);
+        a0 = fma(v, xs[e.x], a0);
+        a1 = fma(v, xs[band_width + e.x], a1);
+        a2 = fma(v, xs[2 * band_width + e.x], a2);
+      }
+      const int k = it.k;
+#pragma unroll
+      for (int kk = 0; kk < KMAX; ++kk)
+        if (kk == k) { acc[kk][0] += a0; acc[kk][1] += a1; acc[kk][2] += a2; }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  // every item has been consumed (so every bulk copy has landed): the ring is
+  // reused as scratch for the per-virtual-thread partial sums
+  __syncthreads();
+  if (wid < kV4Warps) {
+    double* part = reinterpret_cast<double*>(smraw);  // kV4TPU x K x 3
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k >= K) break;
+      part[(tid * K + k) * 3 + 0] = acc[k][0];
+      part[(tid * K + k) * 3 + 1] = acc[k][1];
+      part[(tid * K + k) * 3 + 2] = acc[k][2];
+    }
+  }
+  __syncthreads();
+
+  // ------------------------------ epilogue (all threads) ----------------------
+  const double* part = reinterpret_cast<const double*>(smraw);
+  double* summed = reinterpret_cast<double*>(smraw) + (size_t)kV4TPU * K * 3;  // ntiles x 3 x T2
+  double* tmp = summed + (size_t)ntiles * 3 * T2;
+  const unsigned short* vf = vrow_first + (size_t)unit_tile0[unit] * T2 + unit;  // R + 1 entries
+  for (int r = tid; r < R; r += blockDim.x) {
+    const int t0 = vf[r], t1 = vf[r + 1];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const int row = row0 + r;
+    for (int k = 0; k < K; ++k) {
+      double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+      for (int t = t0; t < t1; ++t) {
+        v0 += part[(t * K + k) * 3 + 0];
+        v1 += part[(t * K + k) * 3 + 1];
+        v2 += part[(t * K + k) * 3 + 2];
+      }
+      double* vo = vk + (size_t)k * 3 * N;
+      vo[row] = v0; vo[N + row] = v1; vo[2 * N + row] = v2;
+      s0 += g[k] * v0;
+      s1 += g[K + k] * v1;
+      s2 += g[2 * K + k] * v2;
+    }
+    const int tj = r / T2, e = r % T2;
+    summed[(tj * 3 + 0) * T2 + e] = s0;
+    summed[(tj * 3 + 1) * T2 + e] = s1;
+    summed[(tj * 3 + 2) * T2 + e] = s2;
+  }
+  __syncthreads();
+  const int tiles_per_row = S / T;
+  for (int j = 0; j < ntiles; ++j) {
+    const int tile = tile0 + j;
+    tile_epilogue(summed + j * 3 * T2, tmp, T, tile / tiles_per_row, tile % tiles_per_row, S,
+                  positions, normals, cam, material, scatter, radiance, radiance_unclamped);
+  }
+}
+
+}  // namespace sss

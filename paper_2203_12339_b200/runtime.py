@@ -126,7 +126,8 @@ class Scene:
         self.material_buf = torch.empty(7, **f64)
         self.cam_buf = torch.empty(3, **f64)
         self._light_kind = None
-        self.transfer_kernel = "stream"  # "stream" (TMA pipeline) | "banded"
+        # "v4" (persistent warp-specialized TMA pipeline) | "stream" | "banded"
+        self.transfer_kernel = "v4"
         self._have_cache = False
         self._sequence = 0
         self._graph = None
@@ -225,6 +226,17 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
+        if self.transfer_kernel == "v4":
+            if getattr(t, "v4", None) is None:
+                from .stream4 import build_v4
+
+                t.v4 = build_v4(t)
+            from .stream4 import launch_v4
+
+            launch_v4(t.v4, t, self.x, self.g, self.positions, self.normals, self.cam_buf,
+                      self.material_buf, self.vk, self.scatter, self.radiance,
+                      self.radiance_unclamped, stream)
+            return
         if self.transfer_kernel == "stream" and t.entries is not None:
             _lib.call("sss_transfer_stream", self.K, self.side, self.levels, t.unit_tiles,
                       t.band_width, t.n_bands, _lib.ptr(t.item_off), _lib.ptr(t.item_len),

@@ -327,13 +327,14 @@ def test_stream_and_banded_kernels_agree(c1):
 
     sc = _scene(c1, SHLight(LT.random_sh_light(3, 23)))
     assert sc.transfer.entries is not None
-    sc.transfer_kernel = "stream"
+    sc.transfer_kernel = "banded"
     a = sc.relight()
     vk_a = sc.vk.clone()
-    sc.transfer_kernel = "banded"
-    b = sc.relight()
-    assert (sc.vk - vk_a).abs().max().item() <= 1e-12 * vk_a.abs().max().item()
-    assert O.parity_error(a.radiance_unclamped, b.radiance_unclamped, TAU) <= 1e-9
+    for kern in ("stream", "v4"):
+        sc.transfer_kernel = kern
+        b = sc.relight()
+        assert (sc.vk - vk_a).abs().max().item() <= 1e-12 * vk_a.abs().max().item(), kern
+        assert O.parity_error(a.radiance_unclamped, b.radiance_unclamped, TAU) <= 1e-9, kern
 
 
 def test_cuda_graph_replay_matches_eager(c1):
