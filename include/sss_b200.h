@@ -136,6 +136,7 @@ int sss_transfer_stream(int K, int side, int levels, int unit_tiles, int band_wi
  *      hand-off only. Layout built by paper_2203_12339_b200/stream4.py;
  *      contract otherwise as sss_transfer_relight. */
 int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes, int units,
+                    int max_unit_items,
                     const int* unit_tile0, const int* unit_ntiles, const int* unit_item0,
                     const int* unit_nitems, const void* items, const void* stream_bytes,
                     const void* vrow_first, const double* x, const double* g,

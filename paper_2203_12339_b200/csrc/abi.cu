@@ -254,6 +254,7 @@ int sss_transfer_stream(int K, int side, int levels, int unit_tiles, int band_wi
 }
 
 int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes, int units,
+                    int max_unit_items,
                     const int* unit_tile0, const int* unit_ntiles, const int* unit_item0,
                     const int* unit_nitems, const void* items, const void* stream_bytes,
                     const void* vrow_first, const double* x, const double* g,
@@ -269,7 +270,8 @@ int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes,
       (band_width * 8) % 16)
     return fail(SSS_EINVAL, "transfer_v4: 16-byte alignment violated");
   const int T = 1 << levels, T2 = T * T;
-  const size_t pipe = (size_t)sss::kV4Slots * slot_bytes + 6 * (size_t)band_width * 8 + 12 * 8;
+  const size_t pipe = (size_t)sss::kV4Slots * slot_bytes + 6 * (size_t)band_width * 8 + 12 * 8 +
+                      (size_t)max_unit_items * sizeof(sss::V4Item);
   const size_t epi = (size_t)sss::kV4TPU * K * 3 * 8 + (size_t)(sss::kV4TPU / T2 + 1) * 3 * T2 * 8 +
                      (size_t)T2 * 8;
   const size_t smem = pipe > epi ? pipe : epi;

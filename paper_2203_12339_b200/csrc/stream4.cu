@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
   const int R = ntiles * T2;
   const int row0 = tile0 * T2;
   const int nitems = unit_nitems[unit];
-  const V4Item* uitems = items + unit_item0[unit];
+  const V4Item* uitems = items + unit_item0[unit];  // re-pointed to shared memory below
 
   // shared memory carve-up
   unsigned char* ring = smraw;                                     // kV4Slots * slot_bytes
@@ -75,12 +75,16 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
 
+  // the unit's item table, staged once (every warp walks it item by item)
+  V4Item* sitems = reinterpret_cast<V4Item*>(xempty + 2);
+  for (int i = tid; i < nitems; i += blockDim.x) sitems[i] = items[unit_item0[unit] + i];
   if (tid == 0) {
     for (int s = 0; s < kV4Slots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kV4Warps); }
     for (int j = 0; j < 2; ++j) { mbar_init(&xfull[j], 1); mbar_init(&xempty[j], kV4Warps); }
     fence_mbar_init();
   }
   __syncthreads();
+  uitems = sitems;
 
   if (wid == kV4Warps) {
     // ------------------------------ producer warp ------------------------------

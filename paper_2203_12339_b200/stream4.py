@@ -38,6 +38,7 @@ class V4Layout:
     n_items: int
     stream_bytes: int
     header_bytes: int
+    max_unit_items: int = 0
 
 
 def _ragged(starts, lens, device):
@@ -156,7 +157,8 @@ def build_v4(dt, slot_bytes: int = 24576, n_sm: int = None) -> V4Layout:
         items=torch.as_tensor(items.view(np.uint8), device=dev),
         stream=stream,
         vrow_first=torch.as_tensor(np.concatenate(vrow_first).view(np.int16), device=dev),
-        n_items=n_items, stream_bytes=total, header_bytes=HDR * n_items)
+        n_items=n_items, stream_bytes=total, header_bytes=HDR * n_items,
+        max_unit_items=int(max(unit_nitems)) if unit_nitems else 0)
 
 
 def _ragged_np(starts, lens):
@@ -195,7 +197,7 @@ def _split(counts, cap):
 def launch_v4(lay: V4Layout, dt, x, g, positions, normals, cam, material, vk, scatter, radiance,
               radiance_unclamped, stream=None):
     _lib.call("sss_transfer_v4", dt.K, dt.side, dt.levels, dt.band_width, lay.slot_bytes,
-              lay.units, _lib.ptr(lay.unit_tile0), _lib.ptr(lay.unit_ntiles),
+              lay.units, lay.max_unit_items, _lib.ptr(lay.unit_tile0), _lib.ptr(lay.unit_ntiles),
               _lib.ptr(lay.unit_item0), _lib.ptr(lay.unit_nitems), _lib.ptr(lay.items),
               _lib.ptr(lay.stream), _lib.ptr(lay.vrow_first), _lib.ptr(x), _lib.ptr(g),
               _lib.ptr(positions), _lib.ptr(normals), _lib.ptr(cam), _lib.ptr(material),
