@@ -272,8 +272,8 @@ int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes,
   const int T = 1 << levels, T2 = T * T;
   const size_t pipe = (size_t)sss::kV4Slots * slot_bytes + 6 * (size_t)band_width * 8 + 12 * 8 +
                       (size_t)max_unit_items * sizeof(sss::V4Item);
-  const size_t epi = (size_t)sss::kV4TPU * K * 3 * 8 + (size_t)(sss::kV4TPU / T2 + 1) * 3 * T2 * 8 +
-                     (size_t)T2 * 8;
+  // partial sums + summed [tile][c][T2] + the batched-Haar scratch of the same size
+  const size_t epi = (size_t)sss::kV4TPU * K * 3 * 8 + 2 * (size_t)(sss::kV4TPU / T2 + 1) * 3 * T2 * 8;
   const size_t smem = pipe > epi ? pipe : epi;
   if (smem > 227 * 1024) return fail(SSS_EINVAL, "transfer_v4: shared memory budget exceeded");
 #define SSS_T4(KM)                                                                               \

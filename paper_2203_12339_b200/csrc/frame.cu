@@ -421,6 +421,40 @@ __device__ void tile_epilogue(double* summed, double* tmp, int T, int tr, int tc
   }
 }
 
+// the same epilogue for `ntiles` consecutive tiles (tile0..) at once:
+// summed is [tile][c][T2]; one batched inverse Haar over all 3*ntiles grids
+__device__ void multi_tile_epilogue(double* summed, double* tmp, int T, int tile0, int ntiles,
+                                    int S, const float* __restrict__ positions,
+                                    const float* __restrict__ normals,
+                                    const double* __restrict__ cam,
+                                    const double* __restrict__ material,
+                                    double* __restrict__ scatter, float* __restrict__ radiance,
+                                    float* __restrict__ radiance_unclamped) {
+  const int T2 = T * T, tpr = S / T;
+  const double eta = material[6];
+  batch_tile_haar_inv(summed, tmp, T, 3 * ntiles);
+  const double inv_pi = 1.0 / 3.141592653589793;
+  for (int q = threadIdx.x; q < ntiles * T2; q += blockDim.x) {
+    const int j = q / T2, e = q % T2;
+    const int tile = tile0 + j, tr = tile / tpr, tc = tile % tpr;
+    const int i = (tr * T + e / T) * S + tc * T + e % T;
+    const double px = positions[i * 3], py = positions[i * 3 + 1], pz = positions[i * 3 + 2];
+    double vx = cam[0] - px, vy = cam[1] - py, vz = cam[2] - pz;
+    const double inv = 1.0 / sqrt(vx * vx + vy * vy + vz * vz);
+    vx *= inv; vy *= inv; vz *= inv;
+    const double cs = (double)normals[i * 3] * vx + (double)normals[i * 3 + 1] * vy +
+                      (double)normals[i * 3 + 2] * vz;
+    const double f = fresnel_transmittance(eta, cs) * inv_pi;
+    for (int c = 0; c < 3; ++c) {
+      const double sc = summed[(j * 3 + c) * T2 + e];
+      const double u = sc * f;
+      if (scatter) scatter[i * 3 + c] = sc;
+      radiance_unclamped[i * 3 + c] = (float)u;
+      radiance[i * 3 + c] = (float)fmax(u, 0.0);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // (b)+(c) fused transfer: CTA per tile, K loop, row-major CSR per k over
 // tile-major rows; v_k cached for edits; epilogue recombines, inverts, shades

@@ -109,6 +109,46 @@ __device__ inline void tile_haar_inv(double* a, double* tmp, int T, int nthreads
   }
 }
 
+// Batched in-place inverse over B independent T x T grids (grid b at
+// a + b * T * T); same arithmetic as tile_haar_inv, 4 barriers per level for
+// the whole batch. tmp: B * T * T doubles.
+__device__ inline void batch_tile_haar_inv(double* a, double* tmp, int T, int B) {
+  const int T2 = T * T, nt = blockDim.x, tid = threadIdx.x;
+  for (int s = 2; s <= T; s <<= 1) {
+    const int h = s >> 1, sh = s * h, ss = s * s;
+    for (int q = tid; q < B * sh; q += nt) {
+      const int b = q / sh, e = q % sh;
+      const int j = e / h, i = e % h;
+      const double* g = a + b * T2;
+      double* o = tmp + b * T2;
+      const double lo = g[i * T + j], hi = g[(h + i) * T + j];
+      o[(2 * i) * T + j] = dmul(dadd(lo, hi), SSS_ISQRT2);
+      o[(2 * i + 1) * T + j] = dmul(dsub(lo, hi), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int q = tid; q < B * ss; q += nt) {
+      const int b = q / ss, e = q % ss;
+      a[b * T2 + (e / s) * T + e % s] = tmp[b * T2 + (e / s) * T + e % s];
+    }
+    __syncthreads();
+    for (int q = tid; q < B * sh; q += nt) {
+      const int b = q / sh, e = q % sh;
+      const int i = e / h, j = e % h;
+      const double* g = a + b * T2;
+      double* o = tmp + b * T2;
+      const double lo = g[i * T + j], hi = g[i * T + h + j];
+      o[i * T + 2 * j] = dmul(dadd(lo, hi), SSS_ISQRT2);
+      o[i * T + 2 * j + 1] = dmul(dsub(lo, hi), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int q = tid; q < B * ss; q += nt) {
+      const int b = q / ss, e = q % ss;
+      a[b * T2 + (e / s) * T + e % s] = tmp[b * T2 + (e / s) * T + e % s];
+    }
+    __syncthreads();
+  }
+}
+
 // F_t(eta, cos) = 1 - F_r, dipole.py:135-152
 __device__ __forceinline__ double fresnel_transmittance(double eta, double ci) {
   ci = fmin(fmax(ci, 0.0), 1.0);

@@ -1,25 +1,26 @@
-// Frame layout v4: persistent, warp-specialized transfer kernel.
+// Frame layout v5: persistent, warp-specialized transfer kernel.
 //
-// One CTA per unit (a contiguous range of G tiles, ~one unit per SM). The
-// unit's operator entries are pre-arranged (host build, stream4.py) into
-// self-describing items, item = (column band, PCA term k[, split]):
+// One CTA per unit (a contiguous range of tiles, ~one unit per SM). The
+// unit's operator entries are pre-arranged (stream4.py, on the GPU) into
+// self-describing items, one per (column band[, split]) holding every PCA
+// term k:
 //
-//   item = [u16 warp_base[NW+1]][u8 count[TPU]] (padded to 16 B)
-//          [entries: {u32 band-local w0 col, f32 val} x n (padded to 16 B)]
+//   item = [u16 warp_base[NW+1]][u8 count[TPU]]  (padded to 16 B)
+//          [entries: {u32 = k << 16 | band-local w0 col, f32 val} x n (16 B pad)]
 //
 // The unit's rows are split into TPU "virtual threads" proportional to their
-// length (long LL rows get several threads) so every consumer thread streams
-// a similar number of entries. Thread t of warp w reads its `count[t]` entries
-// starting at warp_base[w] + (exclusive warp-scan of counts).
+// length (long rows get several threads). Inside an item a thread's entries
+// are contiguous and sorted by k, so it accumulates into acc[k] registers and
+// only switches accumulator when k changes.
 //
 // Warp roles: NW consumer warps + 1 producer warp. The producer streams items
-// into an NS-slot ring with cp.async.bulk (mbarrier full/empty per slot) and
-// the column bands of x into a double buffer (3 bulk copies per band). The
-// consumers never use a CTA-wide barrier in the main loop: each warp releases
-// a slot (or a band buffer) by one mbarrier arrive when it is done with it.
-// Accumulation: fp64 registers acc[k][3] per thread; epilogue reduces the
-// virtual threads of each row, writes v_k, recombines with g, inverse-Haars
-// each tile and shades.
+// into a kV4Slots-slot ring with cp.async.bulk (mbarrier full/empty per slot)
+// and the column bands of x into a double buffer (3 bulk copies per band).
+// Consumers never use a CTA-wide barrier in the main loop: each warp releases
+// a slot (or a band buffer) with one mbarrier arrive. Accumulation in fp64
+// registers; the epilogue reduces the virtual threads of each row, writes
+// v_k, recombines with g, inverse-Haars all the unit's tiles in one batch and
+// shades.
 #include "sss_common.cuh"
 
 namespace sss {
@@ -33,12 +34,19 @@ struct V4Item {
   unsigned long long off;  // byte offset of the item in the stream
   unsigned bytes;          // item size (header + entries), multiple of 16
   unsigned short band;     // column band
-  unsigned char k;         // PCA term
-  unsigned char pad;
+  unsigned short pad;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int KMAX>
+__device__ __forceinline__ void acc_add(double (&acc)[KMAX][3], int k, double a0, double a1,
+                                        double a2) {
+#pragma unroll
+  for (int kk = 0; kk < KMAX; ++kk)
+    if (kk == k) { acc[kk][0] += a0; acc[kk][1] += a1; acc[kk][2] += a2; }
 }
 
 template <int KMAX>
@@ -60,31 +68,28 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
   const int R = ntiles * T2;
   const int row0 = tile0 * T2;
   const int nitems = unit_nitems[unit];
-  const V4Item* uitems = items + unit_item0[unit];  // re-pointed to shared memory below
 
   // shared memory carve-up
-  unsigned char* ring = smraw;                                     // kV4Slots * slot_bytes
+  unsigned char* ring = smraw;                                            // kV4Slots * slot_bytes
   double* xsb = reinterpret_cast<double*>(ring + kV4Slots * slot_bytes);  // 2 x 3 x band_width
   uint64_t* bars = reinterpret_cast<uint64_t*>(xsb + 6 * band_width);
   uint64_t* full = bars;                  // kV4Slots
   uint64_t* empty = bars + kV4Slots;      // kV4Slots
   uint64_t* xfull = bars + 2 * kV4Slots;  // 2
   uint64_t* xempty = xfull + 2;           // 2
+  V4Item* uitems = reinterpret_cast<V4Item*>(xempty + 2);  // the unit's item table
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   double acc[KMAX][3];
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
 
-  // the unit's item table, staged once (every warp walks it item by item)
-  V4Item* sitems = reinterpret_cast<V4Item*>(xempty + 2);
-  for (int i = tid; i < nitems; i += blockDim.x) sitems[i] = items[unit_item0[unit] + i];
+  for (int i = tid; i < nitems; i += blockDim.x) uitems[i] = items[unit_item0[unit] + i];
   if (tid == 0) {
     for (int s = 0; s < kV4Slots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kV4Warps); }
     for (int j = 0; j < 2; ++j) { mbar_init(&xfull[j], 1); mbar_init(&xempty[j], kV4Warps); }
     fence_mbar_init();
   }
   __syncthreads();
-  uitems = sitems;
 
   if (wid == kV4Warps) {
     // ------------------------------ producer warp ------------------------------
@@ -93,8 +98,7 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
       for (int i = 0; i < nitems; ++i) {
         const V4Item it = uitems[i];
         if (it.band != last_band) {
-          ++bs;
-          // x band for this bandseq: buffer bs & 1, use number bs >> 1
+          ++bs;  // x band buffer bs & 1, use number bs >> 1
           const int j = bs & 1, use = bs >> 1;
           if (use >= 1) mbar_wait(&xempty[j], (use - 1) & 1);
           const int c0 = it.band * band_width;
@@ -141,19 +145,26 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
       }
       const unsigned start = (unsigned)wbase[wid] + incl - cnt;
       const uint2* ent = reinterpret_cast<const uint2*>(item + hdr_bytes) + start;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      if (cnt) {
+        int kc = (int)(ent[0].x >> 16);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll 4
-      for (unsigned p = 0; p < cnt; ++p) {
-        const uint2 e = ent[p];
-        const double v = (double)__uint_as_float(e.y);
-        a0 = fma(v, xs[e.x], a0);
-        a1 = fma(v, xs[band_width + e.x], a1);
-        a2 = fma(v, xs[2 * band_width + e.x], a2);
+        for (unsigned p = 0; p < cnt; ++p) {
+          const uint2 e = ent[p];
+          const int k = (int)(e.x >> 16);
+          if (k != kc) {
+            acc_add<KMAX>(acc, kc, a0, a1, a2);
+            a0 = a1 = a2 = 0.0;
+            kc = k;
+          }
+          const int col = (int)(e.x & 0xffffu);
+          const double v = (double)__uint_as_float(e.y);
+          a0 = fma(v, xs[col], a0);
+          a1 = fma(v, xs[band_width + col], a1);
+          a2 = fma(v, xs[2 * band_width + col], a2);
+        }
+        acc_add<KMAX>(acc, kc, a0, a1, a2);
       }
-      const int k = it.k;
-#pragma unroll
-      for (int kk = 0; kk < KMAX; ++kk)
-        if (kk == k) { acc[kk][0] += a0; acc[kk][1] += a1; acc[kk][2] += a2; }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -177,7 +188,7 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
   const double* part = reinterpret_cast<const double*>(smraw);
   double* summed = reinterpret_cast<double*>(smraw) + (size_t)kV4TPU * K * 3;  // ntiles x 3 x T2
   double* tmp = summed + (size_t)ntiles * 3 * T2;
-  const unsigned short* vf = vrow_first + (size_t)unit_tile0[unit] * T2 + unit;  // R + 1 entries
+  const unsigned short* vf = vrow_first + (size_t)row0 + unit;  // R + 1 entries of this unit
   for (int r = tid; r < R; r += blockDim.x) {
     const int t0 = vf[r], t1 = vf[r + 1];
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -201,12 +212,8 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
     summed[(tj * 3 + 2) * T2 + e] = s2;
   }
   __syncthreads();
-  const int tiles_per_row = S / T;
-  for (int j = 0; j < ntiles; ++j) {
-    const int tile = tile0 + j;
-    tile_epilogue(summed + j * 3 * T2, tmp, T, tile / tiles_per_row, tile % tiles_per_row, S,
-                  positions, normals, cam, material, scatter, radiance, radiance_unclamped);
-  }
+  multi_tile_epilogue(summed, tmp, T, tile0, ntiles, S, positions, normals, cam, material, scatter,
+                      radiance, radiance_unclamped);
 }
 
 }  // namespace sss

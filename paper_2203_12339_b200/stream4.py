@@ -1,8 +1,12 @@
-"""Build the frame layout v4 (csrc/stream4.cu) from the canonical tile-major
-CSR operator: per-SM units, virtual threads, self-describing (band, k) items.
+"""Build frame layout v5 (csrc/stream4.cu) from the canonical tile-major CSR
+operator, on the GPU: per-SM units, virtual threads, self-describing items
+(one per unit x column band [x split]) carrying every PCA term.
 
-Host-side planning in numpy (row splits, per-thread counts, item headers,
-item table); the 8-byte entries are gathered into the stream on the GPU.
+Stream order inside an item: virtual thread, then k, then column. A row's
+(band, k) segment is cut into its m_r virtual threads' pieces with
+piece(p) = ((p + 1) m - 1) // len. The order is produced by one device sort
+on a composite key; headers (per-thread counts + warp bases) are small
+bincounts.
 """
 
 from __future__ import annotations
@@ -19,14 +23,16 @@ TPU = NW * 32
 SLOTS = 4
 HDR = (2 * (NW + 1) + TPU + 15) & ~15  # u16 warp bases + u8 counts, 16-B padded
 MAXCNT = 255
+SLOT_BYTES = 32768
+BAND_WIDTH = 1024  # w0 ids per x band (3 x 1024 doubles per buffer, double-buffered)
 
-ITEM_DTYPE = np.dtype([("off", "<u8"), ("bytes", "<u4"), ("band", "<u2"), ("k", "u1"),
-                       ("pad", "u1")])
+ITEM_DTYPE = np.dtype([("off", "<u8"), ("bytes", "<u4"), ("band", "<u2"), ("pad", "<u2")])
 
 
 @dataclass
 class V4Layout:
     slot_bytes: int
+    band_width: int
     units: int
     unit_tile0: torch.Tensor
     unit_ntiles: torch.Tensor
@@ -38,165 +44,151 @@ class V4Layout:
     n_items: int
     stream_bytes: int
     header_bytes: int
-    max_unit_items: int = 0
+    max_unit_items: int
 
 
-def _ragged(starts, lens, device):
-    """concat(arange(s, s + l)) on the device."""
-    starts = torch.as_tensor(starts, dtype=torch.int64, device=device)
-    lens = torch.as_tensor(lens, dtype=torch.int64, device=device)
-    total = int(lens.sum().item())
-    if total == 0:
-        return torch.empty(0, dtype=torch.int64, device=device)
-    rep_s = torch.repeat_interleave(starts, lens)
-    base = torch.repeat_interleave(torch.cumsum(lens, 0) - lens, lens)
-    return torch.arange(total, device=device) - base + rep_s
+def _threads_per_row(row_tot: np.ndarray, R: int) -> np.ndarray:
+    """1 thread per row + the spare ones proportional to row length."""
+    m = np.ones(R, np.int64)
+    spare = TPU - R
+    tot = float(row_tot.sum())
+    if spare > 0 and tot > 0:
+        share = spare * row_tot / tot
+        extra = np.floor(share).astype(np.int64)
+        rem = spare - int(extra.sum())
+        if rem > 0:
+            extra[np.argsort(-(share - extra), kind="stable")[:rem]] += 1
+        m += extra
+    return m
 
 
-def build_v4(dt, slot_bytes: int = 24576, n_sm: int = None) -> V4Layout:
+def build_v4(dt, slot_bytes: int = SLOT_BYTES, band_width: int = BAND_WIDTH,
+             n_sm: int = None) -> V4Layout:
     dev = dt.rowptr.device
     if n_sm is None:
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    n, K, NB, BW = dt.n, dt.K, dt.n_bands, dt.band_width
+    n, K = dt.n, dt.K
+    BW = min(band_width, n)
+    NB = (n + BW - 1) // BW
     T2 = (1 << dt.levels) ** 2
     ntiles = n // T2
     G = -(-ntiles // n_sm)
     if G * T2 > TPU:
         raise ValueError(f"{G} tiles x {T2} rows per unit exceed {TPU} threads")
     units = -(-ntiles // G)
+    R_unit = G * T2
     cap = (slot_bytes - HDR) // 8
     cap -= cap & 1
     rp = dt.rowptr.cpu().numpy()
-    bo = dt.bandoff.cpu().numpy().astype(np.int64)  # (K, n, NB+1)
-    seg_len_all = np.diff(bo, axis=2)  # (K, n, NB)
-    row_tot = seg_len_all.sum(axis=(0, 2))
-
-    item_recs, item_hdrs, item_n = [], [], []
-    seg_starts, seg_lens = [], []
-    unit_tile0, unit_ntiles, unit_item0, unit_nitems, vrow_first = [], [], [], [], []
+    row_len = (rp[:, 1:] - rp[:, :-1])  # (K, n)
+    row_tot = row_len.sum(axis=0)
+    # virtual threads per row, unit by unit
+    m_all = np.empty(n, np.int64)
+    vf_list = []
     for u in range(units):
-        t0 = u * G
-        nt = min(G, ntiles - t0)
-        r0, R = t0 * T2, nt * T2
-        rows = np.arange(r0, r0 + R)
-        # virtual threads: 1 per row + the spare ones proportional to length
-        Lr = row_tot[rows].astype(np.float64)
-        spare = TPU - R
-        m = np.ones(R, np.int64)
-        if spare > 0 and Lr.sum() > 0:
-            share = spare * Lr / Lr.sum()
-            extra = np.floor(share).astype(np.int64)
-            rem = spare - int(extra.sum())
-            if rem > 0:
-                extra[np.argsort(-(share - extra), kind="stable")[:rem]] += 1
-            m += extra
-        vf = np.zeros(R + 1, np.int64)
+        r0, r1 = u * R_unit, min((u + 1) * R_unit, n)
+        m = _threads_per_row(row_tot[r0:r1].astype(np.float64), r1 - r0)
+        m_all[r0:r1] = m
+        vf = np.zeros(r1 - r0 + 1, np.int64)
         np.cumsum(m, out=vf[1:])
-        nthreads_used = int(vf[-1])
-        thr_row = np.repeat(np.arange(R), m)  # row of each virtual thread
-        thr_j = np.arange(nthreads_used) - vf[thr_row]
-        thr_m = m[thr_row]
-        unit_tile0.append(t0)
-        unit_ntiles.append(nt)
-        unit_item0.append(len(item_recs))
-        vrow_first.append(vf.astype(np.uint16))
-        lens = seg_len_all[:, rows, :]  # (K, R, NB)
-        starts = rp[:, rows][:, :, None] + bo[:, rows, :NB]  # (K, R, NB)
-        for b in range(NB):
-            for k in range(K):
-                ln = lens[k, :, b]
-                ntot = int(ln.sum())
-                if ntot == 0:
-                    continue
-                lt = ln[thr_row]
-                cnt = (lt * (thr_j + 1)) // thr_m - (lt * thr_j) // thr_m
-                counts = np.zeros(TPU, np.int64)
-                counts[:nthreads_used] = cnt
-                seg_starts.append(starts[k, :, b])
-                seg_lens.append(ln)
-                for sub in _split(counts, cap):
-                    hdr = np.zeros(HDR, np.uint8)
-                    wb = np.zeros(NW + 1, np.int64)
-                    np.cumsum(sub.reshape(NW, 32).sum(axis=1), out=wb[1:])
-                    hdr[: 2 * (NW + 1)] = wb.astype("<u2").view(np.uint8)
-                    hdr[2 * (NW + 1): 2 * (NW + 1) + TPU] = sub.astype(np.uint8)
-                    ns = int(sub.sum())
-                    item_hdrs.append(hdr)
-                    item_n.append(ns)
-                    item_recs.append((b, k))
-        unit_nitems.append(len(item_recs) - unit_item0[-1])
+        vf_list.append(vf)
+    vstart = np.concatenate([vf[:-1] for vf in vf_list])  # first thread of each row (unit-local)
 
-    n_items = len(item_recs)
-    item_n = np.asarray(item_n, np.int64)
-    item_bytes = HDR + 8 * (item_n + (item_n & 1))
+    # ---- per-entry coordinates on the device
+    nnz = dt.nnz
+    k_of = torch.repeat_interleave(torch.arange(K, device=dev),
+                                   torch.as_tensor(row_len.sum(axis=1), device=dev))
+    row_of = torch.repeat_interleave(
+        torch.arange(n, device=dev).repeat(K), torch.as_tensor(row_len.reshape(-1), device=dev))
+    col = dt.cols.to(torch.int64) & 0xFFFFFFFF
+    band = col // BW
+    col_local = col % BW
+    # position inside the (row, band, k) segment: entries are col-sorted within
+    # a row, so segments are contiguous runs
+    seg_key = (k_of * n + row_of) * NB + band
+    seg_start_flag = torch.ones(nnz, dtype=torch.bool, device=dev)
+    seg_start_flag[1:] = seg_key[1:] != seg_key[:-1]
+    idx = torch.arange(nnz, device=dev)
+    seg_first = torch.cummax(torch.where(seg_start_flag, idx, torch.zeros_like(idx)), 0).values
+    pos = idx - seg_first
+    seg_len = torch.bincount(torch.cumsum(seg_start_flag.to(torch.int64), 0) - 1)
+    seg_len_e = seg_len[torch.cumsum(seg_start_flag.to(torch.int64), 0) - 1]
+    m_t = torch.as_tensor(m_all, device=dev)[row_of]
+    piece = ((pos + 1) * m_t - 1) // seg_len_e
+    thread = torch.as_tensor(vstart, device=dev)[row_of] + piece
+    unit = row_of // R_unit
+    # stream order: (unit, band, thread, k, col)
+    key = ((((unit * NB + band) * TPU + thread) * 16 + k_of) << 16) | col_local
+    order = torch.argsort(key)
+    unit_s, band_s, thread_s = unit[order], band[order], thread[order]
+    ub = unit_s * NB + band_s
+    # position inside the (unit, band) group -> sub-item split at `cap`
+    grp_flag = torch.ones(nnz, dtype=torch.bool, device=dev)
+    grp_flag[1:] = ub[1:] != ub[:-1]
+    grp_first = torch.cummax(torch.where(grp_flag, idx, torch.zeros_like(idx)), 0).values
+    gpos = idx - grp_first
+    sub = gpos // cap
+    item_key = ub * 4096 + sub  # (unit, band, sub)
+    ik_flag = torch.ones(nnz, dtype=torch.bool, device=dev)
+    ik_flag[1:] = item_key[1:] != item_key[:-1]
+    item_id = torch.cumsum(ik_flag.to(torch.int64), 0) - 1
+    n_items = int(item_id[-1].item()) + 1 if nnz else 0
+    item_n = torch.bincount(item_id, minlength=n_items)
+    counts = torch.bincount(item_id * TPU + thread_s, minlength=n_items * TPU).view(n_items, TPU)
+    if nnz and int(counts.max().item()) > MAXCNT:
+        raise ValueError("a virtual thread holds more than 255 entries of one item; "
+                         "lower band_width")
+    first_e = torch.nonzero(ik_flag).squeeze(1)
+    item_unit = unit_s[first_e].cpu().numpy()
+    item_band = band_s[first_e].cpu().numpy()
+    item_n_h = item_n.cpu().numpy().astype(np.int64)
+    item_bytes = HDR + 8 * (item_n_h + (item_n_h & 1))
     item_off = np.zeros(n_items + 1, np.int64)
     np.cumsum(item_bytes, out=item_off[1:])
     total = int(item_off[-1])
+    # headers
+    wb = torch.zeros((n_items, NW + 1), dtype=torch.int64, device=dev)
+    wb[:, 1:] = torch.cumsum(counts.view(n_items, NW, 32).sum(dim=2), 1)
+    hdr = torch.zeros((n_items, HDR), dtype=torch.uint8, device=dev)
+    hdr[:, : 2 * (NW + 1)] = wb.to(torch.int16).view(torch.uint8).view(n_items, 2 * (NW + 1))
+    hdr[:, 2 * (NW + 1): 2 * (NW + 1) + TPU] = counts.to(torch.uint8)
+    stream = torch.zeros(total + 16, dtype=torch.uint8, device=dev)[:total]
+    off_d = torch.as_tensor(item_off[:-1], device=dev)
+    hpos = (off_d[:, None] + torch.arange(HDR, device=dev)[None, :]).reshape(-1)
+    stream[hpos] = hdr.reshape(-1)
+    # entries: position inside the item = gpos - sub * cap
+    ipos = gpos - sub * cap
+    dst = (off_d[item_id] + HDR) // 8 + ipos
+    vbits = dt.vals.view(torch.int32).to(torch.int64)[order] & 0xFFFFFFFF
+    packed = ((k_of[order] << 16) | col_local[order]) | (vbits << 32)
+    stream.view(torch.int64)[dst] = packed
+    # unit tables
+    unit_nitems = np.bincount(item_unit, minlength=units)
+    unit_item0 = np.zeros(units, np.int64)
+    unit_item0[1:] = np.cumsum(unit_nitems)[:-1]
     items = np.zeros(n_items, ITEM_DTYPE)
     items["off"] = item_off[:-1]
     items["bytes"] = item_bytes
-    items["band"] = [b for b, _ in item_recs]
-    items["k"] = [k for _, k in item_recs]
-    # stream: headers on the host, entries gathered on the device
-    host = np.zeros(total, np.uint8)
-    hdr_pos = _ragged_np(item_off[:-1], np.full(n_items, HDR))
-    host[hdr_pos] = np.concatenate(item_hdrs) if item_hdrs else np.empty(0, np.uint8)
-    stream = torch.as_tensor(host, device=dev)
-    src = _ragged(np.concatenate(seg_starts), np.concatenate(seg_lens), dev)
-    dst = _ragged((item_off[:-1] + HDR) // 8, item_n, dev)
-    cols = dt.cols[src].to(torch.int64) & 0xFFFFFFFF
-    vbits = dt.vals[src].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-    packed = (cols % BW) | (vbits << 32)
-    stream.view(torch.int64)[dst] = packed
+    items["band"] = item_band
+    unit_tile0 = np.arange(units) * G
+    unit_ntiles = np.minimum(G, ntiles - unit_tile0)
     return V4Layout(
-        slot_bytes=slot_bytes, units=units,
-        unit_tile0=torch.as_tensor(np.asarray(unit_tile0, np.int32), device=dev),
-        unit_ntiles=torch.as_tensor(np.asarray(unit_ntiles, np.int32), device=dev),
-        unit_item0=torch.as_tensor(np.asarray(unit_item0, np.int32), device=dev),
-        unit_nitems=torch.as_tensor(np.asarray(unit_nitems, np.int32), device=dev),
+        slot_bytes=slot_bytes, band_width=BW, units=units,
+        unit_tile0=torch.as_tensor(unit_tile0.astype(np.int32), device=dev),
+        unit_ntiles=torch.as_tensor(unit_ntiles.astype(np.int32), device=dev),
+        unit_item0=torch.as_tensor(unit_item0.astype(np.int32), device=dev),
+        unit_nitems=torch.as_tensor(unit_nitems.astype(np.int32), device=dev),
         items=torch.as_tensor(items.view(np.uint8), device=dev),
         stream=stream,
-        vrow_first=torch.as_tensor(np.concatenate(vrow_first).view(np.int16), device=dev),
+        vrow_first=torch.as_tensor(np.concatenate(vf_list).astype(np.uint16).view(np.int16),
+                                   device=dev),
         n_items=n_items, stream_bytes=total, header_bytes=HDR * n_items,
-        max_unit_items=int(max(unit_nitems)) if unit_nitems else 0)
-
-
-def _ragged_np(starts, lens):
-    starts = np.asarray(starts, np.int64)
-    lens = np.asarray(lens, np.int64)
-    total = int(lens.sum())
-    base = np.repeat(np.cumsum(lens) - lens, lens)
-    return np.arange(total, dtype=np.int64) - base + np.repeat(starts, lens)
-
-
-def _split(counts, cap):
-    """Cut one item's per-thread counts into sub-items with <= cap entries and
-    <= 255 entries per thread; entry order is preserved."""
-    if counts.sum() <= cap and counts.max() <= MAXCNT:
-        return [counts]
-    out, cur, cur_n = [], np.zeros_like(counts), 0
-    for t in range(counts.size):
-        r = int(counts[t])
-        while r > 0:
-            take = min(r, MAXCNT - int(cur[t]), cap - cur_n)
-            if take <= 0:
-                out.append(cur)
-                cur, cur_n = np.zeros_like(counts), 0
-                continue
-            cur[t] += take
-            cur_n += take
-            r -= take
-            if cur_n == cap:
-                out.append(cur)
-                cur, cur_n = np.zeros_like(counts), 0
-    if cur_n:
-        out.append(cur)
-    return out
+        max_unit_items=int(unit_nitems.max()) if units else 0)
 
 
 def launch_v4(lay: V4Layout, dt, x, g, positions, normals, cam, material, vk, scatter, radiance,
               radiance_unclamped, stream=None):
-    _lib.call("sss_transfer_v4", dt.K, dt.side, dt.levels, dt.band_width, lay.slot_bytes,
+    _lib.call("sss_transfer_v4", dt.K, dt.side, dt.levels, lay.band_width, lay.slot_bytes,
               lay.units, lay.max_unit_items, _lib.ptr(lay.unit_tile0), _lib.ptr(lay.unit_ntiles),
               _lib.ptr(lay.unit_item0), _lib.ptr(lay.unit_nitems), _lib.ptr(lay.items),
               _lib.ptr(lay.stream), _lib.ptr(lay.vrow_first), _lib.ptr(x), _lib.ptr(g),
