@@ -5,7 +5,7 @@
 // self-describing items, one per (column band[, split]) holding every PCA
 // term k:
 //
-//   item = [u16 warp_base[NW+1]][u8 count[TPU]]  (padded to 16 B)
+//   item = [u16 warp_base[NW+1]][u16 count[TPU]]  (padded to 16 B)
 //          [entries: {u32 = k << 16 | band-local w0 col, f32 val} x n (16 B pad)]
 //
 // The unit's rows are split into TPU "virtual threads" proportional to their
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
     }
   } else {
     // ------------------------------ consumer warps -----------------------------
-    const int hdr_bytes = ((2 * (kV4Warps + 1) + kV4TPU) + 15) & ~15;
+    const int hdr_bytes = ((2 * (kV4Warps + 1) + 2 * kV4TPU) + 15) & ~15;
     int cur_bs = -1, cur_band = -1;
     const double* xs = xsb;
     for (int i = 0; i < nitems; ++i) {
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
       mbar_wait(&full[s], (i / kV4Slots) & 1);
       const unsigned char* item = ring + (size_t)s * slot_bytes;
       const unsigned short* wbase = reinterpret_cast<const unsigned short*>(item);
-      const unsigned cnt = item[2 * (kV4Warps + 1) + tid];
+      const unsigned cnt = wbase[(kV4Warps + 1) + tid];
       unsigned incl = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {

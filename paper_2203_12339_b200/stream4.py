@@ -21,8 +21,8 @@ from . import _lib
 NW = 16  # consumer warps (csrc/stream4.cu: kV4Warps)
 TPU = NW * 32
 SLOTS = 4
-HDR = (2 * (NW + 1) + TPU + 15) & ~15  # u16 warp bases + u8 counts, 16-B padded
-MAXCNT = 255
+HDR = (2 * (NW + 1) + 2 * TPU + 15) & ~15  # u16 warp bases + u16 counts, 16-B padded
+MAXCNT = 65535
 SLOT_BYTES = 32768
 BAND_WIDTH = 1024  # w0 ids per x band (3 x 1024 doubles per buffer, double-buffered)
 
@@ -136,8 +136,7 @@ def build_v4(dt, slot_bytes: int = SLOT_BYTES, band_width: int = BAND_WIDTH,
     item_n = torch.bincount(item_id, minlength=n_items)
     counts = torch.bincount(item_id * TPU + thread_s, minlength=n_items * TPU).view(n_items, TPU)
     if nnz and int(counts.max().item()) > MAXCNT:
-        raise ValueError("a virtual thread holds more than 255 entries of one item; "
-                         "lower band_width")
+        raise ValueError("a virtual thread holds more than 65535 entries of one item")
     first_e = torch.nonzero(ik_flag).squeeze(1)
     item_unit = unit_s[first_e].cpu().numpy()
     item_band = band_s[first_e].cpu().numpy()
@@ -151,7 +150,8 @@ def build_v4(dt, slot_bytes: int = SLOT_BYTES, band_width: int = BAND_WIDTH,
     wb[:, 1:] = torch.cumsum(counts.view(n_items, NW, 32).sum(dim=2), 1)
     hdr = torch.zeros((n_items, HDR), dtype=torch.uint8, device=dev)
     hdr[:, : 2 * (NW + 1)] = wb.to(torch.int16).view(torch.uint8).view(n_items, 2 * (NW + 1))
-    hdr[:, 2 * (NW + 1): 2 * (NW + 1) + TPU] = counts.to(torch.uint8)
+    hdr[:, 2 * (NW + 1): 2 * (NW + 1) + 2 * TPU] = (
+        counts.to(torch.int32).to(torch.int16).view(torch.uint8).view(n_items, 2 * TPU))
     stream = torch.zeros(total + 16, dtype=torch.uint8, device=dev)[:total]
     off_d = torch.as_tensor(item_off[:-1], device=dev)
     hpos = (off_d[:, None] + torch.arange(HDR, device=dev)[None, :]).reshape(-1)
