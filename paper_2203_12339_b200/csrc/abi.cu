@@ -99,12 +99,14 @@ int sss_sh_irradiance(const float* T_l, const double* Lsh, int nl, int side, int
                       double* E_out, double* ehat, void* stream) {
   if (int r = check_geom(side, levels)) return r;
   if (nl <= 0 || !T_l || !Lsh || !ehat) return fail(SSS_EINVAL, "bad SH arguments");
-  const int T = 1 << levels;
-  const size_t smem = 4 * (size_t)T * T * sizeof(double);
-  if (int r = set_smem((const void*)sss::k_sh_irradiance_haar, smem)) return r;
-  sss::k_sh_irradiance_haar<<<(side / T) * (side / T), 128, smem, S_(stream)>>>(
-      T_l, Lsh, nl, side, levels, E_out, ehat);
-  return check_launch("k_sh_irradiance_haar");
+  const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
+  int tpb = 256 / T2 < 1 ? 1 : 256 / T2;
+  while (tpb > 1 && tiles % tpb) tpb >>= 1;
+  const size_t smem = 6 * (size_t)tpb * T2 * sizeof(double);
+  if (int r = set_smem((const void*)sss::k_sh_irradiance_multi, smem)) return r;
+  sss::k_sh_irradiance_multi<<<tiles / tpb, tpb * T2 < 32 ? 32 : tpb * T2, smem, S_(stream)>>>(
+      T_l, Lsh, nl, side, levels, tpb, E_out, ehat);
+  return check_launch("k_sh_irradiance_multi");
 }
 
 int sss_env_project(const double* faces, int env_side, int n_keep, uint32_t* idx, double* val,
@@ -130,13 +132,16 @@ int sss_env_irradiance(const float* W2, int D, const uint32_t* union_idx, const 
   if (int r = check_geom(side, levels)) return r;
   if (!W2 || !union_idx || !union_lc || !n_union || !ehat || n_keep <= 0)
     return fail(SSS_EINVAL, "bad env_irradiance arguments");
-  const int T = 1 << levels;
-  const size_t smem = 4 * (size_t)T * T * sizeof(double) + 9 * (size_t)n_keep * sizeof(double) +
+  const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
+  int tpb = 256 / T2 < 1 ? 1 : 256 / T2;
+  while (tpb > 1 && tiles % tpb) tpb >>= 1;
+  const size_t smem = 6 * (size_t)tpb * T2 * sizeof(double) + 9 * (size_t)n_keep * sizeof(double) +
                       3 * (size_t)n_keep * sizeof(int);
-  if (int r = set_smem((const void*)sss::k_env_irradiance_haar, smem)) return r;
-  sss::k_env_irradiance_haar<<<(side / T) * (side / T), 128, smem, S_(stream)>>>(
-      W2, D, union_idx, union_lc, n_union, n_keep, side, levels, E_out, ehat);
-  return check_launch("k_env_irradiance_haar");
+  if (int r = set_smem((const void*)sss::k_env_irradiance_multi, smem)) return r;
+  (void)D;
+  sss::k_env_irradiance_multi<<<tiles / tpb, tpb * T2 < 32 ? 32 : tpb * T2, smem, S_(stream)>>>(
+      W2, union_idx, union_lc, n_union, n_keep, side, levels, tpb, E_out, ehat);
+  return check_launch("k_env_irradiance_multi");
 }
 
 int sss_env_transfer(const float* normals, int n_points, const double* dirs, const double* dom,
@@ -270,7 +275,9 @@ int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes,
       (band_width * 8) % 16)
     return fail(SSS_EINVAL, "transfer_v4: 16-byte alignment violated");
   const int T = 1 << levels, T2 = T * T;
-  const size_t pipe = (size_t)sss::kV4Slots * slot_bytes + 6 * (size_t)band_width * 8 + 12 * 8 +
+  const size_t pipe = (size_t)sss::kV4Slots * slot_bytes +
+                      3 * (size_t)sss::kV4XBufs * band_width * 8 +
+                      (2 * sss::kV4Slots + 2 * sss::kV4XBufs) * 8 +
                       (size_t)max_unit_items * sizeof(sss::V4Item);
   // partial sums + summed [tile][c][T2] + the batched-Haar scratch of the same size
   const size_t epi = (size_t)sss::kV4TPU * K * 3 * 8 + 2 * (size_t)(sss::kV4TPU / T2 + 1) * 3 * T2 * 8;

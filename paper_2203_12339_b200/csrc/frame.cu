@@ -318,6 +318,105 @@ __global__ void k_env_irradiance_haar(const float* __restrict__ W2, int D,
   }
 }
 
+// Multi-tile versions of the two light-projection kernels: TPB tiles per CTA,
+// one thread per point (blockDim = TPB * 4^L), deeper load prefetch, one
+// batched forward Haar for the 3 * TPB grids. Same arithmetic and summation
+// order as above (bitwise-identical E and ehat).
+__device__ __forceinline__ void scatter_ehat(const double* a, int T, int TPB, int tile0, int L,
+                                             int S, double* __restrict__ ehat) {
+  const int T2 = T * T, N = S * S, tpr = S / T;
+  for (int q = threadIdx.x; q < TPB * T2; q += blockDim.x) {
+    const int j = q / T2, e = q % T2;
+    const int tile = tile0 + j;
+    int gr, gc;
+    local_to_global(e / T, e % T, tile / tpr, tile % tpr, L, S, &gr, &gc);
+    const int g = gr * S + gc;
+    ehat[g] = a[(j * 3 + 0) * T2 + e];
+    ehat[N + g] = a[(j * 3 + 1) * T2 + e];
+    ehat[2 * N + g] = a[(j * 3 + 2) * T2 + e];
+  }
+}
+
+__global__ void k_env_irradiance_multi(const float* __restrict__ W2,
+                                       const uint32_t* __restrict__ union_idx,
+                                       const double* __restrict__ union_lc,
+                                       const int* __restrict__ n_union, int n_keep, int S, int L,
+                                       int TPB, double* __restrict__ E_out,
+                                       double* __restrict__ ehat) {
+  extern __shared__ double sm[];
+  const int T = 1 << L, T2 = T * T, N = S * S, tpr = S / T;
+  double* a = sm;                       // TPB * 3 * T2
+  double* tmp = a + TPB * 3 * T2;       // TPB * 3 * T2
+  double* lc = tmp + TPB * 3 * T2;      // 3 n_keep * 3
+  int* ul = reinterpret_cast<int*>(lc + 9 * n_keep);
+  const int m = *n_union;
+  for (int q = threadIdx.x; q < m; q += blockDim.x) {
+    ul[q] = (int)union_idx[q];
+    lc[q * 3] = union_lc[q * 3]; lc[q * 3 + 1] = union_lc[q * 3 + 1]; lc[q * 3 + 2] = union_lc[q * 3 + 2];
+  }
+  __syncthreads();
+  const int tile0 = blockIdx.x * TPB;
+  for (int q = threadIdx.x; q < TPB * T2; q += blockDim.x) {
+    const int j = q / T2, e = q % T2;
+    const int tile = tile0 + j, tr = tile / tpr, tc = tile % tpr;
+    const int i = (tr * T + e / T) * S + tc * T + e % T;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    constexpr int kPf = 16;
+    for (int q0 = 0; q0 < m; q0 += kPf) {
+      float wv[kPf];
+#pragma unroll
+      for (int u = 0; u < kPf; ++u)
+        wv[u] = (q0 + u < m) ? __ldg(&W2[(size_t)ul[q0 + u] * N + i]) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) {
+        if (q0 + u >= m) break;
+        const int qq = q0 + u;
+        const double w = (double)wv[u];
+        const double l0 = lc[qq * 3], l1 = lc[qq * 3 + 1], l2 = lc[qq * 3 + 2];
+        if (l0 != 0.0) acc0 = dadd(acc0, dmul(w, l0));
+        if (l1 != 0.0) acc1 = dadd(acc1, dmul(w, l1));
+        if (l2 != 0.0) acc2 = dadd(acc2, dmul(w, l2));
+      }
+    }
+    a[(j * 3 + 0) * T2 + e] = acc0;
+    a[(j * 3 + 1) * T2 + e] = acc1;
+    a[(j * 3 + 2) * T2 + e] = acc2;
+    if (E_out) { E_out[i * 3 + 0] = acc0; E_out[i * 3 + 1] = acc1; E_out[i * 3 + 2] = acc2; }
+  }
+  __syncthreads();
+  batch_tile_haar_fwd(a, tmp, T, 3 * TPB);
+  scatter_ehat(a, T, TPB, tile0, L, S, ehat);
+}
+
+__global__ void k_sh_irradiance_multi(const float* __restrict__ T_l, const double* __restrict__ Lsh,
+                                      int nl, int S, int L, int TPB, double* __restrict__ E_out,
+                                      double* __restrict__ ehat) {
+  extern __shared__ double sm[];
+  const int T = 1 << L, T2 = T * T, N = S * S, tpr = S / T;
+  double* a = sm;                  // TPB * 3 * T2
+  double* tmp = a + TPB * 3 * T2;  // TPB * 3 * T2
+  const int tile0 = blockIdx.x * TPB;
+  for (int q = threadIdx.x; q < TPB * T2; q += blockDim.x) {
+    const int j = q / T2, e = q % T2;
+    const int tile = tile0 + j, tr = tile / tpr, tc = tile % tpr;
+    const int i = (tr * T + e / T) * S + tc * T + e % T;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int l = 0; l < nl; ++l) {
+      const double t = (double)__ldg(&T_l[(size_t)l * N + i]);
+      acc0 = dadd(acc0, dmul(t, Lsh[l * 3 + 0]));
+      acc1 = dadd(acc1, dmul(t, Lsh[l * 3 + 1]));
+      acc2 = dadd(acc2, dmul(t, Lsh[l * 3 + 2]));
+    }
+    a[(j * 3 + 0) * T2 + e] = acc0;
+    a[(j * 3 + 1) * T2 + e] = acc1;
+    a[(j * 3 + 2) * T2 + e] = acc2;
+    if (E_out) { E_out[i * 3 + 0] = acc0; E_out[i * 3 + 1] = acc1; E_out[i * 3 + 2] = acc2; }
+  }
+  __syncthreads();
+  batch_tile_haar_fwd(a, tmp, T, 3 * TPB);
+  scatter_ehat(a, T, TPB, tile0, L, S, ehat);
+}
+
 // ---------------------------------------------------------------------------
 // exact top-n of the irradiance spectrum per channel (runtime.py:112-118)
 // grid: 3 CTAs x 1024 threads. x = ehat where kept, else 0.
@@ -368,24 +467,33 @@ __global__ void k_material_weights(const double* __restrict__ bw /* K x nr: base
                                    const double* __restrict__ r_nodes, int K, int nr,
                                    const double* __restrict__ material /* sp[3], sa[3], eta */,
                                    double* __restrict__ g) {
-  extern __shared__ double rd[];  // nr
-  __shared__ double red[32];
+  // all K dot products in one pass: per-thread partials for every k, one
+  // warp reduction per k, one barrier (K <= 16)
+  __shared__ double red[32][16];
   const int c = blockIdx.x;
   const Dipole d = derive_dipole(material[c], material[3 + c], material[6]);
-  for (int j = threadIdx.x; j < nr; j += blockDim.x) rd[j] = eval_rd(d, r_nodes[j]);
+  double part[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) part[k] = 0.0;
+  for (int j = threadIdx.x; j < nr; j += blockDim.x) {
+    const double rd = eval_rd(d, r_nodes[j]);
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < K) part[k] += bw[k * nr + j] * rd;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (k >= K) break;
+    double a = part[k];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+    if (lane == 0) red[wid][k] = a;
+  }
   __syncthreads();
-  for (int k = 0; k < K; ++k) {
-    double acc = 0.0;
-    for (int j = threadIdx.x; j < nr; j += blockDim.x) acc += bw[k * nr + j] * rd[j];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-      g[c * K + k] = s;
-    }
-    __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[w][threadIdx.x];
+    g[c * K + threadIdx.x] = s;
   }
 }
 

@@ -109,6 +109,45 @@ __device__ inline void tile_haar_inv(double* a, double* tmp, int T, int nthreads
   }
 }
 
+// Batched in-place forward full-pyramid Haar over B independent T x T grids
+// (grid b at a + b * T * T); same arithmetic as tile_haar_fwd.
+__device__ inline void batch_tile_haar_fwd(double* a, double* tmp, int T, int B) {
+  const int T2 = T * T, nt = blockDim.x, tid = threadIdx.x;
+  for (int s = T; s >= 2; s >>= 1) {
+    const int h = s >> 1, sh = s * h, ss = s * s;
+    for (int q = tid; q < B * sh; q += nt) {
+      const int b = q / sh, e = q % sh;
+      const int i = e / h, j = e % h;
+      const double* g = a + b * T2;
+      double* o = tmp + b * T2;
+      const double ev = g[i * T + 2 * j], od = g[i * T + 2 * j + 1];
+      o[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+      o[i * T + h + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int q = tid; q < B * ss; q += nt) {
+      const int b = q / ss, e = q % ss;
+      a[b * T2 + (e / s) * T + e % s] = tmp[b * T2 + (e / s) * T + e % s];
+    }
+    __syncthreads();
+    for (int q = tid; q < B * sh; q += nt) {
+      const int b = q / sh, e = q % sh;
+      const int j = e / h, i = e % h;
+      const double* g = a + b * T2;
+      double* o = tmp + b * T2;
+      const double ev = g[(2 * i) * T + j], od = g[(2 * i + 1) * T + j];
+      o[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+      o[(h + i) * T + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int q = tid; q < B * ss; q += nt) {
+      const int b = q / ss, e = q % ss;
+      a[b * T2 + (e / s) * T + e % s] = tmp[b * T2 + (e / s) * T + e % s];
+    }
+    __syncthreads();
+  }
+}
+
 // Batched in-place inverse over B independent T x T grids (grid b at
 // a + b * T * T); same arithmetic as tile_haar_inv, 4 barriers per level for
 // the whole batch. tmp: B * T * T doubles.
@@ -225,6 +264,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// warp-level wait: only lane 0 polls the barrier (with a suspend-time hint),
+// the other lanes park on __syncwarp, so 16+ waiting warps do not flood the
+// SM's barrier unit that also signals TMA transaction completion
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, unsigned parity) {
+  if ((threadIdx.x & 31) == 0) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAITW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, "
+        "%2;\n @!p bra WAITW_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x10000u)
+        : "memory");
+  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {

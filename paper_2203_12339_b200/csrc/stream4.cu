@@ -28,6 +28,7 @@ namespace sss {
 constexpr int kV4Warps = 16;              // consumer warps
 constexpr int kV4TPU = kV4Warps * 32;     // consumer threads (virtual rows)
 constexpr int kV4Slots = 4;
+constexpr int kV4XBufs = 3;               // x band buffers
 constexpr int kV4Threads = kV4TPU + 32;   // + producer warp
 
 struct V4Item {
@@ -71,13 +72,13 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
 
   // shared memory carve-up
   unsigned char* ring = smraw;                                            // kV4Slots * slot_bytes
-  double* xsb = reinterpret_cast<double*>(ring + kV4Slots * slot_bytes);  // 2 x 3 x band_width
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xsb + 6 * band_width);
+  double* xsb = reinterpret_cast<double*>(ring + kV4Slots * slot_bytes);  // kV4XBufs x 3 x band_width
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xsb + kV4XBufs * 3 * band_width);
   uint64_t* full = bars;                  // kV4Slots
   uint64_t* empty = bars + kV4Slots;      // kV4Slots
-  uint64_t* xfull = bars + 2 * kV4Slots;  // 2
-  uint64_t* xempty = xfull + 2;           // 2
-  V4Item* uitems = reinterpret_cast<V4Item*>(xempty + 2);  // the unit's item table
+  uint64_t* xfull = bars + 2 * kV4Slots;  // kV4XBufs
+  uint64_t* xempty = xfull + kV4XBufs;    // kV4XBufs
+  V4Item* uitems = reinterpret_cast<V4Item*>(xempty + kV4XBufs);  // the unit's item table
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   double acc[KMAX][3];
 #pragma unroll
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
   for (int i = tid; i < nitems; i += blockDim.x) uitems[i] = items[unit_item0[unit] + i];
   if (tid == 0) {
     for (int s = 0; s < kV4Slots; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kV4Warps); }
-    for (int j = 0; j < 2; ++j) { mbar_init(&xfull[j], 1); mbar_init(&xempty[j], kV4Warps); }
+    for (int j = 0; j < kV4XBufs; ++j) { mbar_init(&xfull[j], 1); mbar_init(&xempty[j], kV4Warps); }
     fence_mbar_init();
   }
   __syncthreads();
@@ -98,8 +99,8 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
       for (int i = 0; i < nitems; ++i) {
         const V4Item it = uitems[i];
         if (it.band != last_band) {
-          ++bs;  // x band buffer bs & 1, use number bs >> 1
-          const int j = bs & 1, use = bs >> 1;
+          ++bs;  // x band buffer bs % kV4XBufs, use number bs / kV4XBufs
+          const int j = bs % kV4XBufs, use = bs / kV4XBufs;
           if (use >= 1) mbar_wait(&xempty[j], (use - 1) & 1);
           const int c0 = it.band * band_width;
           const int bw = min(band_width, N - c0);
@@ -125,15 +126,15 @@ __global__ void __launch_bounds__(kV4Threads, 1) k_transfer_v4(
       if (it.band != cur_band) {
         if (cur_bs >= 0) {
           __syncwarp();
-          if (lane == 0) mbar_arrive(&xempty[cur_bs & 1]);
+          if (lane == 0) mbar_arrive(&xempty[cur_bs % kV4XBufs]);
         }
         ++cur_bs;
         cur_band = it.band;
-        mbar_wait(&xfull[cur_bs & 1], (cur_bs >> 1) & 1);
-        xs = xsb + (cur_bs & 1) * 3 * band_width;
+        mbar_wait_warp(&xfull[cur_bs % kV4XBufs], (cur_bs / kV4XBufs) & 1);
+        xs = xsb + (cur_bs % kV4XBufs) * 3 * band_width;
       }
       const int s = i % kV4Slots;
-      mbar_wait(&full[s], (i / kV4Slots) & 1);
+      mbar_wait_warp(&full[s], (i / kV4Slots) & 1);
       const unsigned char* item = ring + (size_t)s * slot_bytes;
       const unsigned short* wbase = reinterpret_cast<const unsigned short*>(item);
       const unsigned cnt = wbase[(kV4Warps + 1) + tid];
