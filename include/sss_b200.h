@@ -144,6 +144,20 @@ int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes,
                     const double* material, double* vk, double* scatter, float* radiance,
                     float* radiance_unclamped, void* stream);
 
+/* ---- relight on frame layout v6 (persistent, warp-specialized, merge-path):
+ *      items = (unit, column band[, split]) of entries {u32 (row_local << 4 | k)
+ *      << 11 | band-local col, f32 val} sorted by (row, k, col); every item is
+ *      split evenly over 512 consumer threads; segment partials merge by warp
+ *      affine scans + 16 boundary records into a shared-memory accumulator.
+ *      Layout built by paper_2203_12339_b200/stream6.py. */
+int sss_transfer_v6(int K, int side, int levels, int band_width, int slot_bytes, int units,
+                    int max_unit_items, int max_unit_rows, const int* unit_tile0,
+                    const int* unit_ntiles, const int* unit_item0, const int* unit_nitems,
+                    const void* items, const void* stream_bytes, const double* x, const double* g,
+                    const float* positions, const float* normals, const double* cam,
+                    const double* material, double* vk, double* scatter, float* radiance,
+                    float* radiance_unclamped, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

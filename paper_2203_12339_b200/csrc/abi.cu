@@ -11,6 +11,7 @@
 #include "stream.cu"
 #include "select_cluster.cu"
 #include "stream4.cu"
+#include "stream6.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -299,6 +300,38 @@ int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes,
   else SSS_T4(16)
 #undef SSS_T4
   return check_launch("k_transfer_v4");
+}
+
+int sss_transfer_v6(int K, int side, int levels, int band_width, int slot_bytes, int units,
+                    int max_unit_items, int max_unit_rows, const int* unit_tile0,
+                    const int* unit_ntiles, const int* unit_item0, const int* unit_nitems,
+                    const void* items, const void* stream_bytes, const double* x, const double* g,
+                    const float* positions, const float* normals, const double* cam,
+                    const double* material, double* vk, double* scatter, float* radiance,
+                    float* radiance_unclamped, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (K <= 0 || K > 16 || units <= 0 || max_unit_rows <= 0 || max_unit_rows > 512 || !unit_tile0 ||
+      !unit_ntiles || !unit_item0 || !unit_nitems || !items || !stream_bytes || !x || !g ||
+      !positions || !normals || !cam || !material || !vk || !radiance || !radiance_unclamped)
+    return fail(SSS_EINVAL, "bad transfer_v6 arguments");
+  if (slot_bytes % 16 || reinterpret_cast<uintptr_t>(stream_bytes) % 16 || band_width > 2048 ||
+      (band_width * 8) % 16)
+    return fail(SSS_EINVAL, "transfer_v6: alignment / band width");
+  const int T = 1 << levels, T2 = T * T;
+  const size_t smem = (size_t)sss::kV6Slots * slot_bytes +
+                      3 * (size_t)sss::kV6XBufs * band_width * 8 +
+                      (size_t)max_unit_rows * K * 3 * 8 + 2 * sss::kV6Warps * sizeof(sss::V6Rec) +
+                      (2 * sss::kV6Slots + 2 * sss::kV6XBufs) * 8 +
+                      (size_t)max_unit_items * sizeof(sss::V6Item);
+  const size_t epi = 2 * (size_t)(max_unit_rows / T2 + 1) * 3 * T2 * 8;
+  if (smem > 227 * 1024 || epi > (size_t)sss::kV6Slots * slot_bytes)
+    return fail(SSS_EINVAL, "transfer_v6: shared memory budget exceeded");
+  if (int r = set_smem((const void*)sss::k_transfer_v6, smem)) return r;
+  sss::k_transfer_v6<<<units, sss::kV6Threads, smem, S_(stream)>>>(
+      K, side, levels, band_width, slot_bytes, unit_tile0, unit_ntiles, unit_item0, unit_nitems,
+      reinterpret_cast<const sss::V6Item*>(items), reinterpret_cast<const unsigned char*>(stream_bytes),
+      x, g, positions, normals, cam, material, vk, scatter, radiance, radiance_unclamped);
+  return check_launch("k_transfer_v6");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

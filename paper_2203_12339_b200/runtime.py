@@ -126,8 +126,9 @@ class Scene:
         self.material_buf = torch.empty(7, **f64)
         self.cam_buf = torch.empty(3, **f64)
         self._light_kind = None
-        # "v4" (persistent warp-specialized TMA pipeline) | "stream" | "banded"
-        self.transfer_kernel = "v4"
+        # "v6" (persistent, warp-specialized TMA pipeline, merge-path items)
+        # | "v4" | "stream" | "banded" (earlier layouts, kept for A/B checks)
+        self.transfer_kernel = "v6"
         self._have_cache = False
         self._sequence = 0
         self._graph = None
@@ -226,6 +227,17 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
+        if self.transfer_kernel == "v6":
+            if getattr(t, "v6", None) is None:
+                from .stream6 import build_v6
+
+                t.v6 = build_v6(t)
+            from .stream6 import launch_v6
+
+            launch_v6(t.v6, t, self.x, self.g, self.positions, self.normals, self.cam_buf,
+                      self.material_buf, self.vk, self.scatter, self.radiance,
+                      self.radiance_unclamped, stream)
+            return
         if self.transfer_kernel == "v4":
             if getattr(t, "v4", None) is None:
                 from .stream4 import build_v4

@@ -59,16 +59,15 @@ def main():
         "sss_select_topn", _lib.ptr(sc.ehat), 3, sc.n, keep, _lib.ptr(sc.f2t), _lib.ptr(sc.x),
         _lib.ptr(sc.mask), _lib.ptr(sc.energy), sp), a.reps)
     out["material_weights"] = timed(sc._launch_weights, a.reps)
-    for kern in ("stream", "banded", "v4"):
+    for kern in ("v6", "stream"):
         sc.transfer_kernel = kern
         out[f"transfer_{kern}"] = timed(sc._launch_transfer, a.reps)
-    sc.transfer_kernel = "v4"
-    lay = dt.v4
-    out["v4_units"] = lay.units
-    out["v4_items"] = lay.n_items
-    out["v4_stream_MB"] = lay.stream_bytes / 1e6
-    out["v4_header_MB"] = lay.header_bytes / 1e6
-    out["v4_GBps_stream"] = lay.stream_bytes / (out["transfer_v4"] * 1e-6) / 1e9
+    sc.transfer_kernel = "v6"
+    lay = dt.v6
+    out["v6_units"] = lay.units
+    out["v6_items"] = lay.n_items
+    out["v6_stream_MB"] = lay.stream_bytes / 1e6
+    out["v6_GBps_stream"] = lay.stream_bytes / (out["transfer_v6"] * 1e-6) / 1e9
     out["edit_finish"] = timed(sc._launch_edit, a.reps)
     sc.capture()
     out["relight_graph"] = timed(lambda: sc.replay(False), a.reps)
