@@ -158,6 +158,20 @@ int sss_transfer_v6(int K, int side, int levels, int band_width, int slot_bytes,
                     const double* material, double* vk, double* scatter, float* radiance,
                     float* radiance_unclamped, void* stream);
 
+/* ---- x (3, N) -> packed (N, 4) {x0, x1, x2, 0} doubles (32-byte aligned) */
+int sss_pack_x(const double* x, int n, void* xp, void* stream);
+
+/* ---- relight, v7: warp-per-(row, k) CSR SpMV on the canonical tile-major CSR
+ *      (rowptr / cols / vals as in sss_transfer_relight), CTA = unit_tiles
+ *      tiles with an in-CTA longest-first work list `order` (per CTA,
+ *      R*K u16 = row_local << 4 | k), x packed (sss_pack_x) and gathered
+ *      through L1. Same outputs as sss_transfer_relight. */
+int sss_transfer_csr7(int K, int side, int levels, int unit_tiles, const uint64_t* rowptr,
+                      const uint32_t* cols, const float* vals, const void* order, const void* xp,
+                      const double* g, const float* positions, const float* normals,
+                      const double* cam, const double* material, double* vk, double* scatter,
+                      float* radiance, float* radiance_unclamped, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

@@ -29,6 +29,9 @@ _SIGS = {
     "sss_material_weights": [_P, _P, _I, _I, _P, _P, _P],
     "sss_transfer_relight": [_I, _I, _I, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_band_offsets": [_P, _P, _I, _I, _I, _I, _P, _P],
+    "sss_pack_x": [_P, _I, _P, _P],
+    "sss_transfer_csr7": [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                          _P, _P],
     "sss_transfer_v6": [_I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                         _P, _P, _P, _P, _P, _P, _P],
     "sss_transfer_v4": [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,

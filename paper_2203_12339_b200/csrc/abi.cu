@@ -12,6 +12,7 @@
 #include "select_cluster.cu"
 #include "stream4.cu"
 #include "stream6.cu"
+#include "csr7.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -332,6 +333,34 @@ int sss_transfer_v6(int K, int side, int levels, int band_width, int slot_bytes,
       reinterpret_cast<const sss::V6Item*>(items), reinterpret_cast<const unsigned char*>(stream_bytes),
       x, g, positions, normals, cam, material, vk, scatter, radiance, radiance_unclamped);
   return check_launch("k_transfer_v6");
+}
+
+int sss_pack_x(const double* x, int n, void* xp, void* stream) {
+  if (!x || !xp || n <= 0) return fail(SSS_EINVAL, "bad pack_x arguments");
+  if (reinterpret_cast<uintptr_t>(xp) % 32) return fail(SSS_EINVAL, "xp must be 32-byte aligned");
+  sss::k_pack_x<<<(n + 255) / 256, 256, 0, S_(stream)>>>(x, n, reinterpret_cast<double4*>(xp));
+  return check_launch("k_pack_x");
+}
+
+int sss_transfer_csr7(int K, int side, int levels, int unit_tiles, const uint64_t* rowptr,
+                      const uint32_t* cols, const float* vals, const void* order, const void* xp,
+                      const double* g, const float* positions, const float* normals,
+                      const double* cam, const double* material, double* vk, double* scatter,
+                      float* radiance, float* radiance_unclamped, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (K <= 0 || K > 16 || !rowptr || !cols || !vals || !order || !xp || !g || !positions ||
+      !normals || !cam || !material || !vk || !radiance || !radiance_unclamped)
+    return fail(SSS_EINVAL, "bad transfer_csr7 arguments");
+  const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
+  if (unit_tiles <= 0 || tiles % unit_tiles || unit_tiles * T2 > 4096)
+    return fail(SSS_EINVAL, "transfer_csr7: unit_tiles must divide the tile count (<= 4096 rows)");
+  const size_t smem = 2 * (size_t)unit_tiles * 3 * T2 * sizeof(double);
+  if (int r = set_smem((const void*)sss::k_transfer_csr7, smem)) return r;
+  sss::k_transfer_csr7<<<tiles / unit_tiles, sss::kV7Threads, smem, S_(stream)>>>(
+      K, side, levels, unit_tiles, rowptr, cols, vals,
+      reinterpret_cast<const unsigned short*>(order), reinterpret_cast<const double4*>(xp), g,
+      positions, normals, cam, material, vk, scatter, radiance, radiance_unclamped);
+  return check_launch("k_transfer_csr7");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

@@ -227,6 +227,20 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
+        if self.transfer_kernel == "csr7":
+            if getattr(t, "csr7_order", None) is None:
+                t.csr7_tiles, t.csr7_order = csr7_schedule(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
+            _lib.call("sss_transfer_csr7", self.K, self.side, self.levels, t.csr7_tiles,
+                      _lib.ptr(t.rowptr), _lib.ptr(t.cols), _lib.ptr(t.vals),
+                      _lib.ptr(t.csr7_order), _lib.ptr(self.xp), _lib.ptr(self.g),
+                      _lib.ptr(self.positions), _lib.ptr(self.normals), _lib.ptr(self.cam_buf),
+                      _lib.ptr(self.material_buf), _lib.ptr(self.vk), _lib.ptr(self.scatter),
+                      _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped), sp)
+            return
         if self.transfer_kernel == "v6":
             if getattr(t, "v6", None) is None:
                 from .stream6 import build_v6
@@ -382,6 +396,25 @@ class Scene:
         words = self.mask[c].cpu().numpy().view(np.uint32)
         bits = np.unpackbits(words.view(np.uint8), bitorder="little")[: self.n]
         return np.flatnonzero(bits).astype(np.uint32)
+
+
+def csr7_schedule(t: DeviceTransfer, rows_per_cta: int = 256):
+    """Per-CTA longest-first (row, k) work lists for sss_transfer_csr7."""
+    T2 = (1 << t.levels) ** 2
+    ntiles = t.n // T2
+    G = max(1, min(ntiles, rows_per_cta // T2))
+    while ntiles % G:
+        G -= 1
+    R = G * T2
+    rp = t.rowptr.cpu().numpy()
+    seg = (rp[:, 1:] - rp[:, :-1]).T  # (n, K) segment lengths
+    ctas = ntiles // G
+    order = np.empty((ctas, R * t.K), np.uint16)
+    for c in range(ctas):
+        lens = seg[c * R:(c + 1) * R].reshape(-1)  # index = row_local * K + k
+        o = np.argsort(-lens, kind="stable")
+        order[c] = ((o // t.K) << 4) | (o % t.K)
+    return G, torch.as_tensor(order.view(np.int16), device=t.rowptr.device)
 
 
 def bench(scene: Scene, iterations: int = 20) -> dict:
