@@ -172,6 +172,16 @@ int sss_transfer_csr7(int K, int side, int levels, int unit_tiles, const uint64_
                       const double* cam, const double* material, double* vk, double* scatter,
                       float* radiance, float* radiance_unclamped, void* stream);
 
+/* ---- transfer, v8: persistent merge-path CSR SpMV. pieces = {u32 start, u32
+ *      len, u32 row*16+k, pad} cut from the (row, k)-ordered segments of the
+ *      canonical CSR; warp w processes pieces [warp_begin[w], warp_begin[w+1]).
+ *      Zeroes vk (K, 3, n_rows) and accumulates it with red.global.add.f64;
+ *      follow with sss_edit_finish for recombine + inverse + shade. n_warps is
+ *      a multiple of 8. */
+int sss_transfer_csr8(int K, int n_rows, const uint32_t* cols, const float* vals,
+                      const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                      double* vk, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

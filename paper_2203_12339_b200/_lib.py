@@ -30,6 +30,7 @@ _SIGS = {
     "sss_transfer_relight": [_I, _I, _I, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_band_offsets": [_P, _P, _I, _I, _I, _I, _P, _P],
     "sss_pack_x": [_P, _I, _P, _P],
+    "sss_transfer_csr8": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
     "sss_transfer_csr7": [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                           _P, _P],
     "sss_transfer_v6": [_I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,

@@ -13,6 +13,7 @@
 #include "stream4.cu"
 #include "stream6.cu"
 #include "csr7.cu"
+#include "csr8.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -361,6 +362,20 @@ int sss_transfer_csr7(int K, int side, int levels, int unit_tiles, const uint64_
       reinterpret_cast<const unsigned short*>(order), reinterpret_cast<const double4*>(xp), g,
       positions, normals, cam, material, vk, scatter, radiance, radiance_unclamped);
   return check_launch("k_transfer_csr7");
+}
+
+int sss_transfer_csr8(int K, int n_rows, const uint32_t* cols, const float* vals,
+                      const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                      double* vk, void* stream) {
+  if (K <= 0 || n_rows <= 0 || !cols || !vals || !pieces || !warp_begin || !xp || !vk ||
+      n_warps <= 0 || n_warps % (sss::kV8Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_csr8 arguments");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  sss::k_transfer_csr8<<<n_warps / (sss::kV8Threads / 32), sss::kV8Threads, 0, S_(stream)>>>(
+      n_rows, cols, vals, reinterpret_cast<const sss::V8Piece*>(pieces), warp_begin,
+      reinterpret_cast<const double4*>(xp), vk);
+  return check_launch("k_transfer_csr8");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

@@ -227,6 +227,18 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
+        if self.transfer_kernel == "csr8":
+            if getattr(t, "csr8", None) is None:
+                t.csr8 = csr8_schedule(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            pieces, wbeg, W = t.csr8
+            _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
+            _lib.call("sss_transfer_csr8", self.K, self.n, _lib.ptr(t.cols), _lib.ptr(t.vals),
+                      _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
         if self.transfer_kernel == "csr7":
             if getattr(t, "csr7_order", None) is None:
                 t.csr7_tiles, t.csr7_order = csr7_schedule(t)
@@ -398,8 +410,12 @@ class Scene:
         return np.flatnonzero(bits).astype(np.uint32)
 
 
-def csr7_schedule(t: DeviceTransfer, rows_per_cta: int = 256):
+def csr7_schedule(t: DeviceTransfer, rows_per_cta: int = None):
     """Per-CTA longest-first (row, k) work lists for sss_transfer_csr7."""
+    if rows_per_cta is None:
+        import os
+
+        rows_per_cta = int(os.environ.get("SSS_CSR7_ROWS", "64"))
     T2 = (1 << t.levels) ** 2
     ntiles = t.n // T2
     G = max(1, min(ntiles, rows_per_cta // T2))
@@ -415,6 +431,41 @@ def csr7_schedule(t: DeviceTransfer, rows_per_cta: int = 256):
         o = np.argsort(-lens, kind="stable")
         order[c] = ((o // t.K) << 4) | (o % t.K)
     return G, torch.as_tensor(order.view(np.int16), device=t.rowptr.device)
+
+
+def csr8_schedule(t: DeviceTransfer, split: int = None, warps_per_sm: int = None):
+    """(row, k)-ordered segment pieces cut into entry-balanced contiguous
+    per-warp ranges for sss_transfer_csr8."""
+    import os
+
+    split = split or int(os.environ.get("SSS_CSR8_SPLIT", "2048"))
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_CSR8_WPS", "48"))
+    dev = t.rowptr.device
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    W = nsm * warps_per_sm
+    W -= W % 8
+    rp = t.rowptr.cpu().numpy()
+    starts = rp[:, :-1].T.reshape(-1)  # (row, k) order
+    lens = (rp[:, 1:] - rp[:, :-1]).T.reshape(-1)
+    rowk = (np.arange(t.n)[:, None] * 16 + np.arange(t.K)[None, :]).reshape(-1)
+    keep = lens > 0
+    starts, lens, rowk = starts[keep], lens[keep], rowk[keep]
+    npc = (lens + split - 1) // split
+    rep = np.repeat(np.arange(lens.size), npc)
+    j = np.arange(rep.size) - np.repeat(np.cumsum(npc) - npc, npc)
+    p_start = starts[rep] + j * split
+    p_len = np.minimum(split, lens[rep] - j * split)
+    p_rowk = rowk[rep]
+    cum = np.concatenate([[0], np.cumsum(p_len)])
+    targets = np.arange(W + 1) * (cum[-1] / W)
+    wbeg = np.searchsorted(cum, targets, side="left").astype(np.uint32)
+    wbeg[-1] = p_len.size
+    pieces = np.zeros((p_len.size, 4), np.uint32)
+    pieces[:, 0] = p_start
+    pieces[:, 1] = p_len
+    pieces[:, 2] = p_rowk
+    return (torch.as_tensor(pieces.view(np.int32), device=dev),
+            torch.as_tensor(wbeg.view(np.int32), device=dev), W)
 
 
 def bench(scene: Scene, iterations: int = 20) -> dict:
