@@ -182,6 +182,20 @@ int sss_transfer_csr8(int K, int n_rows, const uint32_t* cols, const float* vals
                       const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
                       double* vk, void* stream);
 
+/* ---- padded copy of the canonical CSR for v9: segment i (seg_src[i],
+ *      seg_len[i]) copied to seg_dst[i] (multiple of 4) and padded to a
+ *      multiple of 4 entries with (col 0, val 0). */
+int sss_pad_segments(const uint64_t* seg_src, const uint32_t* seg_len, const uint64_t* seg_dst,
+                     long long nseg, const uint32_t* cols, const float* vals, uint32_t* pcols,
+                     float* pvals, void* stream);
+
+/* ---- transfer, v9: as sss_transfer_csr8 on the padded arrays, pieces {u32
+ *      start (multiple of 4), u32 len (multiple of 4), u32 row*16+k, pad};
+ *      4 pieces per warp in flight (8-lane groups, 16-byte vector loads). */
+int sss_transfer_csr9(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                      const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                      double* vk, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

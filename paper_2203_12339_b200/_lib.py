@@ -31,6 +31,8 @@ _SIGS = {
     "sss_band_offsets": [_P, _P, _I, _I, _I, _I, _P, _P],
     "sss_pack_x": [_P, _I, _P, _P],
     "sss_transfer_csr8": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
+    "sss_pad_segments": [_P, _P, _P, C.c_longlong, _P, _P, _P, _P, _P],
+    "sss_transfer_csr9": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
     "sss_transfer_csr7": [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                           _P, _P],
     "sss_transfer_v6": [_I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,

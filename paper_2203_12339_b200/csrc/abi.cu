@@ -14,6 +14,7 @@
 #include "stream6.cu"
 #include "csr7.cu"
 #include "csr8.cu"
+#include "csr9.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -376,6 +377,35 @@ int sss_transfer_csr8(int K, int n_rows, const uint32_t* cols, const float* vals
       n_rows, cols, vals, reinterpret_cast<const sss::V8Piece*>(pieces), warp_begin,
       reinterpret_cast<const double4*>(xp), vk);
   return check_launch("k_transfer_csr8");
+}
+
+int sss_pad_segments(const uint64_t* seg_src, const uint32_t* seg_len, const uint64_t* seg_dst,
+                     long long nseg, const uint32_t* cols, const float* vals, uint32_t* pcols,
+                     float* pvals, void* stream) {
+  if (!seg_src || !seg_len || !seg_dst || nseg < 0 || !cols || !vals || !pcols || !pvals)
+    return fail(SSS_EINVAL, "bad pad_segments arguments");
+  if (nseg == 0) return SSS_OK;
+  sss::k_pad_segments<<<(unsigned)((nseg + 7) / 8), 256, 0, S_(stream)>>>(seg_src, seg_len, seg_dst,
+                                                                          nseg, cols, vals, pcols,
+                                                                          pvals);
+  return check_launch("k_pad_segments");
+}
+
+int sss_transfer_csr9(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                      const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                      double* vk, void* stream) {
+  if (K <= 0 || n_rows <= 0 || !pcols || !pvals || !pieces || !warp_begin || !xp || !vk ||
+      n_warps <= 0 || n_warps % (sss::kV9Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_csr9 arguments");
+  if (reinterpret_cast<uintptr_t>(pcols) % 16 || reinterpret_cast<uintptr_t>(pvals) % 16)
+    return fail(SSS_EINVAL, "transfer_csr9: padded arrays must be 16-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  sss::k_transfer_csr9<<<n_warps / (sss::kV9Threads / 32), sss::kV9Threads, 0, S_(stream)>>>(
+      n_rows, reinterpret_cast<const uint4*>(pcols), reinterpret_cast<const float4*>(pvals),
+      reinterpret_cast<const sss::V9Piece*>(pieces), warp_begin,
+      reinterpret_cast<const double4*>(xp), vk);
+  return check_launch("k_transfer_csr9");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

@@ -227,6 +227,18 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
+        if self.transfer_kernel == "csr9":
+            if getattr(t, "csr9", None) is None:
+                t.csr9 = csr9_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            pcols, pvals, pieces, wbeg, W = t.csr9
+            _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
+            _lib.call("sss_transfer_csr9", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals),
+                      _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
         if self.transfer_kernel == "csr8":
             if getattr(t, "csr8", None) is None:
                 t.csr8 = csr8_schedule(t)
@@ -465,6 +477,52 @@ def csr8_schedule(t: DeviceTransfer, split: int = None, warps_per_sm: int = None
     pieces[:, 1] = p_len
     pieces[:, 2] = p_rowk
     return (torch.as_tensor(pieces.view(np.int32), device=dev),
+            torch.as_tensor(wbeg.view(np.int32), device=dev), W)
+
+
+def csr9_layout(t: DeviceTransfer, split: int = None, warps_per_sm: int = None):
+    """Padded (multiple-of-4) segment copy + balanced per-warp piece ranges for
+    sss_transfer_csr9. Pieces follow (row, k) order (x locality)."""
+    import os
+
+    split = split or int(os.environ.get("SSS_CSR9_SPLIT", "1024"))
+    split -= split % 4
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_CSR9_WPS", "32"))
+    dev = t.rowptr.device
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    W = nsm * warps_per_sm
+    W -= W % 8
+    rp = t.rowptr.cpu().numpy()
+    starts = rp[:, :-1].T.reshape(-1)  # (row, k) order
+    lens = (rp[:, 1:] - rp[:, :-1]).T.reshape(-1)
+    rowk = (np.arange(t.n)[:, None] * 16 + np.arange(t.K)[None, :]).reshape(-1)
+    keep = lens > 0
+    starts, lens, rowk = starts[keep], lens[keep], rowk[keep]
+    lens4 = (lens + 3) // 4 * 4
+    dst = np.zeros(lens.size, np.int64)
+    np.cumsum(lens4[:-1], out=dst[1:])
+    total = int(lens4.sum())
+    pcols = torch.empty(max(total, 4), dtype=torch.int32, device=dev)
+    pvals = torch.empty(max(total, 4), dtype=torch.float32, device=dev)
+    _lib.call("sss_pad_segments", _lib.ptr(torch.as_tensor(starts.astype(np.int64), device=dev)),
+              _lib.ptr(torch.as_tensor(lens.astype(np.int32), device=dev)),
+              _lib.ptr(torch.as_tensor(dst, device=dev)), int(lens.size), _lib.ptr(t.cols),
+              _lib.ptr(t.vals), _lib.ptr(pcols), _lib.ptr(pvals), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    npc = (lens4 + split - 1) // split
+    rep = np.repeat(np.arange(lens4.size), npc)
+    j = np.arange(rep.size) - np.repeat(np.cumsum(npc) - npc, npc)
+    p_start = dst[rep] + j * split
+    p_len = np.minimum(split, lens4[rep] - j * split)
+    cum = np.concatenate([[0], np.cumsum(p_len)])
+    targets = np.arange(W + 1) * (cum[-1] / W)
+    wbeg = np.searchsorted(cum, targets, side="left").astype(np.uint32)
+    wbeg[-1] = p_len.size
+    pieces = np.zeros((p_len.size, 4), np.uint32)
+    pieces[:, 0] = p_start
+    pieces[:, 1] = p_len
+    pieces[:, 2] = rowk[rep]
+    return (pcols, pvals, torch.as_tensor(pieces.view(np.int32), device=dev),
             torch.as_tensor(wbeg.view(np.int32), device=dev), W)
 
 

@@ -330,7 +330,7 @@ def test_stream_and_banded_kernels_agree(c1):
     sc.transfer_kernel = "banded"
     a = sc.relight()
     vk_a = sc.vk.clone()
-    for kern in ("stream", "v4", "v6", "csr7", "csr8"):
+    for kern in ("stream", "v4", "v6", "csr7", "csr8", "csr9"):
         sc.transfer_kernel = kern
         b = sc.relight()
         assert (sc.vk - vk_a).abs().max().item() <= 1e-12 * vk_a.abs().max().item(), kern

@@ -59,7 +59,7 @@ def main():
         "sss_select_topn", _lib.ptr(sc.ehat), 3, sc.n, keep, _lib.ptr(sc.f2t), _lib.ptr(sc.x),
         _lib.ptr(sc.mask), _lib.ptr(sc.energy), sp), a.reps)
     out["material_weights"] = timed(sc._launch_weights, a.reps)
-    for kern in ("csr8", "csr7", "v6"):
+    for kern in ("csr9", "csr8", "csr7", "v6"):
         sc.transfer_kernel = kern
         out[f"transfer_{kern}"] = timed(sc._launch_transfer, a.reps)
     sc.transfer_kernel = "v6"
