@@ -504,11 +504,16 @@ def csr9_layout(t: DeviceTransfer, split: int = None, warps_per_sm: int = None):
     total = int(lens4.sum())
     pcols = torch.empty(max(total, 4), dtype=torch.int32, device=dev)
     pvals = torch.empty(max(total, 4), dtype=torch.float32, device=dev)
-    _lib.call("sss_pad_segments", _lib.ptr(torch.as_tensor(starts.astype(np.int64), device=dev)),
-              _lib.ptr(torch.as_tensor(lens.astype(np.int32), device=dev)),
-              _lib.ptr(torch.as_tensor(dst, device=dev)), int(lens.size), _lib.ptr(t.cols),
-              _lib.ptr(t.vals), _lib.ptr(pcols), _lib.ptr(pvals), _lib.stream_ptr())
+    # keep the staging tensors referenced until the kernel has consumed them
+    # (a temporary freed before launch can be recycled by the next allocation)
+    d_src = torch.as_tensor(starts.astype(np.int64), device=dev)
+    d_len = torch.as_tensor(lens.astype(np.int32), device=dev)
+    d_dst = torch.as_tensor(dst, device=dev)
+    _lib.call("sss_pad_segments", _lib.ptr(d_src), _lib.ptr(d_len), _lib.ptr(d_dst),
+              int(lens.size), _lib.ptr(t.cols), _lib.ptr(t.vals), _lib.ptr(pcols), _lib.ptr(pvals),
+              _lib.stream_ptr())
     torch.cuda.synchronize()
+    del d_src, d_len, d_dst
     npc = (lens4 + split - 1) // split
     rep = np.repeat(np.arange(lens4.size), npc)
     j = np.arange(rep.size) - np.repeat(np.cumsum(npc) - npc, npc)
