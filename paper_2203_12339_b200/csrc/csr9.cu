@@ -23,15 +23,18 @@ struct V9Piece {
   unsigned pad;
 };
 
+// one 256-bit read-only load (LDG.E.ENL2.256 on sm_100a): the packed
+// {x0, x1, x2, 0} of a column in a single L1 request
 __device__ __forceinline__ void v9_acc(const double4* __restrict__ xp, uint32_t c, float v,
                                        double& a0, double& a1, double& a2) {
-  const double2* q = reinterpret_cast<const double2*>(xp + c);
-  const double2 a = __ldg(q);
-  const double b = __ldg(reinterpret_cast<const double*>(q + 1));
+  double x0, x1, x2, x3;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3)
+               : "l"(xp + c));
   const double dv = (double)v;
-  a0 = fma(dv, a.x, a0);
-  a1 = fma(dv, a.y, a1);
-  a2 = fma(dv, b, a2);
+  a0 = fma(dv, x0, a0);
+  a1 = fma(dv, x1, a1);
+  a2 = fma(dv, x2, a2);
 }
 
 __global__ void __launch_bounds__(kV9Threads) k_transfer_csr9(
