@@ -196,6 +196,68 @@ int sss_transfer_csr9(int K, int n_rows, const uint32_t* pcols, const float* pva
                       const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
                       double* vk, void* stream);
 
+/* ---- transfer v10: K-packed (row, column) pairs. meta[p] = column (24 bits)
+ * | k-mask (8 bits) << 24; vals holds the f32 coefficients of the terms in
+ * the mask (k ascending), pair after pair. pieces = {pair0, npair, val0, row}
+ * (uint32 x4), warp_begin (n_warps + 1) balanced ranges. Requires K <= 8 and
+ * n_rows <= 2^24. Zeroes and fills vk; shade with sss_edit_finish. Same
+ * contract as sss_transfer_csr9 (runtime.py:148-153). */
+int sss_transfer_kpack(int K, int n_rows, const uint32_t* meta, const float* vals,
+                       const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                       double* vk, void* stream);
+
+/* ---- transfer v11: the v10 layout with a cp.async software pipeline (meta two
+ * steps ahead, values one step ahead, x gathers one step ahead); pairs_per_lane
+ * 2 or 4. n_warps a multiple of 4. Same contract as sss_transfer_kpack. */
+int sss_transfer_kpack_pipe(int K, int n_rows, const uint32_t* meta, const float* vals,
+                            const void* pieces, const unsigned* warp_begin, int n_warps,
+                            int pairs_per_lane, const void* xp, double* vk, void* stream);
+
+/* ---- transfer v12: mask-sorted K-fused warp steps. steps (uint32 x4 each):
+ * {pair0, val0, row, kmask | count << 8 | row_end << 16}; cols[pair0 + l]
+ * (l < count) = tile-major columns; for every k in kmask (ascending) 32 f32
+ * values at vals[val0 + j * 32 + l] (j = rank of k in kmask, 0 where pair l
+ * lacks term k). Steps of a row are consecutive; warp_begin (n_warps + 1)
+ * gives each warp a contiguous step range. K <= 8, n_warps a multiple of 4.
+ * Zeroes and fills vk; shade with sss_edit_finish (runtime.py:148-153). */
+int sss_transfer_kstep(int K, int n_rows, const uint32_t* cols, const float* vals,
+                       const void* steps, const unsigned* warp_begin, int n_warps, const void* xp,
+                       double* vk, void* stream);
+
+/* ---- transfer v13: the v12 warp steps as contiguous blobs, TMA-streamed.
+ * blob: per step [32 u32 tile-major columns (0-padded) | popc(kmask) x 32 f32
+ * values, k ascending, lane order], 16-byte aligned; recs (uint32 x4 per step)
+ * {blob offset in 16-byte units, row, kmask | count << 8 | row_end << 16, 0};
+ * steps of a row consecutive, warp_begin (n_warps + 1) contiguous per-warp
+ * ranges. depth = steps in flight per warp (4, 8 or 12). K <= 8, n_warps a
+ * multiple of 8. Zeroes and fills vk; shade with sss_edit_finish. */
+int sss_transfer_kstream(int K, int n_rows, const void* blob, const void* recs,
+                         const unsigned* warp_begin, int n_warps, int depth, const void* xp,
+                         double* vk, void* stream);
+
+/* ---- packed x (n, 4) doubles {x0, x1, x2, 0} + kept-column bitmap: bit c of
+ * bits ((n + 31) / 32 words) set iff any channel of x[:, c] is nonzero. */
+int sss_pack_x_bits(const double* x, int n, void* xp, uint32_t* bits, void* stream);
+
+/* ---- sss_transfer_csr9 visiting only kept columns (bits from
+ * sss_pack_x_bits): entries whose column is not kept issue no x gather and
+ * no FMA, like the reference's csc_apply over the kept columns
+ * (transfer.py:66-71). Same v_k bit for bit. */
+int sss_transfer_csr9s(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                       const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                       const uint32_t* bits, double* vk, void* stream);
+
+/* ---- transfer v14: K-packed pairs (meta = column | k-mask << 24, values of
+ * the present terms, k ascending) with every row padded to a multiple of 32
+ * pairs (meta 0 = empty); pieces (uint32 x4 each) = {pair0, npair, val0, row}
+ * runs of <= split pairs of one row (multiples of 32); warp_begin
+ * (n_warps + 1) contiguous per-warp piece ranges; bits = kept-column bitmap
+ * from sss_pack_x_bits. Zeroes and fills vk; shade with sss_edit_finish
+ * (runtime.py:148-153). K <= 8. */
+int sss_transfer_kgroup(int K, int n_rows, const uint32_t* meta, const float* vals,
+                        const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                        const uint32_t* bits, double* vk, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

@@ -33,6 +33,13 @@ _SIGS = {
     "sss_transfer_csr8": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
     "sss_pad_segments": [_P, _P, _P, C.c_longlong, _P, _P, _P, _P, _P],
     "sss_transfer_csr9": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
+    "sss_transfer_kpack": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
+    "sss_transfer_kstep": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
+    "sss_pack_x_bits": [_P, _I, _P, _P, _P],
+    "sss_transfer_kgroup": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
+    "sss_transfer_csr9s": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
+    "sss_transfer_kstream": [_I, _I, _P, _P, _P, _I, _I, _P, _P, _P],
+    "sss_transfer_kpack_pipe": [_I, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P],
     "sss_transfer_csr7": [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                           _P, _P],
     "sss_transfer_v6": [_I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,

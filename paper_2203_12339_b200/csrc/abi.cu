@@ -15,6 +15,10 @@
 #include "csr7.cu"
 #include "csr8.cu"
 #include "csr9.cu"
+#include "kpack10.cu"
+#include "kstep12.cu"
+#include "kstream13.cu"
+#include "kgroup14.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -406,6 +410,146 @@ int sss_transfer_csr9(int K, int n_rows, const uint32_t* pcols, const float* pva
       reinterpret_cast<const sss::V9Piece*>(pieces), warp_begin,
       reinterpret_cast<const double4*>(xp), vk);
   return check_launch("k_transfer_csr9");
+}
+
+int sss_transfer_kpack(int K, int n_rows, const uint32_t* meta, const float* vals,
+                       const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                       double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || n_rows > (1 << 24) || !meta || !vals || !pieces ||
+      !warp_begin || !xp || !vk || n_warps <= 0 || n_warps % (sss::kV10Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_kpack arguments");
+  if (reinterpret_cast<uintptr_t>(meta) % 16)
+    return fail(SSS_EINVAL, "transfer_kpack: meta must be 16-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const unsigned grid = n_warps / (sss::kV10Threads / 32);
+  const auto* pc = reinterpret_cast<const sss::V10Piece*>(pieces);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+  const auto* m4 = reinterpret_cast<const uint4*>(meta);
+  if (K <= 4)
+    sss::k_transfer_kpack<4><<<grid, sss::kV10Threads, 0, S_(stream)>>>(K, n_rows, m4, vals, pc,
+                                                                       warp_begin, x4, vk);
+  else
+    sss::k_transfer_kpack<8><<<grid, sss::kV10Threads, 0, S_(stream)>>>(K, n_rows, m4, vals, pc,
+                                                                       warp_begin, x4, vk);
+  return check_launch("k_transfer_kpack");
+}
+
+int sss_transfer_kpack_pipe(int K, int n_rows, const uint32_t* meta, const float* vals,
+                            const void* pieces, const unsigned* warp_begin, int n_warps,
+                            int pairs_per_lane, const void* xp, double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || n_rows > (1 << 24) || !meta || !vals || !pieces ||
+      !warp_begin || !xp || !vk || n_warps <= 0 || n_warps % (sss::kV11Threads / 32) ||
+      (pairs_per_lane != 2 && pairs_per_lane != 4))
+    return fail(SSS_EINVAL, "bad transfer_kpack_pipe arguments");
+  if (reinterpret_cast<uintptr_t>(meta) % 16)
+    return fail(SSS_EINVAL, "transfer_kpack_pipe: meta must be 16-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const unsigned grid = n_warps / (sss::kV11Threads / 32);
+  const auto* pc = reinterpret_cast<const sss::V10Piece*>(pieces);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+#define SSS_KP(KM, PP)                                                                     \
+  sss::k_transfer_kpack_pipe<KM, PP><<<grid, sss::kV11Threads, 0, S_(stream)>>>(K, n_rows, meta, \
+                                                                               vals, pc,   \
+                                                                               warp_begin, \
+                                                                               x4, vk)
+  if (K <= 4) {
+    if (pairs_per_lane == 4) SSS_KP(4, 4); else SSS_KP(4, 2);
+  } else {
+    if (pairs_per_lane == 4) SSS_KP(8, 4); else SSS_KP(8, 2);
+  }
+#undef SSS_KP
+  return check_launch("k_transfer_kpack_pipe");
+}
+
+int sss_transfer_kstep(int K, int n_rows, const uint32_t* cols, const float* vals,
+                       const void* steps, const unsigned* warp_begin, int n_warps, const void* xp,
+                       double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || !cols || !vals || !steps || !warp_begin || !xp || !vk ||
+      n_warps <= 0 || n_warps % (sss::kV12Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_kstep arguments");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  sss::k_transfer_kstep<<<n_warps / (sss::kV12Threads / 32), sss::kV12Threads, 0, S_(stream)>>>(
+      K, n_rows, cols, vals, reinterpret_cast<const uint4*>(steps), warp_begin,
+      reinterpret_cast<const double4*>(xp), vk);
+  return check_launch("k_transfer_kstep");
+}
+
+int sss_transfer_kstream(int K, int n_rows, const void* blob, const void* recs,
+                         const unsigned* warp_begin, int n_warps, int depth, const void* xp,
+                         double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || !blob || !recs || !warp_begin || !xp || !vk ||
+      n_warps <= 0 || n_warps % (sss::kV13Threads / 32) || (depth != 4 && depth != 8 && depth != 12))
+    return fail(SSS_EINVAL, "bad transfer_kstream arguments");
+  if (reinterpret_cast<uintptr_t>(blob) % 16 || reinterpret_cast<uintptr_t>(recs) % 16 ||
+      reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_kstream: blob/recs 16-byte and xp 32-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const unsigned grid = n_warps / (sss::kV13Threads / 32);
+  const auto* b8 = reinterpret_cast<const uint8_t*>(blob);
+  const auto* r4 = reinterpret_cast<const uint4*>(recs);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+#define SSS_KS(DD, GG)                                                                             \
+  do {                                                                                             \
+    const size_t smem = (sss::kV13Threads / 32) * sss::V13Smem<DD, GG>::per_warp;                  \
+    const void* fn = (const void*)sss::k_transfer_kstream<DD, GG>;                                 \
+    if (int r = set_smem(fn, smem)) return r;                                                      \
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                 \
+    sss::k_transfer_kstream<DD, GG><<<grid, sss::kV13Threads, smem, S_(stream)>>>(                 \
+        K, n_rows, b8, r4, warp_begin, x4, vk);                                                    \
+  } while (0)
+  if (depth == 4) SSS_KS(4, 2);
+  else if (depth == 8) SSS_KS(8, 3);
+  else SSS_KS(12, 4);
+#undef SSS_KS
+  return check_launch("k_transfer_kstream");
+}
+
+int sss_pack_x_bits(const double* x, int n, void* xp, uint32_t* bits, void* stream) {
+  if (!x || !xp || !bits || n <= 0) return fail(SSS_EINVAL, "bad pack_x_bits arguments");
+  if (reinterpret_cast<uintptr_t>(xp) % 32) return fail(SSS_EINVAL, "xp must be 32-byte aligned");
+  sss::k_pack_x_bits<<<(n + 255) / 256, 256, 0, S_(stream)>>>(x, n, reinterpret_cast<double4*>(xp),
+                                                             bits);
+  return check_launch("k_pack_x_bits");
+}
+
+int sss_transfer_csr9s(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                       const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                       const uint32_t* bits, double* vk, void* stream) {
+  if (K <= 0 || n_rows <= 0 || !pcols || !pvals || !pieces || !warp_begin || !xp || !bits || !vk ||
+      n_warps <= 0 || n_warps % (sss::kV9Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_csr9s arguments");
+  if (reinterpret_cast<uintptr_t>(pcols) % 16 || reinterpret_cast<uintptr_t>(pvals) % 16)
+    return fail(SSS_EINVAL, "transfer_csr9s: padded arrays must be 16-byte aligned");
+  const size_t smem = (size_t)((n_rows + 31) / 32) * 4;
+  if (int r = set_smem((const void*)sss::k_transfer_csr9s, smem)) return r;
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  sss::k_transfer_csr9s<<<n_warps / (sss::kV9Threads / 32), sss::kV9Threads, smem, S_(stream)>>>(
+      n_rows, reinterpret_cast<const uint4*>(pcols), reinterpret_cast<const float4*>(pvals),
+      reinterpret_cast<const sss::V9Piece*>(pieces), warp_begin,
+      reinterpret_cast<const double4*>(xp), bits, vk);
+  return check_launch("k_transfer_csr9s");
+}
+
+int sss_transfer_kgroup(int K, int n_rows, const uint32_t* meta, const float* vals,
+                        const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
+                        const uint32_t* bits, double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || n_rows > (1 << 24) || !meta || !vals || !pieces ||
+      !warp_begin || !xp || !bits || !vk || n_warps <= 0 || n_warps % (sss::kV14Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_kgroup arguments");
+  if (reinterpret_cast<uintptr_t>(xp) % 32) return fail(SSS_EINVAL, "xp must be 32-byte aligned");
+  const size_t smem = (size_t)((n_rows + 31) / 32) * 4;
+  if (int r = set_smem((const void*)sss::k_transfer_kgroup, smem)) return r;
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  sss::k_transfer_kgroup<<<n_warps / (sss::kV14Threads / 32), sss::kV14Threads, smem, S_(stream)>>>(
+      K, n_rows, meta, vals, reinterpret_cast<const sss::V14Row*>(pieces), warp_begin,
+      reinterpret_cast<const double4*>(xp), bits, vk);
+  return check_launch("k_transfer_kgroup");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

@@ -87,6 +87,81 @@ __global__ void __launch_bounds__(kV9Threads) k_transfer_csr9(
   }
 }
 
+// csr9 with selection skip: the packed x comes with a tile-major bitmap of
+// the columns some channel keeps (x != 0); it is staged in shared memory and
+// an entry whose column is not kept issues no gather and no FMA (its
+// contribution is an exact zero, so v_k is unchanged bit for bit). The
+// reference's csc_apply only visits kept columns (transfer.py:66-71); this is
+// the row-major equivalent.
+__device__ __forceinline__ void v9s_acc(const double4* __restrict__ xp, const uint32_t* sbits,
+                                        uint32_t c, float v, double& a0, double& a1, double& a2) {
+  if ((sbits[c >> 5] >> (c & 31u)) & 1u) v9_acc(xp, c, v, a0, a1, a2);
+}
+
+__global__ void __launch_bounds__(kV9Threads) k_transfer_csr9s(
+    int N, const uint4* __restrict__ cols4, const float4* __restrict__ vals4,
+    const V9Piece* __restrict__ pieces, const unsigned* __restrict__ warp_begin,
+    const double4* __restrict__ xp, const uint32_t* __restrict__ bits, double* __restrict__ vk) {
+  extern __shared__ uint32_t sbits[];
+  const int nw = (N + 31) >> 5;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) sbits[i] = bits[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned b = warp_begin[w], e_end = warp_begin[w + 1];
+  const unsigned rounds = (e_end - b + 3) / 4;
+  for (unsigned r = 0; r < rounds; ++r) {
+    const unsigned pi = b + r * 4 + grp;
+    const bool act = pi < e_end;
+    V9Piece pc = {0u, 0u, 0u, 0u};
+    if (act) pc = pieces[pi];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const unsigned q0 = pc.start >> 2, qn = pc.len4 >> 2;
+    unsigned q = gl;
+    for (; q + 8 < qn; q += 16) {
+      const uint4 c0 = __ldg(&cols4[q0 + q]), c1 = __ldg(&cols4[q0 + q + 8]);
+      const float4 v0 = __ldg(&vals4[q0 + q]), v1 = __ldg(&vals4[q0 + q + 8]);
+      v9s_acc(xp, sbits, c0.x, v0.x, a0, a1, a2); v9s_acc(xp, sbits, c0.y, v0.y, a0, a1, a2);
+      v9s_acc(xp, sbits, c0.z, v0.z, a0, a1, a2); v9s_acc(xp, sbits, c0.w, v0.w, a0, a1, a2);
+      v9s_acc(xp, sbits, c1.x, v1.x, a0, a1, a2); v9s_acc(xp, sbits, c1.y, v1.y, a0, a1, a2);
+      v9s_acc(xp, sbits, c1.z, v1.z, a0, a1, a2); v9s_acc(xp, sbits, c1.w, v1.w, a0, a1, a2);
+    }
+    if (q < qn) {
+      const uint4 c0 = __ldg(&cols4[q0 + q]);
+      const float4 v0 = __ldg(&vals4[q0 + q]);
+      v9s_acc(xp, sbits, c0.x, v0.x, a0, a1, a2); v9s_acc(xp, sbits, c0.y, v0.y, a0, a1, a2);
+      v9s_acc(xp, sbits, c0.z, v0.z, a0, a1, a2); v9s_acc(xp, sbits, c0.w, v0.w, a0, a1, a2);
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (act && gl == 0) {
+      const int row = (int)(pc.rowk >> 4), k = (int)(pc.rowk & 15u);
+      double* vo = vk + (size_t)k * 3 * N;
+      atomicAdd(&vo[row], a0);
+      atomicAdd(&vo[N + row], a1);
+      atomicAdd(&vo[2 * N + row], a2);
+    }
+  }
+}
+
+// packed x + kept-column bitmap (bit c of bits set iff any channel of x[:, c]
+// is nonzero); n a multiple of 32
+__global__ void k_pack_x_bits(const double* __restrict__ x, int N, double4* __restrict__ xp,
+                              uint32_t* __restrict__ bits) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double a = 0.0, b = 0.0, c = 0.0;
+  if (i < N) {
+    a = x[i]; b = x[N + i]; c = x[2 * N + i];
+    xp[i] = make_double4(a, b, c, 0.0);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, i < N && (a != 0.0 || b != 0.0 || c != 0.0));
+  if ((threadIdx.x & 31) == 0 && i < N) bits[i >> 5] = m;
+}
+
 // padded copy of the canonical CSR: segment i (start s, len l) -> new start
 // ps (multiple of 4), entries copied, padding (col 0, val 0)
 __global__ void k_pad_segments(const uint64_t* __restrict__ seg_src, const uint32_t* __restrict__ seg_len,

@@ -280,6 +280,18 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, unsigned parity) {
   __syncwarp();
 }
 
+// warp-level wait without a suspend-time hint (lane 0 spins on try_wait)
+__device__ __forceinline__ void mbar_wait_warp_spin(uint64_t* bar, unsigned parity) {
+  if ((threadIdx.x & 31) == 0) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n "
+        "@!p bra WAITS_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra "

@@ -227,6 +227,93 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
+        if self.transfer_kernel == "kgroup":
+            if getattr(t, "kgroup", None) is None:
+                t.kgroup = kgroup_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            if getattr(self, "xbits", None) is None:
+                self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            meta, vals, pieces, wbeg, W, _ = t.kgroup
+            _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                      _lib.ptr(self.xbits), sp)
+            _lib.call("sss_transfer_kgroup", self.K, self.n, _lib.ptr(meta), _lib.ptr(vals),
+                      _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.xbits),
+                      _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
+        if self.transfer_kernel == "csr9s":
+            if getattr(t, "csr9", None) is None:
+                t.csr9 = csr9_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            if getattr(self, "xbits", None) is None:
+                self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            pcols, pvals, pieces, wbeg, W = t.csr9
+            _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                      _lib.ptr(self.xbits), sp)
+            _lib.call("sss_transfer_csr9s", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals),
+                      _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.xbits),
+                      _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
+        if self.transfer_kernel == "kstream":
+            import os
+
+            if getattr(t, "kstream", None) is None:
+                t.kstream = kstream_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            blob, recs, wbeg, W, _ = t.kstream
+            depth = int(os.environ.get("SSS_KSTREAM_DEPTH", "8"))
+            _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
+            _lib.call("sss_transfer_kstream", self.K, self.n, _lib.ptr(blob), _lib.ptr(recs),
+                      _lib.ptr(wbeg), W, depth, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
+        if self.transfer_kernel == "kstep":
+            if getattr(t, "kstep", None) is None:
+                t.kstep = kstep_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            cols, vals, steps, wbeg, W, _ = t.kstep
+            _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
+            _lib.call("sss_transfer_kstep", self.K, self.n, _lib.ptr(cols), _lib.ptr(vals),
+                      _lib.ptr(steps), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
+        if self.transfer_kernel == "kpackp":
+            import os
+
+            if getattr(t, "kpack", None) is None:
+                t.kpack = kpack_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            meta, vals, pieces, wbeg, W, _ = t.kpack
+            ppl = int(os.environ.get("SSS_KPACK_PPL", "4"))
+            _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
+            _lib.call("sss_transfer_kpack_pipe", self.K, self.n, _lib.ptr(meta), _lib.ptr(vals),
+                      _lib.ptr(pieces), _lib.ptr(wbeg), W, ppl, _lib.ptr(self.xp),
+                      _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
+        if self.transfer_kernel == "kpack":
+            if getattr(t, "kpack", None) is None:
+                t.kpack = kpack_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            meta, vals, pieces, wbeg, W, _ = t.kpack
+            _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
+            _lib.call("sss_transfer_kpack", self.K, self.n, _lib.ptr(meta), _lib.ptr(vals),
+                      _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
         if self.transfer_kernel == "csr9":
             if getattr(t, "csr9", None) is None:
                 t.csr9 = csr9_layout(t)
@@ -529,6 +616,301 @@ def csr9_layout(t: DeviceTransfer, split: int = None, warps_per_sm: int = None):
     pieces[:, 2] = rowk[rep]
     return (pcols, pvals, torch.as_tensor(pieces.view(np.int32), device=dev),
             torch.as_tensor(wbeg.view(np.int32), device=dev), W)
+
+
+def kpack_layout(t: DeviceTransfer, split: int = None, warps_per_sm: int = None):
+    """K-packed pair layout + balanced per-warp piece ranges for
+    sss_transfer_kpack (built on the device). Every (row, column) pair of the
+    K operators is stored once: meta = col | mask << 24, then the f32 values
+    of the terms in the mask, k ascending."""
+    import os
+
+    split = split or int(os.environ.get("SSS_KPACK_SPLIT", "512"))
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_KPACK_WPS", "16"))
+    if t.K > 8 or t.n > (1 << 24):
+        raise ValueError("kpack layout needs K <= 8 and N <= 2^24")
+    dev = t.rowptr.device
+    n, K = t.n, t.K
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    W = nsm * warps_per_sm
+    W -= W % 8
+    rp = t.rowptr.to(torch.int64)
+    lens = (rp[:, 1:] - rp[:, :-1]).reshape(-1)  # (k, row) order, matches entry order
+    kr = torch.arange(K * n, device=dev, dtype=torch.int64)
+    # entries of one k are contiguous from rp[k, 0]; the arrays are k-major
+    base = int(rp[0, 0].item())
+    total = int(lens.sum().item())
+    row_of = torch.repeat_interleave(kr % n, lens)
+    k_of = torch.repeat_interleave(kr // n, lens)
+    col = t.cols[base:base + total].to(torch.int64) & 0xFFFFFFFF
+    key = ((row_of * n + col) << 4) | k_of
+    key, order = torch.sort(key)
+    vals = t.vals[base:base + total][order].contiguous()
+    del order, row_of, k_of, col
+    pair = key >> 4
+    kbit = torch.bitwise_left_shift(torch.ones_like(key), key & 15)
+    del key
+    upair, inv = torch.unique_consecutive(pair, return_inverse=True)
+    del pair
+    mask = torch.zeros(upair.numel(), dtype=torch.int64, device=dev)
+    mask.index_add_(0, inv, kbit)  # distinct bits: sum == OR
+    del kbit, inv
+    prow = upair // n
+    pcol = upair % n
+    meta = pcol | (mask << 24)
+    meta = torch.where(meta >= (1 << 31), meta - (1 << 32), meta).to(torch.int32).contiguous()
+    cnt = torch.zeros_like(mask)
+    for k in range(K):
+        cnt += (mask >> k) & 1
+    npairs = upair.numel()
+    vstart = torch.cumsum(cnt, 0) - cnt  # first value of each pair
+    rowcnt = torch.bincount(prow, minlength=n)  # pairs per row
+    rowstart = torch.cumsum(rowcnt, 0) - rowcnt
+    # rows padded to a multiple of 4 pairs (meta 0 = empty) for 16-byte loads
+    rowpad = (rowcnt + 3) // 4 * 4
+    padstart = torch.cumsum(rowpad, 0) - rowpad
+    npad = int(rowpad.sum().item())
+    meta_p = torch.zeros(max(npad, 4), dtype=torch.int32, device=dev)
+    meta_p[torch.arange(npairs, device=dev) - rowstart[prow] + padstart[prow]] = meta
+    del upair, pcol, mask, prow, meta
+    # pieces: rows split into runs of <= split (padded) pairs
+    npc = (rowcnt + split - 1) // split
+    rows = torch.arange(n, device=dev, dtype=torch.int64)
+    rep = torch.repeat_interleave(rows, npc)
+    first = torch.cumsum(npc, 0) - npc
+    j = torch.arange(rep.numel(), device=dev, dtype=torch.int64) - first[rep]
+    p0 = padstart[rep] + j * split
+    pn = torch.minimum(torch.full_like(p0, split), rowpad[rep] - j * split)
+    u0 = rowstart[rep] + j * split  # first real pair of the piece
+    un = torch.minimum(torch.full_like(u0, split), rowcnt[rep] - j * split)
+    v0 = vstart[u0]
+    vend = torch.where(u0 + un < npairs, vstart[torch.clamp(u0 + un, max=npairs - 1)],
+                       torch.full_like(u0, total))
+    cost = pn + (vend - v0)  # meta + value loads
+    cum = torch.cat([torch.zeros(1, device=dev, dtype=torch.int64), torch.cumsum(cost, 0)])
+    targets = (torch.arange(W + 1, device=dev, dtype=torch.float64) * (float(cum[-1]) / W))
+    wbeg = torch.searchsorted(cum.to(torch.float64), targets, side="left")
+    wbeg[-1] = p0.numel()
+    pieces = torch.stack([p0, pn, v0, rep], 1).to(torch.int32).contiguous()
+    return (meta_p, vals, pieces, wbeg.to(torch.int32).contiguous(), W, npairs)
+
+
+def _kpacked_pairs(t: DeviceTransfer):
+    """(row, column) pairs of the K operators in (row, column) order: meta =
+    column | k-mask << 24 (int64), the values sorted by (row, column, k), the
+    pair count per row and each pair's first value."""
+    if t.K > 8 or t.n > (1 << 24):
+        raise ValueError("K-packed layouts need K <= 8 and N <= 2^24")
+    dev = t.rowptr.device
+    n, K = t.n, t.K
+    i64 = dict(dtype=torch.int64, device=dev)
+    rp = t.rowptr.to(torch.int64)
+    lens = (rp[:, 1:] - rp[:, :-1]).reshape(-1)
+    base = int(rp[0, 0].item())
+    total = int(lens.sum().item())
+    kr = torch.arange(K * n, **i64)
+    row_of = torch.repeat_interleave(kr % n, lens)
+    k_of = torch.repeat_interleave(kr // n, lens)
+    col = t.cols[base:base + total].to(torch.int64) & 0xFFFFFFFF
+    key = ((row_of * n + col) << 4) | k_of
+    del row_of, k_of, col
+    key, order = torch.sort(key)
+    vals = t.vals[base:base + total][order].contiguous()
+    del order
+    upair, inv = torch.unique_consecutive(key >> 4, return_inverse=True)
+    mask = torch.zeros(upair.numel(), **i64)
+    mask.index_add_(0, inv, torch.bitwise_left_shift(torch.ones_like(key), key & 15))
+    del key, inv
+    prow = upair // n
+    meta = (upair % n) | (mask << 24)
+    cnt = torch.zeros_like(mask)
+    for k in range(K):
+        cnt += (mask >> k) & 1
+    vstart = torch.cumsum(cnt, 0) - cnt
+    rowcnt = torch.bincount(prow, minlength=n)
+    return meta, vals, prow, rowcnt, vstart, cnt, total
+
+
+def kgroup_layout(t: DeviceTransfer, warps_per_sm: int = None, split: int = None):
+    """K-packed pairs with rows padded to 32 pairs, cut into pieces of <= split
+    pairs, + cost-balanced warp ranges for sss_transfer_kgroup (built on the
+    device)."""
+    import os
+
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_KGROUP_WPS", "24"))
+    split = split or int(os.environ.get("SSS_KGROUP_SPLIT", "512"))
+    split -= split % 32
+    dev = t.rowptr.device
+    n = t.n
+    i64 = dict(dtype=torch.int64, device=dev)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+    W = nsm * warps_per_sm
+    W -= W % 8
+    meta, vals, prow, rowcnt, vstart, cnt, total = _kpacked_pairs(t)
+    npairs = meta.numel()
+    rowstart = torch.cumsum(rowcnt, 0) - rowcnt
+    rowpad = (rowcnt + 31) // 32 * 32
+    padstart = torch.cumsum(rowpad, 0) - rowpad
+    npad = int(rowpad.sum().item())
+    meta_p = torch.zeros(max(npad, 32), dtype=torch.int32, device=dev)
+    meta = torch.where(meta >= (1 << 31), meta - (1 << 32), meta).to(torch.int32)
+    meta_p[torch.arange(npairs, **i64) - rowstart[prow] + padstart[prow]] = meta
+    # pieces
+    npc = (rowcnt + split - 1) // split
+    rep = torch.repeat_interleave(torch.arange(n, **i64), npc)
+    j = torch.arange(rep.numel(), **i64) - (torch.cumsum(npc, 0) - npc)[rep]
+    p0 = padstart[rep] + j * split
+    pn = torch.minimum(torch.full_like(p0, split), rowpad[rep] - j * split)
+    u0 = rowstart[rep] + j * split  # first real pair of the piece
+    un = torch.clamp(torch.minimum(torch.full_like(u0, split), rowcnt[rep] - j * split), min=0)
+    vend_all = torch.cat([vstart, torch.tensor([total], **i64)])
+    v0 = vend_all[u0]
+    nval = vend_all[u0 + un] - v0
+    pieces = torch.stack([p0, pn, v0, rep], 1).to(torch.int32).contiguous()
+    cost = pn * 2 + nval + 24  # meta + shuffles, values, per-piece overhead
+    cum = torch.cat([torch.zeros(1, **i64), torch.cumsum(cost, 0)])
+    targets = torch.arange(W + 1, dtype=torch.float64, device=dev) * (float(cum[-1]) / W)
+    wbeg = torch.searchsorted(cum.to(torch.float64), targets, side="left")
+    wbeg[-1] = p0.numel()
+    stats = {"pairs": npairs, "padded_pairs": npad, "values": total, "pieces": int(p0.numel()),
+             "max_row_pairs": int(rowcnt.max().item()),
+             "bytes": npad * 4 + total * 4 + int(p0.numel()) * 16}
+    return (meta_p, vals, pieces, wbeg.to(torch.int32).contiguous(), W, stats)
+
+
+def kstep_layout(t: DeviceTransfer, warps_per_sm: int = None):
+    """Mask-sorted K-fused warp steps for sss_transfer_kstep (built on the
+    device): per row, (row, column) pairs sorted by (popcount, k-mask), cut
+    into 32-pair steps; per step the columns and, for each k in the OR of the
+    step's masks, 32 lane-ordered f32 values (0 where a pair lacks k)."""
+    import os
+
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_KSTEP_WPS", "20"))
+    if t.K > 8:
+        raise ValueError("kstep layout needs K <= 8")
+    dev = t.rowptr.device
+    n, K = t.n, t.K
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+    W = nsm * warps_per_sm
+    W -= W % 4
+    i64 = dict(dtype=torch.int64, device=dev)
+    rp = t.rowptr.to(torch.int64)
+    lens = (rp[:, 1:] - rp[:, :-1]).reshape(-1)
+    base = int(rp[0, 0].item())
+    total = int(lens.sum().item())
+    kr = torch.arange(K * n, **i64)
+    row_of = torch.repeat_interleave(kr % n, lens)
+    k_of = torch.repeat_interleave(kr // n, lens)
+    col = t.cols[base:base + total].to(torch.int64) & 0xFFFFFFFF
+    ent_val = t.vals[base:base + total]
+    # pairs in (row, col) order
+    pkey = row_of * n + col
+    upair, pinv = torch.unique(pkey, return_inverse=True)
+    del pkey, col
+    npairs = upair.numel()
+    mask = torch.zeros(npairs, **i64)
+    mask.index_add_(0, pinv, torch.bitwise_left_shift(torch.ones_like(k_of), k_of))
+    prow = upair // n
+    pcol = upair % n
+    pc = torch.zeros_like(mask)
+    for k in range(K):
+        pc += (mask >> k) & 1
+    # per row: sort by (popcount, mask), stable in column order
+    skey = (prow << 12) | (pc << 8) | mask
+    skey, order = torch.sort(skey, stable=True)
+    del skey
+    newpos = torch.empty_like(order)
+    newpos[order] = torch.arange(npairs, **i64)
+    prow_s, pcol_s, mask_s = prow[order], pcol[order], mask[order]
+    del order
+    rowcnt = torch.bincount(prow_s, minlength=n)
+    rowstart = torch.cumsum(rowcnt, 0) - rowcnt
+    pos = torch.arange(npairs, **i64) - rowstart[prow_s]
+    nst = (rowcnt + 31) // 32
+    ststart = torch.cumsum(nst, 0) - nst
+    nsteps = int(nst.sum().item())
+    step_of = ststart[prow_s] + pos // 32
+    lane_of = pos % 32
+    umask = torch.zeros(nsteps, **i64)
+    for k in range(K):
+        bit = ((mask_s >> k) & 1)
+        has = torch.zeros(nsteps, **i64).scatter_reduce_(0, step_of, bit, "amax")
+        umask |= has << k
+    upc = torch.zeros_like(umask)
+    for k in range(K):
+        upc += (umask >> k) & 1
+    val0 = (torch.cumsum(upc, 0) - upc) * 32
+    nvals = int(upc.sum().item()) * 32
+    # scatter every coefficient to its (step, rank of k, lane) slot
+    p_new = newpos[pinv]
+    st = step_of[p_new]
+    below = umask[st] & (torch.bitwise_left_shift(torch.ones_like(k_of), k_of) - 1)
+    rank = torch.zeros_like(below)
+    for k in range(K):
+        rank += (below >> k) & 1
+    dest = val0[st] + rank * 32 + lane_of[p_new]
+    vals_out = torch.zeros(max(nvals, 32), dtype=torch.float32, device=dev)
+    vals_out[dest] = ent_val
+    del p_new, st, below, rank, dest, pinv, k_of, row_of
+    cols_out = pcol_s.to(torch.int32).contiguous()
+    # step records
+    srow = torch.repeat_interleave(torch.arange(n, **i64), nst)
+    sidx = torch.arange(nsteps, **i64) - ststart[srow]
+    pair0 = rowstart[srow] + sidx * 32
+    count = torch.minimum(torch.full_like(pair0, 32), rowcnt[srow] - sidx * 32)
+    row_end = (sidx == nst[srow] - 1).to(torch.int64)
+    info = umask | (count << 8) | (row_end << 16)
+    steps = torch.stack([pair0, val0, srow, info], 1).to(torch.int32).contiguous()
+    cost = count + 32 * upc + 48  # columns + values + per-step overhead (in 4-byte units)
+    cum = torch.cat([torch.zeros(1, **i64), torch.cumsum(cost, 0)])
+    targets = torch.arange(W + 1, dtype=torch.float64, device=dev) * (float(cum[-1]) / W)
+    wbeg = torch.searchsorted(cum.to(torch.float64), targets, side="left")
+    wbeg[-1] = nsteps
+    stats = {"pairs": npairs, "steps": nsteps, "values": nvals,
+             "bytes": npairs * 4 + nvals * 4 + nsteps * 16}
+    return (cols_out, vals_out, steps, wbeg.to(torch.int32).contiguous(), W, stats)
+
+
+def kstream_layout(t: DeviceTransfer, warps_per_sm: int = None):
+    """The kstep warp steps re-packed as contiguous per-step blobs for
+    sss_transfer_kstream: [32 u32 columns | popc(mask) x 32 f32 values]."""
+    import os
+
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_KSTREAM_WPS", "16"))
+    cols, vals, steps, _, _, stats = kstep_layout(t, warps_per_sm=1)
+    dev = cols.device
+    i64 = dict(dtype=torch.int64, device=dev)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+    W = nsm * warps_per_sm
+    W -= W % 8
+    st = steps.to(torch.int64) & 0xFFFFFFFF
+    pair0, val0, row, info = st[:, 0], st[:, 1], st[:, 2], st[:, 3]
+    nsteps = st.shape[0]
+    umask = info & 0xFF
+    count = (info >> 8) & 0xFF
+    upc = torch.zeros_like(umask)
+    for k in range(8):
+        upc += (umask >> k) & 1
+    words = 32 * (1 + upc)  # 4-byte words per step blob
+    off = torch.cumsum(words, 0) - words
+    blob = torch.zeros(max(int(words.sum().item()), 4), dtype=torch.int32, device=dev)
+    # columns (padded lanes stay 0)
+    sid = torch.repeat_interleave(torch.arange(nsteps, **i64), count)
+    lane = torch.arange(sid.numel(), **i64) - (torch.cumsum(count, 0) - count)[sid]
+    blob[off[sid] + lane] = cols[pair0[sid] + lane]
+    # values, already lane-ordered per k slot
+    sid = torch.repeat_interleave(torch.arange(nsteps, **i64), 32 * upc)
+    v = torch.arange(sid.numel(), **i64)
+    blob[off[sid] + 32 + (v - val0[sid])] = vals[v].view(torch.int32)
+    del sid, v, lane
+    recs = torch.stack([off // 4, row, info, torch.zeros_like(off)], 1).to(torch.int32).contiguous()
+    cost = words + 48
+    cum = torch.cat([torch.zeros(1, **i64), torch.cumsum(cost, 0)])
+    targets = torch.arange(W + 1, dtype=torch.float64, device=dev) * (float(cum[-1]) / W)
+    wbeg = torch.searchsorted(cum.to(torch.float64), targets, side="left")
+    wbeg[-1] = nsteps
+    stats = dict(stats, bytes=int(blob.numel()) * 4 + nsteps * 16)
+    return (blob, recs, wbeg.to(torch.int32).contiguous(), W, stats)
 
 
 def bench(scene: Scene, iterations: int = 20) -> dict:

@@ -330,9 +330,12 @@ def test_stream_and_banded_kernels_agree(c1):
     sc.transfer_kernel = "banded"
     a = sc.relight()
     vk_a = sc.vk.clone()
-    for kern in ("stream", "v4", "v6", "csr7", "csr8", "csr9"):
+    for kern in ("stream", "v4", "v6", "csr7", "csr8", "csr9", "kpack", "kpackp", "kstep", "kstream", "csr9s", "kgroup"):
         sc.transfer_kernel = kern
+        sc.vk.fill_(float("nan"))  # a kernel that leaves v_k untouched must fail
+        sc.radiance_unclamped.fill_(float("nan"))
         b = sc.relight()
+        assert torch.isfinite(sc.vk).all(), kern
         assert (sc.vk - vk_a).abs().max().item() <= 1e-12 * vk_a.abs().max().item(), kern
         assert O.parity_error(a.radiance_unclamped, b.radiance_unclamped, TAU) <= 1e-9, kern
 

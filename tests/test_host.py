@@ -92,6 +92,73 @@ def test_operator_layout_round_trip():
     assert np.all(pr // R == np.arange(n) // R)
 
 
+def _random_device_transfer(rng, side, L, K, per_col):
+    n = side * side
+    ops = []
+    shared = np.sort(rng.choice(n, per_col, replace=False))  # overlapping supports across k
+    for _ in range(K):
+        cols = np.sort(rng.choice(n, 60, replace=False)).astype(np.uint32)
+        colptr = np.zeros(cols.size + 1, np.int64)
+        rows = []
+        for i in range(cols.size):
+            pick = np.unique(np.concatenate([rng.choice(shared, per_col // 2, replace=False),
+                                             rng.choice(n, rng.integers(0, per_col), replace=False)]))
+            rows.append(pick)
+            colptr[i + 1] = colptr[i] + pick.size
+        rowidx = np.concatenate(rows).astype(np.uint32)
+        vals = rng.standard_normal(rowidx.size).astype(np.float32).astype(np.float64)
+        ops.append(TransferOperator(cols, colptr, rowidx, vals))
+    return DeviceTransfer.from_reference(ops, side, L, device="cpu")
+
+
+def _csr_vk(dt, x_tm):
+    rp = dt.rowptr.numpy()
+    cols = dt.cols.numpy().view(np.uint32)
+    vals = dt.vals.numpy().astype(np.float64)
+    vk = np.zeros((dt.K, 3, dt.n))
+    for k in range(dt.K):
+        for r in range(dt.n):
+            sl = slice(rp[k, r], rp[k, r + 1])
+            vk[k, :, r] = vals[sl] @ x_tm[cols[sl]]
+    return vk
+
+
+def test_kstep_layout_reproduces_csr_product():
+    """The mask-sorted K-fused warp-step layout (sss_transfer_kstep) computes
+    the same v_k as the per-term CSR: emulate the kernel over the layout."""
+    from paper_2203_12339_b200.runtime import kstep_layout
+
+    rng = np.random.default_rng(12)
+    dt = _random_device_transfer(rng, 32, 2, 5, 24)
+    x_tm = rng.standard_normal((dt.n, 3))
+    want = _csr_vk(dt, x_tm)
+    cols, vals, steps, wbeg, W, stats = kstep_layout(dt, warps_per_sm=1)
+    cols = cols.numpy().view(np.uint32)
+    vals = vals.numpy().astype(np.float64)
+    steps = steps.numpy().view(np.uint32)
+    wbeg = wbeg.numpy()
+    assert wbeg[0] == 0 and wbeg[-1] == steps.shape[0] and np.all(np.diff(wbeg) >= 0)
+    assert stats["pairs"] <= int(dt.rowptr[:, -1].max() - dt.rowptr[0, 0])
+    got = np.zeros_like(want)
+    rows_seen = []
+    for s in range(steps.shape[0]):
+        p0, v0, row, info = (int(v) for v in steps[s])
+        mask, cnt, end = info & 0xFF, (info >> 8) & 0xFF, (info >> 16) & 1
+        assert 1 <= cnt <= 32 and v0 % 32 == 0
+        xs = x_tm[cols[p0:p0 + cnt]]
+        j = 0
+        for k in range(8):
+            if mask >> k & 1:
+                v = vals[v0 + 32 * j: v0 + 32 * j + 32]
+                assert np.all(v[cnt:] == 0)
+                got[k, :, row] += v[:cnt] @ xs
+                j += 1
+        if end:
+            rows_seen.append(row)
+    assert len(rows_seen) == len(set(rows_seen))
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
 def test_library_exports_every_header_symbol():
     from paper_2203_12339_b200 import _lib, build
 
@@ -175,3 +242,68 @@ def test_configs_frozen():
     assert C.C1.n == 1024 and C.C2.n == 16384 and C.C3.n == 65536
     assert C.C1.n_materials == 16 and C.C2.n_materials == 32 and C.C5.n_materials == 64
     assert C.STEP2_FRACTION == 0.95 and C.E_KEEP == 0.25
+
+
+def test_kstream_blobs_reproduce_csr_product():
+    """sss_transfer_kstream's per-step blobs [32 columns | popc x 32 values]
+    carry the same v_k as the per-term CSR (kernel emulated on the host)."""
+    from paper_2203_12339_b200.runtime import kstream_layout
+
+    rng = np.random.default_rng(13)
+    dt = _random_device_transfer(rng, 32, 2, 6, 20)
+    x_tm = rng.standard_normal((dt.n, 3))
+    want = _csr_vk(dt, x_tm)
+    blob, recs, wbeg, W, stats = kstream_layout(dt, warps_per_sm=1)
+    blob = blob.numpy()
+    recs = recs.numpy().view(np.uint32)
+    wbeg = wbeg.numpy()
+    assert wbeg[0] == 0 and wbeg[-1] == recs.shape[0] and W % 8 == 0
+    bcols = blob.view(np.uint32)
+    bvals = blob.view(np.float32).astype(np.float64)
+    got = np.zeros_like(want)
+    for s in range(recs.shape[0]):
+        off, row, info = int(recs[s, 0]) * 4, int(recs[s, 1]), int(recs[s, 2])
+        mask, cnt = info & 0xFF, (info >> 8) & 0xFF
+        assert np.all(bcols[off + cnt: off + 32] == 0)
+        xs = x_tm[bcols[off: off + 32]]
+        j = 0
+        for k in range(8):
+            if mask >> k & 1:
+                got[k, :, row] += bvals[off + 32 + 32 * j: off + 64 + 32 * j] @ xs
+                j += 1
+        if s + 1 < recs.shape[0]:
+            assert int(recs[s + 1, 0]) * 4 == off + 32 * (1 + j)  # contiguous blobs
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_kgroup_layout_reproduces_csr_product():
+    """sss_transfer_kgroup's K-packed, 32-padded row pieces carry the same v_k
+    as the per-term CSR (kernel emulated on the host, unkept columns skipped)."""
+    from paper_2203_12339_b200.runtime import kgroup_layout
+
+    rng = np.random.default_rng(14)
+    dt = _random_device_transfer(rng, 32, 2, 7, 40)
+    x_tm = rng.standard_normal((dt.n, 3))
+    x_tm[rng.random(dt.n) < 0.6] = 0.0  # unkept columns
+    want = _csr_vk(dt, x_tm)
+    meta, vals, pieces, wbeg, W, stats = kgroup_layout(dt, warps_per_sm=1, split=64)
+    assert stats["pieces"] > dt.n - np.count_nonzero(
+        (dt.rowptr[:, 1:] - dt.rowptr[:, :-1]).sum(0).numpy() == 0)  # some rows split
+    meta = meta.numpy().view(np.uint32)
+    vals = vals.numpy().astype(np.float64)
+    pieces = pieces.numpy().view(np.uint32)
+    wbeg = wbeg.numpy()
+    assert wbeg[0] == 0 and wbeg[-1] == pieces.shape[0] and np.all(np.diff(wbeg) >= 0)
+    kept = np.any(x_tm != 0, axis=1)
+    got = np.zeros_like(want)
+    for p0, npair, v0, row in pieces:
+        assert p0 % 32 == 0 and npair % 32 == 0 and 0 < npair <= 64
+        off = v0
+        for m in meta[p0:p0 + npair]:
+            mask, col = int(m) >> 24, int(m) & 0xFFFFFF
+            for k in range(8):
+                if mask >> k & 1:
+                    if kept[col]:
+                        got[k, :, row] += vals[off] * x_tm[col]
+                    off += 1
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)

@@ -59,9 +59,23 @@ def main():
         "sss_select_topn", _lib.ptr(sc.ehat), 3, sc.n, keep, _lib.ptr(sc.f2t), _lib.ptr(sc.x),
         _lib.ptr(sc.mask), _lib.ptr(sc.energy), sp), a.reps)
     out["material_weights"] = timed(sc._launch_weights, a.reps)
-    for kern in ("csr9", "csr8", "csr7", "v6"):
+    ref_vk = None
+    for kern in ("csr9", "kgroup", "kstream", "v6"):
         sc.transfer_kernel = kern
+        sc.vk.fill_(float("nan"))
+        sc._launch_transfer()
+        torch.cuda.synchronize()
+        out[f"finite_{kern}"] = bool(torch.isfinite(sc.vk).all())
         out[f"transfer_{kern}"] = timed(sc._launch_transfer, a.reps)
+        if ref_vk is None:
+            ref_vk = sc.vk.clone()
+        else:
+            out[f"relerr_{kern}"] = float((sc.vk - ref_vk).abs().max() / ref_vk.abs().max())
+    out.update({f"kgroup_{k}": v for k, v in dt.kgroup[5].items()})
+    out["kgroup_MB"] = dt.kgroup[5]["bytes"] / 1e6
+    out["kgroup_GBps"] = dt.kgroup[5]["bytes"] / (out["transfer_kgroup"] * 1e-6) / 1e9
+    out["kstream_MB"] = dt.kstream[4]["bytes"] / 1e6
+    out["kstream_GBps"] = dt.kstream[4]["bytes"] / (out["transfer_kstream"] * 1e-6) / 1e9
     sc.transfer_kernel = "v6"
     lay = dt.v6
     out["v6_units"] = lay.units
