@@ -258,6 +258,39 @@ int sss_transfer_kgroup(int K, int n_rows, const uint32_t* meta, const float* va
                         const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
                         const uint32_t* bits, double* vk, void* stream);
 
+/* ---- transfer v15: flat stream over csr9's padded operator copy (every
+ * (row, k) segment padded to a multiple of 4 entries; n_entries total).
+ * heads: bit l of word i set iff 4-entry group 32 i + l starts a segment;
+ * head_prefix[i] = segments started before word i; seg_rowk[s] = row * 16 + k
+ * of segment s (segments in stream order); warp_begin (n_warps + 1) = word
+ * ranges per warp. n_warps a multiple of 8. bits (may be NULL) = kept-column
+ * bitmap from sss_pack_x_bits: entries over unkept columns skip their x
+ * gather (exact zeros). Zeroes and fills vk; shade with sss_edit_finish
+ * (runtime.py:148-153). */
+int sss_transfer_flat(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                      unsigned long long n_entries, const uint32_t* heads,
+                      const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                      const unsigned* warp_begin, int n_warps, const void* xp,
+                      const uint32_t* bits, double* vk, void* stream);
+
+/* ---- transfer v16: sss_transfer_flat with a depth-iteration cp.async
+ * prefetch ring per warp (depth 4, 8 or 12); n_warps a multiple of 4. */
+int sss_transfer_flatp(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                       unsigned long long n_entries, const uint32_t* heads,
+                       const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                       const unsigned* warp_begin, int n_warps, int depth, const void* xp,
+                       double* vk, void* stream);
+
+/* ---- transfer v17: sss_transfer_flat over a copy with every (row, k)
+ * segment padded to a multiple of 8 entries (pcols/pvals 32-byte aligned);
+ * heads bit l of word i marks 8-entry group 32 i + l; gather_ahead != 0 issues
+ * the x gathers one iteration ahead. n_warps a multiple of 4. Same contract. */
+int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                       unsigned long long n_entries, const uint32_t* heads,
+                       const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                       const unsigned* warp_begin, int n_warps, const void* xp,
+                       const uint32_t* bits, int gather_ahead, double* vk, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

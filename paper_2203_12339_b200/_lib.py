@@ -36,6 +36,9 @@ _SIGS = {
     "sss_transfer_kpack": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
     "sss_transfer_kstep": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
     "sss_pack_x_bits": [_P, _I, _P, _P, _P],
+    "sss_transfer_flat": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _P, _P, _P, _P],
+    "sss_transfer_flat8": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P],
+    "sss_transfer_flatp": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _I, _P, _P, _P],
     "sss_transfer_kgroup": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "sss_transfer_csr9s": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "sss_transfer_kstream": [_I, _I, _P, _P, _P, _I, _I, _P, _P, _P],

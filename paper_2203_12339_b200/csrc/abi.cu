@@ -19,6 +19,7 @@
 #include "kstep12.cu"
 #include "kstream13.cu"
 #include "kgroup14.cu"
+#include "flat15.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -550,6 +551,98 @@ int sss_transfer_kgroup(int K, int n_rows, const uint32_t* meta, const float* va
       K, n_rows, meta, vals, reinterpret_cast<const sss::V14Row*>(pieces), warp_begin,
       reinterpret_cast<const double4*>(xp), bits, vk);
   return check_launch("k_transfer_kgroup");
+}
+
+int sss_transfer_flat(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                      unsigned long long n_entries, const uint32_t* heads,
+                      const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                      const unsigned* warp_begin, int n_warps, const void* xp,
+                      const uint32_t* bits, double* vk, void* stream) {
+  if (K <= 0 || n_rows <= 0 || !pcols || !pvals || !heads || !head_prefix || !seg_rowk ||
+      !warp_begin || !xp || !vk || n_warps <= 0 || n_warps % (sss::kV15Threads / 32) ||
+      n_entries % 4 || n_entries / 4 >= (1ull << 32) - 64)
+    return fail(SSS_EINVAL, "bad transfer_flat arguments");
+  if (reinterpret_cast<uintptr_t>(pcols) % 16 || reinterpret_cast<uintptr_t>(pvals) % 16 ||
+      reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_flat: pcols/pvals 16-byte, xp 32-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const size_t smem = bits ? (size_t)((n_rows + 31) / 32) * 4 : 0;
+  if (int r = set_smem((const void*)sss::k_transfer_flat<0>, smem)) return r;
+  sss::k_transfer_flat<0><<<n_warps / (sss::kV15Threads / 32), sss::kV15Threads, smem,
+                            S_(stream)>>>(
+      n_rows, (unsigned)(n_entries / 4), reinterpret_cast<const uint4*>(pcols),
+      reinterpret_cast<const float4*>(pvals), heads, head_prefix, seg_rowk, warp_begin,
+      reinterpret_cast<const double4*>(xp), bits, vk);
+  return check_launch("k_transfer_flat");
+}
+
+int sss_transfer_flatp(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                       unsigned long long n_entries, const uint32_t* heads,
+                       const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                       const unsigned* warp_begin, int n_warps, int depth, const void* xp,
+                       double* vk, void* stream) {
+  if (K <= 0 || n_rows <= 0 || !pcols || !pvals || !heads || !head_prefix || !seg_rowk ||
+      !warp_begin || !xp || !vk || n_warps <= 0 || n_warps % (sss::kV16Threads / 32) ||
+      n_entries % 4 || n_entries / 4 >= (1ull << 32) - 64 ||
+      (depth != 4 && depth != 8 && depth != 12))
+    return fail(SSS_EINVAL, "bad transfer_flatp arguments");
+  if (reinterpret_cast<uintptr_t>(pcols) % 16 || reinterpret_cast<uintptr_t>(pvals) % 16 ||
+      reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_flatp: pcols/pvals 16-byte, xp 32-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const unsigned grid = n_warps / (sss::kV16Threads / 32);
+  const auto* c4 = reinterpret_cast<const uint4*>(pcols);
+  const auto* v4 = reinterpret_cast<const float4*>(pvals);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+  const unsigned n4 = (unsigned)(n_entries / 4);
+#define SSS_FP(RR)                                                                                \
+  do {                                                                                            \
+    const size_t smem = (size_t)(sss::kV16Threads / 32) * RR * sizeof(sss::V16Slot<RR>);          \
+    const void* fn = (const void*)sss::k_transfer_flatp<RR>;                                      \
+    if (int r = set_smem(fn, smem)) return r;                                                     \
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                \
+    sss::k_transfer_flatp<RR><<<grid, sss::kV16Threads, smem, S_(stream)>>>(                      \
+        n_rows, n4, c4, v4, heads, head_prefix, seg_rowk, warp_begin, x4, vk);                    \
+  } while (0)
+  if (depth == 4) SSS_FP(4);
+  else if (depth == 8) SSS_FP(8);
+  else SSS_FP(12);
+#undef SSS_FP
+  return check_launch("k_transfer_flatp");
+}
+
+int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                       unsigned long long n_entries, const uint32_t* heads,
+                       const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                       const unsigned* warp_begin, int n_warps, const void* xp,
+                       const uint32_t* bits, int gather_ahead, double* vk, void* stream) {
+  if (K <= 0 || n_rows <= 0 || !pcols || !pvals || !heads || !head_prefix || !seg_rowk ||
+      !warp_begin || !xp || !vk || n_warps <= 0 || n_warps % (sss::kV17Threads / 32) ||
+      n_entries % 8 || n_entries / 8 >= (1ull << 32) - 64)
+    return fail(SSS_EINVAL, "bad transfer_flat8 arguments");
+  if (reinterpret_cast<uintptr_t>(pcols) % 32 || reinterpret_cast<uintptr_t>(pvals) % 32 ||
+      reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_flat8: pcols/pvals/xp must be 32-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const size_t smem = bits ? (size_t)((n_rows + 31) / 32) * 4 : 0;
+  const auto* c8 = reinterpret_cast<const unsigned long long*>(pcols);
+  const auto* v8 = reinterpret_cast<const unsigned long long*>(pvals);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+  const unsigned grid = n_warps / (sss::kV17Threads / 32);
+  const unsigned n8 = (unsigned)(n_entries / 8);
+  if (gather_ahead) {
+    if (int r = set_smem((const void*)sss::k_transfer_flat8<true>, smem)) return r;
+    sss::k_transfer_flat8<true><<<grid, sss::kV17Threads, smem, S_(stream)>>>(
+        n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);
+  } else {
+    if (int r = set_smem((const void*)sss::k_transfer_flat8<false>, smem)) return r;
+    sss::k_transfer_flat8<false><<<grid, sss::kV17Threads, smem, S_(stream)>>>(
+        n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);
+  }
+  return check_launch("k_transfer_flat8");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

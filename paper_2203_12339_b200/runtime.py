@@ -21,6 +21,7 @@ buffer the kernels read.
 
 from __future__ import annotations
 
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -126,9 +127,10 @@ class Scene:
         self.material_buf = torch.empty(7, **f64)
         self.cam_buf = torch.empty(3, **f64)
         self._light_kind = None
-        # "v6" (persistent, warp-specialized TMA pipeline, merge-path items)
-        # | "v4" | "stream" | "banded" (earlier layouts, kept for A/B checks)
-        self.transfer_kernel = "v6"
+        # "flat8" (flat-stream CSR, 8 entries per lane, head flags, kept-column
+        # skip: the default) | "flat" | "csr9" | "v6" | ... (earlier layouts,
+        # kept for A/B checks)
+        self.transfer_kernel = os.environ.get("SSS_TRANSFER", "flat8")
         self._have_cache = False
         self._sequence = 0
         self._graph = None
@@ -227,6 +229,26 @@ class Scene:
 
     def _launch_transfer(self, stream=None):
         t = self.transfer
+        if self.transfer_kernel == "flatp":
+            if getattr(t, "flatp", None) is None:
+                t.flatp = flat_layout(t, warps_per_sm=int(os.environ.get("SSS_FLATP_WPS", "20")))
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            sp = _lib.stream_ptr(stream)
+            pcols, pvals, ne, heads, hpre, rowk, wbeg, W, _ = t.flatp
+            depth = int(os.environ.get("SSS_FLATP_DEPTH", "8"))
+            _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
+            _lib.call("sss_transfer_flatp", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
+                      _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W, depth,
+                      _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
+        if self.transfer_kernel in ("flat", "flat8"):
+            sp = _lib.stream_ptr(stream)
+            self._flat_prep(sp)
+            self._flat_core(sp)
+            self._launch_edit(stream)
+            return
         if self.transfer_kernel == "kgroup":
             if getattr(t, "kgroup", None) is None:
                 t.kgroup = kgroup_layout(t)
@@ -260,8 +282,6 @@ class Scene:
             self._launch_edit(stream)
             return
         if self.transfer_kernel == "kstream":
-            import os
-
             if getattr(t, "kstream", None) is None:
                 t.kstream = kstream_layout(t)
             if getattr(self, "xp", None) is None:
@@ -287,8 +307,6 @@ class Scene:
             self._launch_edit(stream)
             return
         if self.transfer_kernel == "kpackp":
-            import os
-
             if getattr(t, "kpack", None) is None:
                 t.kpack = kpack_layout(t)
             if getattr(self, "xp", None) is None:
@@ -391,6 +409,40 @@ class Scene:
                   _lib.ptr(self.material_buf), _lib.ptr(self.vk), _lib.ptr(self.scatter),
                   _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped),
                   _lib.stream_ptr(stream))
+
+    def _flat_prep(self, sp):
+        t = self.transfer
+        if self.transfer_kernel == "flat8" and getattr(t, "flat8", None) is None:
+            t.flat8 = flat_layout(t, group=8,
+                                  warps_per_sm=int(os.environ.get("SSS_FLAT8_WPS", "16")))
+        if self.transfer_kernel == "flat" and getattr(t, "flat", None) is None:
+            t.flat = flat_layout(t)
+        if getattr(self, "xp", None) is None:
+            self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+        if getattr(self, "xbits", None) is None:
+            self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+        _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                  _lib.ptr(self.xbits), sp)
+
+    def _flat_core(self, sp):
+        if self.transfer_kernel == "flat8":
+            pcols, pvals, ne, heads, hpre, rowk, wbeg, W, _ = self.transfer.flat8
+            _lib.call("sss_transfer_flat8", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
+                      _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W,
+                      _lib.ptr(self.xp), _lib.ptr(self.xbits),
+                      int(os.environ.get("SSS_FLAT8_AHEAD", "0")), _lib.ptr(self.vk), sp)
+            return
+        pcols, pvals, ne, heads, hpre, rowk, wbeg, W, _ = self.transfer.flat
+        _lib.call("sss_transfer_flat", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
+                  _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W,
+                  _lib.ptr(self.xp), _lib.ptr(self.xbits), _lib.ptr(self.vk), sp)
+
+    def launch_transfer_core(self, stream=None):
+        """The dominant kernel alone (default path), on inputs the last frame
+        prepared: for roofline timing."""
+        if self.transfer_kernel not in ("flat", "flat8"):
+            return self._launch_transfer(stream)
+        self._flat_core(_lib.stream_ptr(stream))
 
     def _launch_edit(self, stream=None):
         _lib.call("sss_edit_finish", self.K, self.side, self.levels, _lib.ptr(self.vk),
@@ -567,16 +619,16 @@ def csr8_schedule(t: DeviceTransfer, split: int = None, warps_per_sm: int = None
             torch.as_tensor(wbeg.view(np.int32), device=dev), W)
 
 
-def csr9_layout(t: DeviceTransfer, split: int = None, warps_per_sm: int = None):
+def csr9_layout(t: DeviceTransfer, split: int = None, warps_per_sm: int = None, pad: int = 4):
     """Padded (multiple-of-4) segment copy + balanced per-warp piece ranges for
     sss_transfer_csr9. Pieces follow (row, k) order (x locality)."""
     import os
 
     split = split or int(os.environ.get("SSS_CSR9_SPLIT", "1024"))
-    split -= split % 4
+    split -= split % pad
     warps_per_sm = warps_per_sm or int(os.environ.get("SSS_CSR9_WPS", "32"))
     dev = t.rowptr.device
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
     W = nsm * warps_per_sm
     W -= W % 8
     rp = t.rowptr.cpu().numpy()
@@ -585,22 +637,34 @@ def csr9_layout(t: DeviceTransfer, split: int = None, warps_per_sm: int = None):
     rowk = (np.arange(t.n)[:, None] * 16 + np.arange(t.K)[None, :]).reshape(-1)
     keep = lens > 0
     starts, lens, rowk = starts[keep], lens[keep], rowk[keep]
-    lens4 = (lens + 3) // 4 * 4
+    lens4 = (lens + pad - 1) // pad * pad
     dst = np.zeros(lens.size, np.int64)
     np.cumsum(lens4[:-1], out=dst[1:])
     total = int(lens4.sum())
-    pcols = torch.empty(max(total, 4), dtype=torch.int32, device=dev)
-    pvals = torch.empty(max(total, 4), dtype=torch.float32, device=dev)
+    # zero-filled: k_pad_segments pads each segment to 4 entries; larger pads
+    # (and the tail) must read as column 0, value 0
+    pcols = torch.zeros(max(total, pad), dtype=torch.int32, device=dev)
+    pvals = torch.zeros(max(total, pad), dtype=torch.float32, device=dev)
     # keep the staging tensors referenced until the kernel has consumed them
     # (a temporary freed before launch can be recycled by the next allocation)
-    d_src = torch.as_tensor(starts.astype(np.int64), device=dev)
-    d_len = torch.as_tensor(lens.astype(np.int32), device=dev)
-    d_dst = torch.as_tensor(dst, device=dev)
-    _lib.call("sss_pad_segments", _lib.ptr(d_src), _lib.ptr(d_len), _lib.ptr(d_dst),
-              int(lens.size), _lib.ptr(t.cols), _lib.ptr(t.vals), _lib.ptr(pcols), _lib.ptr(pvals),
-              _lib.stream_ptr())
-    torch.cuda.synchronize()
-    del d_src, d_len, d_dst
+    if dev.type == "cuda":
+        d_src = torch.as_tensor(starts.astype(np.int64), device=dev)
+        d_len = torch.as_tensor(lens.astype(np.int32), device=dev)
+        d_dst = torch.as_tensor(dst, device=dev)
+        _lib.call("sss_pad_segments", _lib.ptr(d_src), _lib.ptr(d_len), _lib.ptr(d_dst),
+                  int(lens.size), _lib.ptr(t.cols), _lib.ptr(t.vals), _lib.ptr(pcols),
+                  _lib.ptr(pvals), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        del d_src, d_len, d_dst
+    else:  # host layout tests
+        pcols.zero_()
+        pvals.zero_()
+        seg = np.repeat(np.arange(lens.size), lens)
+        j = np.arange(seg.size) - np.repeat(np.cumsum(lens) - lens, lens)
+        src = torch.as_tensor(starts[seg] + j)
+        dsti = torch.as_tensor(dst[seg] + j)
+        pcols[dsti] = t.cols[src]
+        pvals[dsti] = t.vals[src]
     npc = (lens4 + split - 1) // split
     rep = np.repeat(np.arange(lens4.size), npc)
     j = np.arange(rep.size) - np.repeat(np.cumsum(npc) - npc, npc)
@@ -776,6 +840,40 @@ def kgroup_layout(t: DeviceTransfer, warps_per_sm: int = None, split: int = None
              "max_row_pairs": int(rowcnt.max().item()),
              "bytes": npad * 4 + total * 4 + int(p0.numel()) * 16}
     return (meta_p, vals, pieces, wbeg.to(torch.int32).contiguous(), W, stats)
+
+
+def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4):
+    """Head-flag bitmap + per-word segment prefix + segment (row, k) ids over
+    csr9's padded operator copy, and equal word ranges per warp, for
+    sss_transfer_flat."""
+    import os
+
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_FLAT_WPS", "16"))
+    attr = "csr9" if group == 4 else f"csr9_pad{group}"
+    if getattr(t, attr, None) is None:
+        setattr(t, attr, csr9_layout(t, split=1 << 30, pad=group))
+    pcols, pvals, pieces, _, _ = getattr(t, attr)
+    dev = pcols.device
+    i64 = dict(dtype=torch.int64, device=dev)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+    W = nsm * warps_per_sm
+    W -= W % 8
+    n_entries = pcols.numel()
+    n4 = n_entries // group
+    nw = (n4 + 31) // 32
+    pc = pieces.to(torch.int64) & 0xFFFFFFFF
+    s4 = pc[:, 0] // group
+    heads = torch.zeros(nw, **i64).index_add_(0, s4 // 32, torch.bitwise_left_shift(
+        torch.ones_like(s4), s4 % 32))
+    heads = torch.where(heads >= (1 << 31), heads - (1 << 32), heads).to(torch.int32)
+    cnt = torch.bincount(s4 // 32, minlength=nw)
+    hpre = (torch.cumsum(cnt, 0) - cnt).to(torch.int32)
+    rowk = pc[:, 2].to(torch.int32).contiguous()
+    wbeg = (torch.arange(W + 1, **i64) * nw) // W
+    stats = {"entries": n_entries, "words": nw, "segments": int(s4.numel()),
+             "bytes": n_entries * 8 + nw * 8 + int(s4.numel()) * 4}
+    return (pcols, pvals, n_entries, heads.contiguous(), hpre.contiguous(), rowk,
+            wbeg.to(torch.int32).contiguous(), W, stats)
 
 
 def kstep_layout(t: DeviceTransfer, warps_per_sm: int = None):

@@ -307,3 +307,38 @@ def test_kgroup_layout_reproduces_csr_product():
                         got[k, :, row] += vals[off] * x_tm[col]
                     off += 1
     assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("group", [4, 8])
+def test_flat_stream_layout_reproduces_csr_product(group):
+    """sss_transfer_flat's head-flag bitmap / segment prefix over the padded
+    operator copy recover every segment's (row, k): emulate the segmented
+    warp-stream on the host, including warp ranges that cut segments."""
+    from paper_2203_12339_b200.runtime import flat_layout
+
+    rng = np.random.default_rng(15)
+    dt = _random_device_transfer(rng, 32, 2, 5, 30)
+    x_tm = rng.standard_normal((dt.n, 3))
+    want = _csr_vk(dt, x_tm)
+    pcols, pvals, ne, heads, hpre, rowk, wbeg, W, stats = flat_layout(dt, warps_per_sm=1,
+                                                                       group=group)
+    c4 = pcols.numpy().view(np.uint32).reshape(-1, group)
+    v4 = pvals.numpy().astype(np.float64).reshape(-1, group)
+    heads = heads.numpy().view(np.uint32)
+    hpre = hpre.numpy().view(np.uint32)
+    rowk = rowk.numpy().view(np.uint32)
+    wbeg = wbeg.numpy()
+    assert ne == c4.size and wbeg[0] == 0 and wbeg[-1] == heads.size
+    got = np.zeros_like(want)
+    n4 = c4.shape[0]
+    for w in range(W):
+        for i in range(wbeg[w], wbeg[w + 1]):
+            for lane in range(32):
+                q = 32 * i + lane
+                if q >= n4:
+                    continue
+                hm = int(heads[i]) & ((2 << lane) - 1)
+                pid = int(hpre[i]) + bin(hm).count("1") - 1
+                rk = int(rowk[pid])
+                got[rk & 15, :, rk >> 4] += v4[q] @ x_tm[c4[q]]
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)

@@ -60,7 +60,7 @@ def main():
         _lib.ptr(sc.mask), _lib.ptr(sc.energy), sp), a.reps)
     out["material_weights"] = timed(sc._launch_weights, a.reps)
     ref_vk = None
-    for kern in ("csr9", "kgroup", "kstream", "v6"):
+    for kern in ("csr9", "flat", "flat8"):
         sc.transfer_kernel = kern
         sc.vk.fill_(float("nan"))
         sc._launch_transfer()
@@ -71,17 +71,10 @@ def main():
             ref_vk = sc.vk.clone()
         else:
             out[f"relerr_{kern}"] = float((sc.vk - ref_vk).abs().max() / ref_vk.abs().max())
-    out.update({f"kgroup_{k}": v for k, v in dt.kgroup[5].items()})
-    out["kgroup_MB"] = dt.kgroup[5]["bytes"] / 1e6
-    out["kgroup_GBps"] = dt.kgroup[5]["bytes"] / (out["transfer_kgroup"] * 1e-6) / 1e9
-    out["kstream_MB"] = dt.kstream[4]["bytes"] / 1e6
-    out["kstream_GBps"] = dt.kstream[4]["bytes"] / (out["transfer_kstream"] * 1e-6) / 1e9
-    sc.transfer_kernel = "v6"
-    lay = dt.v6
-    out["v6_units"] = lay.units
-    out["v6_items"] = lay.n_items
-    out["v6_stream_MB"] = lay.stream_bytes / 1e6
-    out["v6_GBps_stream"] = lay.stream_bytes / (out["transfer_v6"] * 1e-6) / 1e9
+    out.update({f"flat_{k}": v for k, v in dt.flat[8].items()})
+    out["flat_GBps"] = dt.flat[8]["bytes"] / (out["transfer_flat"] * 1e-6) / 1e9
+    out["flat8_MB"] = dt.flat8[8]["bytes"] / 1e6
+    sc.transfer_kernel = "flat"
     out["edit_finish"] = timed(sc._launch_edit, a.reps)
     sc.capture()
     out["relight_graph"] = timed(lambda: sc.replay(False), a.reps)
