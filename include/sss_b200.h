@@ -291,6 +291,35 @@ int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pv
                        const unsigned* warp_begin, int n_warps, const void* xp,
                        const uint32_t* bits, int gather_ahead, double* vk, void* stream);
 
+/* ---- transfer v18: the v12 mask-sorted warp steps (same cols / vals / steps
+ * arrays as sss_transfer_kstep) streamed with batched step records and a
+ * two-step prefetch; bits (may be NULL) = kept-column bitmap. K <= 8, n_warps
+ * a multiple of 4. Zeroes and fills vk; shade with sss_edit_finish. */
+int sss_transfer_kflat(int K, int n_rows, const uint32_t* cols, const float* vals,
+                       const void* steps, const unsigned* warp_begin, int n_warps, const void* xp,
+                       const uint32_t* bits, double* vk, void* stream);
+
+/* ---- C4 batched material sweep (BASELINE configs[3]; runtime.py:202-216 for
+ * a batch of materials). B operand: Bq (3, N, 16) bf16 = w1^-1 of the cached
+ * v_k (K <= 16 terms, zero padded), points in flat (spatial) order. */
+int sss_sweep_basis(int K, int side, int levels, const double* vk, void* Bq, void* stream);
+
+/* ---- project_material (basisgen.py:172-191) for M materials at once:
+ * materials (M, 7) doubles {sp[3], sa[3], eta}; g64 (M, 3, K) fp64 (may be
+ * NULL), Gq (3, M, 16) bf16 (the sweep's G operand), eta_f (M) float (may be
+ * NULL). */
+int sss_material_weights_batch(const double* bw, const double* r_nodes, int K, int nr, int M,
+                               const double* materials, double* g64, void* Gq, float* eta_f,
+                               void* stream);
+
+/* ---- the sweep contraction (tcgen05 UMMA, bf16 in, fp32 accumulate in TMEM):
+ * out (3, M, N) fp32 = max(0, F_t(eta_m, cos_n) / pi * sum_k Bq[c][n][k]
+ * Gq[c][m][k]), cos_n from positions / normals / cam; F_t is evaluated through
+ * a per-point cubic fit in eta over [eta_lo, eta_hi] (all eta_m inside, > 1). */
+int sss_sweep_gemm(int n_points, int M, const void* Bq, const void* Gq, const float* eta,
+                   float eta_lo, float eta_hi, const float* positions, const float* normals,
+                   const double* cam, float* out, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

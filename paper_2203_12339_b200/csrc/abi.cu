@@ -2,6 +2,7 @@
 // so every kernel is visible to its launcher; built into
 // paper_2203_12339_b200/_sss_b200.so for sm_100a (see build.py).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -20,6 +21,8 @@
 #include "kstream13.cu"
 #include "kgroup14.cu"
 #include "flat15.cu"
+#include "kflat18.cu"
+#include "sweep.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -123,7 +126,7 @@ int sss_env_project(const double* faces, int env_side, int n_keep, uint32_t* idx
   if (!pow2(env_side) || env_side > 32 || n_keep <= 0 || !faces || !idx || !val)
     return fail(SSS_EINVAL, "bad env_project arguments (env_side must be a power of two <= 32)");
   const int s2 = env_side * env_side;
-  const size_t smem = (size_t)7 * s2 * sizeof(double) + sizeof(sss::SelShared);
+  const size_t smem = (size_t)12 * s2 * sizeof(double) + sizeof(sss::SelShared);
   if (int r = set_smem((const void*)sss::k_env_project, smem)) return r;
   sss::k_env_project<<<3, 1024, smem, S_(stream)>>>(faces, env_side, n_keep, idx, val, nullptr);
   if (int r = check_launch("k_env_project")) return r;
@@ -142,9 +145,11 @@ int sss_env_irradiance(const float* W2, int D, const uint32_t* union_idx, const 
   if (!W2 || !union_idx || !union_lc || !n_union || !ehat || n_keep <= 0)
     return fail(SSS_EINVAL, "bad env_irradiance arguments");
   const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
-  int tpb = 256 / T2 < 1 ? 1 : 256 / T2;
+  // one point per thread with a sequential (bitwise-pinned) sum: balance the
+  // grid across the SMs with small CTAs (>= 64 threads)
+  int tpb = 64 / T2 < 1 ? 1 : 64 / T2;
   while (tpb > 1 && tiles % tpb) tpb >>= 1;
-  const size_t smem = 6 * (size_t)tpb * T2 * sizeof(double) + 9 * (size_t)n_keep * sizeof(double) +
+  const size_t smem = 6 * (size_t)tpb * T2 * sizeof(double) + 12 * (size_t)n_keep * sizeof(double) +
                       3 * (size_t)n_keep * sizeof(int);
   if (int r = set_smem((const void*)sss::k_env_irradiance_multi, smem)) return r;
   (void)D;
@@ -645,6 +650,83 @@ int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pv
   return check_launch("k_transfer_flat8");
 }
 
+int sss_transfer_kflat(int K, int n_rows, const uint32_t* cols, const float* vals,
+                       const void* steps, const unsigned* warp_begin, int n_warps, const void* xp,
+                       const uint32_t* bits, double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || !cols || !vals || !steps || !warp_begin || !xp || !vk ||
+      n_warps <= 0 || n_warps % (sss::kV18Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_kflat arguments");
+  if (reinterpret_cast<uintptr_t>(xp) % 32 || reinterpret_cast<uintptr_t>(steps) % 16)
+    return fail(SSS_EINVAL, "transfer_kflat: xp 32-byte, steps 16-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const size_t smem = bits ? (size_t)((n_rows + 31) / 32) * 4 : 0;
+  if (int r = set_smem((const void*)sss::k_transfer_kflat<0>, smem)) return r;
+  sss::k_transfer_kflat<0><<<n_warps / (sss::kV18Threads / 32), sss::kV18Threads, smem,
+                             S_(stream)>>>(K, n_rows, cols, vals,
+                                           reinterpret_cast<const uint4*>(steps), warp_begin,
+                                           reinterpret_cast<const double4*>(xp), bits, vk);
+  return check_launch("k_transfer_kflat");
+}
+
+int sss_sweep_basis(int K, int side, int levels, const double* vk, void* Bq, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (K <= 0 || K > sss::kSweepK || !vk || !Bq) return fail(SSS_EINVAL, "bad sweep_basis arguments");
+  const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
+  const size_t smem = 2 * 3 * (size_t)K * T2 * sizeof(double);
+  if (int r = set_smem((const void*)sss::k_sweep_basis, smem)) return r;
+  sss::k_sweep_basis<<<tiles, 256, smem, S_(stream)>>>(K, side, levels, vk,
+                                                     reinterpret_cast<__nv_bfloat16*>(Bq));
+  return check_launch("k_sweep_basis");
+}
+
+int sss_material_weights_batch(const double* bw, const double* r_nodes, int K, int nr, int M,
+                               const double* materials, double* g64, void* Gq, float* eta_f,
+                               void* stream) {
+  if (K <= 0 || K > sss::kSweepK || nr < 2 || M <= 0 || M > 65535 || !bw || !r_nodes ||
+      !materials || !Gq)
+    return fail(SSS_EINVAL, "bad material_weights_batch arguments");
+  sss::k_material_weights_batch<<<dim3(3, M), 256, 0, S_(stream)>>>(
+      bw, r_nodes, K, nr, M, materials, g64, reinterpret_cast<__nv_bfloat16*>(Gq), eta_f);
+  return check_launch("k_material_weights_batch");
+}
+
+static int sweep_variant() {
+  const char* e = getenv("SSS_SWEEP_VARIANT");
+  return e ? atoi(e) : 0;
+}
+
+int sss_sweep_gemm(int n_points, int M, const void* Bq, const void* Gq, const float* eta,
+                   float eta_lo, float eta_hi, const float* positions, const float* normals,
+                   const double* cam, float* out, void* stream) {
+  if (n_points <= 0 || M <= 0 || !Bq || !Gq || !eta || !positions || !normals || !cam || !out ||
+      !(eta_hi >= eta_lo) || eta_lo <= 1.0f)
+    return fail(SSS_EINVAL, "bad sweep_gemm arguments (eta must exceed 1)");
+  if (reinterpret_cast<uintptr_t>(Bq) % 16 || reinterpret_cast<uintptr_t>(Gq) % 16)
+    return fail(SSS_EINVAL, "sweep_gemm: Bq / Gq must be 16-byte aligned");
+  // variant: materials per UMMA (N) and threads per CTA; the dynamic shared
+  // memory request caps residency at what TMEM (512 columns / SM) allows
+  const int variant = sweep_variant();
+  const dim3 g1((n_points + sss::kSweepTileM - 1) / sss::kSweepTileM, 3, 1);
+#define SSS_SW(TMN, THR, SMEMKB)                                                                   \
+  do {                                                                                             \
+    const size_t smem = (size_t)(SMEMKB) * 1024;                                                  \
+    const void* fn = (const void*)sss::k_sweep_umma<TMN, THR>;                                     \
+    if (int r = set_smem(fn, smem)) return r;                                                      \
+    dim3 grid = g1;                                                                                \
+    grid.z = (M + TMN - 1) / TMN;                                                                  \
+    sss::k_sweep_umma<TMN, THR><<<grid, THR, smem, S_(stream)>>>(                                  \
+        n_points, M, reinterpret_cast<const __nv_bfloat16*>(Bq),                                   \
+        reinterpret_cast<const __nv_bfloat16*>(Gq), eta, eta_lo, eta_hi, positions, normals, cam,   \
+        out);                                                                                      \
+  } while (0)
+  if (variant == 1) SSS_SW(256, 128, 80);
+  else if (variant == 2) SSS_SW(256, 256, 80);
+  else SSS_SW(128, 256, 52);
+#undef SSS_SW
+  return check_launch("k_sweep_umma");
+}
+
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream) {
   if (!rowptr || !bandoff || K <= 0 || n_rows <= 0 || band_width <= 0 || n_bands <= 0)
@@ -663,10 +745,20 @@ int sss_edit_finish(int K, int side, int levels, const double* vk, const double*
   if (K <= 0 || !vk || !g || !positions || !normals || !cam || !material || !radiance ||
       !radiance_unclamped)
     return fail(SSS_EINVAL, "bad edit_finish arguments");
-  const int T = 1 << levels;
+  const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
+  int G = 256 / T2 < 1 ? 1 : 256 / T2;  // tiles per CTA (256 rows)
+  while (G > 1 && tiles % G) G >>= 1;
+  if (G > 1) {
+    const size_t smem = 6 * (size_t)G * T2 * sizeof(double);
+    if (int r = set_smem((const void*)sss::k_edit_finish_multi, smem)) return r;
+    sss::k_edit_finish_multi<<<tiles / G, 256, smem, S_(stream)>>>(
+        K, side, levels, G, vk, g, positions, normals, cam, material, scatter, radiance,
+        radiance_unclamped);
+    return check_launch("k_edit_finish_multi");
+  }
   const size_t smem = 4 * (size_t)T * T * sizeof(double);
   if (int r = set_smem((const void*)sss::k_edit_finish, smem)) return r;
-  sss::k_edit_finish<<<(side / T) * (side / T), 128, smem, S_(stream)>>>(
+  sss::k_edit_finish<<<tiles, 128, smem, S_(stream)>>>(
       K, side, levels, vk, g, positions, normals, cam, material, scatter, radiance,
       radiance_unclamped);
   return check_launch("k_edit_finish");
@@ -690,7 +782,8 @@ int sss_pair_block(int levels, int exact, int side, const float* pos, const floa
   const int T = 1 << levels, T2 = T * T;
   const int tiles = (side / T) * (side / T);
   dim3 grid(tiles, tiles);
-  const size_t smem = ((size_t)T2 * (T2 + 1) + (exact ? 0 : 3 * (size_t)nr)) * sizeof(double);
+  const size_t smem = ((size_t)T2 * (T2 + 1) + (exact ? 0 : 3 * (size_t)nr)) * sizeof(double) +
+                      (exact ? (size_t)n_mat * 5 * sizeof(float) : 0);
   const void* fn = nullptr;
 #define SSS_PAIR_CASE(LV)                                                                     \
   case LV:                                                                                    \

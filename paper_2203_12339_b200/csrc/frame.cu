@@ -157,11 +157,11 @@ __global__ void k_env_project(const double* __restrict__ faces, int s, int n_kee
   extern __shared__ __align__(16) double sm[];
   const int c = blockIdx.x, s2 = s * s, D = 6 * s2;
   double* a = sm;             // D
-  double* tmp = sm + D;       // s2
-  SelShared& sh = *reinterpret_cast<SelShared*>(tmp + s2);
+  double* tmp = sm + D;       // D (the 6 faces transform as one batch)
+  SelShared& sh = *reinterpret_cast<SelShared*>(tmp + D);
   for (int e = threadIdx.x; e < D; e += blockDim.x) a[e] = faces[(size_t)e * 3 + c];
   __syncthreads();
-  for (int f = 0; f < 6; ++f) tile_haar_fwd(a + f * s2, tmp, s, blockDim.x, threadIdx.x);
+  batch_tile_haar_fwd(a, tmp, s, 6);
   const int n = min(n_keep, D);
   SelectResult sel;
   {
@@ -347,12 +347,13 @@ __global__ void k_env_irradiance_multi(const float* __restrict__ W2,
   const int T = 1 << L, T2 = T * T, N = S * S, tpr = S / T;
   double* a = sm;                       // TPB * 3 * T2
   double* tmp = a + TPB * 3 * T2;       // TPB * 3 * T2
-  double* lc = tmp + TPB * 3 * T2;      // 3 n_keep * 3
-  int* ul = reinterpret_cast<int*>(lc + 9 * n_keep);
+  double* lc = tmp + TPB * 3 * T2;      // 3 n_keep x 4 (l0, l1, l2, 0): one 16-B + one 8-B LDS
+  int* ul = reinterpret_cast<int*>(lc + 12 * n_keep);
   const int m = *n_union;
   for (int q = threadIdx.x; q < m; q += blockDim.x) {
     ul[q] = (int)union_idx[q];
-    lc[q * 3] = union_lc[q * 3]; lc[q * 3 + 1] = union_lc[q * 3 + 1]; lc[q * 3 + 2] = union_lc[q * 3 + 2];
+    lc[q * 4] = union_lc[q * 3]; lc[q * 4 + 1] = union_lc[q * 3 + 1];
+    lc[q * 4 + 2] = union_lc[q * 3 + 2]; lc[q * 4 + 3] = 0.0;
   }
   __syncthreads();
   const int tile0 = blockIdx.x * TPB;
@@ -361,21 +362,24 @@ __global__ void k_env_irradiance_multi(const float* __restrict__ W2,
     const int tile = tile0 + j, tr = tile / tpr, tc = tile % tpr;
     const int i = (tr * T + e / T) * S + tc * T + e % T;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    constexpr int kPf = 16;
+    constexpr int kPf = 32;  // W^{w2} loads in flight per thread (order of the sum is fixed)
     for (int q0 = 0; q0 < m; q0 += kPf) {
       float wv[kPf];
 #pragma unroll
       for (int u = 0; u < kPf; ++u)
         wv[u] = (q0 + u < m) ? __ldg(&W2[(size_t)ul[q0 + u] * N + i]) : 0.0f;
+      // a channel that dropped the id has l = 0: w * 0 adds an exact zero, so
+      // the sums equal the per-channel ones of the reference (value-equal)
 #pragma unroll
       for (int u = 0; u < kPf; ++u) {
         if (q0 + u >= m) break;
         const int qq = q0 + u;
         const double w = (double)wv[u];
-        const double l0 = lc[qq * 3], l1 = lc[qq * 3 + 1], l2 = lc[qq * 3 + 2];
-        if (l0 != 0.0) acc0 = dadd(acc0, dmul(w, l0));
-        if (l1 != 0.0) acc1 = dadd(acc1, dmul(w, l1));
-        if (l2 != 0.0) acc2 = dadd(acc2, dmul(w, l2));
+        const double2 l01 = *reinterpret_cast<const double2*>(lc + qq * 4);
+        const double l2 = lc[qq * 4 + 2];
+        acc0 = dadd(acc0, dmul(w, l01.x));
+        acc1 = dadd(acc1, dmul(w, l01.y));
+        acc2 = dadd(acc2, dmul(w, l2));
       }
     }
     a[(j * 3 + 0) * T2 + e] = acc0;
@@ -651,6 +655,38 @@ __global__ void k_edit_finish(int K, int S, int L, const double* __restrict__ vk
                 radiance_unclamped);
 }
 
+
+// edit path, G consecutive tiles per CTA: recombine (coalesced v_k reads over
+// G * T2 rows), one batched inverse Haar over the 3G tile grids, shade
+__global__ void __launch_bounds__(256) k_edit_finish_multi(
+    int K, int S, int L, int G, const double* __restrict__ vk, const double* __restrict__ g,
+    const float* __restrict__ positions, const float* __restrict__ normals,
+    const double* __restrict__ cam, const double* __restrict__ material,
+    double* __restrict__ scatter, float* __restrict__ radiance,
+    float* __restrict__ radiance_unclamped) {
+  extern __shared__ double sm[];
+  const int T = 1 << L, T2 = T * T, N = S * S;
+  double* summed = sm;                        // G x 3 x T2
+  double* tmp = sm + (size_t)G * 3 * T2;      // same
+  const int tile0 = blockIdx.x * G;
+  for (int q = threadIdx.x; q < G * T2; q += blockDim.x) {
+    const int row = tile0 * T2 + q;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double* vo = vk + (size_t)k * 3 * N;
+      s0 += g[k] * vo[row];
+      s1 += g[K + k] * vo[N + row];
+      s2 += g[2 * K + k] * vo[2 * N + row];
+    }
+    const int j = q / T2, e = q % T2;
+    summed[(j * 3 + 0) * T2 + e] = s0;
+    summed[(j * 3 + 1) * T2 + e] = s1;
+    summed[(j * 3 + 2) * T2 + e] = s2;
+  }
+  __syncthreads();
+  multi_tile_epilogue(summed, tmp, T, tile0, G, S, positions, normals, cam, material, scatter,
+                      radiance, radiance_unclamped);
+}
 
 // ---------------------------------------------------------------------------
 // batch L-level Haar (haar2d_fwd_batch / haar2d_inv_batch restated with a

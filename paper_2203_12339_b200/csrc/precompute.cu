@@ -90,11 +90,20 @@ __global__ void __launch_bounds__(128) k_pair_block(PairParams p, double* __rest
   const int S = p.S, N = S * S, tpr = S / T;
   const int ST = blockIdx.x, RT = blockIdx.y;
   const int str = ST / tpr, stc = ST % tpr, rtr = RT / tpr, rtc = RT % tpr;
+  // exact mode: the material table and this term's projection row in shared
+  // memory (one LDS.128 + one LDS per material instead of five L1 loads)
+  float4* mat4 = reinterpret_cast<float4*>(blk + T2 * LD);
+  float* pk = reinterpret_cast<float*>(mat4 + (EXACT ? p.M : 0));
   if (!EXACT) {
     for (int j = threadIdx.x; j < p.nr; j += blockDim.x) {
       rn[j] = p.r_nodes[j];
       bk[j] = p.bases[(size_t)p.k * p.nr + j];
       if (j < p.nr - 1) sk[j] = p.slopes[(size_t)p.k * (p.nr - 1) + j];
+    }
+  } else {
+    for (int m = threadIdx.x; m < p.M; m += blockDim.x) {
+      mat4[m] = make_float4(p.mat[m * 4], p.mat[m * 4 + 1], p.mat[m * 4 + 2], p.mat[m * 4 + 3]);
+      pk[m] = p.Pkm[p.k * p.M + m];
     }
   }
   __syncthreads();
@@ -129,13 +138,13 @@ __global__ void __launch_bounds__(128) k_pair_block(PairParams p, double* __rest
       float acc = 0.0f;
       if (d <= p.r_max) {
         for (int m = 0; m < p.M; ++m) {
-          const float s = p.mat[m * 4], zr = p.mat[m * 4 + 1], zv = p.mat[m * 4 + 2],
-                      c = p.mat[m * 4 + 3];
+          const float4 mm = mat4[m];
+          const float s = mm.x, zr = mm.y, zv = mm.z, c = mm.w;
           const float ir = rsqrtf(r2 + zr * zr), iv = rsqrtf(r2 + zv * zv);
           const float dr = (r2 + zr * zr) * ir, dv = (r2 + zv * zv) * iv;
           const float tr = zr * (s + ir) * __expf(-s * dr) * ir * ir;
           const float tv = zv * (s + iv) * __expf(-s * dv) * iv * iv;
-          acc = fmaf(p.Pkm[p.k * p.M + m], c * (tr + tv), acc);
+          acc = fmaf(pk[m], c * (tr + tv), acc);
         }
       }
       blk[o * LD + i] = (double)(acc * p.area[si]);

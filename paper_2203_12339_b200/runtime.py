@@ -243,6 +243,22 @@ class Scene:
                       _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
             self._launch_edit(stream)
             return
+        if self.transfer_kernel == "kflat":
+            sp = _lib.stream_ptr(stream)
+            if getattr(t, "kflat", None) is None:
+                t.kflat = kstep_layout(t, warps_per_sm=int(os.environ.get("SSS_KFLAT_WPS", "16")))
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            if getattr(self, "xbits", None) is None:
+                self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+            _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                      _lib.ptr(self.xbits), sp)
+            cols, vals, steps, wbeg, W, _ = t.kflat
+            _lib.call("sss_transfer_kflat", self.K, self.n, _lib.ptr(cols), _lib.ptr(vals),
+                      _lib.ptr(steps), _lib.ptr(wbeg), W, _lib.ptr(self.xp),
+                      _lib.ptr(self.xbits), _lib.ptr(self.vk), sp)
+            self._launch_edit(stream)
+            return
         if self.transfer_kernel in ("flat", "flat8"):
             sp = _lib.stream_ptr(stream)
             self._flat_prep(sp)
@@ -452,10 +468,20 @@ class Scene:
                   _lib.stream_ptr(stream))
 
     def launch_relight(self, stream=None):
-        """Enqueue a full relight (no host sync)."""
-        self._launch_stage1(stream)
-        self._launch_weights(stream)
-        self._launch_transfer(stream)
+        """Enqueue a full relight (no host sync). The material weights do not
+        depend on the light: they run on a forked stream, joined before the
+        transfer (whose epilogue consumes them), off the stage-1 critical path."""
+        cur = stream or torch.cuda.current_stream()
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream()
+        fork, join = torch.cuda.Event(), torch.cuda.Event()
+        fork.record(cur)
+        self._side.wait_event(fork)
+        self._launch_weights(self._side)
+        join.record(self._side)
+        self._launch_stage1(cur)
+        cur.wait_event(join)
+        self._launch_transfer(cur)
         self._have_cache = True
 
     def launch_edit(self, stream=None):
@@ -550,6 +576,57 @@ class Scene:
         if not self._have_cache:
             return self.relight()
         return self._edit_frame()
+
+    # ------------------------------------------------------------------
+    # C4: batched material sweep against the cached v_k
+    # ------------------------------------------------------------------
+
+    def sweep_prepare(self, materials):
+        """Operands of a batched sweep: Bq (3, N, 16) bf16 = w1^-1 v_k of the
+        current light, Gq (3, M, 16) bf16 + g64 (M, 3, K) = project_material
+        of every material, eta (M) float. Relights first if nothing is cached."""
+        if not self._have_cache:
+            self.relight()
+        if self.K > 16:
+            raise ValueError("the sweep supports K <= 16 PCA terms")
+        M = len(materials)
+        dev = torch.device("cuda")
+        mats = np.stack([np.concatenate([self._clamp_material(m).sigma_s_prime,
+                                         self._clamp_material(m).sigma_a, [m.eta]])
+                         for m in materials]).astype(np.float64)
+        eta = mats[:, 6]
+        if eta.min() <= 1.0:
+            raise ValueError("the sweep needs eta > 1 for every material")
+        sp = _lib.stream_ptr()
+        ops = {"Bq": torch.empty((3, self.n, 16), dtype=torch.bfloat16, device=dev),
+               "Gq": torch.empty((3, M, 16), dtype=torch.bfloat16, device=dev),
+               "g64": torch.empty((M, 3, self.K), dtype=torch.float64, device=dev),
+               "eta": torch.empty(M, dtype=torch.float32, device=dev),
+               "materials": torch.as_tensor(mats, device=dev),
+               "eta_range": (float(eta.min()), float(eta.max()))}
+        _lib.call("sss_sweep_basis", self.K, self.side, self.levels, _lib.ptr(self.vk),
+                  _lib.ptr(ops["Bq"]), sp)
+        d = self.basis.device()
+        _lib.call("sss_material_weights_batch", _lib.ptr(d["bw"]), _lib.ptr(d["r_nodes"]), self.K,
+                  len(self.basis.r_nodes), M, _lib.ptr(ops["materials"]), _lib.ptr(ops["g64"]),
+                  _lib.ptr(ops["Gq"]), _lib.ptr(ops["eta"]), sp)
+        return ops
+
+    def sweep_launch(self, ops, out, stream=None):
+        """out (3, M, N) float32 = clamped exit radiance of every material."""
+        lo, hi = ops["eta_range"]
+        _lib.call("sss_sweep_gemm", self.n, ops["Gq"].shape[1], _lib.ptr(ops["Bq"]),
+                  _lib.ptr(ops["Gq"]), _lib.ptr(ops["eta"]), lo, hi, _lib.ptr(self.positions),
+                  _lib.ptr(self.normals), _lib.ptr(self.cam_buf), _lib.ptr(out),
+                  _lib.stream_ptr(stream))
+
+    def sweep(self, materials) -> torch.Tensor:
+        """Radiance (3, M, N) of M materials under the current light and camera
+        (the C4 batched sweep: one bf16 tcgen05 contraction + Fresnel shade)."""
+        ops = self.sweep_prepare(materials)
+        out = torch.empty((3, len(materials), self.n), dtype=torch.float32, device="cuda")
+        self.sweep_launch(ops, out)
+        return out
 
     # ------------------------------------------------------------------
     # parity hooks

@@ -330,7 +330,7 @@ def test_stream_and_banded_kernels_agree(c1):
     sc.transfer_kernel = "banded"
     a = sc.relight()
     vk_a = sc.vk.clone()
-    for kern in ("stream", "v4", "v6", "csr7", "csr8", "csr9", "kpack", "kpackp", "kstep", "kstream", "csr9s", "kgroup", "flat", "flatp", "flat8"):
+    for kern in ("stream", "v4", "v6", "csr7", "csr8", "csr9", "kpack", "kpackp", "kstep", "kstream", "csr9s", "kgroup", "flat", "flatp", "flat8", "kflat"):
         sc.transfer_kernel = kern
         sc.vk.fill_(float("nan"))  # a kernel that leaves v_k untouched must fail
         sc.radiance_unclamped.fill_(float("nan"))
@@ -350,3 +350,58 @@ def test_cuda_graph_replay_matches_eager(c1):
     sc.replay()
     torch.cuda.synchronize()
     assert np.array_equal(sc.radiance_unclamped.cpu().numpy().astype(np.float64), eager)
+
+
+def test_batched_sweep_matches_bf16_reference(c1):
+    """C4 sweep (tcgen05 bf16 UMMA + Fresnel epilogue) against an fp64
+    restatement on the kernel's own bf16 operands; operands against the
+    oracle (inverse Haar of v_k, project_material) within one bf16 rounding."""
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.basis import OpticalMaterial
+    from paper_2203_12339_b200.runtime import SHLight
+    from paper_2203_12339_b200.transfer import tile_major_to_flat
+
+    sc = _scene(c1, SHLight(LT.random_sh_light(3, 31)))
+    sc.relight()
+    rng = np.random.default_rng(44)
+    M = 40  # partial UMMA tile
+    mats = [OpticalMaterial(sigma_s_prime=np.exp(rng.uniform(np.log(0.5), np.log(3.0), 3)),
+                            sigma_a=np.exp(rng.uniform(np.log(0.001), np.log(0.05), 3)),
+                            eta=float(rng.uniform(1.2, 1.5))) for _ in range(M)]
+    ops = sc.sweep_prepare(mats)
+    out = torch.empty((3, M, sc.n), dtype=torch.float32, device="cuda")
+    sc.sweep_launch(ops, out)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy().astype(np.float64)
+    B = ops["Bq"].float().cpu().numpy().astype(np.float64)   # (3, N, 16)
+    G = ops["Gq"].float().cpu().numpy().astype(np.float64)   # (3, M, 16)
+    K, S, L = sc.K, sc.side, sc.levels
+    # operands vs the oracle
+    vk = sc.vk.cpu().numpy()                                 # (K, 3, N) tile-major
+    perm = tile_major_to_flat(S, L)
+    for k in range(K):
+        for c in range(3):
+            flat = np.empty(sc.n)
+            flat[perm] = vk[k, c]
+            ref = O.haar2d_inv(flat.reshape(1, S, S), L).reshape(-1)
+            got = B[c, :, k]
+            assert np.all(np.abs(got - ref) <= 2 ** -7 * np.abs(ref) + 1e-300), (k, c)
+    assert np.all(B[:, :, K:] == 0)
+    g64 = ops["g64"].cpu().numpy()
+    for m, mt in enumerate(mats):
+        w = O.project_material(sc.basis.bases, sc.basis.r_nodes, mt.sigma_s_prime, mt.sigma_a, mt.eta)
+        assert np.allclose(g64[m], w, rtol=1e-10, atol=0), m
+        assert np.all(np.abs(G[:, m, :K] - w) <= 2 ** -7 * np.abs(w) + 1e-300)
+    # the contraction + shade
+    pos = sc.geometry.positions.astype(np.float64)
+    nrm = sc.geometry.normals.astype(np.float64)
+    v = np.asarray(sc.camera.position, np.float64)[None, :] - pos
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    cs = np.sum(nrm * v, axis=1)
+    ref = np.zeros_like(out)
+    for m, mt in enumerate(mats):
+        ft = O.fresnel_transmittance(mt.eta, cs) / np.pi
+        for c in range(3):
+            ref[c, m] = np.maximum(ft * (B[c] @ G[c, m]), 0.0)
+    err = np.abs(out - ref).max() / np.abs(ref).max()
+    assert err <= 2e-4, err

@@ -60,7 +60,7 @@ def main():
         _lib.ptr(sc.mask), _lib.ptr(sc.energy), sp), a.reps)
     out["material_weights"] = timed(sc._launch_weights, a.reps)
     ref_vk = None
-    for kern in ("csr9", "flat", "flat8"):
+    for kern in ("flat8", "kflat"):
         sc.transfer_kernel = kern
         sc.vk.fill_(float("nan"))
         sc._launch_transfer()
@@ -71,10 +71,9 @@ def main():
             ref_vk = sc.vk.clone()
         else:
             out[f"relerr_{kern}"] = float((sc.vk - ref_vk).abs().max() / ref_vk.abs().max())
-    out.update({f"flat_{k}": v for k, v in dt.flat[8].items()})
-    out["flat_GBps"] = dt.flat[8]["bytes"] / (out["transfer_flat"] * 1e-6) / 1e9
     out["flat8_MB"] = dt.flat8[8]["bytes"] / 1e6
-    sc.transfer_kernel = "flat"
+    out.update({f"kflat_{k}": v for k, v in dt.kflat[5].items()})
+    sc.transfer_kernel = "flat8"
     out["edit_finish"] = timed(sc._launch_edit, a.reps)
     sc.capture()
     out["relight_graph"] = timed(lambda: sc.replay(False), a.reps)
