@@ -46,6 +46,8 @@ def _args():
     ap.add_argument("--cpu-sample-rows", type=int, default=32, help="1/x of tiles in the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--side", type=int, default=None, help="override the geometry-image side (testing)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the C4 sweep / C5 pair-pass measurements in the JSON line")
     return ap.parse_args()
 
 
@@ -206,11 +208,12 @@ def run_ours(a, cfg):
     for f in range(min(a.steps, 20)):
         ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ka.record(stream)
-        scene._launch_transfer()
+        scene.launch_transfer_core()
         kb.record(stream)
         kt.append((ka, kb))
     torch.cuda.synchronize()
     k_ms = float(np.mean([x.elapsed_time(y) for x, y in kt]))
+    kname = scene.transfer_kernel
     # algorithmic bytes of one transfer launch (SURVEY §8d B_T + B_c), with the
     # selection of the current frame: entries whose w0 column is kept by any
     # channel (8 B each: u32 col + f32 val) + row pointers + v_k cache write +
@@ -276,6 +279,30 @@ def run_ours(a, cfg):
     cpu = None
     if rank == 0 and ws == 1 and not a.no_cpu_baseline:
         cpu = cpu_baseline(cfg, scene, dt, g, b, faces, mats, a.cpu_sample_rows, steps=2, warmup=0)
+    secondary = None
+    if rank == 0 and not a.no_secondary and a.side is None:
+        # the other §8 rows, measured in the same run on the same GPU: C4 sweep
+        # (HBM-write roofline) and the C5 pair pass (FP32/SFU), one term each mode
+        del scene
+        torch.cuda.empty_cache()
+        sys.path.insert(0, str(ROOT / "tools"))
+        import precompute_bench
+        import sweep_bench
+
+        c4 = sweep_bench.measure(256, 20)
+        c5 = precompute_bench.measure(256, skip_full=True, ks=1)
+        secondary = {
+            "c4_batched_sweep": {"kernel": "k_sweep_umma (tcgen05 bf16 UMMA, fp32 TMEM accum)",
+                                 "us": c4["sweep_gemm_us"], "achieved_GBps": c4["achieved_GBps"],
+                                 "peak_GBps": c4["peak_GBps"], "frac": c4["frac"],
+                                 "bound": "hbm (fp32 output write)", "materials": c4["materials"],
+                                 "K": c4["K"]},
+            "c5_pair_pass": {"lerp_s_per_term": c5["pair_pass_lerp_s_per_k"],
+                             "exact_s_per_term": c5["pair_pass_exact_s_per_k"],
+                             "lerp_pairs_per_s_all_K": c5["pair_pass_lerp_pairs_per_s_all_K"],
+                             "exact_pairs_per_s_all_K": c5["pair_pass_exact_pairs_per_s_all_K"],
+                             "exact_mufu_per_s": c5["exact_mufu_per_s_per_k"],
+                             "pairs": c5["pairs"], "bound": "SFU/FP32 (exact), FP64 (lerp)"}}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
@@ -295,16 +322,20 @@ def run_ours(a, cfg):
                 "parallelism": f"{ws} independent objects (1 per GPU)" if ws > 1 else "1 GPU",
                 "precompute_s": stats.get("precompute_s"), "precompute_pairs": stats.get("pairs"),
             },
-            "roofline": {"bound": "hbm", "kernel": "k_transfer_relight", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": f"transfer[{kname}]",
+                         "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes, "stored_bytes_per_launch": all_bytes,
                          "touched_nnz": touched, "kernel_ms": k_ms},
             "e2e": e2e,
-            "gpu_launches": 6 * a.steps + 2 * n_edit,
+            # per relight: env_project, env_union, env_irradiance, select, weights,
+            # pack_x_bits, transfer, edit_finish; per edit: weights, edit_finish
+            "gpu_launches": 8 * a.steps + 2 * n_edit,
             "clocks": clk,
             "relight_ms": relight_ms, "edit_ms": edit_ms,
             "cpu_baseline": cpu,
+            "secondary": secondary,
         }
         print(json.dumps(line))
     if ws > 1:
@@ -312,9 +343,10 @@ def run_ours(a, cfg):
 
 
 def cpu_baseline(cfg, scene, dt, g, b, faces, mats, sample, steps=2, warmup=0):
-    """Oracle port of the C3 frame on the host (numpy, 1 thread of BLAS-free
-    code): stage 1 in full, stage 2 on every `sample`-th tile's rows (scaled),
-    stages 3-5 in full. Returns the cpu_baseline object."""
+    """Oracle port of the C3 frame on the host (numpy; stage 2 split over all
+    host cores with a thread pool): stage 1 in full, stage 2 on every
+    `sample`-th tile's rows (scaled), stages 3-5 in full. Returns the
+    cpu_baseline object."""
     import torch
 
     from oracle import sss_oracle as O
@@ -331,6 +363,11 @@ def cpu_baseline(cfg, scene, dt, g, b, faces, mats, sample, steps=2, warmup=0):
     tiles = np.arange(0, n // T2, sample)
     rows = (tiles[:, None] * T2 + np.arange(T2)[None, :]).reshape(-1)
     cam = np.array(scene.camera.position)
+    import concurrent.futures as cf
+
+    cores = os.cpu_count() or 1
+    chunks = np.array_split(rows, cores)
+    pool = cf.ThreadPoolExecutor(max_workers=cores)
     times = []
     for i in range(warmup + steps):
         f = i
@@ -343,8 +380,10 @@ def cpu_baseline(cfg, scene, dt, g, b, faces, mats, sample, steps=2, warmup=0):
             x[c, sel[c].indices] = sel[c].values
         x = x[:, tm2flat]  # the operator's columns are tile-major ids
         t1 = time.perf_counter()
-        for k in range(K):
-            O.csr_rows_apply(rp[k], cols, vals, rows, x)
+        # stage 2 on every host core: (k, row chunk) tasks in a thread pool
+        # (numpy's gather / bincount release the GIL)
+        list(pool.map(lambda kc: O.csr_rows_apply(rp[kc[0]], cols, vals, kc[1], x),
+                      [(k, ch) for k in range(K) for ch in chunks]))
         t2 = time.perf_counter()
         m = scene.material
         w = O.project_material(b.bases, b.r_nodes, m.sigma_s_prime, m.sigma_a, m.eta)
@@ -354,10 +393,12 @@ def cpu_baseline(cfg, scene, dt, g, b, faces, mats, sample, steps=2, warmup=0):
         t3 = time.perf_counter()
         if i >= warmup:
             times.append((t1 - t0) + (t2 - t1) * (n / rows.size) + (t3 - t2))
+    pool.shutdown()
     per_frame = float(np.mean(times))
-    return {"value": n / per_frame, "unit": UNIT, "cores": 1, "kind": "port",
+    return {"value": n / per_frame, "unit": UNIT, "cores": cores, "kind": "port",
             "ms_per_step": per_frame * 1e3,
-            "sample": f"C3 frame, oracle (numpy) port: stage 1 + stages 3-5 in full, stage 2 on "
+            "sample": f"C3 frame, oracle (numpy) port on {cores} host threads: stage 1 + stages 3-5 "
+                      f"in full, stage 2 on "
                       f"1/{sample} of the tiles ({rows.size} of {n} rows, scaled linearly), "
                       f"{steps} frames, operator from the GPU precompute"}
 

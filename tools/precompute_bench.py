@@ -17,12 +17,8 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--side", type=int, default=256)
-    ap.add_argument("--skip-full", action="store_true")
-    ap.add_argument("--ks", type=int, default=2, help="PCA terms timed for the pair pass")
-    a = ap.parse_args()
+def measure(side=256, skip_full=False, ks=2):
+    """C5 measurement dict (used by bench.py and main)."""
     from paper_2203_12339_b200 import _lib
     from paper_2203_12339_b200.basis import build_basis
     from paper_2203_12339_b200.config import CONFIGS
@@ -30,7 +26,7 @@ def main():
     from paper_2203_12339_b200.precompute import PairPass, precompute_compressed
 
     _lib.load()
-    cfg = CONFIGS["dipole_precompute_256"].with_(side=a.side)
+    cfg = CONFIGS["dipole_precompute_256"].with_(side=side)
     g = make_geometry_image(cfg.side, cfg.radius, cfg.bump_amp, cfg.bump_terms, cfg.seed)
     b = build_basis(cfg.K, cfg.lattice)
     n = g.count
@@ -43,7 +39,7 @@ def main():
         pp.run(0, D, M)
         torch.cuda.synchronize()
         ms = []
-        for k in range(a.ks):
+        for k in range(ks):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             pp.run(k, D, M)
@@ -62,7 +58,7 @@ def main():
             out["exact_mufu_per_s_per_k"] = mufu / t
     del D, M
     torch.cuda.empty_cache()
-    if not a.skip_full:
+    if not skip_full:
         for exact in (False, True):
             st = {}
             torch.cuda.synchronize()
@@ -75,7 +71,16 @@ def main():
             out[f"precompute_{key}_nnz"] = int(dt.nnz)
             del dt
             torch.cuda.empty_cache()
-    print(json.dumps(out))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--side", type=int, default=256)
+    ap.add_argument("--skip-full", action="store_true")
+    ap.add_argument("--ks", type=int, default=2, help="PCA terms timed for the pair pass")
+    a = ap.parse_args()
+    print(json.dumps(measure(a.side, a.skip_full, a.ks)))
 
 
 if __name__ == "__main__":

@@ -26,11 +26,8 @@ def timed(fn, reps):
     return float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--side", type=int, default=256)
-    ap.add_argument("--reps", type=int, default=20)
-    a = ap.parse_args()
+def measure(side=256, reps=20):
+    """C4 sweep measurement dict (used by bench.py and main)."""
     from paper_2203_12339_b200 import _lib
     from paper_2203_12339_b200 import lighting as LT
     from paper_2203_12339_b200.basis import OpticalMaterial, build_basis
@@ -40,7 +37,7 @@ def main():
     from paper_2203_12339_b200.runtime import Scene, SHLight
 
     _lib.load()
-    cfg = CONFIGS["batched_sweep_256"].with_(side=a.side)
+    cfg = CONFIGS["batched_sweep_256"].with_(side=side)
     M = cfg.extra["materials"]
     g = make_geometry_image(cfg.side, cfg.radius, cfg.bump_amp, cfg.bump_terms, cfg.seed)
     b = build_basis(cfg.K, cfg.lattice)
@@ -55,8 +52,8 @@ def main():
                             eta=float(rng.uniform(lo_e, hi_e))) for _ in range(M)]
     ops = sc.sweep_prepare(mats)
     out = torch.empty((3, M, sc.n), dtype=torch.float32, device="cuda")
-    us_gemm = timed(lambda: sc.sweep_launch(ops, out), a.reps)
-    us_prep = timed(lambda: sc.sweep_prepare(mats), max(3, a.reps // 4))
+    us_gemm = timed(lambda: sc.sweep_launch(ops, out), reps)
+    us_prep = timed(lambda: sc.sweep_prepare(mats), max(3, reps // 4))
     out_bytes = out.numel() * 4
     in_bytes = 3 * sc.n * 16 * 2 + 3 * M * 16 * 2 + sc.n * 24 + M * 4
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
@@ -68,7 +65,17 @@ def main():
            "flops": 2 * 3 * sc.n * M * cfg.K,
            "radiance_points_per_s": 3 * M * sc.n / (us_gemm * 1e-6) / 3,
            "finite": bool(torch.isfinite(out).all()), "max": float(out.max())}
-    print(json.dumps(res))
+    del sc, dt, ops, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--side", type=int, default=256)
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    print(json.dumps(measure(a.side, a.reps)))
 
 
 if __name__ == "__main__":
