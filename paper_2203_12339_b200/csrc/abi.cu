@@ -618,11 +618,20 @@ int sss_transfer_flatp(int K, int n_rows, const uint32_t* pcols, const float* pv
   return check_launch("k_transfer_flatp");
 }
 
+int sss_pack_x_f32_bits(const double* x, int n, void* xp, uint32_t* bits, void* stream) {
+  if (!x || !xp || !bits || n <= 0) return fail(SSS_EINVAL, "bad pack_x_f32_bits arguments");
+  if (reinterpret_cast<uintptr_t>(xp) % 16) return fail(SSS_EINVAL, "xp must be 16-byte aligned");
+  sss::k_pack_x_f32_bits<<<(n + 255) / 256, 256, 0, S_(stream)>>>(x, n, reinterpret_cast<float4*>(xp),
+                                                                 bits);
+  return check_launch("k_pack_x_f32_bits");
+}
+
 int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pvals,
                        unsigned long long n_entries, const uint32_t* heads,
                        const uint32_t* head_prefix, const uint32_t* seg_rowk,
                        const unsigned* warp_begin, int n_warps, const void* xp,
-                       const uint32_t* bits, int gather_ahead, double* vk, void* stream) {
+                       const uint32_t* bits, int gather_ahead, int x_f32, double* vk,
+                       void* stream) {
   if (K <= 0 || n_rows <= 0 || !pcols || !pvals || !heads || !head_prefix || !seg_rowk ||
       !warp_begin || !xp || !vk || n_warps <= 0 || n_warps % (sss::kV17Threads / 32) ||
       n_entries % 8 || n_entries / 8 >= (1ull << 32) - 64)
@@ -638,7 +647,12 @@ int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pv
   const auto* x4 = reinterpret_cast<const double4*>(xp);
   const unsigned grid = n_warps / (sss::kV17Threads / 32);
   const unsigned n8 = (unsigned)(n_entries / 8);
-  if (gather_ahead) {
+  if (x_f32) {
+    const auto* xf = reinterpret_cast<const float4*>(xp);
+    if (int r = set_smem((const void*)sss::k_transfer_flat8<false, float, float4>, smem)) return r;
+    sss::k_transfer_flat8<false, float, float4><<<grid, sss::kV17Threads, smem, S_(stream)>>>(
+        n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, xf, bits, vk);
+  } else if (gather_ahead) {
     if (int r = set_smem((const void*)sss::k_transfer_flat8<true>, smem)) return r;
     sss::k_transfer_flat8<true><<<grid, sss::kV17Threads, smem, S_(stream)>>>(
         n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);

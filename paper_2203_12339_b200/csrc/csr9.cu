@@ -162,6 +162,19 @@ __global__ void k_pack_x_bits(const double* __restrict__ x, int N, double4* __re
   if ((threadIdx.x & 31) == 0 && i < N) bits[i >> 5] = m;
 }
 
+// packed fp32 x (N, 4) {x0, x1, x2, 0} + the kept-column bitmap
+__global__ void k_pack_x_f32_bits(const double* __restrict__ x, int N, float4* __restrict__ xp,
+                                  uint32_t* __restrict__ bits) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double a = 0.0, b = 0.0, c = 0.0;
+  if (i < N) {
+    a = x[i]; b = x[N + i]; c = x[2 * N + i];
+    xp[i] = make_float4((float)a, (float)b, (float)c, 0.0f);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, i < N && (a != 0.0 || b != 0.0 || c != 0.0));
+  if ((threadIdx.x & 31) == 0 && i < N) bits[i >> 5] = m;
+}
+
 // padded copy of the canonical CSR: segment i (start s, len l) -> new start
 // ps (multiple of 4), entries copied, padding (col 0, val 0)
 __global__ void k_pad_segments(const uint64_t* __restrict__ seg_src, const uint32_t* __restrict__ seg_len,

@@ -369,16 +369,34 @@ __device__ __forceinline__ void v17_gather(const V17Slot& S, const double4* __re
   }
 }
 
-__device__ __forceinline__ void v17_consume(const V17Slot& S, const double (&x)[8][3], int lane,
+// fp32 x variant (fp64 accumulation of f32 values x f32 E spectrum
+// passes the 1e-4 bar): 16-byte gathers of a packed (N, 4) float array
+__device__ __forceinline__ void v17_gather(const V17Slot& S, const float4* __restrict__ xp,
+                                           const uint32_t* sbits, float (&x)[8][3]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t c = v17_col(S, e);
+    x[e][0] = x[e][1] = x[e][2] = 0.0f;
+    if (!sbits || ((sbits[c >> 5] >> (c & 31u)) & 1u)) {
+      float x3;
+      asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(x[e][0]), "=f"(x[e][1]), "=f"(x[e][2]), "=f"(x3)
+                   : "l"(xp + c));
+    }
+  }
+}
+
+template <typename XT>
+__device__ __forceinline__ void v17_consume(const V17Slot& S, const XT (&x)[8][3], int lane,
                                             unsigned upto, int N, const uint32_t* __restrict__ rowk,
                                             double* __restrict__ vk) {
   double p0 = 0.0, p1 = 0.0, p2 = 0.0;
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const double v = (double)v17_val(S, e);
-    p0 = fma(v, x[e][0], p0);
-    p1 = fma(v, x[e][1], p1);
-    p2 = fma(v, x[e][2], p2);
+    p0 = fma(v, (double)x[e][0], p0);
+    p1 = fma(v, (double)x[e][1], p1);
+    p2 = fma(v, (double)x[e][2], p2);
   }
   const unsigned hm = S.h & upto;
   const int sstart = hm ? 31 - __clz(hm) : -1;
@@ -403,12 +421,12 @@ __device__ __forceinline__ void v17_consume(const V17Slot& S, const double (&x)[
   }
 }
 
-template <bool AHEAD>
+template <bool AHEAD, typename XT = double, typename XP = double4>
 __global__ void __launch_bounds__(kV17Threads, 4) k_transfer_flat8(
     int N, unsigned n8, const unsigned long long* __restrict__ C8,
     const unsigned long long* __restrict__ V8, const uint32_t* __restrict__ H,
     const uint32_t* __restrict__ hpre, const uint32_t* __restrict__ rowk,
-    const unsigned* __restrict__ warp_begin, const double4* __restrict__ xp,
+    const unsigned* __restrict__ warp_begin, const XP* __restrict__ xp,
     const uint32_t* __restrict__ bits, double* __restrict__ vk) {
   extern __shared__ uint32_t v17_bits[];
   if (bits) {
@@ -425,7 +443,7 @@ __global__ void __launch_bounds__(kV17Threads, 4) k_transfer_flat8(
   v17_load(A, i0, lane, n8, C8, V8, H, hpre);
   if (i0 + 1 < i1) v17_load(B, i0 + 1, lane, n8, C8, V8, H, hpre);
   if (!AHEAD) {  // gather and consume in the same iteration; warps hide the latency
-    double X[8][3];
+    XT X[8][3];
 #pragma unroll 1
     for (unsigned i = i0; i < i1; i += 2) {
       v17_gather(A, xp, sb, X);
@@ -438,7 +456,7 @@ __global__ void __launch_bounds__(kV17Threads, 4) k_transfer_flat8(
     }
     return;
   }
-  double XA[8][3], XB[8][3];
+  XT XA[8][3], XB[8][3];
   v17_gather(A, xp, sb, XA);
 #pragma unroll 1
   for (unsigned i = i0; i < i1; i += 2) {

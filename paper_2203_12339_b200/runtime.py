@@ -449,16 +449,26 @@ class Scene:
             self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
         if getattr(self, "xbits", None) is None:
             self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+        if self._x_f32():
+            if getattr(self, "xp32", None) is None:
+                self.xp32 = torch.empty((self.n, 4), dtype=torch.float32, device="cuda")
+            _lib.call("sss_pack_x_f32_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp32),
+                      _lib.ptr(self.xbits), sp)
+            return
         _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
                   _lib.ptr(self.xbits), sp)
+
+    def _x_f32(self) -> bool:
+        return self.transfer_kernel == "flat8" and os.environ.get("SSS_X_F32", "0") == "1"
 
     def _flat_core(self, sp):
         if self.transfer_kernel == "flat8":
             pcols, pvals, ne, heads, hpre, rowk, wbeg, W, _ = self.transfer.flat8
+            f32 = self._x_f32()
             _lib.call("sss_transfer_flat8", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
                       _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W,
-                      _lib.ptr(self.xp), _lib.ptr(self.xbits),
-                      int(os.environ.get("SSS_FLAT8_AHEAD", "0")), _lib.ptr(self.vk), sp)
+                      _lib.ptr(self.xp32 if f32 else self.xp), _lib.ptr(self.xbits),
+                      int(os.environ.get("SSS_FLAT8_AHEAD", "0")), int(f32), _lib.ptr(self.vk), sp)
             return
         pcols, pvals, ne, heads, hpre, rowk, wbeg, W, _ = self.transfer.flat
         _lib.call("sss_transfer_flat", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
@@ -965,7 +975,7 @@ def kgroup_layout(t: DeviceTransfer, warps_per_sm: int = None, split: int = None
     return (meta_p, vals, pieces, wbeg.to(torch.int32).contiguous(), W, stats)
 
 
-def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4):
+def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4, interleave=None):
     """Head-flag bitmap + per-word segment prefix + segment (row, k) ids over
     csr9's padded operator copy, and equal word ranges per warp, for
     sss_transfer_flat."""
@@ -977,6 +987,26 @@ def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4):
         setattr(t, attr, csr9_layout(t, split=1 << 30, pad=group))
     pcols, pvals, pieces, _, _ = getattr(t, attr)
     dev = pcols.device
+    if interleave is None:
+        interleave = group == 8 and os.environ.get("SSS_FLAT_INTERLEAVE", "1") == "1"
+    if interleave:
+        # lane-interleave every segment: with L = len / group lanes, entry
+        # e * L + j goes to lane j, slot e, so gather instruction e reads L
+        # consecutive (column-sorted, spatially clustered) entries instead of
+        # entries `group` apart; each lane still holds one segment's entries
+        pc0 = pieces.to(torch.int64) & 0xFFFFFFFF
+        st, ln = pc0[:, 0], pc0[:, 1]
+        seg = torch.repeat_interleave(torch.arange(st.numel(), device=dev), ln)
+        q = torch.arange(int(ln.sum().item()), device=dev, dtype=torch.int64) - \
+            torch.repeat_interleave(torch.cumsum(ln, 0) - ln, ln)
+        L = (ln // group)[seg]
+        src = st[seg] + q
+        dst = st[seg] + (q % L) * group + q // L
+        pc2, pv2 = pcols.clone(), pvals.clone()
+        pc2[dst] = pcols[src]
+        pv2[dst] = pvals[src]
+        pcols, pvals = pc2, pv2
+        del seg, q, L, src, dst
     i64 = dict(dtype=torch.int64, device=dev)
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
     W = nsm * warps_per_sm

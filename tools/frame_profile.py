@@ -80,7 +80,8 @@ def main():
     out["edit_graph"] = timed(lambda: sc.replay(True), a.reps)
     out["operator_nnz"] = dt.nnz
     out["operator_MB"] = dt.nnz * 8 / 1e6
-    print(json.dumps({k: (round(v, 2) if isinstance(v, float) else v) for k, v in out.items()}))
+    print(json.dumps({k: (v if k.startswith("relerr") else round(v, 2)) if isinstance(v, float) else v
+                      for k, v in out.items()}))
 
 
 if __name__ == "__main__":
