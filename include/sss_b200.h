@@ -283,15 +283,17 @@ int sss_transfer_flatp(int K, int n_rows, const uint32_t* pcols, const float* pv
 
 /* ---- transfer v17: sss_transfer_flat over a copy with every (row, k)
  * segment padded to a multiple of 8 entries (pcols/pvals 32-byte aligned);
- * heads bit l of word i marks 8-entry group 32 i + l; gather_ahead != 0 issues
- * the x gathers one iteration ahead; x_f32 != 0: xp is the packed (N, 4)
+ * heads bit l of word i marks 8-entry group 32 i + l. variant: 0 = gather and
+ * consume per iteration, 1 = x gathers one iteration ahead, 4..8 = gathers in
+ * two halves of 4 entries with a register cap for `variant` resident CTAs per
+ * SM (6 = default: 24 warps / SM); x_f32 != 0: xp is the packed (N, 4)
  * float array of sss_pack_x_f32_bits (fp64 products and sums of f32 operator
  * values x f32 spectrum). n_warps a multiple of 4. Same contract. */
 int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pvals,
                        unsigned long long n_entries, const uint32_t* heads,
                        const uint32_t* head_prefix, const uint32_t* seg_rowk,
                        const unsigned* warp_begin, int n_warps, const void* xp,
-                       const uint32_t* bits, int gather_ahead, int x_f32, double* vk,
+                       const uint32_t* bits, int variant, int x_f32, double* vk,
                        void* stream);
 
 /* ---- packed fp32 x (n, 4) floats {x0, x1, x2, 0} + kept-column bitmap. */

@@ -630,8 +630,9 @@ int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pv
                        unsigned long long n_entries, const uint32_t* heads,
                        const uint32_t* head_prefix, const uint32_t* seg_rowk,
                        const unsigned* warp_begin, int n_warps, const void* xp,
-                       const uint32_t* bits, int gather_ahead, int x_f32, double* vk,
+                       const uint32_t* bits, int variant, int x_f32, double* vk,
                        void* stream) {
+  const int gather_ahead = variant;
   if (K <= 0 || n_rows <= 0 || !pcols || !pvals || !heads || !head_prefix || !seg_rowk ||
       !warp_begin || !xp || !vk || n_warps <= 0 || n_warps % (sss::kV17Threads / 32) ||
       n_entries % 8 || n_entries / 8 >= (1ull << 32) - 64)
@@ -647,7 +648,21 @@ int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pv
   const auto* x4 = reinterpret_cast<const double4*>(xp);
   const unsigned grid = n_warps / (sss::kV17Threads / 32);
   const unsigned n8 = (unsigned)(n_entries / 8);
-  if (x_f32) {
+  if (gather_ahead >= 4) {  // split-half variants with a register cap: 4 + min CTAs/SM - 4
+    const int minb = gather_ahead;
+#define SSS_F8S(MB)                                                                               \
+    do {                                                                                          \
+      if (int r = set_smem((const void*)sss::k_transfer_flat8s<MB>, smem)) return r;              \
+      sss::k_transfer_flat8s<MB><<<grid, sss::kV17Threads, smem, S_(stream)>>>(                   \
+          n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);            \
+    } while (0)
+    if (minb == 4) SSS_F8S(4);
+    else if (minb == 5) SSS_F8S(5);
+    else if (minb == 7) SSS_F8S(7);
+    else if (minb == 8) SSS_F8S(8);
+    else SSS_F8S(6);
+#undef SSS_F8S
+  } else if (x_f32) {
     const auto* xf = reinterpret_cast<const float4*>(xp);
     if (int r = set_smem((const void*)sss::k_transfer_flat8<false, float, float4>, smem)) return r;
     sss::k_transfer_flat8<false, float, float4><<<grid, sss::kV17Threads, smem, S_(stream)>>>(

@@ -421,6 +421,89 @@ __device__ __forceinline__ void v17_consume(const V17Slot& S, const XT (&x)[8][3
   }
 }
 
+// half-slot variants: entries [h*4, h*4+4) of the lane's 8 (fewer live x
+// registers -> more resident warps)
+__device__ __forceinline__ void v17_gather_half(const V17Slot& S, const double4* __restrict__ xp,
+                                                const uint32_t* sbits, int h, double (&x)[4][3]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t c = v17_col(S, h * 4 + e);
+    x[e][0] = x[e][1] = x[e][2] = 0.0;
+    if (!sbits || ((sbits[c >> 5] >> (c & 31u)) & 1u)) v15_gather1(xp, c, x[e]);
+  }
+}
+
+__device__ __forceinline__ void v17_consume_split(const V17Slot& S, const double4* __restrict__ xp,
+                                                  const uint32_t* sbits, int lane, unsigned upto,
+                                                  int N, const uint32_t* __restrict__ rowk,
+                                                  double* __restrict__ vk) {
+  double x[4][3];
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    v17_gather_half(S, xp, sbits, h, x);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double v = (double)v17_val(S, h * 4 + e);
+      p0 = fma(v, x[e][0], p0);
+      p1 = fma(v, x[e][1], p1);
+      p2 = fma(v, x[e][2], p2);
+    }
+  }
+  const unsigned hm = S.h & upto;
+  const int sstart = hm ? 31 - __clz(hm) : -1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y0 = __shfl_up_sync(0xffffffffu, p0, o);
+    const double y1 = __shfl_up_sync(0xffffffffu, p1, o);
+    const double y2 = __shfl_up_sync(0xffffffffu, p2, o);
+    if (lane >= o && lane - o >= sstart) {
+      p0 += y0;
+      p1 += y1;
+      p2 += y2;
+    }
+  }
+  const bool tail = (lane == 31) || ((S.h >> (lane + 1)) & 1u);
+  if (tail && (p0 != 0.0 || p1 != 0.0 || p2 != 0.0)) {
+    const unsigned rk = __ldg(&rowk[S.hp + __popc(hm) - 1u]);
+    double* vo = vk + (size_t)(rk & 15u) * 3 * N + (rk >> 4);
+    atomicAdd(vo, p0);
+    atomicAdd(vo + N, p1);
+    atomicAdd(vo + 2 * (size_t)N, p2);
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kV17Threads, MINB) k_transfer_flat8s(
+    int N, unsigned n8, const unsigned long long* __restrict__ C8,
+    const unsigned long long* __restrict__ V8, const uint32_t* __restrict__ H,
+    const uint32_t* __restrict__ hpre, const uint32_t* __restrict__ rowk,
+    const unsigned* __restrict__ warp_begin, const double4* __restrict__ xp,
+    const uint32_t* __restrict__ bits, double* __restrict__ vk) {
+  extern __shared__ uint32_t v17_bits[];
+  if (bits) {
+    for (int t = threadIdx.x; t < ((N + 31) >> 5); t += blockDim.x) v17_bits[t] = bits[t];
+    __syncthreads();
+  }
+  const uint32_t* sb = bits ? v17_bits : nullptr;
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned i0 = warp_begin[w], i1 = warp_begin[w + 1];
+  if (i0 >= i1) return;
+  const unsigned upto = (2u << lane) - 1u;
+  V17Slot A, B;
+  v17_load(A, i0, lane, n8, C8, V8, H, hpre);
+  if (i0 + 1 < i1) v17_load(B, i0 + 1, lane, n8, C8, V8, H, hpre);
+#pragma unroll 1
+  for (unsigned i = i0; i < i1; i += 2) {
+    v17_consume_split(A, xp, sb, lane, upto, N, rowk, vk);
+    if (i + 2 < i1) v17_load(A, i + 2, lane, n8, C8, V8, H, hpre);
+    if (i + 1 >= i1) break;
+    v17_consume_split(B, xp, sb, lane, upto, N, rowk, vk);
+    if (i + 3 < i1) v17_load(B, i + 3, lane, n8, C8, V8, H, hpre);
+  }
+}
+
 template <bool AHEAD, typename XT = double, typename XP = double4>
 __global__ void __launch_bounds__(kV17Threads, 4) k_transfer_flat8(
     int N, unsigned n8, const unsigned long long* __restrict__ C8,
