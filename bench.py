@@ -113,6 +113,24 @@ def _dist():
     return ws, rank, local
 
 
+def max_over_ranks(x: float, ws: int, device="cuda") -> float:
+    """The job's time is the slowest rank's (timing rule: max over ranks)."""
+    if ws <= 1:
+        return float(x)
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(points_per_rank: int, ws: int, steps: int, ms: float) -> float:
+    """Weak scaling: every rank renders its own object of `points_per_rank`
+    points per step; the job's rate is all ranks' points over the slowest
+    rank's time."""
+    return ws * points_per_rank * steps / (ms / 1e3)
+
+
 def setup_scene(cfg, rank, torch, stats):
     from paper_2203_12339_b200 import lighting as LT
     from paper_2203_12339_b200.basis import OpticalMaterial, build_basis
@@ -195,13 +213,10 @@ def run_ours(a, cfg):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
-    if ws > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, ws)
     n_edit = sum(1 for f in range(a.warmup, total) if f in dev_mats)
     ms_per_step = ms / a.steps
-    value = ws * n * a.steps / (ms / 1e3)
+    value = whole_job_rate(n, ws, a.steps, ms)
 
     # ---- dominant kernel: the K-fused transfer, timed alone on its stream
     kt = []
@@ -248,10 +263,7 @@ def run_ours(a, cfg):
             fr = scene.set_material(mats[f])
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    if ws > 1:
-        t = torch.tensor([e2e_s], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(e2e_s, ws)
     n_edit_e2e = sum(1 for i in range(n_e2e) if a.warmup + i in mats)
     h2d = faces[0].nbytes + (56 * n_edit_e2e) / n_e2e
     d2h = (2 * n * 3 * 4 + 48) * (1 + n_edit_e2e / n_e2e)
