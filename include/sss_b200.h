@@ -286,7 +286,8 @@ int sss_transfer_flatp(int K, int n_rows, const uint32_t* pcols, const float* pv
  * heads bit l of word i marks 8-entry group 32 i + l. variant: 0 = gather and
  * consume per iteration, 1 = x gathers one iteration ahead, 4..8 = gathers in
  * two halves of 4 entries with a register cap for `variant` resident CTAs per
- * SM (6 = default: 24 warps / SM); x_f32 != 0: xp is the packed (N, 4)
+ * SM; 14 / 16 / 18 = the same with a single stream slot and 6 / 8 / 10 CTAs
+ * per SM (16 = default: 32 warps / SM); x_f32 != 0: xp is the packed (N, 4)
  * float array of sss_pack_x_f32_bits (fp64 products and sums of f32 operator
  * values x f32 spectrum). n_warps a multiple of 4. Same contract. */
 int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pvals,

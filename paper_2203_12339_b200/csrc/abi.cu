@@ -656,12 +656,22 @@ int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pv
       sss::k_transfer_flat8s<MB><<<grid, sss::kV17Threads, smem, S_(stream)>>>(                   \
           n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);            \
     } while (0)
-    if (minb == 4) SSS_F8S(4);
+#define SSS_F8S1(MB)                                                                              \
+    do {                                                                                          \
+      if (int r = set_smem((const void*)sss::k_transfer_flat8s<MB, true>, smem)) return r;        \
+      sss::k_transfer_flat8s<MB, true><<<grid, sss::kV17Threads, smem, S_(stream)>>>(             \
+          n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);            \
+    } while (0)
+    if (minb == 14) SSS_F8S1(6);
+    else if (minb == 16) SSS_F8S1(8);
+    else if (minb == 18) SSS_F8S1(10);
+    else if (minb == 4) SSS_F8S(4);
     else if (minb == 5) SSS_F8S(5);
     else if (minb == 7) SSS_F8S(7);
     else if (minb == 8) SSS_F8S(8);
     else SSS_F8S(6);
 #undef SSS_F8S
+#undef SSS_F8S1
   } else if (x_f32) {
     const auto* xf = reinterpret_cast<const float4*>(xp);
     if (int r = set_smem((const void*)sss::k_transfer_flat8<false, float, float4>, smem)) return r;

@@ -473,7 +473,7 @@ __device__ __forceinline__ void v17_consume_split(const V17Slot& S, const double
   }
 }
 
-template <int MINB>
+template <int MINB, bool SINGLE = false>
 __global__ void __launch_bounds__(kV17Threads, MINB) k_transfer_flat8s(
     int N, unsigned n8, const unsigned long long* __restrict__ C8,
     const unsigned long long* __restrict__ V8, const uint32_t* __restrict__ H,
@@ -491,6 +491,15 @@ __global__ void __launch_bounds__(kV17Threads, MINB) k_transfer_flat8s(
   const unsigned i0 = warp_begin[w], i1 = warp_begin[w + 1];
   if (i0 >= i1) return;
   const unsigned upto = (2u << lane) - 1u;
+  if (SINGLE) {  // one slot: stream latency hidden by the extra resident warps
+#pragma unroll 1
+    for (unsigned i = i0; i < i1; ++i) {
+      V17Slot A;
+      v17_load(A, i, lane, n8, C8, V8, H, hpre);
+      v17_consume_split(A, xp, sb, lane, upto, N, rowk, vk);
+    }
+    return;
+  }
   V17Slot A, B;
   v17_load(A, i0, lane, n8, C8, V8, H, hpre);
   if (i0 + 1 < i1) v17_load(B, i0 + 1, lane, n8, C8, V8, H, hpre);

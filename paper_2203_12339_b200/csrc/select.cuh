@@ -151,14 +151,20 @@ template <bool ENERGY>
 __device__ void radix_cut(const double* __restrict__ v, int N, long long need_init, double scale,
                           SelShared& sh, uint64_t* t_out, long long* take_out, long long* tiecnt) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int digits[6] = {53, 42, 31, 20, 9, 0};
-  const int widths[6] = {11, 11, 11, 11, 11, 9};
+  // energy cuts keep 11-bit digits (their fixed-point bucket sums are part of
+  // the bitwise contract); plain top-n uses 8-bit digits and finishes exactly
+  // from the gathered keys once the threshold bucket holds <= 64 of them
+  constexpr int kPasses = ENERGY ? 6 : 8;
+  const int digits_e[6] = {53, 42, 31, 20, 9, 0};
+  const int widths_e[6] = {11, 11, 11, 11, 11, 9};
+  const int digits_p[8] = {56, 48, 40, 32, 24, 16, 8, 0};
   uint64_t prefix = 0, pmask = 0;
   long long need = need_init;
   long long ncand = N;
   bool in_smem = false;
-  for (int p = 0; p < 6; ++p) {
-    const int shf = digits[p], nb = 1 << widths[p];
+  for (int p = 0; p < kPasses; ++p) {
+    const int shf = ENERGY ? digits_e[p] : digits_p[p];
+    const int nb = 1 << (ENERGY ? widths_e[p] : 8);
     for (int b = tid; b < nb; b += nt) {
       sh.hist[b] = 0;
       if (ENERGY) { sh.elo[b] = 0; sh.ehi[b] = 0; }
@@ -209,6 +215,44 @@ __device__ void radix_cut(const double* __restrict__ v, int N, long long need_in
     pmask |= (uint64_t)(nb - 1) << shf;
     if (gather) in_smem = true;
     __syncthreads();
+    if (!ENERGY && p + 1 < kPasses && ncand <= 64) {
+      uint64_t* ek = reinterpret_cast<uint64_t*>(sh.elo);  // 64 keys (unused without ENERGY)
+      if (tid == 0) sh.result = 0;
+      __syncthreads();
+      if (in_smem) {
+        const int nc = sh.ncand_store;
+        for (int q = tid; q < nc; q += nt) {
+          const uint64_t k = sh.cand_key[q];
+          if ((k & pmask) == prefix) ek[atomicAdd(&sh.result, 1)] = k;
+        }
+      } else {
+        for (int i = tid; i < N; i += nt) {
+          const uint64_t k = mkey(v[i]);
+          if ((k & pmask) == prefix) ek[atomicAdd(&sh.result, 1)] = k;
+        }
+      }
+      __syncthreads();
+      const int total = sh.result;
+      if (tid < total) {
+        const uint64_t kj = ek[tid];
+        long long g = 0, e = 0;
+        for (int q = 0; q < total; ++q) {
+          g += ek[q] > kj;
+          e += ek[q] == kj;
+        }
+        if (g < need && need <= g + e) {  // equal keys write equal values
+          sh.scal_cnt = e;
+          sh.scal_need = need - g;
+          reinterpret_cast<uint64_t*>(sh.ehi)[0] = kj;
+        }
+      }
+      __syncthreads();
+      prefix = reinterpret_cast<uint64_t*>(sh.ehi)[0];
+      need = sh.scal_need;
+      ncand = sh.scal_cnt;
+      __syncthreads();
+      break;
+    }
   }
   *t_out = prefix;
   *tiecnt = ncand;

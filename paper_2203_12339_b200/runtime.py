@@ -442,7 +442,7 @@ class Scene:
         t = self.transfer
         if self.transfer_kernel == "flat8" and getattr(t, "flat8", None) is None:
             t.flat8 = flat_layout(t, group=8,
-                                  warps_per_sm=int(os.environ.get("SSS_FLAT8_WPS", "24")))
+                                  warps_per_sm=int(os.environ.get("SSS_FLAT8_WPS", "32")))
         if self.transfer_kernel == "flat" and getattr(t, "flat", None) is None:
             t.flat = flat_layout(t)
         if getattr(self, "xp", None) is None:
@@ -468,7 +468,7 @@ class Scene:
             _lib.call("sss_transfer_flat8", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
                       _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W,
                       _lib.ptr(self.xp32 if f32 else self.xp), _lib.ptr(self.xbits),
-                      int(os.environ.get("SSS_FLAT8_VARIANT", "6")), int(f32), _lib.ptr(self.vk),
+                      int(os.environ.get("SSS_FLAT8_VARIANT", "16")), int(f32), _lib.ptr(self.vk),
                       sp)
             return
         pcols, pvals, ne, heads, hpre, rowk, wbeg, W, _ = self.transfer.flat
