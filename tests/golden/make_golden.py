@@ -196,6 +196,15 @@ def main():
                **{f"E_idx{c}": spectra[c].indices for c in range(3)})
     np.savez_compressed(HERE / "precompute16.npz", **pre)
 
+    # 6b. the same operators + basis + identity atlas written by the
+    #     reference's PRTS1 writer (container.py:81-137): the bridge fixture
+    from sssrelight import container as ctn
+    import hashlib
+
+    mesh_hash = hashlib.sha256(np.ascontiguousarray(samples.positions).tobytes()).digest()
+    ctn.save_container(HERE / "ref16.prts", basis, atlas, ct, mesh_hash,
+                       metadata={"source": "sssrelight reference", "side": side})
+
     # 7. environment light: project_environment + dense ambient irradiance
     env_side = 8
     faces = np.exp(rng.standard_normal((6, env_side, env_side, 3)))

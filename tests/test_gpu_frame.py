@@ -405,3 +405,44 @@ def test_batched_sweep_matches_bf16_reference(c1):
             ref[c, m] = np.maximum(ft * (B[c] @ G[c, m]), 0.0)
     err = np.abs(out - ref).max() / np.abs(ref).max()
     assert err <= 2e-4, err
+
+
+def test_prts1_reference_container_transfer_on_gpu(lib, golden):
+    """Operators precomputed by the reference and written by its PRTS1 writer
+    (tests/golden/ref16.prts) load onto the GPU layout and reproduce the
+    reference's v_k = T_k x (x = the golden kept w0 spectrum); tolerance =
+    the container's f32 value rounding."""
+    from pathlib import Path
+
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200 import prts1
+    from paper_2203_12339_b200.basis import OpticalMaterial, build_basis
+    from paper_2203_12339_b200.geometry import make_geometry_image
+    from paper_2203_12339_b200.runtime import Scene, SHLight
+    from paper_2203_12339_b200.transfer import flat_to_tile_major, tile_major_to_flat
+
+    c = prts1.load_prts1(Path(__file__).resolve().parent / "golden" / "ref16.prts")
+    g16 = golden("precompute16")
+    side, L = 16, 4
+    dt = prts1.to_device(c, levels=L)
+    geom = make_geometry_image(side, 10.0, 0.05, 8, 11)
+    basis = build_basis(dt.K, (4, 4))
+    sc = Scene(geom, dt, basis, OpticalMaterial(sigma_s_prime=[1.2, 1.5, 1.8], sigma_a=[0.01, 0.02, 0.04]),
+               SHLight(LT.random_sh_light(3, 1)))
+    E = g16["E"]
+    n = side * side
+    x = np.zeros((3, n))
+    for ch in range(3):
+        spec = O.haar2d_fwd(E[:, ch].reshape(1, side, side), L).reshape(-1)
+        idx = g16[f"E_idx{ch}"]
+        x[ch, idx] = spec[idx]
+    f2t = flat_to_tile_major(np.arange(n), side, L)
+    x_tm = np.empty_like(x)
+    x_tm[:, f2t] = x
+    sc.x.copy_(torch.as_tensor(x_tm))
+    sc._launch_transfer()
+    torch.cuda.synchronize()
+    vk = sc.vk.cpu().numpy()[:, :, f2t]  # tile-major rows -> flat w1 ids
+    ref = g16["vk"]
+    err = np.abs(vk - ref).max() / np.abs(ref).max()
+    assert err <= 1e-6, err
