@@ -297,6 +297,11 @@ int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pv
                        const uint32_t* bits, int variant, int x_f32, double* vk,
                        void* stream);
 
+/* ---- packed x in a permuted column order: xp[j] = {x0, x1, x2, 0}[perm[j]],
+ * bits over j (the flat8 layout's block-local column space). */
+int sss_pack_x_perm_bits(const double* x, int n, const int* perm, void* xp, uint32_t* bits,
+                         void* stream);
+
 /* ---- packed fp32 x (n, 4) floats {x0, x1, x2, 0} + kept-column bitmap. */
 int sss_pack_x_f32_bits(const double* x, int n, void* xp, uint32_t* bits, void* stream);
 

@@ -43,6 +43,7 @@ _SIGS = {
     "sss_transfer_kflat": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "sss_transfer_flat8": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _P, _P, _I, _I, _P, _P],
     "sss_pack_x_f32_bits": [_P, _I, _P, _P, _P],
+    "sss_pack_x_perm_bits": [_P, _I, _P, _P, _P, _P],
     "sss_transfer_flatp": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _I, _P, _P, _P],
     "sss_transfer_kgroup": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "sss_transfer_csr9s": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],

@@ -618,6 +618,15 @@ int sss_transfer_flatp(int K, int n_rows, const uint32_t* pcols, const float* pv
   return check_launch("k_transfer_flatp");
 }
 
+int sss_pack_x_perm_bits(const double* x, int n, const int* perm, void* xp, uint32_t* bits,
+                         void* stream) {
+  if (!x || !perm || !xp || !bits || n <= 0) return fail(SSS_EINVAL, "bad pack_x_perm_bits arguments");
+  if (reinterpret_cast<uintptr_t>(xp) % 32) return fail(SSS_EINVAL, "xp must be 32-byte aligned");
+  sss::k_pack_x_perm_bits<<<(n + 255) / 256, 256, 0, S_(stream)>>>(
+      x, n, perm, reinterpret_cast<double4*>(xp), bits);
+  return check_launch("k_pack_x_perm_bits");
+}
+
 int sss_pack_x_f32_bits(const double* x, int n, void* xp, uint32_t* bits, void* stream) {
   if (!x || !xp || !bits || n <= 0) return fail(SSS_EINVAL, "bad pack_x_f32_bits arguments");
   if (reinterpret_cast<uintptr_t>(xp) % 16) return fail(SSS_EINVAL, "xp must be 16-byte aligned");

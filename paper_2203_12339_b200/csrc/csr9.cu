@@ -162,6 +162,22 @@ __global__ void k_pack_x_bits(const double* __restrict__ x, int N, double4* __re
   if ((threadIdx.x & 31) == 0 && i < N) bits[i >> 5] = m;
 }
 
+// packed x in a permuted column order (xp[j] = x[:, perm[j]]) + the kept
+// bitmap in that order: the flat8 layout's 2x2-tile-block column space
+__global__ void k_pack_x_perm_bits(const double* __restrict__ x, int N,
+                                   const int* __restrict__ perm, double4* __restrict__ xp,
+                                   uint32_t* __restrict__ bits) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double a = 0.0, b = 0.0, c = 0.0;
+  if (j < N) {
+    const int i = perm[j];
+    a = x[i]; b = x[N + i]; c = x[2 * N + i];
+    xp[j] = make_double4(a, b, c, 0.0);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, j < N && (a != 0.0 || b != 0.0 || c != 0.0));
+  if ((threadIdx.x & 31) == 0 && j < N) bits[j >> 5] = m;
+}
+
 // packed fp32 x (N, 4) {x0, x1, x2, 0} + the kept-column bitmap
 __global__ void k_pack_x_f32_bits(const double* __restrict__ x, int N, float4* __restrict__ xp,
                                   uint32_t* __restrict__ bits) {

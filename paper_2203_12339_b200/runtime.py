@@ -441,7 +441,14 @@ class Scene:
     def _flat_prep(self, sp):
         t = self.transfer
         if self.transfer_kernel == "flat8" and getattr(t, "flat8", None) is None:
-            t.flat8 = flat_layout(t, group=8,
+            order = None
+            if os.environ.get("SSS_COLPERM", "0") == "1":
+                new_of, tm_of = block_column_order(t.side, t.levels)
+                order = new_of
+                t.flat8_perm = torch.as_tensor(tm_of.astype(np.int32), device=t.rowptr.device)
+            else:
+                t.flat8_perm = None
+            t.flat8 = flat_layout(t, group=8, col_order=order,
                                   warps_per_sm=int(os.environ.get("SSS_FLAT8_WPS", "32")))
         if self.transfer_kernel == "flat" and getattr(t, "flat", None) is None:
             t.flat = flat_layout(t)
@@ -449,6 +456,10 @@ class Scene:
             self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
         if getattr(self, "xbits", None) is None:
             self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+        if self.transfer_kernel == "flat8" and getattr(t, "flat8_perm", None) is not None:
+            _lib.call("sss_pack_x_perm_bits", _lib.ptr(self.x), self.n, _lib.ptr(t.flat8_perm),
+                      _lib.ptr(self.xp), _lib.ptr(self.xbits), sp)
+            return
         if self._x_f32():
             if getattr(self, "xp32", None) is None:
                 self.xp32 = torch.empty((self.n, 4), dtype=torch.float32, device="cuda")
@@ -976,7 +987,30 @@ def kgroup_layout(t: DeviceTransfer, warps_per_sm: int = None, split: int = None
     return (meta_p, vals, pieces, wbeg.to(torch.int32).contiguous(), W, stats)
 
 
-def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4, interleave=None):
+def block_column_order(side: int, levels: int, block: int = 2):
+    """Column permutation for the flat8 gathers: tile-major w0 id -> an order
+    where one 128-byte line of the packed x (4 columns x 32 B) holds the same
+    tile-local coefficient of a block x block group of adjacent tiles, so the
+    entries of a row that read one local coefficient of neighbouring source
+    tiles share an L1 line. Returns (new_of_tm, tm_of_new) int64 arrays."""
+    T = 1 << levels
+    T2, tpr = T * T, side // T
+    n = side * side
+    tm = np.arange(n, dtype=np.int64)
+    tile, local = tm // T2, tm % T2
+    tr, tc = tile // tpr, tile % tpr
+    bpr = max(tpr // block, 1)
+    b = block if tpr >= block else 1
+    bt = (tr // b) * bpr + (tc // b)
+    q = (tr % b) * b + (tc % b)
+    new = bt * (T2 * b * b) + local * (b * b) + q
+    inv = np.empty_like(new)
+    inv[new] = tm
+    return new, inv
+
+
+def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4, interleave=None,
+                col_order=None):
     """Head-flag bitmap + per-word segment prefix + segment (row, k) ids over
     csr9's padded operator copy, and equal word ranges per warp, for
     sss_transfer_flat."""
@@ -988,6 +1022,21 @@ def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4, int
         setattr(t, attr, csr9_layout(t, split=1 << 30, pad=group))
     pcols, pvals, pieces, _, _ = getattr(t, attr)
     dev = pcols.device
+    if col_order is not None:
+        # remap the columns and re-sort every segment by the new id (padding
+        # entries, value 0, stay at their segment's end with column 0)
+        new_of = torch.as_tensor(col_order, device=dev)
+        pc0 = pieces.to(torch.int64) & 0xFFFFFFFF
+        st, ln = pc0[:, 0], pc0[:, 1]
+        seg = torch.repeat_interleave(torch.arange(st.numel(), device=dev), ln)
+        pos = torch.arange(seg.numel(), device=dev, dtype=torch.int64)
+        cl = new_of[pcols.to(torch.int64) & 0xFFFFFFFF]
+        pad = pvals == 0
+        key = (seg << 25) | torch.where(pad, torch.full_like(cl, (1 << 24) - 1 + 1), cl)
+        order = torch.argsort(key, stable=True)
+        pcols = torch.where(pad[order], torch.zeros_like(cl), cl[order]).to(torch.int32)
+        pvals = pvals[order].contiguous()
+        del seg, pos, cl, pad, key, order
     if interleave is None:
         interleave = group == 8 and os.environ.get("SSS_FLAT_INTERLEAVE", "1") == "1"
     if interleave:

@@ -309,8 +309,8 @@ def test_kgroup_layout_reproduces_csr_product():
     assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
 
 
-@pytest.mark.parametrize("group", [4, 8])
-def test_flat_stream_layout_reproduces_csr_product(group):
+@pytest.mark.parametrize("group,perm", [(4, False), (8, False), (8, True)])
+def test_flat_stream_layout_reproduces_csr_product(group, perm):
     """sss_transfer_flat's head-flag bitmap / segment prefix over the padded
     operator copy recover every segment's (row, k): emulate the segmented
     warp-stream on the host, including warp ranges that cut segments."""
@@ -320,8 +320,16 @@ def test_flat_stream_layout_reproduces_csr_product(group):
     dt = _random_device_transfer(rng, 32, 2, 5, 30)
     x_tm = rng.standard_normal((dt.n, 3))
     want = _csr_vk(dt, x_tm)
+    from paper_2203_12339_b200.runtime import block_column_order
+
+    order = None
+    if perm:
+        new_of, tm_of = block_column_order(32, 2)
+        assert np.array_equal(np.sort(new_of), np.arange(dt.n))
+        order = new_of
+        x_tm = x_tm[tm_of]  # the kernel reads x in the permuted column order
     pcols, pvals, ne, heads, hpre, rowk, wbeg, W, stats = flat_layout(dt, warps_per_sm=1,
-                                                                       group=group)
+                                                                       group=group, col_order=order)
     c4 = pcols.numpy().view(np.uint32).reshape(-1, group)
     v4 = pvals.numpy().astype(np.float64).reshape(-1, group)
     heads = heads.numpy().view(np.uint32)
