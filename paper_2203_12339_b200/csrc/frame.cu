@@ -151,6 +151,22 @@ __global__ void k_sh_irradiance_haar(const float* __restrict__ T_l, const double
 // ---------------------------------------------------------------------------
 
 // grid: 3 CTAs (channels), faces (6, s, s, 3) doubles
+#ifdef SSS_ENV_TRACE
+__device__ unsigned long long g_env_trace[16];
+#define ENV_TRACE(i)                                                         \
+  do {                                                                       \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                               \
+      unsigned long long t_;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      g_env_trace[i] = t_;                                                   \
+    }                                                                        \
+  } while (0)
+#else
+#define ENV_TRACE(i) \
+  do {               \
+  } while (0)
+#endif
+
 __global__ void k_env_project(const double* __restrict__ faces, int s, int n_keep,
                               uint32_t* __restrict__ idx_out, double* __restrict__ val_out,
                               double* __restrict__ energy) {
@@ -159,9 +175,12 @@ __global__ void k_env_project(const double* __restrict__ faces, int s, int n_kee
   double* a = sm;             // D
   double* tmp = sm + D;       // D (the 6 faces transform as one batch)
   SelShared& sh = *reinterpret_cast<SelShared*>(tmp + D);
+  ENV_TRACE(0);
   for (int e = threadIdx.x; e < D; e += blockDim.x) a[e] = faces[(size_t)e * 3 + c];
   __syncthreads();
+  ENV_TRACE(1);
   batch_tile_haar_fwd(a, tmp, s, 6);
+  ENV_TRACE(2);
   const int n = min(n_keep, D);
   SelectResult sel;
   {
@@ -171,11 +190,13 @@ __global__ void k_env_project(const double* __restrict__ faces, int s, int n_kee
     sel.key = t;
     sel.take_eq = (int)take;
   }
+  ENV_TRACE(3);
   // compaction in index order: rank via a second scan
   int* wsum = reinterpret_cast<int*>(sh.wsum);
   // mark kept into tmp-as-flags then compact with a block scan
   unsigned char* keep = (unsigned char*)tmp;  // reuse (s2 doubles >= D bytes)
   block_apply_selection(a, D, sel, wsum, [&](int i, bool k) { keep[i] = k; });
+  ENV_TRACE(4);
   // ordered compaction (chunked, like block_apply_selection)
   const int nt = blockDim.x, tid = threadIdx.x;
   const int chunk = (D + nt - 1) / nt;
@@ -199,6 +220,7 @@ __global__ void k_env_project(const double* __restrict__ faces, int s, int n_kee
   for (int i = lo; i < hi; ++i)
     if (keep[i]) { idx_out[c * n_keep + pos] = i; val_out[c * n_keep + pos] = a[i]; ++pos; }
   for (int q = n + tid; q < n_keep; q += nt) { idx_out[c * n_keep + q] = 0xffffffffu; val_out[c * n_keep + q] = 0.0; }
+  ENV_TRACE(5);
   if (energy && tid == 0) {
     double tot = 0.0, kept = 0.0;
     for (int i = 0; i < D; ++i) { tot += a[i] * a[i]; if (keep[i]) kept += a[i] * a[i]; }
@@ -444,6 +466,7 @@ __global__ void __launch_bounds__(1024) k_select_topn(const double* __restrict__
     sel.key = t;
     sel.take_eq = (int)take;
   }
+  ENV_TRACE(3);
   double tot = 0.0, kept = 0.0;
   double* xo = x + (size_t)c * n_dom;
   uint32_t* mo = mask ? mask + (size_t)c * ((n_dom + 31) / 32) : nullptr;

@@ -57,28 +57,29 @@ __device__ __forceinline__ void global_to_tile(int r, int c, int L, int S,
 // (row-major, stride T), following haar2d_fwd_batch (_kernels_np.py:53-62):
 // per level rows then columns. Called by all threads of the block; uses
 // `tmp` (T*T doubles) as scratch. Bitwise equal to the reference.
+// Per level the row pass writes the level's s x s block into tmp and the
+// column pass reads it back into a (two passes, two barriers; no copy-back),
+// indices by shifts (all sizes are powers of two). The per-element
+// arithmetic (dadd / dmul order) is the reference's, so results are bitwise
+// those of haar2d_fwd_batch / haar2d_inv_batch.
+__device__ __forceinline__ int ilog2i(int v) { return 31 - __clz(v); }
+
 __device__ inline void tile_haar_fwd(double* a, double* tmp, int T, int nthreads, int tid) {
   for (int s = T; s >= 2; s >>= 1) {
-    const int h = s >> 1;
-    // rows
-    for (int e = tid; e < s * h; e += nthreads) {
-      const int i = e / h, j = e % h;
+    const int h = s >> 1, lh = ilog2i(h);
+    for (int e = tid; e < s * h; e += nthreads) {  // rows a -> tmp
+      const int i = e >> lh, j = e & (h - 1);
       const double ev = a[i * T + 2 * j], od = a[i * T + 2 * j + 1];
       tmp[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
       tmp[i * T + h + j] = dmul(dsub(ev, od), SSS_ISQRT2);
     }
     __syncthreads();
-    for (int e = tid; e < s * s; e += nthreads) a[(e / s) * T + e % s] = tmp[(e / s) * T + e % s];
-    __syncthreads();
-    // columns
-    for (int e = tid; e < s * h; e += nthreads) {
-      const int j = e / h, i = e % h;
-      const double ev = a[(2 * i) * T + j], od = a[(2 * i + 1) * T + j];
-      tmp[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
-      tmp[(h + i) * T + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+    for (int e = tid; e < s * h; e += nthreads) {  // columns tmp -> a
+      const int j = e >> lh, i = e & (h - 1);
+      const double ev = tmp[(2 * i) * T + j], od = tmp[(2 * i + 1) * T + j];
+      a[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+      a[(h + i) * T + j] = dmul(dsub(ev, od), SSS_ISQRT2);
     }
-    __syncthreads();
-    for (int e = tid; e < s * s; e += nthreads) a[(e / s) * T + e % s] = tmp[(e / s) * T + e % s];
     __syncthreads();
   }
 }
@@ -87,37 +88,33 @@ __device__ inline void tile_haar_fwd(double* a, double* tmp, int T, int nthreads
 // columns then rows, s = 2 .. T.
 __device__ inline void tile_haar_inv(double* a, double* tmp, int T, int nthreads, int tid) {
   for (int s = 2; s <= T; s <<= 1) {
-    const int h = s >> 1;
-    for (int e = tid; e < s * h; e += nthreads) {
-      const int j = e / h, i = e % h;
+    const int h = s >> 1, lh = ilog2i(h);
+    for (int e = tid; e < s * h; e += nthreads) {  // columns a -> tmp
+      const int j = e >> lh, i = e & (h - 1);
       const double lo = a[i * T + j], hi = a[(h + i) * T + j];
       tmp[(2 * i) * T + j] = dmul(dadd(lo, hi), SSS_ISQRT2);
       tmp[(2 * i + 1) * T + j] = dmul(dsub(lo, hi), SSS_ISQRT2);
     }
     __syncthreads();
-    for (int e = tid; e < s * s; e += nthreads) a[(e / s) * T + e % s] = tmp[(e / s) * T + e % s];
-    __syncthreads();
-    for (int e = tid; e < s * h; e += nthreads) {
-      const int i = e / h, j = e % h;
-      const double lo = a[i * T + j], hi = a[i * T + h + j];
-      tmp[i * T + 2 * j] = dmul(dadd(lo, hi), SSS_ISQRT2);
-      tmp[i * T + 2 * j + 1] = dmul(dsub(lo, hi), SSS_ISQRT2);
+    for (int e = tid; e < s * h; e += nthreads) {  // rows tmp -> a
+      const int i = e >> lh, j = e & (h - 1);
+      const double lo = tmp[i * T + j], hi = tmp[i * T + h + j];
+      a[i * T + 2 * j] = dmul(dadd(lo, hi), SSS_ISQRT2);
+      a[i * T + 2 * j + 1] = dmul(dsub(lo, hi), SSS_ISQRT2);
     }
-    __syncthreads();
-    for (int e = tid; e < s * s; e += nthreads) a[(e / s) * T + e % s] = tmp[(e / s) * T + e % s];
     __syncthreads();
   }
 }
 
 // Batched in-place forward full-pyramid Haar over B independent T x T grids
-// (grid b at a + b * T * T); same arithmetic as tile_haar_fwd.
+// (grid b at a + b * T * T); same arithmetic as tile_haar_fwd. tmp: B * T * T.
 __device__ inline void batch_tile_haar_fwd(double* a, double* tmp, int T, int B) {
   const int T2 = T * T, nt = blockDim.x, tid = threadIdx.x;
   for (int s = T; s >= 2; s >>= 1) {
-    const int h = s >> 1, sh = s * h, ss = s * s;
-    for (int q = tid; q < B * sh; q += nt) {
-      const int b = q / sh, e = q % sh;
-      const int i = e / h, j = e % h;
+    const int h = s >> 1, lh = ilog2i(h), lsh = ilog2i(s * h);
+    for (int q = tid; q < (B << lsh); q += nt) {
+      const int b = q >> lsh, e = q & ((1 << lsh) - 1);
+      const int i = e >> lh, j = e & (h - 1);
       const double* g = a + b * T2;
       double* o = tmp + b * T2;
       const double ev = g[i * T + 2 * j], od = g[i * T + 2 * j + 1];
@@ -125,39 +122,28 @@ __device__ inline void batch_tile_haar_fwd(double* a, double* tmp, int T, int B)
       o[i * T + h + j] = dmul(dsub(ev, od), SSS_ISQRT2);
     }
     __syncthreads();
-    for (int q = tid; q < B * ss; q += nt) {
-      const int b = q / ss, e = q % ss;
-      a[b * T2 + (e / s) * T + e % s] = tmp[b * T2 + (e / s) * T + e % s];
-    }
-    __syncthreads();
-    for (int q = tid; q < B * sh; q += nt) {
-      const int b = q / sh, e = q % sh;
-      const int j = e / h, i = e % h;
-      const double* g = a + b * T2;
-      double* o = tmp + b * T2;
+    for (int q = tid; q < (B << lsh); q += nt) {
+      const int b = q >> lsh, e = q & ((1 << lsh) - 1);
+      const int j = e >> lh, i = e & (h - 1);
+      const double* g = tmp + b * T2;
+      double* o = a + b * T2;
       const double ev = g[(2 * i) * T + j], od = g[(2 * i + 1) * T + j];
       o[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
       o[(h + i) * T + j] = dmul(dsub(ev, od), SSS_ISQRT2);
-    }
-    __syncthreads();
-    for (int q = tid; q < B * ss; q += nt) {
-      const int b = q / ss, e = q % ss;
-      a[b * T2 + (e / s) * T + e % s] = tmp[b * T2 + (e / s) * T + e % s];
     }
     __syncthreads();
   }
 }
 
 // Batched in-place inverse over B independent T x T grids (grid b at
-// a + b * T * T); same arithmetic as tile_haar_inv, 4 barriers per level for
-// the whole batch. tmp: B * T * T doubles.
+// a + b * T * T); same arithmetic as tile_haar_inv. tmp: B * T * T doubles.
 __device__ inline void batch_tile_haar_inv(double* a, double* tmp, int T, int B) {
   const int T2 = T * T, nt = blockDim.x, tid = threadIdx.x;
   for (int s = 2; s <= T; s <<= 1) {
-    const int h = s >> 1, sh = s * h, ss = s * s;
-    for (int q = tid; q < B * sh; q += nt) {
-      const int b = q / sh, e = q % sh;
-      const int j = e / h, i = e % h;
+    const int h = s >> 1, lh = ilog2i(h), lsh = ilog2i(s * h);
+    for (int q = tid; q < (B << lsh); q += nt) {
+      const int b = q >> lsh, e = q & ((1 << lsh) - 1);
+      const int j = e >> lh, i = e & (h - 1);
       const double* g = a + b * T2;
       double* o = tmp + b * T2;
       const double lo = g[i * T + j], hi = g[(h + i) * T + j];
@@ -165,24 +151,14 @@ __device__ inline void batch_tile_haar_inv(double* a, double* tmp, int T, int B)
       o[(2 * i + 1) * T + j] = dmul(dsub(lo, hi), SSS_ISQRT2);
     }
     __syncthreads();
-    for (int q = tid; q < B * ss; q += nt) {
-      const int b = q / ss, e = q % ss;
-      a[b * T2 + (e / s) * T + e % s] = tmp[b * T2 + (e / s) * T + e % s];
-    }
-    __syncthreads();
-    for (int q = tid; q < B * sh; q += nt) {
-      const int b = q / sh, e = q % sh;
-      const int i = e / h, j = e % h;
-      const double* g = a + b * T2;
-      double* o = tmp + b * T2;
+    for (int q = tid; q < (B << lsh); q += nt) {
+      const int b = q >> lsh, e = q & ((1 << lsh) - 1);
+      const int i = e >> lh, j = e & (h - 1);
+      const double* g = tmp + b * T2;
+      double* o = a + b * T2;
       const double lo = g[i * T + j], hi = g[i * T + h + j];
       o[i * T + 2 * j] = dmul(dadd(lo, hi), SSS_ISQRT2);
       o[i * T + 2 * j + 1] = dmul(dsub(lo, hi), SSS_ISQRT2);
-    }
-    __syncthreads();
-    for (int q = tid; q < B * ss; q += nt) {
-      const int b = q / ss, e = q % ss;
-      a[b * T2 + (e / s) * T + e % s] = tmp[b * T2 + (e / s) * T + e % s];
     }
     __syncthreads();
   }
