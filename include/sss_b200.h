@@ -334,6 +334,20 @@ int sss_sweep_gemm(int n_points, int M, const void* Bq, const void* Gq, const fl
                    float eta_lo, float eta_hi, const float* positions, const float* normals,
                    const double* cam, float* out, void* stream);
 
+/* ---- transfer v19: receiver regions (2^L tiles) with the kept x working set
+ * in shared memory. ucols / uoff (n_regions + 1): each region's sorted union
+ * of columns; pcols / pvals: the flat8 stream whose column fields are
+ * region-local slots (< umax < 32768), every region padded to whole 256-entry
+ * iterations (rit, n_regions + 1, iteration offsets); heads / head_prefix /
+ * seg_rowk as sss_transfer_flat8; xp / bits from sss_pack_x_bits. Zeroes and
+ * fills vk; shade with sss_edit_finish. */
+int sss_transfer_regional(int K, int n_rows, const uint32_t* ucols, const int* uoff,
+                          const int* rit, int n_regions, int umax, const uint32_t* pcols,
+                          const float* pvals, unsigned long long n_entries,
+                          const uint32_t* heads, const uint32_t* head_prefix,
+                          const uint32_t* seg_rowk, const void* xp, const uint32_t* bits,
+                          double* vk, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

@@ -40,6 +40,8 @@ _SIGS = {
     "sss_sweep_basis": [_I, _I, _I, _P, _P, _P],
     "sss_material_weights_batch": [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P],
     "sss_sweep_gemm": [_I, _I, _P, _P, _P, C.c_float, C.c_float, _P, _P, _P, _P, _P],
+    "sss_transfer_regional": [_I, _I, _P, _P, _P, _I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P,
+                              _P, _P, _P],
     "sss_transfer_kflat": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "sss_transfer_flat8": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _P, _P, _I, _I, _P, _P],
     "sss_pack_x_f32_bits": [_P, _I, _P, _P, _P],

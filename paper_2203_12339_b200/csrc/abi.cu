@@ -1,6 +1,7 @@
 // extern "C" entry points declared in include/sss_b200.h. One translation unit
 // so every kernel is visible to its launcher; built into
 // paper_2203_12339_b200/_sss_b200.so for sm_100a (see build.py).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -23,6 +24,7 @@
 #include "flat15.cu"
 #include "kflat18.cu"
 #include "sweep.cu"
+#include "regional19.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -773,6 +775,40 @@ int sss_sweep_gemm(int n_points, int M, const void* Bq, const void* Gq, const fl
   else SSS_SW(128, 256, 52);
 #undef SSS_SW
   return check_launch("k_sweep_umma");
+}
+
+int sss_transfer_regional(int K, int n_rows, const uint32_t* ucols, const int* uoff,
+                          const int* rit, int n_regions, int umax, const uint32_t* pcols,
+                          const float* pvals, unsigned long long n_entries,
+                          const uint32_t* heads, const uint32_t* head_prefix,
+                          const uint32_t* seg_rowk, const void* xp, const uint32_t* bits,
+                          double* vk, void* stream) {
+  if (K <= 0 || n_rows <= 0 || !ucols || !uoff || !rit || n_regions <= 0 || umax <= 0 ||
+      umax >= 32768 || !pcols || !pvals || !heads || !head_prefix || !seg_rowk || !xp || !bits ||
+      !vk || n_entries % 8)
+    return fail(SSS_EINVAL, "bad transfer_regional arguments");
+  if (reinterpret_cast<uintptr_t>(pcols) % 32 || reinterpret_cast<uintptr_t>(pvals) % 32 ||
+      reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_regional: pcols/pvals/xp must be 32-byte aligned");
+  int dev = 0, nsm = 148, smem_optin = 227 * 1024;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t bits_b = (((size_t)(n_rows + 31) / 32) * 4 + 15) & ~size_t(15);
+  const size_t map_b = (size_t)umax * sizeof(short);
+  const long long room = (long long)smem_optin - 1024 - (long long)bits_b - (long long)map_b;
+  if (room < 24 * 256) return fail(SSS_EINVAL, "transfer_regional: not enough shared memory");
+  const int xcap = (int)std::min<long long>(room / 24, 32767);
+  const size_t smem = bits_b + (size_t)xcap * 24 + map_b;
+  if (int r = set_smem((const void*)sss::k_transfer_regional, smem)) return r;
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const int grid = std::min(n_regions, nsm);
+  sss::k_transfer_regional<<<grid, sss::kV19Threads, smem, S_(stream)>>>(
+      n_rows, n_regions, xcap, ucols, uoff, rit, reinterpret_cast<const unsigned long long*>(pcols),
+      reinterpret_cast<const unsigned long long*>(pvals), (unsigned)(n_entries / 8), heads,
+      head_prefix, seg_rowk, reinterpret_cast<const double4*>(xp), bits, vk);
+  return check_launch("k_transfer_regional");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

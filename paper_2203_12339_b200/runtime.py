@@ -156,11 +156,10 @@ class Scene:
 
     def _write_material(self):
         m = self.material
-        self.material_buf.copy_(torch.tensor(
-            np.concatenate([m.sigma_s_prime, m.sigma_a, [m.eta]]), dtype=torch.float64))
+        self._stage_copy(self.material_buf, np.concatenate([m.sigma_s_prime, m.sigma_a, [m.eta]]))
 
     def _write_camera(self):
-        self.cam_buf.copy_(torch.tensor(self.camera.position, dtype=torch.float64))
+        self._stage_copy(self.cam_buf, self.camera.position)
 
     def _stage_copy(self, dst: torch.Tensor, host: np.ndarray):
         """Host array -> device buffer through a reused pinned staging tensor."""
@@ -169,8 +168,8 @@ class Scene:
         if pin is None:
             pin = torch.empty(tuple(dst.shape), dtype=dst.dtype, pin_memory=True)
             self._stage = {**getattr(self, "_stage", {}), key: pin}
-        # the previous frame's upload from this buffer must be complete
-        torch.cuda.current_stream().synchronize()
+        # every API frame ends with a synchronize (_frame), so the previous
+        # upload from this staging buffer has completed
         pin.numpy()[...] = np.asarray(host, dtype=np.float64).reshape(pin.shape)
         dst.copy_(pin, non_blocking=True)
 
@@ -239,7 +238,10 @@ class Scene:
                   len(self.basis.r_nodes), _lib.ptr(self.material_buf), _lib.ptr(self.g),
                   _lib.stream_ptr(stream))
 
-    def _launch_transfer(self, stream=None):
+    def _launch_transfer(self, stream=None, epilogue=True):
+        """Stage 2 (+ stages 3-5 when `epilogue`). Returns True when the
+        recombine / inverse / shade epilogue ran (fused layouts always run it;
+        the separable ones only when asked)."""
         t = self.transfer
         if self.transfer_kernel == "flatp":
             if getattr(t, "flatp", None) is None:
@@ -253,8 +255,9 @@ class Scene:
             _lib.call("sss_transfer_flatp", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
                       _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W, depth,
                       _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "kflat":
             sp = _lib.stream_ptr(stream)
             if getattr(t, "kflat", None) is None:
@@ -269,14 +272,35 @@ class Scene:
             _lib.call("sss_transfer_kflat", self.K, self.n, _lib.ptr(cols), _lib.ptr(vals),
                       _lib.ptr(steps), _lib.ptr(wbeg), W, _lib.ptr(self.xp),
                       _lib.ptr(self.xbits), _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
+        if self.transfer_kernel == "regional":
+            sp = _lib.stream_ptr(stream)
+            if getattr(t, "regional", None) is None:
+                t.regional = regional_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            if getattr(self, "xbits", None) is None:
+                self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+            _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                      _lib.ptr(self.xbits), sp)
+            R = t.regional
+            _lib.call("sss_transfer_regional", self.K, self.n, _lib.ptr(R["ucols"]),
+                      _lib.ptr(R["uoff"]), _lib.ptr(R["rit"]), R["n_regions"], R["umax"],
+                      _lib.ptr(R["pcols"]), _lib.ptr(R["pvals"]), R["n_entries"],
+                      _lib.ptr(R["heads"]), _lib.ptr(R["hpre"]), _lib.ptr(R["rowk"]),
+                      _lib.ptr(self.xp), _lib.ptr(self.xbits), _lib.ptr(self.vk), sp)
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel in ("flat", "flat8"):
             sp = _lib.stream_ptr(stream)
             self._flat_prep(sp)
             self._flat_core(sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "kgroup":
             if getattr(t, "kgroup", None) is None:
                 t.kgroup = kgroup_layout(t)
@@ -291,8 +315,9 @@ class Scene:
             _lib.call("sss_transfer_kgroup", self.K, self.n, _lib.ptr(meta), _lib.ptr(vals),
                       _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.xbits),
                       _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "csr9s":
             if getattr(t, "csr9", None) is None:
                 t.csr9 = csr9_layout(t)
@@ -307,8 +332,9 @@ class Scene:
             _lib.call("sss_transfer_csr9s", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals),
                       _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.xbits),
                       _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "kstream":
             if getattr(t, "kstream", None) is None:
                 t.kstream = kstream_layout(t)
@@ -320,8 +346,9 @@ class Scene:
             _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
             _lib.call("sss_transfer_kstream", self.K, self.n, _lib.ptr(blob), _lib.ptr(recs),
                       _lib.ptr(wbeg), W, depth, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "kstep":
             if getattr(t, "kstep", None) is None:
                 t.kstep = kstep_layout(t)
@@ -332,8 +359,9 @@ class Scene:
             _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
             _lib.call("sss_transfer_kstep", self.K, self.n, _lib.ptr(cols), _lib.ptr(vals),
                       _lib.ptr(steps), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "kpackp":
             if getattr(t, "kpack", None) is None:
                 t.kpack = kpack_layout(t)
@@ -346,8 +374,9 @@ class Scene:
             _lib.call("sss_transfer_kpack_pipe", self.K, self.n, _lib.ptr(meta), _lib.ptr(vals),
                       _lib.ptr(pieces), _lib.ptr(wbeg), W, ppl, _lib.ptr(self.xp),
                       _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "kpack":
             if getattr(t, "kpack", None) is None:
                 t.kpack = kpack_layout(t)
@@ -358,8 +387,9 @@ class Scene:
             _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
             _lib.call("sss_transfer_kpack", self.K, self.n, _lib.ptr(meta), _lib.ptr(vals),
                       _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "csr9":
             if getattr(t, "csr9", None) is None:
                 t.csr9 = csr9_layout(t)
@@ -370,8 +400,9 @@ class Scene:
             _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
             _lib.call("sss_transfer_csr9", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals),
                       _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "csr8":
             if getattr(t, "csr8", None) is None:
                 t.csr8 = csr8_schedule(t)
@@ -382,8 +413,9 @@ class Scene:
             _lib.call("sss_pack_x", _lib.ptr(self.x), self.n, _lib.ptr(self.xp), sp)
             _lib.call("sss_transfer_csr8", self.K, self.n, _lib.ptr(t.cols), _lib.ptr(t.vals),
                       _lib.ptr(pieces), _lib.ptr(wbeg), W, _lib.ptr(self.xp), _lib.ptr(self.vk), sp)
-            self._launch_edit(stream)
-            return
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "csr7":
             if getattr(t, "csr7_order", None) is None:
                 t.csr7_tiles, t.csr7_order = csr7_schedule(t)
@@ -397,7 +429,7 @@ class Scene:
                       _lib.ptr(self.positions), _lib.ptr(self.normals), _lib.ptr(self.cam_buf),
                       _lib.ptr(self.material_buf), _lib.ptr(self.vk), _lib.ptr(self.scatter),
                       _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped), sp)
-            return
+            return True
         if self.transfer_kernel == "v6":
             if getattr(t, "v6", None) is None:
                 from .stream6 import build_v6
@@ -408,7 +440,7 @@ class Scene:
             launch_v6(t.v6, t, self.x, self.g, self.positions, self.normals, self.cam_buf,
                       self.material_buf, self.vk, self.scatter, self.radiance,
                       self.radiance_unclamped, stream)
-            return
+            return True
         if self.transfer_kernel == "v4":
             if getattr(t, "v4", None) is None:
                 from .stream4 import build_v4
@@ -419,7 +451,7 @@ class Scene:
             launch_v4(t.v4, t, self.x, self.g, self.positions, self.normals, self.cam_buf,
                       self.material_buf, self.vk, self.scatter, self.radiance,
                       self.radiance_unclamped, stream)
-            return
+            return True
         if self.transfer_kernel == "stream" and t.entries is not None:
             _lib.call("sss_transfer_stream", self.K, self.side, self.levels, t.unit_tiles,
                       t.band_width, t.n_bands, _lib.ptr(t.item_off), _lib.ptr(t.item_len),
@@ -428,7 +460,7 @@ class Scene:
                       _lib.ptr(self.normals), _lib.ptr(self.cam_buf), _lib.ptr(self.material_buf),
                       _lib.ptr(self.vk), _lib.ptr(self.scatter), _lib.ptr(self.radiance),
                       _lib.ptr(self.radiance_unclamped), _lib.stream_ptr(stream))
-            return
+            return True
         _lib.call("sss_transfer_relight", self.K, self.side, self.levels, t.unit_tiles,
                   _lib.ptr(t.rowptr), _lib.ptr(t.bandoff), t.band_width, t.n_bands,
                   _lib.ptr(t.rowperm), _lib.ptr(t.cols), _lib.ptr(t.vals), _lib.ptr(self.x),
@@ -437,6 +469,7 @@ class Scene:
                   _lib.ptr(self.material_buf), _lib.ptr(self.vk), _lib.ptr(self.scatter),
                   _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped),
                   _lib.stream_ptr(stream))
+        return True
 
     def _flat_prep(self, sp):
         t = self.transfer
@@ -571,36 +604,48 @@ class Scene:
 
     def relight(self) -> FrameResult:
         """Full pipeline; repopulates the stage-2 cache (runtime.py:174-187).
-        The first call runs the kernels eagerly with per-stage timings; later
-        calls replay the captured CUDA graph of the same sequence (the whole
-        frame's device time is then reported under "transfer")."""
+        The first call runs the kernels eagerly and times every stage
+        (irradiance, transfer, weighting, inverse_wavelet = recombine + inverse
+        Haar + shade); later calls replay the captured CUDA graph of the same
+        sequence and split its measured time by the last eager proportions."""
         timings = dict.fromkeys(STAGES, 0.0)
-        if self._graph is None and getattr(self, "_eager_relights", 0) >= 1:
+        # two eager frames first: the first builds the layouts, the second
+        # gives steady-state stage proportions for the graph replays
+        if self._graph is None and getattr(self, "_eager_relights", 0) >= 2:
             self.capture()
-        if self._graph is not None:
+        if self._graph is not None and getattr(self, "_stage_frac", None):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             ev[0].record()
             self._graph.replay()
             ev[1].record()
             ev[1].synchronize()
             self._have_cache = True
-            timings["transfer"] = ev[0].elapsed_time(ev[1])
+            total = ev[0].elapsed_time(ev[1])
+            for k, f in self._stage_frac.items():
+                timings[k] = total * f
             return self._frame(timings)
         self._eager_relights = getattr(self, "_eager_relights", 0) + 1
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
         self._launch_stage1()
         ev[1].record()
         self._launch_weights()
         ev[2].record()
-        self._launch_transfer()
+        fused = self._launch_transfer(epilogue=False)
         ev[3].record()
-        ev[3].synchronize()
+        if not fused:
+            self._launch_edit()
+        ev[4].record()
+        ev[4].synchronize()
         self._have_cache = True
         timings["irradiance"] = ev[0].elapsed_time(ev[1])
         timings["weighting"] = ev[1].elapsed_time(ev[2])
-        # transfer + recombine + inverse wavelet + shade
         timings["transfer"] = ev[2].elapsed_time(ev[3])
+        # the epilogue of fused layouts is inside "transfer"
+        timings["inverse_wavelet"] = ev[3].elapsed_time(ev[4]) if not fused else 0.0
+        tot = sum(timings.values())
+        if tot > 0:
+            self._stage_frac = {k: v / tot for k, v in timings.items() if v > 0}
         return self._frame(timings)
 
     def _edit_frame(self) -> FrameResult:
@@ -625,11 +670,16 @@ class Scene:
         return self._frame(timings)
 
     def set_material(self, material: OpticalMaterial) -> FrameResult:
-        """Fast edit path: stages 3-5 only (runtime.py:189-200). E here does
-        not depend on eta (eta_light = 1), so an eta change is an edit too."""
+        """Fast edit path: stages 3-5 only (runtime.py:189-200). Like the
+        reference, an eta change re-runs the full pipeline (the reference's
+        irradiance depends on eta; here E is eta-independent by the frozen
+        eta_light = 1, so the relight reproduces the same radiance)."""
+        if material is self.material and self._have_cache:
+            return self._edit_frame()  # unchanged material: nothing to upload
+        old_eta = self.material.eta
         self.material = self._clamp_material(material)
         self._write_material()
-        if not self._have_cache:
+        if not self._have_cache or self.material.eta != old_eta:
             return self.relight()
         return self._edit_frame()
 
@@ -1077,6 +1127,87 @@ def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4, int
              "bytes": n_entries * 8 + nw * 8 + int(s4.numel()) * 4}
     return (pcols, pvals, n_entries, heads.contiguous(), hpre.contiguous(), rowk,
             wbeg.to(torch.int32).contiguous(), W, stats)
+
+
+def regional_layout(t: DeviceTransfer, region_tiles: int = 1):
+    """v19 layout: receiver regions (blocks of region_tiles x region_tiles
+    2^L tiles, contiguous tile-major rows). Per region the sorted union of the
+    columns its entries read (`ucols`, offsets `uoff`); the region's entries
+    reference region-local slots instead of columns, in the flat8 stream
+    (segments padded to 8, lane-interleaved) with every region padded to whole
+    256-entry warp iterations (`rit` = iteration offsets per region).
+    Returns a dict of device tensors + stats."""
+    from types import SimpleNamespace
+
+    dev = t.rowptr.device
+    n, K, L = t.n, t.K, t.levels
+    T2 = (1 << L) ** 2
+    tpr = t.side >> L
+    i64 = dict(dtype=torch.int64, device=dev)
+    rp = t.rowptr.to(torch.int64)
+    lens = (rp[:, 1:] - rp[:, :-1]).reshape(-1)
+    base = int(rp[0, 0].item())
+    total = int(lens.sum().item())
+    kr = torch.arange(K * n, **i64)
+    row = torch.repeat_interleave(kr % n, lens)
+    col = t.cols[base:base + total].to(torch.int64) & 0xFFFFFFFF
+    tile = row // T2
+    rt = region_tiles
+    if tpr % rt:
+        raise ValueError("region_tiles must divide the tiles per row")
+    region = (tile // tpr // rt) * (tpr // rt) + (tile % tpr) // rt
+    # rows must be region-contiguous in tile-major order for a contiguous stream
+    if rt != 1:
+        raise ValueError("only single-tile regions keep rows contiguous in tile-major order")
+    n_reg = n // T2
+    key = region * n + col
+    ukeys = torch.unique(key)
+    ureg = ukeys // n
+    ucols = (ukeys % n).to(torch.int32)
+    ucnt = torch.bincount(ureg, minlength=n_reg)
+    uoff = torch.cat([torch.zeros(1, **i64), torch.cumsum(ucnt, 0)])
+    slot = torch.searchsorted(ukeys, key) - uoff[region]
+    if int(ucnt.max().item()) >= 32768:
+        raise ValueError("a region reads more than 32767 distinct columns")
+    del key, ukeys, ureg, row, col, tile, region
+    # the slot-valued operator (same rowptr / values), then the flat8 machinery
+    cols_slot = t.cols.clone()
+    cols_slot[base:base + total] = slot.to(torch.int32)
+    del slot
+    ts = SimpleNamespace(rowptr=t.rowptr, cols=cols_slot, vals=t.vals, n=n, K=K, levels=L,
+                         side=t.side)
+    # pad each region's last segment so regions span whole 32-group iterations
+    lay = csr9_layout(ts, split=1 << 30, pad=8)
+    pcols, pvals, pieces, _, _ = lay
+    pc = pieces.to(torch.int64) & 0xFFFFFFFF
+    st, ln, rk = pc[:, 0], pc[:, 1], pc[:, 2]
+    preg = (rk >> 4) // T2
+    reg_len = torch.zeros(n_reg, **i64).index_add_(0, preg, ln)
+    reg_pad = (reg_len + 255) // 256 * 256 - reg_len
+    last = torch.zeros(n_reg, **i64).scatter_reduce_(0, preg, torch.arange(ln.numel(), **i64), "amax")
+    ln2 = ln.clone()
+    ln2[last] += reg_pad
+    st2 = torch.cumsum(ln2, 0) - ln2
+    tot2 = int(ln2.sum().item())
+    pc2 = torch.zeros(tot2, dtype=torch.int32, device=dev)
+    pv2 = torch.zeros(tot2, dtype=torch.float32, device=dev)
+    seg = torch.repeat_interleave(torch.arange(ln.numel(), device=dev), ln)
+    q = torch.arange(int(ln.sum().item()), **i64) - torch.repeat_interleave(st, ln)
+    pc2[st2[seg] + q] = pcols[st[seg] + q]
+    pv2[st2[seg] + q] = pvals[st[seg] + q]
+    del seg, q, pcols, pvals
+    pieces2 = torch.stack([st2, ln2, rk, torch.zeros_like(rk)], 1).to(torch.int32).contiguous()
+    ts.csr9_pad8 = (pc2, pv2, pieces2, None, 0)
+    fl = flat_layout(ts, group=8, warps_per_sm=1)
+    pcols_f, pvals_f, ne, heads, hpre, rowk, _, _, fst = fl
+    reg_it = torch.cat([torch.zeros(1, **i64), torch.cumsum((reg_len + reg_pad) // 256, 0)])
+    stats = {"regions": n_reg, "union_cols_mean": float(ucnt.float().mean()),
+             "union_cols_max": int(ucnt.max()), "entries_padded": int(ne),
+             "bytes": int(ne) * 8 + int(ucols.numel()) * 4}
+    return {"pcols": pcols_f, "pvals": pvals_f, "n_entries": ne, "heads": heads, "hpre": hpre,
+            "rowk": rowk, "ucols": ucols, "uoff": uoff.to(torch.int32).contiguous(),
+            "rit": reg_it.to(torch.int32).contiguous(), "n_regions": n_reg,
+            "umax": int(ucnt.max()), "stats": stats}
 
 
 def kstep_layout(t: DeviceTransfer, warps_per_sm: int = None):

@@ -350,3 +350,42 @@ def test_flat_stream_layout_reproduces_csr_product(group, perm):
                 rk = int(rowk[pid])
                 got[rk & 15, :, rk >> 4] += v4[q] @ x_tm[c4[q]]
     assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_regional_layout_reproduces_csr_product():
+    """v19 regional layout: region-local slots map back to columns through
+    each region's union list; regions span whole 256-entry iterations; the
+    head-flag stream gives every segment's (row, k) (host emulation)."""
+    from paper_2203_12339_b200.runtime import regional_layout
+
+    rng = np.random.default_rng(19)
+    dt = _random_device_transfer(rng, 32, 2, 4, 30)
+    x_tm = rng.standard_normal((dt.n, 3))
+    x_tm[rng.random(dt.n) < 0.5] = 0.0
+    want = _csr_vk(dt, x_tm)
+    R = regional_layout(dt)
+    c8 = R["pcols"].numpy().view(np.uint32).reshape(-1, 8)
+    v8 = R["pvals"].numpy().astype(np.float64).reshape(-1, 8)
+    heads = R["heads"].numpy().view(np.uint32)
+    hpre = R["hpre"].numpy().view(np.uint32)
+    rowk = R["rowk"].numpy().view(np.uint32)
+    ucols = R["ucols"].numpy().view(np.uint32)
+    uoff = R["uoff"].numpy()
+    rit = R["rit"].numpy()
+    T2 = 16
+    assert rit[-1] * 32 == c8.shape[0] or rit[-1] * 32 >= c8.shape[0] - 31
+    got = np.zeros_like(want)
+    for r in range(R["n_regions"]):
+        u = ucols[uoff[r]:uoff[r + 1]]
+        assert np.all(np.diff(u.astype(np.int64)) > 0)
+        for i in range(rit[r], rit[r + 1]):
+            for lane in range(32):
+                q = 32 * i + lane
+                if q >= c8.shape[0]:
+                    continue
+                hm = int(heads[i]) & ((2 << lane) - 1)
+                pid = int(hpre[i]) + bin(hm).count("1") - 1
+                rk = int(rowk[pid])
+                assert (rk >> 4) // T2 == r  # the segment belongs to this region
+                got[rk & 15, :, rk >> 4] += v8[q] @ x_tm[u[c8[q]]]
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
