@@ -348,6 +348,32 @@ int sss_transfer_regional(int K, int n_rows, const uint32_t* ucols, const int* u
                           const uint32_t* seg_rowk, const void* xp, const uint32_t* bits,
                           double* vk, void* stream);
 
+/* ---- transfer v20: dense K-fused pairs. cols (npairs) = tile-major column
+ * per (row, column) pair (N = padding); vals (npairs, 8) f32 = the pair's
+ * terms 0..K-1 (0 where absent); rows padded to 32 pairs; pieces (uint32 x4)
+ * {pair0, npair (multiples of 32), row, 0}; warp_begin (n_warps + 1);
+ * min_ctas = occupancy target (1..3 CTAs of 256 threads per SM); bits / xp
+ * from sss_pack_x_bits. Zeroes and fills vk; shade with sss_edit_finish. */
+int sss_transfer_k8(int K, int n_rows, const uint32_t* cols, const float* vals, const void* pieces,
+                    const unsigned* warp_begin, int n_warps, int min_ctas, const void* xp,
+                    const uint32_t* bits, double* vk, void* stream);
+
+/* ---- (a) direct lights with shadow rays: irradiance_direct
+ * (lighting.py:208-290) with BVH any-hit visibility (lighting.py:101-176,
+ * _kernels_nb.py:208-298). lights: n_lights x 12 doubles {kind (0 point, 1
+ * directional, 2 sphere), a[3] (position / unit direction light->scene /
+ * center), b[3] (intensity / irradiance / radiance), radius, 0...};
+ * material[6] = eta (the incident Fresnel term); ray origins offset
+ * ray_offset along the normal; the BVH as built by shadows.build_bvh (node
+ * bounds (M, 3) f64, children / leaf ranges i32, triangles v0 / e1 / e2
+ * (T, 3) f64 in leaf order). E: planar (3, N) doubles. */
+int sss_direct_irradiance(int n_points, const float* positions, const float* normals,
+                          int n_lights, const double* lights, const double* material,
+                          double ray_offset, double bbox_diagonal, const double* node_min,
+                          const double* node_max, const int* node_left, const int* node_right,
+                          const int* node_start, const int* node_count, const double* v0,
+                          const double* e1, const double* e2, double* E, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

@@ -756,3 +756,146 @@ def csr_rows_apply(rowptr, cols, vals, rows, x):
     for ch in range(x.shape[0]):
         out[:, ch] = np.bincount(seg, weights=v * x[ch, c], minlength=rows.size)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Direct lights with shadow rays: lighting.py:101-290,
+# _kernels_nb.py:208-298 / _kernels_np.py:165-232. The geometry image's grid
+# triangulation is the mesh the shadow rays see.
+# ---------------------------------------------------------------------------
+RAY_OFFSET_SCALE = 1e-4       # lighting.py:23 (of the bbox diagonal)
+SPHERE_LIGHT_SAMPLES = 64     # lighting.py:24 (8 x 8 midpoint cone strata)
+
+
+def grid_triangles(side):
+    """Two triangles per geometry-image cell: (i00, i01, i11), (i00, i11, i10)."""
+    r, c = np.meshgrid(np.arange(side - 1), np.arange(side - 1), indexing="ij")
+    i00 = (r * side + c).reshape(-1)
+    i01, i10 = i00 + 1, i00 + side
+    i11 = i10 + 1
+    t = np.empty((i00.size * 2, 3), np.int32)
+    t[0::2] = np.stack([i00, i01, i11], 1)
+    t[1::2] = np.stack([i00, i11, i10], 1)
+    return t
+
+
+def tri_any_hit(o, d, tmax, v0, e1, e2):  # _kernels_np.py:165-176 (row-aligned batches)
+    pv = np.cross(d, e2)
+    det = np.einsum("ij,ij->i", e1, pv)
+    ok = np.abs(det) > 1e-14
+    inv = np.where(ok, 1.0 / np.where(ok, det, 1.0), 0.0)
+    tv = o - v0
+    u = np.einsum("ij,ij->i", tv, pv) * inv
+    qv = np.cross(tv, e1)
+    v = np.einsum("ij,ij->i", d, qv) * inv
+    t = np.einsum("ij,ij->i", e2, qv) * inv
+    return ok & (u >= 0.0) & (u <= 1.0) & (v >= 0.0) & (u + v <= 1.0) & (t > 1e-9) & (t < tmax)
+
+
+def any_hit(origins, dirs, tmax, vertices, tris, chunk=1 << 22):
+    """Brute force over every triangle (the checker; any-hit is independent
+    of the acceleration structure)."""
+    v = np.asarray(vertices, np.float64)
+    v0 = v[tris[:, 0]]
+    e1 = v[tris[:, 1]] - v0
+    e2 = v[tris[:, 2]] - v0
+    nt = v0.shape[0]
+    out = np.zeros(origins.shape[0], bool)
+    per = max(1, chunk // nt)
+    for a in range(0, origins.shape[0], per):
+        b = min(a + per, origins.shape[0])
+        m = b - a
+        o = np.repeat(origins[a:b], nt, axis=0)
+        d = np.repeat(dirs[a:b], nt, axis=0)
+        tm = np.repeat(tmax[a:b], nt)
+        h = tri_any_hit(o, d, tm, np.tile(v0, (m, 1)), np.tile(e1, (m, 1)), np.tile(e2, (m, 1)))
+        out[a:b] = h.reshape(m, nt).any(axis=1)
+    return out
+
+
+def _cone_strata():  # lighting.py:191-195
+    side = int(np.sqrt(SPHERE_LIGHT_SAMPLES))
+    u = (np.arange(side) + 0.5) / side
+    u1, u2 = np.meshgrid(u, u, indexing="ij")
+    return u1.ravel(), u2.ravel()
+
+
+def _orthonormal_frame(axis):  # lighting.py:200-205
+    helper = np.where(np.abs(axis[..., 2:3]) < 0.9, [0.0, 0.0, 1.0], [1.0, 0.0, 0.0])
+    t1 = np.cross(axis, helper)
+    t1 /= np.linalg.norm(t1, axis=-1, keepdims=True)
+    t2 = np.cross(axis, t1)
+    return t1, t2
+
+
+def irradiance_direct(positions, normals, lights, vertices, tris, eta):
+    """lighting.py:208-249 (+ _sphere_light_irradiance :252-290). lights: list
+    of ("point", position, intensity) / ("directional", direction (unit,
+    light -> scene), irradiance) / ("sphere", center, radius, radiance)."""
+    pos = np.asarray(positions, np.float64)
+    nrm = np.asarray(normals, np.float64)
+    n = pos.shape[0]
+    v = np.asarray(vertices, np.float64)
+    bbox_diag = float(np.linalg.norm(v.max(axis=0) - v.min(axis=0)))
+    origins = pos + RAY_OFFSET_SCALE * bbox_diag * nrm
+    e_out = np.zeros((n, 3))
+    for light in lights:
+        kind = light[0]
+        if kind == "point":
+            _, lp, inten = light
+            dvec = np.asarray(lp, np.float64)[None, :] - pos
+            dist = np.linalg.norm(dvec, axis=1)
+            wi = dvec / dist[:, None]
+            cos = np.einsum("ij,ij->i", nrm, wi)
+            lit = cos > 0.0
+            vis = np.zeros(n, bool)
+            if lit.any():
+                vis[lit] = ~any_hit(origins[lit], wi[lit], dist[lit], v, tris)
+            weight = np.where(lit & vis, fresnel_transmittance(eta, np.clip(cos, 0.0, 1.0))
+                              * np.clip(cos, 0.0, 1.0) / (dist * dist), 0.0)
+            e_out += weight[:, None] * np.asarray(inten, np.float64)[None, :]
+        elif kind == "directional":
+            _, direction, irr = light
+            wi = -np.asarray(direction, np.float64)
+            cos = nrm @ wi
+            lit = cos > 0.0
+            vis = np.zeros(n, bool)
+            if lit.any():
+                far = np.full(int(lit.sum()), 4.0 * bbox_diag + 1.0)
+                vis[lit] = ~any_hit(origins[lit], np.tile(wi, (int(lit.sum()), 1)), far, v, tris)
+            weight = np.where(lit & vis, fresnel_transmittance(eta, np.clip(cos, 0.0, 1.0))
+                              * np.clip(cos, 0.0, 1.0), 0.0)
+            e_out += weight[:, None] * np.asarray(irr, np.float64)[None, :]
+        elif kind == "sphere":
+            _, center, radius, rad = light
+            axis = np.asarray(center, np.float64)[None, :] - pos
+            dist = np.linalg.norm(axis, axis=1)
+            if np.any(dist <= radius):
+                raise ValueError("sphere light overlaps the surface")
+            axis = axis / dist[:, None]
+            sin_max = radius / dist
+            cos_max = np.sqrt(np.clip(1.0 - sin_max * sin_max, 0.0, 1.0))
+            omega = 2.0 * np.pi * (1.0 - cos_max)
+            u1, u2 = _cone_strata()
+            t1, t2 = _orthonormal_frame(axis)
+            ct = 1.0 - u1[None, :] * (1.0 - cos_max[:, None])
+            st = np.sqrt(np.clip(1.0 - ct * ct, 0.0, 1.0))
+            phi = 2.0 * np.pi * u2[None, :]
+            dirs = (axis[:, None, :] * ct[..., None]
+                    + t1[:, None, :] * (st * np.cos(phi))[..., None]
+                    + t2[:, None, :] * (st * np.sin(phi))[..., None])
+            cos = np.einsum("ij,isj->is", nrm, dirs)
+            lit = cos > 0.0
+            proj = dist[:, None] * ct
+            under = proj * proj - (dist * dist - radius * radius)[:, None]
+            t_hit = proj - np.sqrt(np.clip(under, 0.0, None))
+            vis = np.zeros_like(lit)
+            if lit.any():
+                ray_o = np.repeat(origins, len(u1), axis=0)[lit.ravel()]
+                vis[lit] = ~any_hit(ray_o, dirs[lit], t_hit[lit], v, tris)
+            weight = np.where(lit & vis, fresnel_transmittance(eta, np.clip(cos, 0.0, 1.0))
+                              * np.clip(cos, 0.0, 1.0), 0.0).mean(axis=1) * omega
+            e_out += weight[:, None] * np.asarray(rad, np.float64)[None, :]
+        else:
+            raise TypeError(f"unsupported light {kind}")
+    return e_out

@@ -25,6 +25,8 @@
 #include "kflat18.cu"
 #include "sweep.cu"
 #include "regional19.cu"
+#include "k8_20.cu"
+#include "direct.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -673,7 +675,12 @@ int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pv
       sss::k_transfer_flat8s<MB, true><<<grid, sss::kV17Threads, smem, S_(stream)>>>(             \
           n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);            \
     } while (0)
-    if (minb == 14) SSS_F8S1(6);
+    if (x_f32 && minb == 16) {
+      const auto* xf = reinterpret_cast<const float4*>(xp);
+      if (int r = set_smem((const void*)sss::k_transfer_flat8s<8, true, float, float4>, smem)) return r;
+      sss::k_transfer_flat8s<8, true, float, float4><<<grid, sss::kV17Threads, smem, S_(stream)>>>(
+          n_rows, n8, c8, v8, heads, head_prefix, seg_rowk, warp_begin, xf, bits, vk);
+    } else if (minb == 14) SSS_F8S1(6);
     else if (minb == 16) SSS_F8S1(8);
     else if (minb == 18) SSS_F8S1(10);
     else if (minb == 4) SSS_F8S(4);
@@ -809,6 +816,53 @@ int sss_transfer_regional(int K, int n_rows, const uint32_t* ucols, const int* u
       reinterpret_cast<const unsigned long long*>(pvals), (unsigned)(n_entries / 8), heads,
       head_prefix, seg_rowk, reinterpret_cast<const double4*>(xp), bits, vk);
   return check_launch("k_transfer_regional");
+}
+
+int sss_transfer_k8(int K, int n_rows, const uint32_t* cols, const float* vals, const void* pieces,
+                    const unsigned* warp_begin, int n_warps, int min_ctas, const void* xp,
+                    const uint32_t* bits, double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || !cols || !vals || !pieces || !warp_begin || !xp ||
+      !bits || !vk || n_warps <= 0 || n_warps % (sss::kV20Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_k8 arguments");
+  if (reinterpret_cast<uintptr_t>(vals) % 16 || reinterpret_cast<uintptr_t>(xp) % 32 ||
+      reinterpret_cast<uintptr_t>(pieces) % 16)
+    return fail(SSS_EINVAL, "transfer_k8: vals / pieces 16-byte, xp 32-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const size_t smem = (size_t)((n_rows + 31) / 32) * 4;
+  const unsigned grid = n_warps / (sss::kV20Threads / 32);
+  const auto* v4 = reinterpret_cast<const float4*>(vals);
+  const auto* pc = reinterpret_cast<const uint4*>(pieces);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+#define SSS_K8(MB)                                                                              \
+  do {                                                                                          \
+    if (int r = set_smem((const void*)sss::k_transfer_k8<MB>, smem)) return r;                  \
+    sss::k_transfer_k8<MB><<<grid, sss::kV20Threads, smem, S_(stream)>>>(K, n_rows, cols, v4,   \
+                                                                         pc, warp_begin, x4,    \
+                                                                         bits, vk);             \
+  } while (0)
+  if (min_ctas >= 3) SSS_K8(3);
+  else if (min_ctas == 2) SSS_K8(2);
+  else SSS_K8(1);
+#undef SSS_K8
+  return check_launch("k_transfer_k8");
+}
+
+int sss_direct_irradiance(int n_points, const float* positions, const float* normals,
+                          int n_lights, const double* lights, const double* material,
+                          double ray_offset, double bbox_diagonal, const double* node_min,
+                          const double* node_max, const int* node_left, const int* node_right,
+                          const int* node_start, const int* node_count, const double* v0,
+                          const double* e1, const double* e2, double* E, void* stream) {
+  if (n_points <= 0 || n_lights < 0 || !positions || !normals || !material || !E ||
+      (n_lights > 0 && !lights) || !node_min || !node_max || !node_left || !node_right ||
+      !node_start || !node_count || !v0 || !e1 || !e2)
+    return fail(SSS_EINVAL, "bad direct_irradiance arguments");
+  const sss::BvhView B{node_min, node_max, node_left, node_right, node_start, node_count,
+                       v0, e1, e2};
+  sss::k_direct_irradiance<<<(n_points + 127) / 128, 128, 0, S_(stream)>>>(
+      n_points, positions, normals, n_lights, lights, material, ray_offset, bbox_diagonal, B, E);
+  return check_launch("k_direct_irradiance");
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

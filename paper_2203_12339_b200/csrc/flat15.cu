@@ -433,11 +433,27 @@ __device__ __forceinline__ void v17_gather_half(const V17Slot& S, const double4*
   }
 }
 
-__device__ __forceinline__ void v17_consume_split(const V17Slot& S, const double4* __restrict__ xp,
+__device__ __forceinline__ void v17_gather_half(const V17Slot& S, const float4* __restrict__ xp,
+                                                const uint32_t* sbits, int h, float (&x)[4][3]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t c = v17_col(S, h * 4 + e);
+    x[e][0] = x[e][1] = x[e][2] = 0.0f;
+    if (!sbits || ((sbits[c >> 5] >> (c & 31u)) & 1u)) {
+      float x3;
+      asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(x[e][0]), "=f"(x[e][1]), "=f"(x[e][2]), "=f"(x3)
+                   : "l"(xp + c));
+    }
+  }
+}
+
+template <typename XT = double, typename XP = double4>
+__device__ __forceinline__ void v17_consume_split(const V17Slot& S, const XP* __restrict__ xp,
                                                   const uint32_t* sbits, int lane, unsigned upto,
                                                   int N, const uint32_t* __restrict__ rowk,
                                                   double* __restrict__ vk) {
-  double x[4][3];
+  XT x[4][3];
   double p0 = 0.0, p1 = 0.0, p2 = 0.0;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -445,9 +461,9 @@ __device__ __forceinline__ void v17_consume_split(const V17Slot& S, const double
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const double v = (double)v17_val(S, h * 4 + e);
-      p0 = fma(v, x[e][0], p0);
-      p1 = fma(v, x[e][1], p1);
-      p2 = fma(v, x[e][2], p2);
+      p0 = fma(v, (double)x[e][0], p0);
+      p1 = fma(v, (double)x[e][1], p1);
+      p2 = fma(v, (double)x[e][2], p2);
     }
   }
   const unsigned hm = S.h & upto;
@@ -473,12 +489,12 @@ __device__ __forceinline__ void v17_consume_split(const V17Slot& S, const double
   }
 }
 
-template <int MINB, bool SINGLE = false>
+template <int MINB, bool SINGLE = false, typename XT = double, typename XP = double4>
 __global__ void __launch_bounds__(kV17Threads, MINB) k_transfer_flat8s(
     int N, unsigned n8, const unsigned long long* __restrict__ C8,
     const unsigned long long* __restrict__ V8, const uint32_t* __restrict__ H,
     const uint32_t* __restrict__ hpre, const uint32_t* __restrict__ rowk,
-    const unsigned* __restrict__ warp_begin, const double4* __restrict__ xp,
+    const unsigned* __restrict__ warp_begin, const XP* __restrict__ xp,
     const uint32_t* __restrict__ bits, double* __restrict__ vk) {
   extern __shared__ uint32_t v17_bits[];
   if (bits) {
@@ -496,7 +512,7 @@ __global__ void __launch_bounds__(kV17Threads, MINB) k_transfer_flat8s(
     for (unsigned i = i0; i < i1; ++i) {
       V17Slot A;
       v17_load(A, i, lane, n8, C8, V8, H, hpre);
-      v17_consume_split(A, xp, sb, lane, upto, N, rowk, vk);
+      v17_consume_split<XT, XP>(A, xp, sb, lane, upto, N, rowk, vk);
     }
     return;
   }
@@ -505,10 +521,10 @@ __global__ void __launch_bounds__(kV17Threads, MINB) k_transfer_flat8s(
   if (i0 + 1 < i1) v17_load(B, i0 + 1, lane, n8, C8, V8, H, hpre);
 #pragma unroll 1
   for (unsigned i = i0; i < i1; i += 2) {
-    v17_consume_split(A, xp, sb, lane, upto, N, rowk, vk);
+    v17_consume_split<XT, XP>(A, xp, sb, lane, upto, N, rowk, vk);
     if (i + 2 < i1) v17_load(A, i + 2, lane, n8, C8, V8, H, hpre);
     if (i + 1 >= i1) break;
-    v17_consume_split(B, xp, sb, lane, upto, N, rowk, vk);
+    v17_consume_split<XT, XP>(B, xp, sb, lane, upto, N, rowk, vk);
     if (i + 3 < i1) v17_load(B, i + 3, lane, n8, C8, V8, H, hpre);
   }
 }

@@ -34,6 +34,7 @@ from .basis import DiffusionBasis, OpticalMaterial
 from .config import CAMERA, E_KEEP, ENV_COEFF_KEEP
 from .geometry import GeometryImage
 from .lighting import face_directions, face_solid_angles, sh_transfer
+from .shadows import LightRig, build_bvh, grid_triangles
 from .transfer import DeviceTransfer, flat_to_tile_major
 
 STAGES = ("irradiance", "transfer", "weighting", "inverse_wavelet", "raster")
@@ -203,6 +204,26 @@ class Scene:
                 self._light_kind = ("env", s)
                 self._graph = None
             self._stage_copy(self.light_buf, light.faces)
+        elif isinstance(light, LightRig):
+            nl = max(len(light.lights), 1)
+            if self._light_kind != ("direct", nl):
+                if getattr(self, "_bvh_dev", None) is None:
+                    bvh = build_bvh(self.geometry.positions.astype(np.float64),
+                                    grid_triangles(self.side))
+                    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dt), device=dev)
+                    self._bvh_dev = {
+                        "nmin": t(bvh.node_min, np.float64), "nmax": t(bvh.node_max, np.float64),
+                        "left": t(bvh.node_left, np.int32), "right": t(bvh.node_right, np.int32),
+                        "start": t(bvh.node_start, np.int32), "count": t(bvh.node_count, np.int32),
+                        "v0": t(bvh.v0, np.float64), "e1": t(bvh.e1, np.float64),
+                        "e2": t(bvh.e2, np.float64), "ray_offset": bvh.ray_offset,
+                        "diag": bvh.bbox_diagonal}
+                self.light_buf = torch.empty((nl, 12), dtype=torch.float64, device=dev)
+                self.E_planar = torch.empty((3, self.n), dtype=torch.float64, device=dev)
+                self._light_kind = ("direct", nl)
+                self._graph = None
+            self._n_direct = len(light.lights)
+            self._stage_copy(self.light_buf, light.packed())
         else:
             raise TypeError(f"unsupported light {type(light).__name__}")
         self.light = light
@@ -216,7 +237,19 @@ class Scene:
         if want_E and self.E is None:
             self.E = torch.empty((self.n, 3), dtype=torch.float64, device="cuda")
         E = self.E if want_E else None
-        if self._light_kind[0] == "sh":
+        if self._light_kind[0] == "direct":
+            b = self._bvh_dev
+            _lib.call("sss_direct_irradiance", self.n, _lib.ptr(self.positions), _lib.ptr(self.normals),
+                      self._n_direct, _lib.ptr(self.light_buf), _lib.ptr(self.material_buf),
+                      b["ray_offset"], b["diag"], _lib.ptr(b["nmin"]), _lib.ptr(b["nmax"]),
+                      _lib.ptr(b["left"]), _lib.ptr(b["right"]), _lib.ptr(b["start"]),
+                      _lib.ptr(b["count"]), _lib.ptr(b["v0"]), _lib.ptr(b["e1"]), _lib.ptr(b["e2"]),
+                      _lib.ptr(self.E_planar), sp)
+            _lib.call("sss_haar2d", _lib.ptr(self.E_planar), _lib.ptr(self.ehat), 3, self.side,
+                      self.levels, 0, sp)
+            if E is not None:
+                E.copy_(self.E_planar.t())
+        elif self._light_kind[0] == "sh":
             _lib.call("sss_sh_irradiance", _lib.ptr(self.T_l), _lib.ptr(self.light_buf),
                       self._light_kind[1], self.side, self.levels, _lib.ptr(E),
                       _lib.ptr(self.ehat), sp)
@@ -272,6 +305,23 @@ class Scene:
             _lib.call("sss_transfer_kflat", self.K, self.n, _lib.ptr(cols), _lib.ptr(vals),
                       _lib.ptr(steps), _lib.ptr(wbeg), W, _lib.ptr(self.xp),
                       _lib.ptr(self.xbits), _lib.ptr(self.vk), sp)
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
+        if self.transfer_kernel == "k8":
+            sp = _lib.stream_ptr(stream)
+            if getattr(t, "k8", None) is None:
+                t.k8 = k8_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            if getattr(self, "xbits", None) is None:
+                self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+            _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                      _lib.ptr(self.xbits), sp)
+            cols, vals, pieces, wbeg, W, _ = t.k8
+            _lib.call("sss_transfer_k8", self.K, self.n, _lib.ptr(cols), _lib.ptr(vals),
+                      _lib.ptr(pieces), _lib.ptr(wbeg), W, int(os.environ.get("SSS_K8_MINB", "2")),
+                      _lib.ptr(self.xp), _lib.ptr(self.xbits), _lib.ptr(self.vk), sp)
             if epilogue:
                 self._launch_edit(stream)
             return epilogue
@@ -1208,6 +1258,62 @@ def regional_layout(t: DeviceTransfer, region_tiles: int = 1):
             "rowk": rowk, "ucols": ucols, "uoff": uoff.to(torch.int32).contiguous(),
             "rit": reg_it.to(torch.int32).contiguous(), "n_regions": n_reg,
             "umax": int(ucnt.max()), "stats": stats}
+
+
+def k8_layout(t: DeviceTransfer, warps_per_sm: int = None, split: int = None):
+    """v20 dense K-fused pairs: every (row, column) pair of the K operators
+    once, its K <= 8 values in one 32-byte slot (0 for absent terms); rows
+    padded to multiples of 32 pairs (column = N marks padding), cut into
+    pieces of <= split pairs; cost-balanced per-warp piece ranges."""
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_K8_WPS", "20"))
+    split = split or int(os.environ.get("SSS_K8_SPLIT", "1024"))
+    split -= split % 32
+    if t.K > 8:
+        raise ValueError("the dense K-fused layout needs K <= 8")
+    dev = t.rowptr.device
+    n, K = t.n, t.K
+    i64 = dict(dtype=torch.int64, device=dev)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+    W = nsm * warps_per_sm
+    W -= W % 8
+    rp = t.rowptr.to(torch.int64)
+    lens = (rp[:, 1:] - rp[:, :-1]).reshape(-1)
+    base = int(rp[0, 0].item())
+    total = int(lens.sum().item())
+    kr = torch.arange(K * n, **i64)
+    row_of = torch.repeat_interleave(kr % n, lens)
+    k_of = torch.repeat_interleave(kr // n, lens)
+    col = t.cols[base:base + total].to(torch.int64) & 0xFFFFFFFF
+    upair, inv = torch.unique(row_of * n + col, return_inverse=True)
+    del col
+    prow = upair // n
+    pcol = upair % n
+    npairs = upair.numel()
+    rowcnt = torch.bincount(prow, minlength=n)
+    rowstart = torch.cumsum(rowcnt, 0) - rowcnt
+    rowpad = (rowcnt + 31) // 32 * 32
+    padstart = torch.cumsum(rowpad, 0) - rowpad
+    npad = int(rowpad.sum().item())
+    ppos = torch.arange(npairs, **i64) - rowstart[prow] + padstart[prow]
+    cols_p = torch.full((max(npad, 32),), n, dtype=torch.int32, device=dev)
+    cols_p[ppos] = pcol.to(torch.int32)
+    vals_p = torch.zeros((max(npad, 32), 8), dtype=torch.float32, device=dev)
+    vals_p[ppos[inv], k_of] = t.vals[base:base + total]
+    del inv, k_of, row_of, upair, pcol
+    npc = (rowpad + split - 1) // split
+    rep = torch.repeat_interleave(torch.arange(n, **i64), npc)
+    j = torch.arange(rep.numel(), **i64) - (torch.cumsum(npc, 0) - npc)[rep]
+    p0 = padstart[rep] + j * split
+    pn = torch.minimum(torch.full_like(p0, split), rowpad[rep] - j * split)
+    pieces = torch.stack([p0, pn, rep, torch.zeros_like(rep)], 1).to(torch.int32).contiguous()
+    cost = pn + 64
+    cum = torch.cat([torch.zeros(1, **i64), torch.cumsum(cost, 0)])
+    targets = torch.arange(W + 1, dtype=torch.float64, device=dev) * (float(cum[-1]) / W)
+    wbeg = torch.searchsorted(cum.to(torch.float64), targets, side="left")
+    wbeg[-1] = p0.numel()
+    stats = {"pairs": npairs, "padded_pairs": npad, "pieces": int(p0.numel()),
+             "bytes": npad * 36 + int(p0.numel()) * 16}
+    return (cols_p, vals_p, pieces, wbeg.to(torch.int32).contiguous(), W, stats)
 
 
 def kstep_layout(t: DeviceTransfer, warps_per_sm: int = None):

@@ -205,6 +205,40 @@ def main():
     ctn.save_container(HERE / "ref16.prts", basis, atlas, ct, mesh_hash,
                        metadata={"source": "sssrelight reference", "side": side})
 
+    # 6c. direct lights with shadow rays on the geometry image's grid mesh
+    #     (lighting.py:101-290): the reference's BVH any-hit and
+    #     irradiance_direct for a point, a directional and a sphere light
+    from sssrelight.surface import TriangleMesh
+    from oracle import sss_oracle as O
+
+    dside = 16
+    dg = make_geometry_image(dside, amp=0.2, seed=5)
+    dpos = dg.positions.astype(np.float64)
+    dnrm = dg.normals.astype(np.float64)
+    tris = O.grid_triangles(dside)
+    mesh = TriangleMesh(vertices=dpos, normals=dnrm, triangles=tris)
+    dsamples = SurfaceSamples(positions=dpos, normals=dnrm, area=dg.area.astype(np.float64),
+                              source_vertex=np.arange(dside * dside, dtype=np.int32))
+    accel = lt.RayAccelerator(mesh)
+    lights = [lt.PointLight(position=[25.0, 18.0, 30.0], intensity=[900.0, 700.0, 500.0]),
+              lt.DirectionalLight(direction=[-0.3, -1.0, -0.4], irradiance=[0.8, 0.9, 1.0]),
+              lt.SphereLight(center=[-14.0, 6.0, 16.0], radius=3.0, radiance=[2.0, 1.5, 1.0])]
+    rig = lt.LightRig(lights=tuple(lights))
+    E_direct = lt.irradiance_direct(dsamples, rig, accel, 1.3)
+    drng = np.random.default_rng(9)
+    ro = dpos + accel.ray_offset * dnrm
+    rd = drng.standard_normal((dside * dside, 3))
+    rd /= np.linalg.norm(rd, axis=1, keepdims=True)
+    rt = np.full(dside * dside, 50.0)
+    hits = accel.any_hit(ro, rd, rt)
+    np.savez_compressed(HERE / "direct.npz", side=np.array(dside), positions=dpos, normals=dnrm,
+                        triangles=tris, E=E_direct, ray_o=ro, ray_d=rd, ray_t=rt, hits=hits,
+                        eta=np.array(1.3), ray_offset=np.array(accel.ray_offset),
+                        p_pos=lights[0].position, p_int=lights[0].intensity,
+                        d_dir=lights[1].direction, d_irr=lights[1].irradiance,
+                        s_c=lights[2].center, s_r=np.array(lights[2].radius),
+                        s_rad=lights[2].radiance)
+
     # 7. environment light: project_environment + dense ambient irradiance
     env_side = 8
     faces = np.exp(rng.standard_normal((6, env_side, env_side, 3)))

@@ -389,3 +389,83 @@ def test_regional_layout_reproduces_csr_product():
                 assert (rk >> 4) // T2 == r  # the segment belongs to this region
                 got[rk & 15, :, rk >> 4] += v8[q] @ x_tm[u[c8[q]]]
     assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_k8_dense_pairs_layout_reproduces_csr_product():
+    """v20 dense K-fused pairs: one lane per (row, column) pair with its K
+    values at slots 0..K-1; padding pairs carry column N (host emulation)."""
+    from paper_2203_12339_b200.runtime import k8_layout
+
+    rng = np.random.default_rng(20)
+    dt = _random_device_transfer(rng, 32, 2, 6, 30)
+    x_tm = rng.standard_normal((dt.n, 3))
+    x_tm[rng.random(dt.n) < 0.5] = 0.0
+    want = _csr_vk(dt, x_tm)
+    cols, vals, pieces, wbeg, W, stats = k8_layout(dt, warps_per_sm=1, split=64)
+    cols = cols.numpy().view(np.uint32)
+    vals = vals.numpy().astype(np.float64)
+    pieces = pieces.numpy()
+    wbeg = wbeg.numpy()
+    assert wbeg[0] == 0 and wbeg[-1] == pieces.shape[0]
+    got = np.zeros_like(want)
+    for p0, pn, row, _ in pieces:
+        assert p0 % 32 == 0 and pn % 32 == 0 and 0 < pn <= 64
+        for p in range(p0, p0 + pn):
+            c = int(cols[p])
+            if c >= dt.n:
+                assert np.all(vals[p] == 0)
+                continue
+            for k in range(dt.K):
+                got[k, :, row] += vals[p, k] * x_tm[c]
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def _bvh_any_hit_py(bvh, o, d, tmax):
+    """The GPU traversal restated (stack, slab AABB test, reference triangle
+    test in the numba operation order): test-side check of the BVH build."""
+    stack = [0]
+    while stack:
+        nd = stack.pop()
+        tn, tf = 0.0, tmax
+        ok = True
+        for ax in range(3):
+            lo, hi = bvh.node_min[nd, ax], bvh.node_max[nd, ax]
+            if d[ax] == 0.0:
+                if o[ax] < lo or o[ax] > hi:
+                    ok = False
+                    break
+            else:
+                inv = 1.0 / d[ax]
+                ta, tb = (lo - o[ax]) * inv, (hi - o[ax]) * inv
+                if ta > tb:
+                    ta, tb = tb, ta
+                tn, tf = max(tn, ta), min(tf, tb)
+                if tn > tf:
+                    ok = False
+                    break
+        if not ok:
+            continue
+        c = bvh.node_count[nd]
+        if c > 0:
+            s = bvh.node_start[nd]
+            if O.tri_any_hit(np.repeat(o[None], c, 0), np.repeat(d[None], c, 0), np.full(c, tmax),
+                             bvh.v0[s:s + c], bvh.e1[s:s + c], bvh.e2[s:s + c]).any():
+                return True
+        else:
+            stack += [bvh.node_left[nd], bvh.node_right[nd]]
+    return False
+
+
+def test_bvh_any_hit_matches_reference_rays(golden):
+    from paper_2203_12339_b200.shadows import build_bvh
+
+    g = golden("direct")
+    bvh = build_bvh(g["positions"], g["triangles"])
+    assert bvh.ray_offset == float(g["ray_offset"])
+    got = np.array([_bvh_any_hit_py(bvh, o, d, t)
+                    for o, d, t in zip(g["ray_o"], g["ray_d"], g["ray_t"])])
+    assert np.array_equal(got, g["hits"])
+    # structure: leaves partition the triangles
+    leaves = bvh.node_count > 0
+    assert bvh.node_count[leaves].sum() == g["triangles"].shape[0]
+    assert np.all(bvh.node_count <= 4)

@@ -185,3 +185,17 @@ def test_env_projection_matches_reference(golden):
     w2 = O.haar2d_fwd(W.reshape(-1, 8, 8)).reshape(W.shape[0], -1)
     E = O.env_irradiance(w2, spectra)  # fp64 w2 here: Parseval identity
     assert np.allclose(E, g["E"], rtol=1e-11, atol=1e-14)
+
+
+def test_direct_lights_oracle_matches_reference(golden):
+    """irradiance_direct (point + directional + sphere light, BVH shadow rays)
+    and any-hit queries, against the reference run on the geometry image's
+    grid mesh (lighting.py:101-290)."""
+    g = golden("direct")
+    h = O.any_hit(g["ray_o"], g["ray_d"], g["ray_t"], g["positions"], g["triangles"])
+    assert np.array_equal(h, g["hits"])
+    lights = [("point", g["p_pos"], g["p_int"]), ("directional", g["d_dir"], g["d_irr"]),
+              ("sphere", g["s_c"], float(g["s_r"]), g["s_rad"])]
+    E = O.irradiance_direct(g["positions"], g["normals"], lights, g["positions"], g["triangles"],
+                            float(g["eta"]))
+    assert np.array_equal(E, g["E"])
