@@ -363,16 +363,18 @@ int sss_transfer_k8(int K, int n_rows, const uint32_t* cols, const float* vals, 
  * _kernels_nb.py:208-298). lights: n_lights x 12 doubles {kind (0 point, 1
  * directional, 2 sphere), a[3] (position / unit direction light->scene /
  * center), b[3] (intensity / irradiance / radiance), radius, 0...};
- * material[6] = eta (the incident Fresnel term); ray origins offset
- * ray_offset along the normal; the BVH as built by shadows.build_bvh (node
- * bounds (M, 3) f64, children / leaf ranges i32, triangles v0 / e1 / e2
- * (T, 3) f64 in leaf order). E: planar (3, N) doubles. */
+ * kinds: the same n_lights kinds in HOST memory (they pick each light's
+ * kernel at launch; a graph captured for one rig structure replays any values
+ * of that structure). material[6] = eta (the incident Fresnel term); ray
+ * origins offset ray_offset along the normal; the packed BVH of
+ * shadows.BVH.packed(): nodes (M, 8) doubles {min[3], max[3], (i32 left,
+ * i32 right), (i32 start, i32 count)}, tris (T, 10) doubles {v0[3], e1[3],
+ * e2[3], 0} in leaf order. E: planar (3, N) doubles (zeroed, then one launch
+ * per light adds its term in light order). */
 int sss_direct_irradiance(int n_points, const float* positions, const float* normals,
-                          int n_lights, const double* lights, const double* material,
-                          double ray_offset, double bbox_diagonal, const double* node_min,
-                          const double* node_max, const int* node_left, const int* node_right,
-                          const int* node_start, const int* node_count, const double* v0,
-                          const double* e1, const double* e2, double* E, void* stream);
+                          int n_lights, const int* kinds, const double* lights,
+                          const double* material, double ray_offset, double bbox_diagonal,
+                          const double* nodes, const double* tris, double* E, void* stream);
 
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

@@ -849,20 +849,48 @@ int sss_transfer_k8(int K, int n_rows, const uint32_t* cols, const float* vals, 
 }
 
 int sss_direct_irradiance(int n_points, const float* positions, const float* normals,
-                          int n_lights, const double* lights, const double* material,
-                          double ray_offset, double bbox_diagonal, const double* node_min,
-                          const double* node_max, const int* node_left, const int* node_right,
-                          const int* node_start, const int* node_count, const double* v0,
-                          const double* e1, const double* e2, double* E, void* stream) {
-  if (n_points <= 0 || n_lights < 0 || !positions || !normals || !material || !E ||
-      (n_lights > 0 && !lights) || !node_min || !node_max || !node_left || !node_right ||
-      !node_start || !node_count || !v0 || !e1 || !e2)
+                          int n_lights, const int* kinds, const double* lights,
+                          const double* material, double ray_offset, double bbox_diagonal,
+                          const double* nodes, const double* tris, double* E, void* stream) {
+  if (n_points <= 0 || n_lights < 0 || !positions || !normals || !material || !E || !nodes ||
+      !tris || (n_lights > 0 && (!lights || !kinds)))
     return fail(SSS_EINVAL, "bad direct_irradiance arguments");
-  const sss::BvhView B{node_min, node_max, node_left, node_right, node_start, node_count,
-                       v0, e1, e2};
-  sss::k_direct_irradiance<<<(n_points + 127) / 128, 128, 0, S_(stream)>>>(
-      n_points, positions, normals, n_lights, lights, material, ray_offset, bbox_diagonal, B, E);
-  return check_launch("k_direct_irradiance");
+  for (int l = 0; l < n_lights; ++l)
+    if (kinds[l] < 0 || kinds[l] > 2) return fail(SSS_EINVAL, "unknown light kind");
+  cudaStream_t st = S_(stream);
+  if (cudaMemsetAsync(E, 0, sizeof(double) * 3 * (size_t)n_points, st) != cudaSuccess)
+    return fail(SSS_ECUDA, "memset E");
+  const sss::BvhView B{reinterpret_cast<const double2*>(nodes),
+                       reinterpret_cast<const double2*>(tris)};
+  const char* sv = getenv("SSS_DIRECT_SPLIT");
+  const int split = sv ? atoi(sv) : 3;
+  for (int l = 0; l < n_lights; ++l) {
+    const double* L = lights + 12 * (size_t)l;
+    if (kinds[l] < 2) {
+#define SSS_DS(K, S)                                                                        \
+  do {                                                                                      \
+    const int grid = (n_points + (sss::kDirectThreads >> S) - 1) / (sss::kDirectThreads >> S); \
+    sss::k_direct_single<K, S><<<grid, sss::kDirectThreads, 0, st>>>(                       \
+        n_points, positions, normals, L, material, ray_offset, bbox_diagonal, B, E);         \
+  } while (0)
+#define SSS_DSK(K)        \
+  if (split <= 0) SSS_DS(K, 0); \
+  else if (split == 1) SSS_DS(K, 1); \
+  else if (split == 2) SSS_DS(K, 2); \
+  else if (split == 3) SSS_DS(K, 3); \
+  else SSS_DS(K, 4)
+      if (kinds[l] == 0) { SSS_DSK(0); } else { SSS_DSK(1); }
+#undef SSS_DSK
+#undef SSS_DS
+    } else {
+      sss::k_direct_sphere<<<(n_points + sss::kSpherePts - 1) / sss::kSpherePts,
+                             64 * sss::kSpherePts, 0, st>>>(n_points, positions, normals, L,
+                                                            material, ray_offset, B, E);
+    }
+    const int rc = check_launch("k_direct_light");
+    if (rc) return rc;
+  }
+  return SSS_OK;
 }
 
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,

@@ -205,24 +205,22 @@ class Scene:
                 self._graph = None
             self._stage_copy(self.light_buf, light.faces)
         elif isinstance(light, LightRig):
-            nl = max(len(light.lights), 1)
-            if self._light_kind != ("direct", nl):
+            kinds = tuple(int(k) for k in light.kinds())
+            if self._light_kind != ("direct", kinds):
                 if getattr(self, "_bvh_dev", None) is None:
                     bvh = build_bvh(self.geometry.positions.astype(np.float64),
                                     grid_triangles(self.side))
-                    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a, dt), device=dev)
-                    self._bvh_dev = {
-                        "nmin": t(bvh.node_min, np.float64), "nmax": t(bvh.node_max, np.float64),
-                        "left": t(bvh.node_left, np.int32), "right": t(bvh.node_right, np.int32),
-                        "start": t(bvh.node_start, np.int32), "count": t(bvh.node_count, np.int32),
-                        "v0": t(bvh.v0, np.float64), "e1": t(bvh.e1, np.float64),
-                        "e2": t(bvh.e2, np.float64), "ray_offset": bvh.ray_offset,
-                        "diag": bvh.bbox_diagonal}
-                self.light_buf = torch.empty((nl, 12), dtype=torch.float64, device=dev)
+                    nodes, tris = bvh.packed()
+                    self._bvh_dev = {"nodes": torch.as_tensor(nodes, device=dev),
+                                     "tris": torch.as_tensor(tris, device=dev),
+                                     "ray_offset": bvh.ray_offset, "diag": bvh.bbox_diagonal}
+                self.light_buf = torch.empty((max(len(kinds), 1), 12), dtype=torch.float64,
+                                             device=dev)
+                self._light_kinds_host = torch.tensor(kinds or (0,), dtype=torch.int32)
                 self.E_planar = torch.empty((3, self.n), dtype=torch.float64, device=dev)
-                self._light_kind = ("direct", nl)
+                self._light_kind = ("direct", kinds)
                 self._graph = None
-            self._n_direct = len(light.lights)
+            self._n_direct = len(kinds)
             self._stage_copy(self.light_buf, light.packed())
         else:
             raise TypeError(f"unsupported light {type(light).__name__}")
@@ -240,11 +238,9 @@ class Scene:
         if self._light_kind[0] == "direct":
             b = self._bvh_dev
             _lib.call("sss_direct_irradiance", self.n, _lib.ptr(self.positions), _lib.ptr(self.normals),
-                      self._n_direct, _lib.ptr(self.light_buf), _lib.ptr(self.material_buf),
-                      b["ray_offset"], b["diag"], _lib.ptr(b["nmin"]), _lib.ptr(b["nmax"]),
-                      _lib.ptr(b["left"]), _lib.ptr(b["right"]), _lib.ptr(b["start"]),
-                      _lib.ptr(b["count"]), _lib.ptr(b["v0"]), _lib.ptr(b["e1"]), _lib.ptr(b["e2"]),
-                      _lib.ptr(self.E_planar), sp)
+                      self._n_direct, _lib.ptr(self._light_kinds_host), _lib.ptr(self.light_buf),
+                      _lib.ptr(self.material_buf), b["ray_offset"], b["diag"], _lib.ptr(b["nodes"]),
+                      _lib.ptr(b["tris"]), _lib.ptr(self.E_planar), sp)
             _lib.call("sss_haar2d", _lib.ptr(self.E_planar), _lib.ptr(self.ehat), 3, self.side,
                       self.levels, 0, sp)
             if E is not None:

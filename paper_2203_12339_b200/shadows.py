@@ -93,6 +93,10 @@ class LightRig:
                 out[i, 0], out[i, 1:4], out[i, 4:7], out[i, 7] = 2, l.center, l.radiance, l.radius
         return out
 
+    def kinds(self) -> np.ndarray:
+        """(n,) int32 kinds in light order (column 0 of packed())."""
+        return self.packed()[: len(self.lights), 0].astype(np.int32)
+
 
 def grid_triangles(side: int) -> np.ndarray:
     """Two triangles per geometry-image cell: (i00, i01, i11), (i00, i11, i10)."""
@@ -119,6 +123,20 @@ class BVH:
     e2: np.ndarray
     bbox_diagonal: float
     ray_offset: float
+
+    def packed(self):
+        """GPU records (sss_direct_irradiance): nodes (M, 8) f64 = {min[3],
+        max[3], i32 (left, right), i32 (start, count)}, tris (T, 10) f64 =
+        {v0[3], e1[3], e2[3], 0}."""
+        m = self.node_min.shape[0]
+        nodes = np.zeros((m, 8), np.float64)
+        nodes[:, 0:3], nodes[:, 3:6] = self.node_min, self.node_max
+        ints = nodes.view(np.int32)  # (m, 16)
+        ints[:, 12], ints[:, 13] = self.node_left, self.node_right
+        ints[:, 14], ints[:, 15] = self.node_start, self.node_count
+        tris = np.zeros((self.v0.shape[0], 10), np.float64)
+        tris[:, 0:3], tris[:, 3:6], tris[:, 6:9] = self.v0, self.e1, self.e2
+        return nodes, tris
 
 
 def _seg_reduce(op, a: np.ndarray, starts: np.ndarray, ends: np.ndarray) -> np.ndarray:

@@ -531,12 +531,11 @@ def _direct_eval(g, lights_packed, n_lights, eta):
     mat = d(np.array([1, 1, 1, 0.01, 0.01, 0.01, eta]), np.float64)
     L = d(lights_packed, np.float64)
     E = torch.empty((3, n), dtype=torch.float64, device="cuda")
-    bufs = [d(bvh.node_min, np.float64), d(bvh.node_max, np.float64), d(bvh.node_left, np.int32),
-            d(bvh.node_right, np.int32), d(bvh.node_start, np.int32), d(bvh.node_count, np.int32),
-            d(bvh.v0, np.float64), d(bvh.e1, np.float64), d(bvh.e2, np.float64)]
-    _lib.call("sss_direct_irradiance", n, _lib.ptr(pos), _lib.ptr(nrm), n_lights, _lib.ptr(L),
-              _lib.ptr(mat), bvh.ray_offset, bvh.bbox_diagonal, *[_lib.ptr(b) for b in bufs],
-              _lib.ptr(E), _lib.stream_ptr())
+    nodes, tris = (d(a, np.float64) for a in bvh.packed())  # keep the tensors alive
+    kinds = torch.tensor(np.asarray(lights_packed)[:n_lights, 0].astype(np.int32))
+    _lib.call("sss_direct_irradiance", n, _lib.ptr(pos), _lib.ptr(nrm), n_lights, _lib.ptr(kinds),
+              _lib.ptr(L), _lib.ptr(mat), bvh.ray_offset, bvh.bbox_diagonal, _lib.ptr(nodes),
+              _lib.ptr(tris), _lib.ptr(E), _lib.stream_ptr())
     torch.cuda.synchronize()
     return E.cpu().numpy().T
 

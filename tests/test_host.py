@@ -469,3 +469,22 @@ def test_bvh_any_hit_matches_reference_rays(golden):
     leaves = bvh.node_count > 0
     assert bvh.node_count[leaves].sum() == g["triangles"].shape[0]
     assert np.all(bvh.node_count <= 4)
+
+
+def test_bvh_packed_records(golden):
+    """The GPU node / triangle records carry the BVH fields bit for bit."""
+    from paper_2203_12339_b200.shadows import LightRig, PointLight, SphereLight, build_bvh
+
+    g = golden("direct")
+    bvh = build_bvh(g["positions"], g["triangles"])
+    nodes, tris = bvh.packed()
+    assert nodes.shape == (bvh.node_min.shape[0], 8) and tris.shape == (bvh.v0.shape[0], 10)
+    assert np.array_equal(nodes[:, :3], bvh.node_min) and np.array_equal(nodes[:, 3:6], bvh.node_max)
+    ints = nodes.view(np.int32)
+    for col, a in zip((12, 13, 14, 15), (bvh.node_left, bvh.node_right, bvh.node_start,
+                                         bvh.node_count)):
+        assert np.array_equal(ints[:, col], a)
+    assert np.array_equal(tris[:, 0:3], bvh.v0) and np.array_equal(tris[:, 6:9], bvh.e2)
+    rig = LightRig(lights=(SphereLight(center=[0, 0, 5], radius=1, radiance=1),
+                           PointLight(position=[1, 2, 3], intensity=4)))
+    assert rig.kinds().tolist() == [2, 0] and rig.kinds().dtype == np.int32
