@@ -899,3 +899,84 @@ def irradiance_direct(positions, normals, lights, vertices, tris, eta):
         else:
             raise TypeError(f"unsupported light {kind}")
     return e_out
+
+
+# ---------------------------------------------------------------------------
+# visibility precompute and ambient folding —
+# transfer.py:368-451, lighting.py:318-329
+# ---------------------------------------------------------------------------
+
+FOLD_FRACTION = 0.9999  # transfer.py:35 DEFAULT_FOLD_FRACTION
+ENV_COEFF_KEEP = 128    # runtime.py:34
+
+
+def precompute_visibility(positions, normals, vertices, tris, face_side=16):
+    """precompute_visibility (transfer.py:368-391): binary upper-hemisphere
+    visibility (N, 6 s^2) over the cubemap texel directions; rays from
+    p + offset n toward every direction with n.d > 0, any hit within
+    4 diag + 1 occludes. Brute-force any-hit (the answer is independent of
+    the acceleration structure)."""
+    v = np.asarray(vertices, np.float64)
+    diag = float(np.linalg.norm(v.max(axis=0) - v.min(axis=0)))
+    ray_offset = RAY_OFFSET_SCALE * diag
+    dirs = face_directions(face_side).reshape(-1, 3)
+    n, d = positions.shape[0], dirs.shape[0]
+    origins = positions + ray_offset * normals
+    cos = normals @ dirs.T
+    far = 4.0 * diag + 1.0
+    vis = np.zeros((n, d))
+    si, di = np.nonzero(cos > 0.0)
+    if si.size:
+        hits = any_hit(origins[si], dirs[di], np.full(si.size, far), v, tris)
+        vis[si, di] = ~hits
+    return vis
+
+
+def fold_visibility(ops, vis, normals, side, face_side, eta, fraction=FOLD_FRACTION,
+                    levels=None):
+    """fold_visibility (transfer.py:394-451) for an identity atlas: per k the
+    operator (w1 rows x kept w0 columns) times v~ = w0(w2(W)) restricted to
+    its columns, then compress_energy per direction column. W =
+    visibility_weights with the material eta; w2 = per-face full Haar over
+    the direction axis; w0 = the L-level (None = full) Haar over samples.
+    Returns the folded operators and the dense (w1, D) products per k."""
+    n = normals.shape[0]
+    d = 6 * face_side * face_side
+    w = visibility_weights(normals, face_side, eta, vis)
+    w2 = haar2d_fwd(np.ascontiguousarray(w.reshape(n * 6, face_side, face_side))).reshape(n, d)
+    v_tilde = haar2d_fwd(np.ascontiguousarray(w2.T.reshape(d, side, side)), levels)
+    v_tilde = v_tilde.reshape(d, n).T
+    out, dense_folded = [], []
+    for op in ops:
+        cols = op.cols.astype(np.int64)
+        dense = np.zeros((n, cols.size))
+        for ci in range(cols.size):
+            sl = slice(op.colptr[ci], op.colptr[ci + 1])
+            dense[op.rowidx[sl].astype(np.int64), ci] = op.vals[sl]
+        folded = dense @ v_tilde[cols, :]
+        dense_folded.append(folded)
+        specs = [compress_energy(folded[:, e], fraction) for e in range(d)]
+        fcols = np.flatnonzero([s.count for s in specs]).astype(np.uint32)
+        keep = [specs[int(c)] for c in fcols]
+        colptr = np.zeros(fcols.size + 1, np.int64)
+        for ci, sp in enumerate(keep):
+            colptr[ci + 1] = colptr[ci] + sp.count
+        out.append(Operator(
+            fcols, colptr,
+            np.concatenate([s.indices for s in keep]).astype(np.uint32) if keep
+            else np.empty(0, np.uint32),
+            np.concatenate([s.values for s in keep]) if keep else np.empty(0),
+            float(sum(s.kept_energy for s in specs)), float(sum(s.total_energy for s in specs)),
+            int(np.count_nonzero(folded))))
+    return out, dense_folded
+
+
+def ambient_vk(folded_ops, spectra, n_dom):
+    """The folded ambient term of _stage2_transfer (runtime.py:146-149):
+    vk[k, c] = folded_k applied to the channel's w2 environment spectrum."""
+    vk = np.zeros((len(folded_ops), 3, n_dom))
+    for k, op in enumerate(folded_ops):
+        for c in range(3):
+            vk[k, c] = csc_apply(op.cols, op.colptr, op.rowidx, op.vals, spectra[c].indices,
+                                 spectra[c].values, n_dom)
+    return vk

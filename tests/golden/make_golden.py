@@ -239,6 +239,35 @@ def main():
                         s_c=lights[2].center, s_r=np.array(lights[2].radius),
                         s_rad=lights[2].radiance)
 
+    # 6d. visibility precompute + ambient folding (transfer.py:368-451) on the
+    #     self-occluding direct-light geometry: reference-built operators,
+    #     binary visibility (face side 4: 96 directions), folded operators at
+    #     the default fraction, and the folded ambient v_k of one environment
+    fct = tr.precompute_compressed(dsamples, atlas, basis, 0.1, 0.95, spill_dir="/tmp")
+    fvis = tr.precompute_visibility(dsamples, accel, face_side=4)
+    fold = tr.fold_visibility(fct, fvis, dsamples, atlas, eta=1.3, fraction=0.9999)
+    frng = np.random.default_rng(13)
+    fenv = em.Cubemap(faces=frng.random((6, 4, 4, 3)) + 0.1)
+    fspec = lt.project_environment(fenv, 32)
+    fvk = np.zeros((basis.K, 3, dside * dside))
+    for ki, op in enumerate(fold.operators):
+        for c in range(3):
+            fvk[ki, c] = op.apply(fspec[c].indices, fspec[c].values, dside * dside)
+    fo = dict(side=np.array(dside), face_side=np.array(4), eta=np.array(1.3),
+              fraction=np.array(0.9999), vis=fvis.matrix.astype(np.uint8), faces=fenv.faces,
+              vk=fvk)
+    for c in range(3):
+        fo[f"env_idx{c}"] = fspec[c].indices
+        fo[f"env_val{c}"] = fspec[c].values
+    for tag, opl in (("op", fct.operators), ("fold", fold.operators)):
+        for ki, op in enumerate(opl):
+            fo[f"{tag}{ki}_cols"] = op.cols
+            fo[f"{tag}{ki}_colptr"] = op.colptr
+            fo[f"{tag}{ki}_rowidx"] = op.rowidx
+            fo[f"{tag}{ki}_vals"] = op.vals
+            fo[f"{tag}{ki}_e"] = np.array([op.kept_energy, op.total_energy, op.step1_entries])
+    np.savez_compressed(HERE / "fold.npz", **fo)
+
     # 7. environment light: project_environment + dense ambient irradiance
     env_side = 8
     faces = np.exp(rng.standard_normal((6, env_side, env_side, 3)))

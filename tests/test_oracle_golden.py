@@ -199,3 +199,32 @@ def test_direct_lights_oracle_matches_reference(golden):
     E = O.irradiance_direct(g["positions"], g["normals"], lights, g["positions"], g["triangles"],
                             float(g["eta"]))
     assert np.array_equal(E, g["E"])
+
+
+def test_fold_oracle_matches_reference(golden):
+    """precompute_visibility + fold_visibility + the folded ambient apply
+    (transfer.py:368-451, runtime.py:146-149) against the reference's own
+    output on a self-occluding 16^2 geometry (96 directions): visibility,
+    folded operators (sets, values, energy ledgers) and v_k bitwise."""
+    g = golden("fold")
+    d = golden("direct")
+    vis = O.precompute_visibility(d["positions"], d["normals"], d["positions"], d["triangles"],
+                                  int(g["face_side"]))
+    assert np.array_equal(vis.astype(np.uint8), g["vis"])
+    assert 0.2 < vis.mean() < 0.8  # genuinely self-occluding
+    K = 4
+    ops = [O.Operator(g[f"op{k}_cols"], g[f"op{k}_colptr"], g[f"op{k}_rowidx"], g[f"op{k}_vals"],
+                      float(g[f"op{k}_e"][0]), float(g[f"op{k}_e"][1]), int(g[f"op{k}_e"][2]))
+           for k in range(K)]
+    folded, _ = O.fold_visibility(ops, g["vis"].astype(np.float64), d["normals"], int(g["side"]),
+                                  int(g["face_side"]), float(g["eta"]), float(g["fraction"]))
+    for k, f in enumerate(folded):
+        for name in ("cols", "colptr", "rowidx", "vals"):
+            assert np.array_equal(getattr(f, name), g[f"fold{k}_{name}"]), (k, name)
+        assert [f.kept_energy, f.total_energy, f.step1_entries] == g[f"fold{k}_e"].tolist()
+    spec = [O.Spectrum(g[f"env_idx{c}"], g[f"env_val{c}"], 96, 0.0, 0.0) for c in range(3)]
+    assert np.array_equal(O.ambient_vk(folded, spec, int(g["side"]) ** 2), g["vk"])
+    # zero visibility folds to zero operators (test_transfer.py:265-273)
+    zero, _ = O.fold_visibility(ops, np.zeros_like(vis), d["normals"], int(g["side"]),
+                                int(g["face_side"]), 1.3)
+    assert all(z.cols.size == 0 and z.rowidx.size == 0 for z in zero)

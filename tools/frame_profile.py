@@ -60,7 +60,7 @@ def main():
         _lib.ptr(sc.mask), _lib.ptr(sc.energy), sp), a.reps)
     out["material_weights"] = timed(sc._launch_weights, a.reps)
     ref_vk = None
-    for kern in ("flat8", "regional"):
+    for kern in ("flat8", "k8"):
         sc.transfer_kernel = kern
         sc.vk.fill_(float("nan"))
         sc._launch_transfer()
@@ -72,7 +72,7 @@ def main():
         else:
             out[f"relerr_{kern}"] = float((sc.vk - ref_vk).abs().max() / ref_vk.abs().max())
     out["flat8_MB"] = dt.flat8[8]["bytes"] / 1e6
-    out.update({f"regional_{k}": v for k, v in dt.regional["stats"].items()})
+    out.update({f"k8_{k}": v for k, v in dt.k8[5].items()})
     sc.transfer_kernel = "flat8"
     out["edit_finish"] = timed(sc._launch_edit, a.reps)
     sc.capture()
