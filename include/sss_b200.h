@@ -376,6 +376,57 @@ int sss_direct_irradiance(int n_points, const float* positions, const float* nor
                           const double* material, double ray_offset, double bbox_diagonal,
                           const double* nodes, const double* tris, double* E, void* stream);
 
+/* ---- visibility precompute + ambient folding (
+ * transfer.py:368-451). D = 6 face_side^2 cubemap texel directions.
+ *
+ * sss_visibility: precompute_visibility (transfer.py:368-391): vis (D, N) u8
+ *   = n.d > 0 and no hit within `far` (4 bbox diagonal + 1) from p + offset n;
+ *   dirs (D, 3) doubles (envmap.face_directions); packed BVH as for
+ *   sss_direct_irradiance. */
+int sss_visibility(int n_points, const float* positions, const float* normals, int n_dirs,
+                   const double* dirs, double ray_offset, double far, const double* nodes,
+                   const double* tris, uint8_t* vis, void* stream);
+
+/* sss_fold_weights: visibility_weights with the material eta
+ *   (lighting.py:318-329) and the per-face full Haar over directions
+ *   (transfer.py:407-411): W2 (D, N) fp64 (then the w0 Haar over samples with
+ *   sss_haar2d, batch D). */
+int sss_fold_weights(const float* normals, int n_points, const double* dirs, const double* dom,
+                     int face_side, const uint8_t* vis, double eta, double* W2, void* stream);
+
+/* out (cols, rows) = in (rows, cols)^T, optionally gathering input columns:
+ * out[j][r] = in[r][col_perm ? col_perm[j] : j]. */
+int sss_transpose_f64(const double* in, int rows, int cols, const uint32_t* col_perm, double* out,
+                      void* stream);
+
+/* sss_fold_spmm: F (n_rows, n_dirs) row-major = T_k v~ (transfer.py:426's
+ *   dense @ v_tilde[cols]) for one operator of the frame layout (rowptr
+ *   absolute int64, tile-major cols, f32 vals); vt (N tm, n_dirs). */
+int sss_fold_spmm(int n_rows, int n_dirs, const long long* rowptr, const uint32_t* cols,
+                  const float* vals, const double* vt, double* F, void* stream);
+
+/* sss_fold_select: compress_energy(fraction) of every direction column of FT
+ *   (n_dirs, n_rows tm) (transfer.py:427, wavelets.py:139-153): threshold
+ *   key, tie bound (flat row), kept count, (kept, total) energy, nonzeros. */
+int sss_fold_select(const double* FT, int n_rows, int n_dirs, double fraction,
+                    const uint32_t* tm2flat, uint64_t* col_t, uint32_t* col_fmax,
+                    uint32_t* col_cnt, double* col_energy, uint32_t* col_nz, void* stream);
+
+/* sss_fold_emit: CSC of the kept entries per direction, rows ascending flat
+ *   ids, vals f32; colptr (n_dirs + 1) = exclusive scan of col_cnt. */
+int sss_fold_emit(const double* FT, int n_rows, int n_dirs, const uint32_t* flat2tm,
+                  const uint64_t* col_t, const uint32_t* col_fmax, const uint32_t* col_cnt,
+                  const uint64_t* colptr, uint32_t* rows, float* vals, void* stream);
+
+/* sss_fold_apply: the folded ambient term of _stage2_transfer
+ *   (runtime.py:146-149): vk[k][c][tm] += sum over the environment union
+ *   (sss_env_project's union_idx / union_lc / n_union, ascending) of
+ *   F_k[r][e] L_c[e], in the reference's serial csc_apply order. colptr
+ *   (K, n_dirs + 1) absolute into rows / vals. */
+int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const uint32_t* rows,
+                   const float* vals, const uint32_t* union_idx, const double* union_lc,
+                   const int* n_union, const uint32_t* flat2tm, double* vk, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);

@@ -42,6 +42,13 @@ _SIGS = {
     "sss_sweep_gemm": [_I, _I, _P, _P, _P, C.c_float, C.c_float, _P, _P, _P, _P, _P],
     "sss_transfer_regional": [_I, _I, _P, _P, _P, _I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P,
                               _P, _P, _P],
+    "sss_visibility": [_I, _P, _P, _I, _P, C.c_double, C.c_double, _P, _P, _P, _P],
+    "sss_fold_weights": [_P, _I, _P, _P, _I, _P, C.c_double, _P, _P],
+    "sss_transpose_f64": [_P, _I, _I, _P, _P, _P],
+    "sss_fold_spmm": [_I, _I, _P, _P, _P, _P, _P, _P],
+    "sss_fold_select": [_P, _I, _I, C.c_double, _P, _P, _P, _P, _P, _P, _P],
+    "sss_fold_emit": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_fold_apply": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_direct_irradiance": [_I, _P, _P, _I, _P, _P, _P, C.c_double, C.c_double, _P, _P, _P, _P],
     "sss_transfer_k8": [_I, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P],
     "sss_transfer_kflat": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],

@@ -27,6 +27,7 @@
 #include "regional19.cu"
 #include "k8_20.cu"
 #include "direct.cu"
+#include "fold.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -893,6 +894,92 @@ int sss_direct_irradiance(int n_points, const float* positions, const float* nor
   return SSS_OK;
 }
 
+int sss_visibility(int n_points, const float* positions, const float* normals, int n_dirs,
+                   const double* dirs, double ray_offset, double far, const double* nodes,
+                   const double* tris, uint8_t* vis, void* stream) {
+  if (n_points <= 0 || n_dirs <= 0 || n_dirs > 65535 || !positions || !normals || !dirs ||
+      !nodes || !tris || !vis)
+    return fail(SSS_EINVAL, "bad visibility arguments");
+  const sss::BvhView B{reinterpret_cast<const double2*>(nodes),
+                       reinterpret_cast<const double2*>(tris)};
+  dim3 grid((n_points + 127) / 128, n_dirs);
+  sss::k_visibility<<<grid, 128, 0, S_(stream)>>>(n_points, positions, normals, dirs, ray_offset,
+                                                  far, B, vis);
+  return check_launch("k_visibility");
+}
+
+int sss_fold_weights(const float* normals, int n_points, const double* dirs, const double* dom,
+                     int face_side, const uint8_t* vis, double eta, double* W2, void* stream) {
+  if (!normals || !dirs || !dom || !vis || !W2 || n_points <= 0 || face_side <= 0 ||
+      (face_side & (face_side - 1)))
+    return fail(SSS_EINVAL, "bad fold_weights arguments");
+  const int s2 = face_side * face_side;
+  const size_t smem = sizeof(double) * (size_t)(sss::kFoldP + 1) * s2;
+  if (int r = set_smem((const void*)sss::k_fold_weights, smem)) return r;
+  dim3 grid((n_points + sss::kFoldP - 1) / sss::kFoldP, 6);
+  sss::k_fold_weights<<<grid, 256, smem, S_(stream)>>>(normals, n_points, dirs, dom, face_side,
+                                                      vis, eta, W2);
+  return check_launch("k_fold_weights");
+}
+
+int sss_transpose_f64(const double* in, int rows, int cols, const uint32_t* col_perm, double* out,
+                      void* stream) {
+  if (!in || !out || rows <= 0 || cols <= 0 || (rows + 31) / 32 > 65535)
+    return fail(SSS_EINVAL, "bad transpose arguments");
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  sss::k_transpose_perm<<<grid, dim3(32, 8), 0, S_(stream)>>>(in, rows, cols, col_perm, out);
+  return check_launch("k_transpose_perm");
+}
+
+int sss_fold_spmm(int n_rows, int n_dirs, const long long* rowptr, const uint32_t* cols,
+                  const float* vals, const double* vt, double* F, void* stream) {
+  if (n_rows <= 0 || n_dirs <= 0 || !rowptr || !cols || !vals || !vt || !F ||
+      (n_dirs + 255) / 256 > 65535)
+    return fail(SSS_EINVAL, "bad fold_spmm arguments");
+  dim3 grid((n_rows + sss::kSpmmWarps - 1) / sss::kSpmmWarps, (n_dirs + 255) / 256);
+  sss::k_fold_spmm<<<grid, 32 * sss::kSpmmWarps, 0, S_(stream)>>>(n_rows, n_dirs, rowptr, cols,
+                                                                 vals, vt, F);
+  return check_launch("k_fold_spmm");
+}
+
+int sss_fold_select(const double* FT, int n_rows, int n_dirs, double fraction,
+                    const uint32_t* tm2flat, uint64_t* col_t, uint32_t* col_fmax,
+                    uint32_t* col_cnt, double* col_energy, uint32_t* col_nz, void* stream) {
+  if (!FT || !tm2flat || !col_t || !col_fmax || !col_cnt || !col_energy || n_rows <= 0 ||
+      n_dirs <= 0 || !(fraction >= 0.0 && fraction <= 1.0))
+    return fail(SSS_EINVAL, "bad fold_select arguments");
+  const size_t smem = sizeof(sss::SelShared) + (size_t)((n_rows + 31) / 32) * 4;
+  if (int r = set_smem((const void*)sss::k_step2_select, smem)) return r;
+  sss::k_step2_select<<<n_dirs, sss::kSelThreads, smem, S_(stream)>>>(
+      FT, n_rows, fraction, nullptr, tm2flat, nullptr, col_t, col_fmax, col_cnt, col_energy,
+      col_nz);
+  return check_launch("k_step2_select");
+}
+
+int sss_fold_emit(const double* FT, int n_rows, int n_dirs, const uint32_t* flat2tm,
+                  const uint64_t* col_t, const uint32_t* col_fmax, const uint32_t* col_cnt,
+                  const uint64_t* colptr, uint32_t* rows, float* vals, void* stream) {
+  if (!FT || !flat2tm || !col_t || !col_fmax || !col_cnt || !colptr || !rows || !vals ||
+      n_rows <= 0 || n_dirs <= 0)
+    return fail(SSS_EINVAL, "bad fold_emit arguments");
+  sss::k_fold_emit<<<n_dirs, sss::kEmitThreads, 0, S_(stream)>>>(FT, n_rows, flat2tm, col_t,
+                                                                 col_fmax, col_cnt, colptr, rows,
+                                                                 vals);
+  return check_launch("k_fold_emit");
+}
+
+int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const uint32_t* rows,
+                   const float* vals, const uint32_t* union_idx, const double* union_lc,
+                   const int* n_union, const uint32_t* flat2tm, double* vk, void* stream) {
+  if (K <= 0 || n_rows <= 0 || n_dirs <= 0 || !colptr || !rows || !vals || !union_idx ||
+      !union_lc || !n_union || !flat2tm || !vk)
+    return fail(SSS_EINVAL, "bad fold_apply arguments");
+  dim3 grid((n_rows + sss::kFoldRows - 1) / sss::kFoldRows, K);
+  sss::k_fold_apply<<<grid, 256, 0, S_(stream)>>>(n_rows, n_dirs, colptr, rows, vals, union_idx,
+                                                  union_lc, n_union, flat2tm, vk);
+  return check_launch("k_fold_apply");
+}
+
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream) {
   if (!rowptr || !bandoff || K <= 0 || n_rows <= 0 || band_width <= 0 || n_bands <= 0)
@@ -989,7 +1076,8 @@ int sss_step2_select(const double* M, int n_dom, double fraction, const uint32_t
   const size_t smem = sizeof(sss::SelShared) + (size_t)((n_dom + 31) / 32) * 4;
   if (int r = set_smem((const void*)sss::k_step2_select, smem)) return r;
   sss::k_step2_select<<<n_dom, sss::kSelThreads, smem, S_(stream)>>>(
-      M, n_dom, fraction, flat2tm, tm2flat, union_bits, col_t, col_fmax, col_cnt, col_energy);
+      M, n_dom, fraction, flat2tm, tm2flat, union_bits, col_t, col_fmax, col_cnt, col_energy,
+      nullptr);
   return check_launch("k_step2_select");
 }
 

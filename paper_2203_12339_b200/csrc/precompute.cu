@@ -221,14 +221,15 @@ __global__ void __launch_bounds__(kSelThreads) k_step2_select(
     const double* __restrict__ M, int N, double fraction, const uint32_t* __restrict__ flat2tm,
     const uint32_t* __restrict__ tm2flat, const uint32_t* __restrict__ union_bits,
     uint64_t* __restrict__ col_t, uint32_t* __restrict__ col_fmax, uint32_t* __restrict__ col_cnt,
-    double* __restrict__ col_energy /* (N, 2): kept, total */) {
+    double* __restrict__ col_energy /* (N, 2): kept, total */,
+    uint32_t* __restrict__ col_nz /* may be null */) {
   extern __shared__ __align__(16) unsigned char dsm[];
   SelShared& sh = *reinterpret_cast<SelShared*>(dsm);
   uint32_t* smb = reinterpret_cast<uint32_t*>(dsm + sizeof(SelShared));  // tie bits
-  const int c = blockIdx.x;  // flat column
+  const int c = blockIdx.x;  // flat column (fold: direction, identity map, no union)
   const int nw = (N + 31) / 32;
-  const int ctm = flat2tm[c];
-  if (!((union_bits[c >> 5] >> (c & 31)) & 1u)) {
+  const int ctm = flat2tm ? (int)flat2tm[c] : c;
+  if (union_bits && !((union_bits[c >> 5] >> (c & 31)) & 1u)) {
     if (threadIdx.x == 0) {
       col_t[ctm] = ~0ULL; col_fmax[ctm] = 0; col_cnt[ctm] = 0;
       col_energy[ctm * 2] = 0.0; col_energy[ctm * 2 + 1] = 0.0;
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(kSelThreads) k_step2_select(
     col_cnt[ctm] = (uint32_t)kept;
     col_energy[ctm * 2] = fmin(ke, tot);
     col_energy[ctm * 2 + 1] = tot;
+    if (col_nz) col_nz[ctm] = (uint32_t)nz;
   }
 }
 
