@@ -34,6 +34,7 @@ from .basis import DiffusionBasis, OpticalMaterial
 from .config import CAMERA, E_KEEP, ENV_COEFF_KEEP
 from .geometry import GeometryImage
 from .lighting import face_directions, face_solid_angles, sh_transfer
+from .folding import fold_apply
 from .shadows import LightRig, build_bvh, grid_triangles
 from .transfer import DeviceTransfer, flat_to_tile_major
 
@@ -95,7 +96,7 @@ class Scene:
     def __init__(self, geometry: GeometryImage, transfer: DeviceTransfer,
                  basis: DiffusionBasis, material: OpticalMaterial, light,
                  camera: Camera = None, e_keep: float = E_KEEP,
-                 env_keep: int = ENV_COEFF_KEEP, keep_scatter: bool = False):
+                 env_keep: int = ENV_COEFF_KEEP, keep_scatter: bool = False, folded=None):
         _lib.load()
         if transfer.side != geometry.side:
             raise ValueError("transfer operator was precomputed for a different geometry image")
@@ -103,6 +104,10 @@ class Scene:
             raise ValueError("operator count != basis K")
         self.geometry = geometry
         self.transfer = transfer
+        self.folded = folded  # folding.DeviceFolded: the ambient term of a LightRig
+        if folded is not None and (folded.side != geometry.side or folded.K != transfer.K or
+                                   folded.levels != transfer.levels):
+            raise ValueError("folded operators do not match the transfer operators")
         self.basis = basis
         self.e_keep = e_keep
         self.env_keep = env_keep
@@ -206,7 +211,19 @@ class Scene:
             self._stage_copy(self.light_buf, light.faces)
         elif isinstance(light, LightRig):
             kinds = tuple(int(k) for k in light.kinds())
-            if self._light_kind != ("direct", kinds):
+            amb = light.ambient
+            if amb is not None:  # runtime.py:120-135
+                if self.folded is None:
+                    raise ValueError("scene lacks folded visibility; build it with "
+                                     "folding.fold_visibility to light environments")
+                if amb.side != self.folded.face_side:
+                    raise ValueError(f"environment face side {amb.side} != folded operator side "
+                                     f"{self.folded.face_side}")
+                if abs(self.folded.eta - self.material.eta) > 1e-9:
+                    warnings.warn(f"folded ambient operator was baked for eta={self.folded.eta:g}; "
+                                  "ambient response uses that Fresnel weighting", stacklevel=3)
+            amb_side = amb.side if amb is not None else 0
+            if self._light_kind != ("direct", kinds, amb_side):
                 if getattr(self, "_bvh_dev", None) is None:
                     bvh = build_bvh(self.geometry.positions.astype(np.float64),
                                     grid_triangles(self.side))
@@ -218,10 +235,21 @@ class Scene:
                                              device=dev)
                 self._light_kinds_host = torch.tensor(kinds or (0,), dtype=torch.int32)
                 self.E_planar = torch.empty((3, self.n), dtype=torch.float64, device=dev)
-                self._light_kind = ("direct", kinds)
+                if amb_side:
+                    kk = self.env_keep
+                    self.amb_buf = torch.empty((6, amb_side, amb_side, 3), dtype=torch.float64,
+                                               device=dev)
+                    self.env_idx = torch.empty((3, kk), dtype=torch.int32, device=dev)
+                    self.env_val = torch.empty((3, kk), dtype=torch.float64, device=dev)
+                    self.env_uidx = torch.empty(3 * kk, dtype=torch.int32, device=dev)
+                    self.env_ulc = torch.empty((3 * kk, 3), dtype=torch.float64, device=dev)
+                    self.env_nu = torch.empty(1, dtype=torch.int32, device=dev)
+                self._light_kind = ("direct", kinds, amb_side)
                 self._graph = None
             self._n_direct = len(kinds)
             self._stage_copy(self.light_buf, light.packed())
+            if amb is not None:
+                self._stage_copy(self.amb_buf, amb.faces)
         else:
             raise TypeError(f"unsupported light {type(light).__name__}")
         self.light = light
@@ -245,6 +273,11 @@ class Scene:
                       self.levels, 0, sp)
             if E is not None:
                 E.copy_(self.E_planar.t())
+            if self._light_kind[2]:  # the ambient environment's w2 spectrum (runtime.py:135)
+                _lib.call("sss_env_project", _lib.ptr(self.amb_buf), self._light_kind[2],
+                          self.env_keep, _lib.ptr(self.env_idx), _lib.ptr(self.env_val),
+                          _lib.ptr(self.env_uidx), _lib.ptr(self.env_ulc), _lib.ptr(self.env_nu),
+                          sp)
         elif self._light_kind[0] == "sh":
             _lib.call("sss_sh_irradiance", _lib.ptr(self.T_l), _lib.ptr(self.light_buf),
                       self._light_kind[1], self.side, self.levels, _lib.ptr(E),
@@ -594,8 +627,19 @@ class Scene:
         join.record(self._side)
         self._launch_stage1(cur)
         cur.wait_event(join)
-        self._launch_transfer(cur)
+        if self._ambient_active():
+            # v_k = T_k x + F_k L^{w2} (runtime.py:138-150), then stages 3-5
+            if self._launch_transfer(cur, epilogue=False):
+                raise ValueError(f"transfer kernel {self.transfer_kernel!r} fuses the epilogue; "
+                                 "ambient folding needs a separable layout (e.g. flat8)")
+            fold_apply(self.folded, self.env_uidx, self.env_ulc, self.env_nu, self.vk, cur)
+            self._launch_edit(cur)
+        else:
+            self._launch_transfer(cur)
         self._have_cache = True
+
+    def _ambient_active(self) -> bool:
+        return self._light_kind[0] == "direct" and bool(self._light_kind[2])
 
     def launch_edit(self, stream=None):
         """Enqueue the edit path (no host sync)."""
@@ -678,6 +722,11 @@ class Scene:
         self._launch_weights()
         ev[2].record()
         fused = self._launch_transfer(epilogue=False)
+        if self._ambient_active():
+            if fused:
+                raise ValueError(f"transfer kernel {self.transfer_kernel!r} fuses the epilogue; "
+                                 "ambient folding needs a separable layout (e.g. flat8)")
+            fold_apply(self.folded, self.env_uidx, self.env_ulc, self.env_nu, self.vk)
         ev[3].record()
         if not fused:
             self._launch_edit()

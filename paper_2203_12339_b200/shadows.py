@@ -67,24 +67,57 @@ class SphereLight:
 
 
 @dataclass(frozen=True)
+class AmbientLight:
+    """An environment cubemap lighting the scene through the folded
+    visibility operators (lighting.py:62-64; runtime.py:120-149).
+    faces: (6, s, s, 3) radiance."""
+
+    faces: np.ndarray
+
+    def __post_init__(self):
+        f = np.asarray(self.faces, np.float64)
+        if f.ndim != 4 or f.shape[0] != 6 or f.shape[1] != f.shape[2] or f.shape[3] != 3:
+            raise ValueError("faces must be (6, s, s, 3)")
+        object.__setattr__(self, "faces", f)
+
+    @property
+    def side(self) -> int:
+        return int(self.faces.shape[1])
+
+
+@dataclass(frozen=True)
 class LightRig:
-    """Direct lights of a frame (the reference's LightRig without the ambient
-    term; environment light is the EnvLight path)."""
+    """The lights of a frame (lighting.py:80-98): point / directional /
+    sphere lights with shadow rays, plus at most one AmbientLight."""
 
     lights: tuple
 
     def __post_init__(self):
         object.__setattr__(self, "lights", tuple(self.lights))
         for l in self.lights:
-            if not isinstance(l, (PointLight, DirectionalLight, SphereLight)):
+            if not isinstance(l, (PointLight, DirectionalLight, SphereLight, AmbientLight)):
                 raise TypeError(f"unsupported light {type(l).__name__}")
+        if sum(isinstance(l, AmbientLight) for l in self.lights) > 1:
+            raise ValueError("at most one ambient light")
+
+    @property
+    def ambient(self):
+        for l in self.lights:
+            if isinstance(l, AmbientLight):
+                return l
+        return None
+
+    @property
+    def direct_lights(self) -> list:
+        return [l for l in self.lights if not isinstance(l, AmbientLight)]
 
     def packed(self) -> np.ndarray:
-        """(n, 12) doubles per light: {kind, a[3], b[3], radius, 0...}; kind 0 =
+        """(n, 12) doubles per direct light: {kind, a[3], b[3], radius, 0...}; kind 0 =
         point (a = position, b = intensity), 1 = directional (a = unit
         direction, b = irradiance), 2 = sphere (a = center, b = radiance)."""
-        out = np.zeros((max(len(self.lights), 1), 12))
-        for i, l in enumerate(self.lights):
+        direct = self.direct_lights
+        out = np.zeros((max(len(direct), 1), 12))
+        for i, l in enumerate(direct):
             if isinstance(l, PointLight):
                 out[i, 0], out[i, 1:4], out[i, 4:7] = 0, l.position, l.intensity
             elif isinstance(l, DirectionalLight):
@@ -95,7 +128,7 @@ class LightRig:
 
     def kinds(self) -> np.ndarray:
         """(n,) int32 kinds in light order (column 0 of packed())."""
-        return self.packed()[: len(self.lights), 0].astype(np.int32)
+        return self.packed()[: len(self.direct_lights), 0].astype(np.int32)
 
 
 def grid_triangles(side: int) -> np.ndarray:

@@ -585,3 +585,47 @@ def test_frame_direct_lights_parity(c1):
                     cfg.levels, "haar", C.E_KEEP, g.normals.astype(np.float64), pos,
                     np.array(C.CAMERA[0]))
     assert O.parity_error(f.radiance_unclamped, ref["radiance_unclamped"], TAU) <= TOL
+
+
+def test_frame_ambient_folded_parity(c1):
+    """A LightRig with a point light and an AmbientLight (runtime.py:109-150):
+    v_k = T_k x + F_k L^{w2} with GPU-folded visibility operators, against
+    the oracle frame on the same operators; edits reuse the summed v_k."""
+    from paper_2203_12339_b200.folding import fold_visibility, precompute_visibility
+    from paper_2203_12339_b200.runtime import Scene
+    from paper_2203_12339_b200.shadows import AmbientLight, LightRig, PointLight, grid_triangles
+    from paper_2203_12339_b200.transfer import DeviceTransfer
+
+    cfg, g, b, ops = c1
+    fs = 8
+    dt = DeviceTransfer.from_reference(ops, cfg.side, cfg.levels)
+    vis = precompute_visibility(g, face_side=fs)
+    sc0 = _scene(c1, LightRig(lights=(PointLight(position=[20.0, 15.0, 25.0], intensity=1.0),)))
+    eta = sc0.material.eta
+    folded = fold_visibility(dt, vis, g, eta)
+    faces = np.random.default_rng(21).random((6, fs, fs, 3)) + 0.2
+    rig = LightRig(lights=(PointLight(position=[20.0, 15.0, 25.0],
+                                      intensity=[800.0, 600.0, 400.0]), AmbientLight(faces)))
+    with pytest.raises(ValueError):
+        _scene(c1, rig)  # no folded operators
+    sc = Scene(g, dt, b, sc0.material, rig, keep_scatter=True, folded=folded)
+    frames = [sc.relight() for _ in range(3)]  # eager, eager, graph replay
+    pos = g.positions.astype(np.float64)
+    nrm = g.normals.astype(np.float64)
+    E = O.irradiance_direct(pos, nrm, [("point", rig.lights[0].position, rig.lights[0].intensity)],
+                            pos, grid_triangles(cfg.side), eta)
+    spectra = O.select_irradiance(E, cfg.side, cfg.levels, C.E_KEEP)
+    vk = O.transfer_stage(ops, spectra, cfg.side ** 2)
+    vk = vk + O.ambient_vk(folded.to_reference(), O.project_environment(faces, 128),
+                           cfg.side ** 2)
+    m = sc.material
+    w = O.project_material(b.bases, b.r_nodes, m.sigma_s_prime, m.sigma_a, m.eta)
+    _, unc, _ = O.finish(vk, w, cfg.side, cfg.levels, "haar", nrm, pos, np.array(C.CAMERA[0]),
+                         m.eta)
+    for f in frames:
+        assert O.parity_error(f.radiance_unclamped, unc, TAU) <= TOL
+    # the ambient term is not negligible in this frame
+    vk_direct = O.transfer_stage(ops, spectra, cfg.side ** 2)
+    _, unc_d, _ = O.finish(vk_direct, w, cfg.side, cfg.levels, "haar", nrm, pos,
+                           np.array(C.CAMERA[0]), m.eta)
+    assert O.parity_error(unc_d, unc, TAU) > 1e-2
