@@ -484,6 +484,40 @@ int sss_scan_u32(const uint32_t* in, uint64_t* out, size_t n, uint64_t* block_su
 int sss_rowptr(const uint64_t* offs, int nchunks, int n_rows, uint64_t base, const uint64_t* total,
                uint64_t* rowptr, void* stream);
 
+/* ---- rasterisation ---------------------------------- */
+
+/* sss_raster_fill: replaces raster_fill (_kernels_nb.py:316-359,
+ *   _kernels_np.py:264-313), called by render_image (runtime.py:242-243).
+ *   In place on zbuf (height, width) f64 and img (height, width, 3) f64, exactly
+ *   the reference's sequential semantics (triangles in order, strict z-test,
+ *   perspective-correct colour; bitwise). tris (n_tris, 3) i64; sx, sy, zn, iw
+ *   (V,) f64; colors (V, 3) f64. Scratch: key (height*width) u64, win
+ *   (height*width) u32. srgb8 (optional, height*width*3 u8) receives render_image's
+ *   (linear_to_srgb(img * exposure) * 255 + 0.5) quantisation (runtime.py:245). */
+int sss_raster_fill(const int64_t* tris, int n_tris, const double* sx, const double* sy,
+                    const double* zn, const double* iw, const double* colors, int height,
+                    int width, double* zbuf, double* img, unsigned long long* key,
+                    uint32_t* win, double exposure, uint8_t* srgb8, void* stream);
+
+/* sss_project_vertices: replaces _project_vertices (runtime.py:247-273).
+ *   cam = {position, right, up, fwd} (12 f64, device; the frame is built on
+ *   the host as runtime.py:248-256 does); f = 1/tan(fov/2), aspect = w/h.
+ *   Dot products evaluated as (x r0 + y r1) + z r2. Outputs sx, sy, zn, iw (V,). */
+int sss_project_vertices(const double* vertices, int n_vertices, const double* cam, double f,
+                         double aspect, int width, int height, double* sx, double* sy,
+                         double* zn, double* iw, void* stream);
+
+/* sss_vertex_colors: colors[source_vertex[i]] = radiance[i] (f32 -> f64), the
+ *   scatter of render_image (runtime.py:236-237) and of the service frame
+ *   payload (service.py:176-177). source_vertex NULL = identity. colors is
+ *   caller-zeroed (V, 3). */
+int sss_vertex_colors(const float* radiance, const int32_t* source_vertex, int n, double* colors,
+                      void* stream);
+
+/* sss_encode_srgb8: out[i] = uint8(linear_to_srgb(x[i] * exposure) * 255 + 0.5),
+ *   the quantised frame payload of the service (service.py:181, envmap.py:74-76). */
+int sss_encode_srgb8(const double* x, long long n, double exposure, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

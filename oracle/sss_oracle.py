@@ -980,3 +980,115 @@ def ambient_vk(folded_ops, spectra, n_dom):
             vk[k, c] = csc_apply(op.cols, op.colptr, op.rowidx, op.vals, spectra[c].indices,
                                  spectra[c].values, n_dom)
     return vk
+
+
+# ---------------------------------------------------------------------------
+# rasterisation: render_image / raster_fill
+# ---------------------------------------------------------------------------
+def camera_basis(position, look_at, up):
+    """The camera frame of _project_vertices (runtime.py:248-256)."""
+    position = np.asarray(position, np.float64)
+    fwd = np.asarray(look_at, np.float64) - position
+    fwd = fwd / np.linalg.norm(fwd)
+    right = np.cross(fwd, np.asarray(up, np.float64))
+    nr = np.linalg.norm(right)
+    if nr < 1e-12:
+        raise ValueError("camera up vector is parallel to the view direction")
+    right /= nr
+    upv = np.cross(right, fwd)
+    return right, upv, fwd
+
+
+def project_vertices(vertices, position, look_at, up, fov_y_degrees, width, height):
+    """_project_vertices (runtime.py:247-273). The three camera-space dot
+    products are written as left-to-right element sums (x·r0 + y·r1) + z·r2
+    (the reference's `rel @ right` goes through BLAS; the GPU uses this same
+    order, so this checker and the kernel agree bitwise)."""
+    right, upv, fwd = camera_basis(position, look_at, up)
+    rel = np.asarray(vertices, np.float64) - np.asarray(position, np.float64)
+
+    def dot(a):
+        return (rel[:, 0] * a[0] + rel[:, 1] * a[1]) + rel[:, 2] * a[2]
+
+    x, y, z = dot(right), dot(upv), dot(fwd)
+    near = 1e-3
+    f = 1.0 / np.tan(np.radians(fov_y_degrees) / 2.0)
+    aspect = width / height
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ndc_x = (x * f / aspect) / z
+        ndc_y = (y * f) / z
+    sx = (ndc_x * 0.5 + 0.5) * width
+    sy = (0.5 - ndc_y * 0.5) * height
+    iw = np.where(z > near, 1.0 / z, 0.0)
+    zn = np.where(z > near, z, np.inf)
+    return sx, sy, zn, iw
+
+
+def raster_fill(tris, sx, sy, zn, iw, colors, zbuf, img):
+    """raster_fill (_kernels_np.py:264-313 / _kernels_nb.py:316-359): triangles
+    in order, strict z-test, perspective-correct colour; zbuf/img in place."""
+    height, width = zbuf.shape
+    for t in range(tris.shape[0]):
+        i0, i1, i2 = int(tris[t, 0]), int(tris[t, 1]), int(tris[t, 2])
+        if iw[i0] <= 0.0 or iw[i1] <= 0.0 or iw[i2] <= 0.0:
+            continue
+        x0, y0, x1, y1, x2, y2 = sx[i0], sy[i0], sx[i1], sy[i1], sx[i2], sy[i2]
+        area = (x1 - x0) * (y2 - y0) - (y1 - y0) * (x2 - x0)
+        if area == 0.0:
+            continue
+        xmin = max(int(math.floor(min(x0, x1, x2))), 0)
+        xmax = min(int(math.ceil(max(x0, x1, x2))), width - 1)
+        ymin = max(int(math.floor(min(y0, y1, y2))), 0)
+        ymax = min(int(math.ceil(max(y0, y1, y2))), height - 1)
+        if xmin > xmax or ymin > ymax:
+            continue
+        pxg = (np.arange(xmin, xmax + 1, dtype=np.float64) + 0.5)[None, :]
+        pyg = (np.arange(ymin, ymax + 1, dtype=np.float64) + 0.5)[:, None]
+        w0 = (x2 - x1) * (pyg - y1) - (y2 - y1) * (pxg - x1)
+        w1 = (x0 - x2) * (pyg - y2) - (y0 - y2) * (pxg - x2)
+        w2 = (x1 - x0) * (pyg - y0) - (y1 - y0) * (pxg - x0)
+        if area > 0.0:
+            inside = (w0 >= 0.0) & (w1 >= 0.0) & (w2 >= 0.0)
+        else:
+            inside = (w0 <= 0.0) & (w1 <= 0.0) & (w2 <= 0.0)
+        l0, l1, l2 = w0 / area, w1 / area, w2 / area
+        z = l0 * zn[i0] + l1 * zn[i1] + l2 * zn[i2]
+        sub_z = zbuf[ymin:ymax + 1, xmin:xmax + 1]
+        upd = inside & (z < sub_z)
+        if not upd.any():
+            continue
+        wi = l0 * iw[i0] + l1 * iw[i1] + l2 * iw[i2]
+        sub_img = img[ymin:ymax + 1, xmin:xmax + 1]
+        for c in range(3):
+            num = (l0 * (colors[i0, c] * iw[i0]) + l1 * (colors[i1, c] * iw[i1])
+                   + l2 * (colors[i2, c] * iw[i2]))
+            with np.errstate(divide="ignore", invalid="ignore"):
+                sub_img[..., c] = np.where(upd, num / wi, sub_img[..., c])
+        sub_z[upd] = z[upd]
+    return zbuf
+
+
+def linear_to_srgb(x):  # envmap.py:74-76
+    x = np.clip(np.asarray(x, np.float64), 0.0, 1.0)
+    return np.where(x <= 0.0031308, x * 12.92, 1.055 * np.power(x, 1.0 / 2.4) - 0.055)
+
+
+def encode_srgb8(x, exposure=1.0):
+    """The 8-bit quantisation of render_image (runtime.py:245) and of the
+    service frame payload (service.py:181)."""
+    return (linear_to_srgb(np.asarray(x, np.float64) * exposure) * 255.0 + 0.5).astype(np.uint8)
+
+
+def render_image(vertices, tris, source_vertex, radiance, position, look_at, up, fov_y_degrees,
+                 width, height, exposure=1.0, background=(0.0, 0.0, 0.0)):
+    """render_image (runtime.py:230-245): returns (u8 image, linear image, zbuf)."""
+    if width < 1 or height < 1:
+        raise ValueError("image dimensions must be positive")
+    colors = np.zeros((np.asarray(vertices).shape[0], 3))
+    colors[np.asarray(source_vertex)] = radiance
+    sx, sy, zn, iw = project_vertices(vertices, position, look_at, up, fov_y_degrees, width, height)
+    zbuf = np.full((height, width), np.inf)
+    img = np.empty((height, width, 3))
+    img[:] = np.asarray(background, np.float64)
+    raster_fill(np.ascontiguousarray(tris, np.int64), sx, sy, zn, iw, colors, zbuf, img)
+    return encode_srgb8(img, exposure), img, zbuf

@@ -76,6 +76,10 @@ _SIGS = {
     "sss_emit": [_I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_scan_u32": [_P, _P, C.c_size_t, _P, _P, _P],
     "sss_rowptr": [_P, _I, _I, C.c_uint64, _P, _P, _P],
+    "sss_raster_fill": [_P, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _D, _P, _P],
+    "sss_project_vertices": [_P, _I, _P, _D, _D, _I, _I, _P, _P, _P, _P, _P],
+    "sss_vertex_colors": [_P, _P, _I, _P, _P],
+    "sss_encode_srgb8": [_P, C.c_longlong, _D, _P, _P],
 }
 
 

@@ -28,6 +28,7 @@
 #include "k8_20.cu"
 #include "direct.cu"
 #include "fold.cu"
+#include "raster.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -1119,6 +1120,57 @@ int sss_rowptr(const uint64_t* offs, int nchunks, int n_rows, uint64_t base, con
   sss::k_rowptr<<<(n_rows + 1 + 255) / 256, 256, 0, S_(stream)>>>(offs, nchunks, n_rows, base,
                                                                    total, rowptr);
   return check_launch("k_rowptr");
+}
+
+int sss_raster_fill(const int64_t* tris, int n_tris, const double* sx, const double* sy,
+                    const double* zn, const double* iw, const double* colors, int height,
+                    int width, double* zbuf, double* img, unsigned long long* key,
+                    uint32_t* win, double exposure, uint8_t* srgb8, void* stream) {
+  if (height < 1 || width < 1) return fail(SSS_EINVAL, "image dimensions must be positive");
+  if ((long long)height * width > (1ll << 31) - 1) return fail(SSS_EINVAL, "image too large");
+  if (n_tris < 0 || (n_tris > 0 && (!tris || !sx || !sy || !zn || !iw || !colors)) || !zbuf ||
+      !img || !key || !win)
+    return fail(SSS_EINVAL, "bad raster_fill arguments");
+  const int n_pix = height * width;
+  cudaStream_t s = S_(stream);
+  sss::k_raster_init<<<(n_pix + 255) / 256, 256, 0, s>>>(zbuf, n_pix, key, win);
+  if (n_tris > 0) {
+    const int g = (n_tris + 255) / 256;
+    sss::k_raster_tri<false><<<g, 256, 0, s>>>(tris, n_tris, sx, sy, zn, iw, zbuf, height, width,
+                                               key, win);
+    sss::k_raster_tri<true><<<g, 256, 0, s>>>(tris, n_tris, sx, sy, zn, iw, zbuf, height, width,
+                                              key, win);
+  }
+  sss::k_raster_resolve<<<(n_pix + 255) / 256, 256, 0, s>>>(tris, sx, sy, zn, iw, colors, height,
+                                                           width, win, zbuf, img, exposure, srgb8);
+  return check_launch("k_raster");
+}
+
+int sss_project_vertices(const double* vertices, int n_vertices, const double* cam, double f,
+                         double aspect, int width, int height, double* sx, double* sy,
+                         double* zn, double* iw, void* stream) {
+  if (n_vertices < 0 || width < 1 || height < 1 ||
+      (n_vertices > 0 && (!vertices || !cam || !sx || !sy || !zn || !iw)))
+    return fail(SSS_EINVAL, "bad project_vertices arguments");
+  if (n_vertices == 0) return SSS_OK;
+  sss::k_raster_project<<<(n_vertices + 255) / 256, 256, 0, S_(stream)>>>(
+      vertices, n_vertices, cam, f, aspect, width, height, sx, sy, zn, iw);
+  return check_launch("k_raster_project");
+}
+
+int sss_vertex_colors(const float* radiance, const int32_t* source_vertex, int n, double* colors,
+                      void* stream) {
+  if (n < 0 || (n > 0 && (!radiance || !colors))) return fail(SSS_EINVAL, "bad vertex_colors arguments");
+  if (n == 0) return SSS_OK;
+  sss::k_vertex_colors<<<(n + 255) / 256, 256, 0, S_(stream)>>>(radiance, source_vertex, n, colors);
+  return check_launch("k_vertex_colors");
+}
+
+int sss_encode_srgb8(const double* x, long long n, double exposure, uint8_t* out, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !out))) return fail(SSS_EINVAL, "bad encode_srgb8 arguments");
+  if (n == 0) return SSS_OK;
+  sss::k_encode_srgb8<<<(unsigned)((n + 255) / 256), 256, 0, S_(stream)>>>(x, n, exposure, out);
+  return check_launch("k_encode_srgb8");
 }
 
 }  // extern "C"

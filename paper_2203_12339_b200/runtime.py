@@ -841,6 +841,19 @@ class Scene:
         self.sweep_launch(ops, out)
         return out
 
+    def render_image(self, width: int, height: int, exposure: float = 1.0,
+                     background=(0.0, 0.0, 0.0)) -> np.ndarray:
+        """render_image (runtime.py:230-245) of the current frame's radiance,
+        straight from the device buffer (no host round trip of the radiance):
+        the geometry image's grid mesh, the scene camera, sRGB u8 out."""
+        from .raster import Rasterizer, mesh_of
+
+        key = (int(width), int(height))
+        r = getattr(self, "_raster", None)
+        if r is None or (r.width, r.height) != key:
+            r = self._raster = Rasterizer(mesh_of(self.geometry), width, height)
+        return r.render(self.radiance, self.camera, exposure, background)
+
     # ------------------------------------------------------------------
     # parity hooks
     # ------------------------------------------------------------------

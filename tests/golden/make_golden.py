@@ -38,9 +38,13 @@ def _import_reference(path):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default=str(ROOT / "baseline" / "_ref"))
+    ap.add_argument("--only", default=None, help="write just this fixture (e.g. raster)")
     args = ap.parse_args()
     _import_reference(args.ref)
     sys.path.insert(0, str(ROOT))
+    if args.only == "raster":
+        raster_fixture()
+        return
 
     from sssrelight import _kernels_np as knp
     from sssrelight import basisgen as bg
@@ -283,6 +287,65 @@ def main():
         env[f"val{c}"] = spectra[c].values
     np.savez_compressed(HERE / "env.npz", **env)
     print("golden fixtures written to", HERE)
+    raster_fixture()
+
+
+def raster_fixture():
+    """8. rasterisation: the reference's raster_fill on random triangles (the
+    test_kernels.py:91-109 pattern plus duplicate / reversed triangles for
+    depth ties and a partly filled initial z-buffer) and render_image's
+    stages on a 16^2 geometry-image mesh (_project_vertices -> raster_fill ->
+    linear_to_srgb), runtime.py:230-273."""
+    from sssrelight import _kernels_np as knp
+    from sssrelight import runtime as rt
+    from sssrelight.envmap import linear_to_srgb
+
+    from paper_2203_12339_b200.geometry import make_geometry_image
+    from paper_2203_12339_b200.shadows import grid_triangles
+
+    rng = np.random.default_rng(2271)
+    out = {}
+    n_tris, h, w = 60, 48, 64
+    nv = 3 * n_tris
+    tris = np.arange(nv, dtype=np.int64).reshape(n_tris, 3)
+    tris[40:50] = tris[0:10]            # exact duplicates: equal depth, first wins
+    tris[50:55] = tris[10:15][:, ::-1]  # reversed winding of earlier triangles
+    sx = rng.uniform(-10, 74, nv)
+    sy = rng.uniform(-10, 58, nv)
+    zn = rng.uniform(0.5, 5.0, nv)
+    iw = rng.uniform(0.2, 2.0, nv)
+    iw[rng.random(nv) < 0.1] = 0.0
+    colors = rng.random((nv, 3))
+    zb = np.full((h, w), np.inf)
+    zb[rng.random((h, w)) < 0.2] = 2.0   # pre-existing depth
+    img = rng.random((h, w, 3))
+    out.update(r_tris=tris, r_sx=sx, r_sy=sy, r_zn=zn, r_iw=iw, r_colors=colors,
+               r_zbuf0=zb.copy(), r_img0=img.copy())
+    knp.raster_fill(tris, sx, sy, zn, iw, colors, zb, img)
+    out.update(r_zbuf=zb, r_img=img)
+
+    g = make_geometry_image(16)
+    verts = g.positions.astype(np.float64)
+    gt = grid_triangles(16).astype(np.int64)
+    rad = np.abs(rng.standard_normal((verts.shape[0], 3))).astype(np.float32).astype(np.float64)
+    out.update(m_vertices=verts, m_tris=gt, m_radiance=rad)
+    cams = [dict(position=[0.0, 0.0, 180.0], look_at=[0.0, 0.0, 0.0], fov_y_degrees=8.0),
+            dict(position=[60.0, 45.0, 150.0], look_at=[0.0, 0.0, 0.0], fov_y_degrees=10.0)]
+    for ci, cam in enumerate(cams):
+        camera = rt.Camera(**cam)
+        W, H = 96, 72
+        sx, sy, zn, iw = rt._project_vertices(verts, camera, W, H)
+        zb = np.full((H, W), np.inf)
+        img = np.empty((H, W, 3))
+        img[:] = (0.02, 0.02, 0.03)
+        knp.raster_fill(gt, sx, sy, zn, iw, np.ascontiguousarray(rad), zb, img)
+        u8 = (linear_to_srgb(img * 2.0) * 255.0 + 0.5).astype(np.uint8)
+        out.update({f"c{ci}_pos": np.array(cam["position"]), f"c{ci}_at": np.array(cam["look_at"]),
+                    f"c{ci}_fov": np.array(cam["fov_y_degrees"]), f"c{ci}_sx": sx,
+                    f"c{ci}_sy": sy, f"c{ci}_zn": zn, f"c{ci}_iw": iw, f"c{ci}_img": img,
+                    f"c{ci}_zbuf": zb, f"c{ci}_u8": u8})
+    np.savez_compressed(HERE / "raster.npz", **out)
+    print("raster fixture written")
 
 
 if __name__ == "__main__":

@@ -228,3 +228,29 @@ def test_fold_oracle_matches_reference(golden):
     zero, _ = O.fold_visibility(ops, np.zeros_like(vis), d["normals"], int(g["side"]),
                                 int(g["face_side"]), 1.3)
     assert all(z.cols.size == 0 and z.rowidx.size == 0 for z in zero)
+
+
+def test_raster_oracle_matches_reference(golden):
+    """raster_fill / _project_vertices / render_image quantisation
+    (runtime.py:230-273, _kernels_np.py:264-313) against the reference run on
+    the same inputs: images and z-buffers bitwise; the projection (BLAS
+    matmul in the reference, ordered sums here) to 1e-12 and, fed the
+    reference's own projected vertices, the raster is bitwise."""
+    g = golden("raster")
+    zb, img = g["r_zbuf0"].copy(), g["r_img0"].copy()
+    O.raster_fill(g["r_tris"], g["r_sx"], g["r_sy"], g["r_zn"], g["r_iw"], g["r_colors"], zb, img)
+    assert np.array_equal(zb, g["r_zbuf"]) and np.array_equal(img, g["r_img"])
+    for ci in range(2):
+        pos, at, fov = g[f"c{ci}_pos"], g[f"c{ci}_at"], float(g[f"c{ci}_fov"])
+        sx, sy, zn, iw = O.project_vertices(g["m_vertices"], pos, at, [0.0, 1.0, 0.0], fov, 96, 72)
+        for a, name in ((sx, "sx"), (sy, "sy"), (zn, "zn"), (iw, "iw")):
+            ref = g[f"c{ci}_{name}"]
+            assert np.allclose(a, ref, rtol=1e-12, atol=1e-12), name
+        zb = np.full((72, 96), np.inf)
+        img = np.empty((72, 96, 3))
+        img[:] = (0.02, 0.02, 0.03)
+        O.raster_fill(g["m_tris"], g[f"c{ci}_sx"], g[f"c{ci}_sy"], g[f"c{ci}_zn"], g[f"c{ci}_iw"],
+                      g["m_radiance"], zb, img)
+        assert np.array_equal(img, g[f"c{ci}_img"]) and np.array_equal(zb, g[f"c{ci}_zbuf"])
+        assert np.array_equal(O.encode_srgb8(img, 2.0), g[f"c{ci}_u8"])
+        assert np.isfinite(zb).mean() > 0.2  # the object covers the frame
