@@ -427,6 +427,18 @@ int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const 
                    const float* vals, const uint32_t* union_idx, const double* union_lc,
                    const int* n_union, const uint32_t* flat2tm, double* vk, void* stream);
 
+/* sss_fold_apply_rows: the same v_k update as sss_fold_apply from a row-major
+ *   copy of the folded operators, ELL-interleaved per 32-row group: group g =
+ *   k * (n_rows / 32) + row / 32 owns [gbase[g], gbase[g + 1]) (absolute), entry
+ *   s of the group's lane j at gbase[g] + 32 s + j, ascending by direction within
+ *   a row, padded with (dir 0, val 0); entries = (dir u32, val f32 bits) pairs. One thread per
+ *   (k, row), per-row sums in the csc_apply order, bitwise equal to
+ *   sss_fold_apply. n_rows % 32 == 0; 24 * n_dirs <= 200 KB of shared memory. */
+int sss_fold_apply_rows(int K, int n_rows, int n_dirs, const uint64_t* gbase,
+                        const uint32_t* entries, const uint32_t* union_idx,
+                        const double* union_lc, const int* n_union, const uint32_t* flat2tm,
+                        double* vk, void* stream);
+
 /* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream);
@@ -498,6 +510,10 @@ int sss_raster_fill(const int64_t* tris, int n_tris, const double* sx, const dou
                     const double* zn, const double* iw, const double* colors, int height,
                     int width, double* zbuf, double* img, unsigned long long* key,
                     uint32_t* win, double exposure, uint8_t* srgb8, void* stream);
+
+/* sss_raster_clear: zbuf = +inf, img = background (runtime.py:239-241). */
+int sss_raster_clear(int height, int width, double b0, double b1, double b2, double* zbuf,
+                     double* img, void* stream);
 
 /* sss_project_vertices: replaces _project_vertices (runtime.py:247-273).
  *   cam = {position, right, up, fwd} (12 f64, device; the frame is built on

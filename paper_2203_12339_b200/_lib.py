@@ -48,6 +48,7 @@ _SIGS = {
     "sss_fold_spmm": [_I, _I, _P, _P, _P, _P, _P, _P],
     "sss_fold_select": [_P, _I, _I, C.c_double, _P, _P, _P, _P, _P, _P, _P],
     "sss_fold_emit": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_fold_apply_rows": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_fold_apply": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_direct_irradiance": [_I, _P, _P, _I, _P, _P, _P, C.c_double, C.c_double, _P, _P, _P, _P],
     "sss_transfer_k8": [_I, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P],
@@ -77,6 +78,7 @@ _SIGS = {
     "sss_scan_u32": [_P, _P, C.c_size_t, _P, _P, _P],
     "sss_rowptr": [_P, _I, _I, C.c_uint64, _P, _P, _P],
     "sss_raster_fill": [_P, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _D, _P, _P],
+    "sss_raster_clear": [_I, _I, _D, _D, _D, _P, _P, _P],
     "sss_project_vertices": [_P, _I, _P, _D, _D, _I, _I, _P, _P, _P, _P, _P],
     "sss_vertex_colors": [_P, _P, _I, _P, _P],
     "sss_encode_srgb8": [_P, C.c_longlong, _D, _P, _P],

@@ -981,6 +981,24 @@ int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const 
   return check_launch("k_fold_apply");
 }
 
+int sss_fold_apply_rows(int K, int n_rows, int n_dirs, const uint64_t* gbase,
+                        const uint32_t* entries, const uint32_t* union_idx,
+                        const double* union_lc, const int* n_union, const uint32_t* flat2tm,
+                        double* vk, void* stream) {
+  if (n_rows % 32) return fail(SSS_EINVAL, "fold_apply_rows: n_rows must be a multiple of 32");
+  if (K <= 0 || n_rows <= 0 || n_dirs <= 0 || !gbase || !entries || !union_idx ||
+      !union_lc || !n_union || !flat2tm || !vk)
+    return fail(SSS_EINVAL, "bad fold_apply_rows arguments");
+  const size_t smem = (size_t)24 * n_dirs;
+  if (smem > 200 * 1024) return fail(SSS_EINVAL, "fold_apply_rows: too many directions (use sss_fold_apply)");
+  if (int r = set_smem((const void*)sss::k_fold_apply_rows, smem)) return r;
+  dim3 grid((n_rows + 255) / 256, K);
+  sss::k_fold_apply_rows<<<grid, 256, smem, S_(stream)>>>(n_rows, n_dirs, gbase,
+                                                          reinterpret_cast<const uint2*>(entries),
+                                                          union_idx, union_lc, n_union, flat2tm, vk);
+  return check_launch("k_fold_apply_rows");
+}
+
 int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
                      int band_width, int n_bands, uint32_t* bandoff, void* stream) {
   if (!rowptr || !bandoff || K <= 0 || n_rows <= 0 || band_width <= 0 || n_bands <= 0)
@@ -1144,6 +1162,14 @@ int sss_raster_fill(const int64_t* tris, int n_tris, const double* sx, const dou
   sss::k_raster_resolve<<<(n_pix + 255) / 256, 256, 0, s>>>(tris, sx, sy, zn, iw, colors, height,
                                                            width, win, zbuf, img, exposure, srgb8);
   return check_launch("k_raster");
+}
+
+int sss_raster_clear(int height, int width, double b0, double b1, double b2, double* zbuf,
+                     double* img, void* stream) {
+  if (height < 1 || width < 1 || !zbuf || !img) return fail(SSS_EINVAL, "bad raster_clear arguments");
+  const int n_pix = height * width;
+  sss::k_raster_clear<<<(n_pix + 255) / 256, 256, 0, S_(stream)>>>(n_pix, b0, b1, b2, zbuf, img);
+  return check_launch("k_raster_clear");
 }
 
 int sss_project_vertices(const double* vertices, int n_vertices, const double* cam, double f,

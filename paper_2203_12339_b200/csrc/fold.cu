@@ -260,4 +260,65 @@ __global__ void __launch_bounds__(256) k_fold_apply(
   }
 }
 
+// ---- frame, row-major form: the same sums with one thread per (k, flat row)
+// walking the row's entries in ascending direction order (the csc_apply
+// order restricted to one row), the union's per-direction L_c gathered from
+// a shared-memory table (zero for directions outside the union: adding
+// v * 0 leaves a +0-started sum unchanged). No per-column barrier or search.
+// Entries are ELL-interleaved per 32-row group (slot-major: entry s of lane
+// j at gbase + 32 s + j, padded with (dir 0, val 0) to the group's longest
+// row), so every warp load is one coalesced 128-B line.
+// grid (N / 256, K), dynamic smem 24 * D bytes; N % 32 == 0.
+__global__ void __launch_bounds__(256) k_fold_apply_rows(
+    int N, int D, const uint64_t* __restrict__ gbase, const uint2* __restrict__ ent,
+    const uint32_t* __restrict__ union_idx, const double* __restrict__ union_lc,
+    const int* __restrict__ n_union, const uint32_t* __restrict__ flat2tm,
+    double* __restrict__ vk) {
+  extern __shared__ double tab[];  // [D][3]
+  for (int t = threadIdx.x; t < 3 * D; t += blockDim.x) tab[t] = 0.0;
+  __syncthreads();
+  const int nu = *n_union;
+  for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+    const uint32_t e = union_idx[u];
+    tab[3 * e] = union_lc[3 * u];
+    tab[3 * e + 1] = union_lc[3 * u + 1];
+    tab[3 * e + 2] = union_lc[3 * u + 2];
+  }
+  __syncthreads();
+  const int k = blockIdx.y;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  const size_t g = (size_t)k * (N >> 5) + (r >> 5);
+  const uint64_t b0 = gbase[g], b1 = gbase[g + 1];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  constexpr int U = 16;  // entries in flight per thread: the loads of a batch
+                         // are independent, only the fp64 sums are serial
+  constexpr int PF = 4;  // L2 prefetch distance in batches (the long, dense
+                         // coarse rows are a serial chain: keep it fed from L2)
+  const int lane = r & 31;
+  for (uint64_t j = b0 + lane; j < b1; j += 32 * U) {
+    {  // lane l prefetches line l of the batch PF ahead (32 lines = 32 * U entries)
+      const uint64_t pj = (j - lane) + (uint64_t)PF * 32 * U + (uint64_t)lane * 16;
+      if (pj < b1) asm volatile("prefetch.global.L2 [%0];" ::"l"(ent + pj));
+    }
+    uint2 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      x[u] = j + 32 * u < b1 ? __ldcs(ent + j + 32 * u) : make_uint2(0u, 0u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double v = (double)__uint_as_float(x[u].y);
+      const double* t = tab + 3 * x[u].x;
+      a0 = dadd(a0, dmul(v, t[0]));
+      a1 = dadd(a1, dmul(v, t[1]));
+      a2 = dadd(a2, dmul(v, t[2]));
+    }
+  }
+  const uint32_t tm = flat2tm[r];
+  double* o = vk + (size_t)k * 3 * N + tm;
+  o[0] = dadd(o[0], a0);
+  o[N] = dadd(o[N], a1);
+  o[2 * (size_t)N] = dadd(o[2 * (size_t)N], a2);
+}
+
 }  // namespace sss

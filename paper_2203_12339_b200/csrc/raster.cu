@@ -7,8 +7,8 @@
 // value acts like a triangle with index -1. The GPU reproduces exactly that
 // order-independent characterisation in three passes over the triangles /
 // pixels, with no ordering races:
-//   1. k_raster_depth : atomicMin of an order-preserving u64 key of z
-//   2. k_raster_pick  : among covering triangles with key(z) == min, atomicMin
+//   1. k_raster_tri<false>: atomicMin of an order-preserving u64 key of z
+//   2. k_raster_tri<true> : among covering triangles with key(z) == min, atomicMin
 //                       of the triangle index
 //   3. k_raster_resolve: per pixel, the winner recomputes its barycentrics and
 //                       writes colour and depth (optionally the sRGB u8 pixel)
@@ -84,6 +84,17 @@ __device__ __forceinline__ bool raster_bary(const RasterTri& r, int px, int py, 
 __device__ __forceinline__ double bary3(double l0, double l1, double l2, double a, double b,
                                         double c) {
   return __dadd_rn(__dadd_rn(__dmul_rn(l0, a), __dmul_rn(l1, b)), __dmul_rn(l2, c));
+}
+
+// render_image's buffer set-up (runtime.py:239-241): zbuf = inf, img = background.
+__global__ void k_raster_clear(int n_pix, double b0, double b1, double b2, double* __restrict__ zbuf,
+                               double* __restrict__ img) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pix) return;
+  zbuf[p] = __longlong_as_double(0x7ff0000000000000ll);
+  img[3 * (int64_t)p] = b0;
+  img[3 * (int64_t)p + 1] = b1;
+  img[3 * (int64_t)p + 2] = b2;
 }
 
 __global__ void k_raster_init(const double* __restrict__ zbuf, int n_pix,

@@ -194,17 +194,66 @@ def fold_visibility(transfer, vis: DeviceVisibility, geometry, eta: float,
         nzs.append(int(col_nz.to(torch.int64).sum()))
     rows = torch.cat(parts_rows) if base else torch.zeros(1, dtype=torch.int32, device=device)
     vals = torch.cat(parts_vals) if base else torch.zeros(1, dtype=torch.float32, device=device)
-    return DeviceFolded(K=K, side=s, levels=L, face_side=fs, eta=float(eta),
-                        fraction=float(fraction), colptr=colptr, rows=rows, vals=vals,
-                        kept_energy=kept, total_energy=total, step1_entries=nzs)
+    out = DeviceFolded(K=K, side=s, levels=L, face_side=fs, eta=float(eta),
+                       fraction=float(fraction), colptr=colptr, rows=rows, vals=vals,
+                       kept_energy=kept, total_energy=total, step1_entries=nzs)
+    if out.n % 32 == 0:
+        row_layout(out)  # the per-frame apply's layout, built before any graph capture
+    return out
 
 
-def fold_apply(folded: DeviceFolded, union_idx, union_lc, n_union, vk, stream=None):
+def row_layout(folded: DeviceFolded):
+    """Row-major, ELL-interleaved copy of the folded CSC (built once, on the
+    device; see sss_fold_apply_rows): per 32-row group g = k * (N / 32) +
+    row / 32, slot-major entries (entry s of lane j at gbase[g] + 32 s + j),
+    ascending by direction within a row — the per-row order csc_apply
+    accumulates in — padded with (dir 0, val 0) to the group's longest row."""
+    if getattr(folded, "_rows_layout", None) is not None:
+        return folded._rows_layout
+    n, d, K = folded.n, folded.direction_count, folded.K
+    dev = folded.colptr.device
+    cp = folded.colptr
+    nnz = int(cp[-1, -1]) if K else 0
+    kk = torch.repeat_interleave(torch.arange(K, device=dev), (cp[:, -1] - cp[:, 0]))
+    dd = torch.cat([torch.repeat_interleave(torch.arange(d, device=dev), torch.diff(cp[k]))
+                    for k in range(K)]) if nnz else torch.zeros(0, dtype=torch.int64, device=dev)
+    rr = folded.rows[:nnz].to(torch.int64) & 0xFFFFFFFF
+    krow = kk * n + rr
+    order = torch.argsort(krow * d + dd, stable=True)
+    krow, dd = krow[order], dd[order]
+    vv = folded.vals[:nnz][order]
+    counts = torch.bincount(krow, minlength=K * n)
+    start = torch.zeros(K * n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=start[1:])
+    slot = torch.arange(nnz, device=dev) - start[krow]          # rank within the row
+    width = counts.view(-1, 32).amax(1)                          # per group
+    gbase = torch.zeros(width.numel() + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(width * 32, 0, out=gbase[1:])
+    total = int(gbase[-1])
+    pos = gbase[krow // 32] + slot * 32 + (krow % 32)
+    ent = torch.zeros((max(total, 1), 2), dtype=torch.int32, device=dev)  # (dir, f32 bits)
+    ent[pos, 0] = dd.to(torch.int32)
+    ent[pos, 1] = vv.contiguous().view(torch.int32)
+    folded._rows_layout = (gbase, ent)
+    return folded._rows_layout
+
+
+def fold_apply(folded: DeviceFolded, union_idx, union_lc, n_union, vk, stream=None,
+               layout: str = "rows"):
     """vk (K, 3, N tm) += folded ambient response (runtime.py:146-149); the
-    union arrays are sss_env_project's (device)."""
+    union arrays are sss_env_project's (device). layout "rows" (default):
+    thread per (k, row) over the row-major copy; "csc": per row block over
+    the CSC columns (the first form; same bits)."""
     _, flat2tm = _maps(folded.side, folded.levels, vk.device) if not hasattr(folded, "_flat2tm") \
         else (None, folded._flat2tm)
     folded._flat2tm = flat2tm
+    if layout == "rows" and 24 * folded.direction_count <= 200 * 1024 and folded.n % 32 == 0:
+        gbase, ent = row_layout(folded)
+        _lib.call("sss_fold_apply_rows", folded.K, folded.n, folded.direction_count,
+                  _lib.ptr(gbase), _lib.ptr(ent), _lib.ptr(union_idx),
+                  _lib.ptr(union_lc), _lib.ptr(n_union), _lib.ptr(flat2tm), _lib.ptr(vk),
+                  _lib.stream_ptr(stream))
+        return
     _lib.call("sss_fold_apply", folded.K, folded.n, folded.direction_count,
               _lib.ptr(folded.colptr), _lib.ptr(folded.rows), _lib.ptr(folded.vals),
               _lib.ptr(union_idx), _lib.ptr(union_lc), _lib.ptr(n_union), _lib.ptr(flat2tm),

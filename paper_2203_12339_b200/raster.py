@@ -112,8 +112,9 @@ class Rasterizer:
 
     def launch(self, exposure: float = 1.0, background=(0.0, 0.0, 0.0)):
         """Clear, rasterise and encode on the current stream (no sync)."""
-        self.zbuf.fill_(float("inf"))
-        self.img.copy_(torch.as_tensor(np.asarray(background, np.float64)).expand_as(self.img))
+        b = np.broadcast_to(np.asarray(background, np.float64), (3,))
+        _lib.call("sss_raster_clear", self.height, self.width, float(b[0]), float(b[1]),
+                  float(b[2]), _lib.ptr(self.zbuf), _lib.ptr(self.img), _lib.stream_ptr())
         sx, sy, zn, iw = self.proj
         _lib.call("sss_raster_fill", _lib.ptr(self.tris), self.n_tris, _lib.ptr(sx), _lib.ptr(sy),
                   _lib.ptr(zn), _lib.ptr(iw), _lib.ptr(self.colors), self.height, self.width,

@@ -133,13 +133,14 @@ def test_fold_apply_bitwise(lib, golden):
     spectra = [O.Spectrum(g[f"env_idx{c}"], g[f"env_val{c}"], 6 * fs * fs, 0.0, 0.0)
                for c in range(3)]
     base = np.random.default_rng(3).standard_normal((4, 3, n))
-    vk = torch.as_tensor(base, device="cuda")  # tile-major rows
-    fold_apply(folded, *_union(spectra), vk)
-    torch.cuda.synchronize()
     perm = tile_major_to_flat(side, int(np.log2(side)))
-    got = vk.cpu().numpy()[:, :, np.argsort(perm)]  # -> flat rows
     amb = O.ambient_vk(folded.to_reference(), spectra, n)
-    assert np.array_equal(got, base[:, :, np.argsort(perm)] + amb)
+    for layout in ("rows", "csc"):  # the row-major (default) and CSC kernels
+        vk = torch.as_tensor(base, device="cuda")  # tile-major rows
+        fold_apply(folded, *_union(spectra), vk, layout=layout)
+        torch.cuda.synchronize()
+        got = vk.cpu().numpy()[:, :, np.argsort(perm)]  # -> flat rows
+        assert np.array_equal(got, base[:, :, np.argsort(perm)] + amb), layout
     # the reference's folded ambient v_k (its own f64 fold of f64 operators)
     assert np.abs(amb - g["vk"]).max() <= 1e-5 * np.abs(g["vk"]).max()
 
