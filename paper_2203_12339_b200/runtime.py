@@ -90,6 +90,20 @@ class FrameResult:
     sequence: int = 0
 
 
+_POOL = None
+
+
+def _host_pool():
+    """One helper thread for the second float64 conversion of a frame
+    (numpy releases the GIL in the cast loop)."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="sss-frame")
+    return _POOL
+
+
 class Scene:
     """Owns the relight state and the stage-2 (v_k) cache, all in HBM."""
 
@@ -671,26 +685,45 @@ class Scene:
     # reference API (runtime.py:174-227)
     # ------------------------------------------------------------------
 
-    def _frame(self, timings) -> FrameResult:
-        """One device->host round trip per frame: radiance, unclamped radiance
-        and the kept-energy sums land in pinned buffers, one synchronize."""
+    def _enqueue_readback(self):
+        """Queue the device->host copies of the frame's results (radiance,
+        unclamped radiance, kept-energy sums) into pinned buffers on the
+        current stream, behind the frame's kernels: no host round trip
+        between the frame and its read-back."""
         if getattr(self, "_pin", None) is None:
-            self._pin = {"rad": torch.empty((self.n, 3), dtype=torch.float32, pin_memory=True),
-                         "radu": torch.empty((self.n, 3), dtype=torch.float32, pin_memory=True),
+            self._pin = {"radu": torch.empty((self.n, 3), dtype=torch.float32, pin_memory=True),
                          "energy": torch.empty((3, 2), dtype=torch.float64, pin_memory=True)}
         pin = self._pin
-        pin["rad"].copy_(self.radiance, non_blocking=True)
+        # radiance = max(unclamped, 0) exactly (runtime.py:212), so only the
+        # unclamped f32 values cross the bus; the clamp is redone on the host
         pin["radu"].copy_(self.radiance_unclamped, non_blocking=True)
         pin["energy"].copy_(self.energy, non_blocking=True)
+
+    def _frame(self, timings, queued: bool = False) -> FrameResult:
+        """One device->host round trip per frame: the unclamped radiance and
+        the kept-energy sums land in pinned buffers, one synchronize; the two
+        float64 arrays of the reference's FrameResult (unclamped, and clamped
+        at 0 — bitwise the device's clamped radiance) are built on two host
+        threads."""
+        if not queued:
+            self._enqueue_readback()
+        pin = self._pin
         torch.cuda.current_stream().synchronize()
         e = pin["energy"].numpy()
         total, kept = float(e[:, 0].sum()), float(e[:, 1].sum())
         self._cache_energy = kept / total if total else 1.0
         self._sequence += 1
-        return FrameResult(radiance=pin["rad"].numpy().astype(np.float64),
-                           radiance_unclamped=pin["radu"].numpy().astype(np.float64),
+        u32 = pin["radu"].numpy()
+        fut = _host_pool().submit(np.maximum, u32, 0.0, dtype=np.float64)
+        radu = u32.astype(np.float64)
+        return FrameResult(radiance=fut.result(), radiance_unclamped=radu,
                            timings_ms=timings, kept_energy_ratio=self._cache_energy,
                            sequence=self._sequence)
+
+    def _replay_events(self):
+        if getattr(self, "_ev_pair", None) is None:
+            self._ev_pair = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        return self._ev_pair
 
     def relight(self) -> FrameResult:
         """Full pipeline; repopulates the stage-2 cache (runtime.py:174-187).
@@ -704,16 +737,17 @@ class Scene:
         if self._graph is None and getattr(self, "_eager_relights", 0) >= 2:
             self.capture()
         if self._graph is not None and getattr(self, "_stage_frac", None):
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev = self._replay_events()
             ev[0].record()
             self._graph.replay()
             ev[1].record()
-            ev[1].synchronize()
+            self._enqueue_readback()
             self._have_cache = True
+            fr = self._frame(timings, queued=True)  # synchronizes: ev[1] is complete
             total = ev[0].elapsed_time(ev[1])
             for k, f in self._stage_frac.items():
                 timings[k] = total * f
-            return self._frame(timings)
+            return fr
         self._eager_relights = getattr(self, "_eager_relights", 0) + 1
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
@@ -746,13 +780,14 @@ class Scene:
     def _edit_frame(self) -> FrameResult:
         timings = dict.fromkeys(STAGES, 0.0)
         if getattr(self, "_graph_edit", None) is not None and self._graph is not None:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev = self._replay_events()
             ev[0].record()
             self._graph_edit.replay()
             ev[1].record()
-            ev[1].synchronize()
+            self._enqueue_readback()
+            fr = self._frame(timings, queued=True)
             timings["inverse_wavelet"] = ev[0].elapsed_time(ev[1])
-            return self._frame(timings)
+            return fr
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
         self._launch_weights()
