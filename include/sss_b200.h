@@ -427,6 +427,35 @@ int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const 
                    const float* vals, const uint32_t* union_idx, const double* union_lc,
                    const int* n_union, const uint32_t* flat2tm, double* vk, void* stream);
 
+/* sss_transfer_flat8c: stage 2 (runtime.py:138-150; csc_apply,
+ *   _kernels_nb.py:301-313) over the column-partitioned flat8 stream of
+ *   runtime.flat8c_layout: entries (u16 partition-local column, f32 value)
+ *   partition-major, (partition, row, k) sub-segments padded to 8 entries,
+ *   head bits / word prefixes / segment ids (row * 16 + k) as
+ *   sss_transfer_flat8; CTA b serves partition cta_part[b] with that
+ *   partition's x (from xp, (n_rows, 4) f64) and kept bits staged in shared
+ *   memory; warp w streams words [warp_begin[w], warp_begin[w + 1]). Zeroes vk
+ *   (K, 3, n_rows) f64 and accumulates into it. part_width in {1024, 2048, 4096}. */
+int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals,
+                        unsigned long long n_entries, const uint32_t* heads,
+                        const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                        const unsigned* warp_begin, const int* cta_part, int n_ctas,
+                        int part_width, const void* xp, const uint32_t* bits, double* vk,
+                        void* stream);
+
+/* sss_transfer_kpairs: stage 2 of the frame (runtime.py:138-150, the K x 3
+ *   csc_apply calls of _kernels_nb.py:301-313) over the pair layout of
+ *   transfer.kpairs_layout: per (row, column) pair one header (column | term
+ *   mask << 16), the pair's values pair-major (terms ascending), chunk
+ *   descriptors {row, first pair, count <= 32, first value} (uint4, every row
+ *   >= 1 chunk) and per-warp chunk ranges covering whole rows. One x gather
+ *   per kept pair for all K terms; writes every vk[(k * 3 + c) * n_rows + row]
+ *   (no memset needed, deterministic). xp (n_rows, 4) f64 = sss_pack_x_bits's,
+ *   bits its kept bitmap. K <= 8, n_rows <= 65536, n_warps % 8 == 0. */
+int sss_transfer_kpairs(int K, int n_rows, const void* chunks, const uint32_t* hdr,
+                        const float* vals, const uint32_t* chunk_begin, int n_warps,
+                        const void* xp, const uint32_t* bits, double* vk, void* stream);
+
 /* sss_fold_apply_rows: the same v_k update as sss_fold_apply from a row-major
  *   copy of the folded operators, ELL-interleaved per 32-row group: group g =
  *   k * (n_rows / 32) + row / 32 owns [gbase[g], gbase[g + 1]) (absolute), entry

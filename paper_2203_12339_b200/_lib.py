@@ -48,6 +48,9 @@ _SIGS = {
     "sss_fold_spmm": [_I, _I, _P, _P, _P, _P, _P, _P],
     "sss_fold_select": [_P, _I, _I, C.c_double, _P, _P, _P, _P, _P, _P, _P],
     "sss_fold_emit": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_transfer_flat8c": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P,
+                            _P],
+    "sss_transfer_kpairs": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "sss_fold_apply_rows": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_fold_apply": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_direct_irradiance": [_I, _P, _P, _I, _P, _P, _P, C.c_double, C.c_double, _P, _P, _P, _P],

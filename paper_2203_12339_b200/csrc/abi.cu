@@ -29,6 +29,8 @@
 #include "direct.cu"
 #include "fold.cu"
 #include "raster.cu"
+#include "kpairs21.cu"
+#include "flat8c22.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -979,6 +981,66 @@ int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const 
   sss::k_fold_apply<<<grid, 256, 0, S_(stream)>>>(n_rows, n_dirs, colptr, rows, vals, union_idx,
                                                   union_lc, n_union, flat2tm, vk);
   return check_launch("k_fold_apply");
+}
+
+int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals,
+                        unsigned long long n_entries, const uint32_t* heads,
+                        const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                        const unsigned* warp_begin, const int* cta_part, int n_ctas,
+                        int part_width, const void* xp, const uint32_t* bits, double* vk,
+                        void* stream) {
+  if (K <= 0 || K > 16 || n_rows <= 0 || !cols16 || !vals || !heads || !head_prefix ||
+      !seg_rowk || !warp_begin || !cta_part || !xp || !bits || !vk || n_ctas <= 0 ||
+      n_entries % 256 || n_entries / 8 >= (1ull << 32) - 64)
+    return fail(SSS_EINVAL, "bad transfer_flat8c arguments");
+  if (reinterpret_cast<uintptr_t>(cols16) % 16 || reinterpret_cast<uintptr_t>(vals) % 32 ||
+      reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_flat8c: cols16 16-B, vals / xp 32-B aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const auto* c16 = reinterpret_cast<const uint4*>(cols16);
+  const auto* v8 = reinterpret_cast<const unsigned long long*>(vals);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+#define SSS_V22(CWV)                                                                             \
+  case CWV: {                                                                                    \
+    const size_t smem = (size_t)3 * CWV * 8 + CWV / 8;                                           \
+    if (int r = set_smem((const void*)sss::k_transfer_flat8c<CWV>, smem)) return r;             \
+    sss::k_transfer_flat8c<CWV><<<n_ctas, sss::kV22Threads, smem, S_(stream)>>>(                 \
+        n_rows, c16, v8, heads, head_prefix, seg_rowk, warp_begin, cta_part, x4, bits, vk);      \
+    break;                                                                                       \
+  }
+  switch (part_width) {
+    SSS_V22(1024) SSS_V22(2048) SSS_V22(4096)
+    default:
+      return fail(SSS_EINVAL, "transfer_flat8c: part_width must be 1024, 2048 or 4096");
+  }
+#undef SSS_V22
+  return check_launch("k_transfer_flat8c");
+}
+
+int sss_transfer_kpairs(int K, int n_rows, const void* chunks, const uint32_t* hdr,
+                        const float* vals, const uint32_t* chunk_begin, int n_warps,
+                        const void* xp, const uint32_t* bits, double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || n_rows > 65536 || !chunks || !hdr || !vals ||
+      !chunk_begin || !xp || !bits || !vk || n_warps <= 0 || n_warps % (sss::kV21Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_kpairs arguments");
+  if (reinterpret_cast<uintptr_t>(chunks) % 16 || reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_kpairs: chunks must be 16-byte and xp 32-byte aligned");
+  const size_t smem = (size_t)((n_rows + 31) / 32) * 4;
+  const unsigned grid = n_warps / (sss::kV21Threads / 32);
+  const auto* c4 = reinterpret_cast<const uint4*>(chunks);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+#define SSS_V21(KK)                                                                              \
+  case KK:                                                                                       \
+    if (int r = set_smem((const void*)sss::k_transfer_kpairs<KK>, smem)) return r;               \
+    sss::k_transfer_kpairs<KK><<<grid, sss::kV21Threads, smem, S_(stream)>>>(                    \
+        n_rows, c4, hdr, vals, chunk_begin, x4, bits, vk);                                       \
+    break;
+  switch (K) {
+    SSS_V21(1) SSS_V21(2) SSS_V21(3) SSS_V21(4) SSS_V21(5) SSS_V21(6) SSS_V21(7) SSS_V21(8)
+  }
+#undef SSS_V21
+  return check_launch("k_transfer_kpairs");
 }
 
 int sss_fold_apply_rows(int K, int n_rows, int n_dirs, const uint64_t* gbase,

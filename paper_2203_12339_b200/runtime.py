@@ -387,6 +387,27 @@ class Scene:
             if epilogue:
                 self._launch_edit(stream)
             return epilogue
+        if self.transfer_kernel == "flat8c":
+            sp = _lib.stream_ptr(stream)
+            if getattr(t, "flat8c", None) is None:
+                t.flat8c = flat8c_layout(t)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            if getattr(self, "xbits", None) is None:
+                self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+            _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                      _lib.ptr(self.xbits), sp)
+            self._flat8c_core(sp)
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
+        if self.transfer_kernel == "kpairs":
+            sp = _lib.stream_ptr(stream)
+            self._kpairs_prep(sp)
+            self._kpairs_core(sp)
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel in ("flat", "flat8"):
             sp = _lib.stream_ptr(stream)
             self._flat_prep(sp)
@@ -595,6 +616,30 @@ class Scene:
         _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
                   _lib.ptr(self.xbits), sp)
 
+    def _kpairs_prep(self, sp):
+        t = self.transfer
+        if getattr(t, "kpairs", None) is None:
+            t.kpairs = kpairs_layout(t)
+        if getattr(self, "xp", None) is None:
+            self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+        if getattr(self, "xbits", None) is None:
+            self.xbits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device="cuda")
+        _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                  _lib.ptr(self.xbits), sp)
+
+    def _flat8c_core(self, sp):
+        c16, v32, heads, hpre, rowk, wbeg, cta_part, G, parts, cw, _ = self.transfer.flat8c
+        _lib.call("sss_transfer_flat8c", self.K, self.n, _lib.ptr(c16), _lib.ptr(v32),
+                  c16.numel(), _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg),
+                  _lib.ptr(cta_part), G, cw, _lib.ptr(self.xp), _lib.ptr(self.xbits),
+                  _lib.ptr(self.vk), sp)
+
+    def _kpairs_core(self, sp):
+        chunks, hdr, vals, cbeg, W, _ = self.transfer.kpairs
+        _lib.call("sss_transfer_kpairs", self.K, self.n, _lib.ptr(chunks), _lib.ptr(hdr),
+                  _lib.ptr(vals), _lib.ptr(cbeg), W, _lib.ptr(self.xp), _lib.ptr(self.xbits),
+                  _lib.ptr(self.vk), sp)
+
     def _x_f32(self) -> bool:
         return self.transfer_kernel == "flat8" and os.environ.get("SSS_X_F32", "0") == "1"
 
@@ -616,6 +661,10 @@ class Scene:
     def launch_transfer_core(self, stream=None):
         """The dominant kernel alone (default path), on inputs the last frame
         prepared: for roofline timing."""
+        if self.transfer_kernel == "kpairs":
+            return self._kpairs_core(_lib.stream_ptr(stream))
+        if self.transfer_kernel == "flat8c":
+            return self._flat8c_core(_lib.stream_ptr(stream))
         if self.transfer_kernel not in ("flat", "flat8"):
             return self._launch_transfer(stream)
         self._flat_core(_lib.stream_ptr(stream))
@@ -1270,6 +1319,161 @@ def flat_layout(t: DeviceTransfer, warps_per_sm: int = None, group: int = 4, int
              "bytes": n_entries * 8 + nw * 8 + int(s4.numel()) * 4}
     return (pcols, pvals, n_entries, heads.contiguous(), hpre.contiguous(), rowk,
             wbeg.to(torch.int32).contiguous(), W, stats)
+
+
+def flat8c_layout(t: DeviceTransfer, parts: int = None, ctas_per_sm: int = 2):
+    """v22 column-partitioned flat8 stream (csrc/flat8c22.cu): entries sorted
+    by (column partition, row, k, column), every (partition, row, k)
+    sub-segment padded to a multiple of 8 entries, partition streams padded
+    to whole 32-group words; 16-bit partition-local columns + f32 values;
+    head bits / word prefixes / segment (row, k) ids as flat8; CTAs assigned
+    to partitions in proportion to their words, the words of a partition
+    split evenly over its CTAs' warps."""
+    import os
+
+    n, K = t.n, t.K
+    parts = parts or int(os.environ.get("SSS_FLAT8C_PARTS", "16"))
+    if n % parts or (n // parts) > 65536 or (n // parts) % 32:
+        raise ValueError("flat8c: the column partition width must divide n, be a multiple of 32 "
+                         "and fit 16 bits")
+    cw = n // parts
+    dev = t.rowptr.device
+    rp = t.rowptr.to(torch.int64)
+    nnz = int(rp[-1, -1])
+    kk = torch.repeat_interleave(torch.arange(K, device=dev), rp[:, -1] - rp[:, 0])
+    rows = torch.cat([torch.repeat_interleave(torch.arange(n, device=dev), torch.diff(rp[k]))
+                      for k in range(K)])
+    cols = t.cols[:nnz].to(torch.int64) & 0xFFFFFFFF
+    part = cols // cw
+    seg = (part * n + rows) * 16 + kk          # (partition, row, k) sub-segment key
+    key = seg * n + cols
+    del rows
+    key, order = torch.sort(key)
+    seg = key // n
+    lcol = (key % n) % cw
+    vals = t.vals[:nnz][order]
+    del key, order, cols, kk, part
+    useg, cnt = torch.unique_consecutive(seg, return_counts=True)
+    plen = (cnt + 7) // 8 * 8                 # padded sub-segment lengths
+    spart = useg // (16 * n)
+    # partition streams padded to whole words (32 groups = 256 entries)
+    pent = torch.zeros(parts, dtype=torch.int64, device=dev).index_add_(0, spart, plen)
+    ppad = (pent + 255) // 256 * 256
+    pbase = torch.zeros(parts + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(ppad, 0, out=pbase[1:])
+    sstart_in_part = torch.cumsum(plen, 0) - plen
+    # sub-segments are sorted partition-major: a partition's first one is at
+    # the cumulative count of the partitions before it
+    nseg_p = torch.bincount(spart, minlength=parts)
+    first_idx = torch.cumsum(nseg_p, 0) - nseg_p
+    first_of_part = torch.where(nseg_p > 0, sstart_in_part[torch.clamp(first_idx, max=max(
+        0, sstart_in_part.numel() - 1))], torch.zeros_like(nseg_p))
+    sstart = pbase[spart] + sstart_in_part - first_of_part[spart]
+    total = int(pbase[-1])
+    eseg = torch.repeat_interleave(torch.arange(useg.numel(), device=dev), cnt)
+    pos = sstart[eseg] + (torch.arange(nnz, device=dev) - (torch.cumsum(cnt, 0) - cnt)[eseg])
+    c16 = torch.zeros(total, dtype=torch.int16, device=dev)
+    v32 = torch.zeros(total, dtype=torch.float32, device=dev)
+    c16[pos] = lcol.to(torch.int32).to(torch.int16)
+    v32[pos] = vals
+    del eseg, pos, lcol, vals
+    g0 = sstart // 8                            # first group of each sub-segment
+    nwords = total // 256
+    heads = torch.zeros(nwords, dtype=torch.int64, device=dev).index_add_(
+        0, g0 // 32, torch.bitwise_left_shift(torch.ones_like(g0), g0 % 32))
+    heads = torch.where(heads >= (1 << 31), heads - (1 << 32), heads).to(torch.int32)
+    wc = torch.bincount(g0 // 32, minlength=nwords)
+    hpre = (torch.cumsum(wc, 0) - wc).to(torch.int32)
+    rowk = (useg % (16 * n)).to(torch.int32)    # row * 16 + k
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+    G = nsm * ctas_per_sm
+    pw = (ppad // 256).cpu()
+    share = pw.double() / max(1, int(pw.sum())) * G
+    cta_n = torch.clamp(share.floor().long(), min=1)
+    while int(cta_n.sum()) < G:                 # largest remainders first
+        cta_n[int(torch.argmax(share - cta_n.double()))] += 1
+    while int(cta_n.sum()) > G:
+        cta_n[int(torch.argmax(cta_n - share))] -= 1
+    wpc = 512 // 32
+    cta_part, wbeg = [], []
+    pb = (pbase // 256).cpu()
+    for p_ in range(parts):
+        nw_ = int(cta_n[p_]) * wpc
+        b0, b1 = int(pb[p_]), int(pb[p_ + 1])
+        cta_part += [p_] * int(cta_n[p_])
+        wbeg += [b0 + (b1 - b0) * j // nw_ for j in range(nw_)]
+    wbeg.append(int(pb[-1]))
+    stats = {"entries": total, "nnz": nnz, "parts": parts, "part_width": cw, "ctas": G,
+             "bytes": total * 6 + nwords * 8 + int(useg.numel()) * 4}
+    return (c16, v32, heads.contiguous(), hpre.contiguous(), rowk.contiguous(),
+            torch.tensor(wbeg, dtype=torch.int32, device=dev),
+            torch.tensor(cta_part, dtype=torch.int32, device=dev), G, parts, cw, stats)
+
+
+def kpairs_layout(t: DeviceTransfer, warps_per_sm: int = None):
+    """v21 pair layout (csrc/kpairs21.cu): the K operators merged per (row,
+    column) pair — header = column | term mask << 16, values pair-major with
+    terms ascending — rows cut into chunks of <= 32 pairs, and whole-row warp
+    ranges of about equal chunk count. Built on the device from the frame CSR."""
+    import os
+
+    n, K = t.n, t.K
+    if n > 65536 or K > 8:
+        raise ValueError("kpairs layout needs n <= 65536 and K <= 8")
+    dev = t.rowptr.device
+    rp = t.rowptr.to(torch.int64)
+    nnz = int(rp[-1, -1])
+    kk = torch.repeat_interleave(torch.arange(K, device=dev), rp[:, -1] - rp[:, 0])
+    rows = torch.cat([torch.repeat_interleave(torch.arange(n, device=dev), torch.diff(rp[k]))
+                      for k in range(K)])
+    cols = t.cols[:nnz].to(torch.int64) & 0xFFFFFFFF
+    key = (rows * n + cols) * 8 + kk
+    del rows, cols
+    key, order = torch.sort(key)
+    vals = t.vals[:nnz][order].contiguous()
+    del order
+    pk = key >> 3                      # row * n + col
+    kbit = torch.bitwise_left_shift(torch.ones_like(key), key & 7)
+    del key
+    first = torch.ones(nnz, dtype=torch.bool, device=dev)
+    first[1:] = pk[1:] != pk[:-1]
+    pid = torch.cumsum(first, 0) - 1
+    npairs = int(pid[-1]) + 1 if nnz else 0
+    mask = torch.zeros(npairs, dtype=torch.int64, device=dev).index_add_(0, pid, kbit)
+    pstart = torch.nonzero(first).squeeze(1)          # value index of each pair's first term
+    pkey = pk[pstart]
+    del pk, kbit, first, pid
+    prow = pkey // n
+    hdr = ((pkey % n) | (mask << 16)).to(torch.int32)
+    cnt = torch.bincount(prow, minlength=n)            # pairs per row
+    pp = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(cnt, 0, out=pp[1:])
+    nch = torch.clamp((cnt + 31) // 32, min=1)         # every row >= 1 chunk
+    cp = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(nch, 0, out=cp[1:])
+    C = int(cp[-1])
+    crow = torch.repeat_interleave(torch.arange(n, device=dev), nch)
+    ci = torch.arange(C, device=dev) - cp[crow]
+    cfirst = pp[crow] + 32 * ci
+    ccount = torch.clamp(pp[crow + 1] - cfirst, min=0, max=32)
+    vstart = torch.cat([pstart, torch.tensor([nnz], device=dev)])
+    cv = vstart[torch.clamp(cfirst, max=npairs)]
+    chunks = torch.stack([crow, cfirst, ccount, cv], 1).to(torch.int32).contiguous()
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_KPAIRS_WPS", "16"))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+    W = nsm * warps_per_sm
+    W -= W % 8
+    # whole-row warp ranges: warp w starts at the first row whose chunk prefix
+    # reaches w * C / W
+    target = (torch.arange(W + 1, device=dev, dtype=torch.int64) * C) // W
+    rstart = torch.searchsorted(cp[:-1].contiguous(), target, right=False)
+    rstart = torch.clamp(rstart, max=n)
+    cbeg = cp[rstart]
+    cbeg[-1] = C
+    cbeg = torch.cummax(cbeg, 0).values
+    stats = {"pairs": npairs, "chunks": C, "values": nnz,
+             "bytes": npairs * 4 + nnz * 4 + C * 16, "kfill": nnz / max(1, npairs * K)}
+    return chunks, hdr.contiguous(), vals, cbeg.to(torch.int32).contiguous(), W, stats
 
 
 def regional_layout(t: DeviceTransfer, region_tiles: int = 1):
