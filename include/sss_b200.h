@@ -443,6 +443,18 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
                         int part_width, const void* xp, const uint32_t* bits, double* vk,
                         void* stream);
 
+/* sss_transfer_pairgroup: stage 2 (runtime.py:138-150; csc_apply,
+ *   _kernels_nb.py:301-313) over the kpairs headers / pair-major values with
+ *   per-row pair starts pair_ptr (n_rows + 1) and value starts val_ptr (n_rows +
+ *   1), warps owning rows [row_begin[w], row_begin[w + 1]). Four lanes per (row,
+ *   column) pair (lane g: terms g, g + 4), one x gather per kept pair; writes
+ *   every vk[(k * 3 + c) * n_rows + row] (no memset, deterministic). K <= 8,
+ *   n_rows <= 65536, n_warps % 8 == 0. */
+int sss_transfer_pairgroup(int K, int n_rows, const uint32_t* pair_ptr, const uint32_t* val_ptr,
+                           const uint32_t* hdr, const float* vals, const uint32_t* row_begin,
+                           int n_warps, const void* xp, const uint32_t* bits, double* vk,
+                           void* stream);
+
 /* sss_transfer_kpairs: stage 2 of the frame (runtime.py:138-150, the K x 3
  *   csc_apply calls of _kernels_nb.py:301-313) over the pair layout of
  *   transfer.kpairs_layout: per (row, column) pair one header (column | term

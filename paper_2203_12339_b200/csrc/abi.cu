@@ -31,6 +31,7 @@
 #include "raster.cu"
 #include "kpairs21.cu"
 #include "flat8c22.cu"
+#include "kgroup23.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -1016,6 +1017,31 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
   }
 #undef SSS_V22
   return check_launch("k_transfer_flat8c");
+}
+
+int sss_transfer_pairgroup(int K, int n_rows, const uint32_t* pair_ptr, const uint32_t* val_ptr,
+                           const uint32_t* hdr, const float* vals, const uint32_t* row_begin,
+                           int n_warps, const void* xp, const uint32_t* bits, double* vk,
+                           void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || n_rows > 65536 || !pair_ptr || !val_ptr || !hdr ||
+      !vals || !row_begin || !xp || !bits || !vk || n_warps <= 0 ||
+      n_warps % (sss::kV23Threads / 32))
+    return fail(SSS_EINVAL, "bad transfer_pairgroup arguments");
+  if (reinterpret_cast<uintptr_t>(xp) % 32) return fail(SSS_EINVAL, "xp must be 32-byte aligned");
+  const size_t smem = (size_t)((n_rows + 31) / 32) * 4;
+  const unsigned grid = n_warps / (sss::kV23Threads / 32);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+#define SSS_V23(KK)                                                                              \
+  case KK:                                                                                       \
+    if (int r = set_smem((const void*)sss::k_transfer_pairgroup<KK>, smem)) return r;            \
+    sss::k_transfer_pairgroup<KK><<<grid, sss::kV23Threads, smem, S_(stream)>>>(                 \
+        n_rows, pair_ptr, val_ptr, hdr, vals, row_begin, x4, bits, vk);                          \
+    break;
+  switch (K) {
+    SSS_V23(1) SSS_V23(2) SSS_V23(3) SSS_V23(4) SSS_V23(5) SSS_V23(6) SSS_V23(7) SSS_V23(8)
+  }
+#undef SSS_V23
+  return check_launch("k_transfer_pairgroup");
 }
 
 int sss_transfer_kpairs(int K, int n_rows, const void* chunks, const uint32_t* hdr,

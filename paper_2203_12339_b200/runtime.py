@@ -401,6 +401,15 @@ class Scene:
             if epilogue:
                 self._launch_edit(stream)
             return epilogue
+        if self.transfer_kernel == "pairgroup":
+            sp = _lib.stream_ptr(stream)
+            if getattr(t, "pairgroup", None) is None:
+                t.pairgroup = pairgroup_layout(t)
+            self._kpairs_prep(sp, build=False)
+            self._pairgroup_core(sp)
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "kpairs":
             sp = _lib.stream_ptr(stream)
             self._kpairs_prep(sp)
@@ -616,9 +625,9 @@ class Scene:
         _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
                   _lib.ptr(self.xbits), sp)
 
-    def _kpairs_prep(self, sp):
+    def _kpairs_prep(self, sp, build=True):
         t = self.transfer
-        if getattr(t, "kpairs", None) is None:
+        if build and getattr(t, "kpairs", None) is None:
             t.kpairs = kpairs_layout(t)
         if getattr(self, "xp", None) is None:
             self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
@@ -633,6 +642,12 @@ class Scene:
                   c16.numel(), _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg),
                   _lib.ptr(cta_part), G, cw, _lib.ptr(self.xp), _lib.ptr(self.xbits),
                   _lib.ptr(self.vk), sp)
+
+    def _pairgroup_core(self, sp):
+        pp, vp, hdr, vals, rbeg, W, _ = self.transfer.pairgroup
+        _lib.call("sss_transfer_pairgroup", self.K, self.n, _lib.ptr(pp), _lib.ptr(vp),
+                  _lib.ptr(hdr), _lib.ptr(vals), _lib.ptr(rbeg), W, _lib.ptr(self.xp),
+                  _lib.ptr(self.xbits), _lib.ptr(self.vk), sp)
 
     def _kpairs_core(self, sp):
         chunks, hdr, vals, cbeg, W, _ = self.transfer.kpairs
@@ -665,6 +680,8 @@ class Scene:
             return self._kpairs_core(_lib.stream_ptr(stream))
         if self.transfer_kernel == "flat8c":
             return self._flat8c_core(_lib.stream_ptr(stream))
+        if self.transfer_kernel == "pairgroup":
+            return self._pairgroup_core(_lib.stream_ptr(stream))
         if self.transfer_kernel not in ("flat", "flat8"):
             return self._launch_transfer(stream)
         self._flat_core(_lib.stream_ptr(stream))
@@ -1473,7 +1490,36 @@ def kpairs_layout(t: DeviceTransfer, warps_per_sm: int = None):
     cbeg = torch.cummax(cbeg, 0).values
     stats = {"pairs": npairs, "chunks": C, "values": nnz,
              "bytes": npairs * 4 + nnz * 4 + C * 16, "kfill": nnz / max(1, npairs * K)}
+    # per-row pair / value starts (the pair-group kernel's row table)
+    t.kpairs_rows = (pp.to(torch.int32).contiguous(),
+                     vstart[torch.clamp(pp, max=npairs)].to(torch.int32).contiguous())
     return chunks, hdr.contiguous(), vals, cbeg.to(torch.int32).contiguous(), W, stats
+
+
+def pairgroup_layout(t: DeviceTransfer, warps_per_sm: int = None):
+    """v23 (csrc/kgroup23.cu): the kpairs headers / values with per-row pair
+    and value starts, and whole-row warp ranges of about equal pair counts."""
+    import os
+
+    if getattr(t, "kpairs", None) is None:
+        t.kpairs = kpairs_layout(t)
+    _, hdr, vals, _, _, st = t.kpairs
+    pp, vp = t.kpairs_rows
+    dev = pp.device
+    warps_per_sm = warps_per_sm or int(os.environ.get("SSS_PAIRGROUP_WPS", "48"))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+    W = nsm * warps_per_sm
+    W -= W % 8
+    n = t.n
+    # cost of a row ~ its 8-pair steps + a fixed row overhead
+    steps = (torch.diff(pp.to(torch.int64)) + 7) // 8 + 2
+    cum = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(steps, 0, out=cum[1:])
+    target = (torch.arange(W + 1, device=dev, dtype=torch.int64) * int(cum[-1])) // W
+    rbeg = torch.clamp(torch.searchsorted(cum[:-1].contiguous(), target), max=n)
+    rbeg[-1] = n
+    rbeg = torch.cummax(rbeg, 0).values
+    return pp, vp, hdr, vals, rbeg.to(torch.int32).contiguous(), W, dict(st, warps=W)
 
 
 def regional_layout(t: DeviceTransfer, region_tiles: int = 1):
