@@ -384,12 +384,18 @@ __global__ void k_env_irradiance_multi(const float* __restrict__ W2,
     const int tile = tile0 + j, tr = tile / tpr, tc = tile % tpr;
     const int i = (tr * T + e / T) * S + tc * T + e % T;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    constexpr int kPf = 32;  // W^{w2} loads in flight per thread (order of the sum is fixed)
+    // W^{w2} loads: one batch of kPf in flight while the previous batch is
+    // summed (the order of the sum is fixed: ascending union position)
+    constexpr int kPf = 32;
+    float wv[kPf], wn[kPf];
+#pragma unroll
+    for (int u = 0; u < kPf; ++u) wn[u] = (u < m) ? __ldg(&W2[(size_t)ul[u] * N + i]) : 0.0f;
     for (int q0 = 0; q0 < m; q0 += kPf) {
-      float wv[kPf];
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) wv[u] = wn[u];
 #pragma unroll
       for (int u = 0; u < kPf; ++u)
-        wv[u] = (q0 + u < m) ? __ldg(&W2[(size_t)ul[q0 + u] * N + i]) : 0.0f;
+        wn[u] = (q0 + kPf + u < m) ? __ldg(&W2[(size_t)ul[q0 + kPf + u] * N + i]) : 0.0f;
       // a channel that dropped the id has l = 0: w * 0 adds an exact zero, so
       // the sums equal the per-channel ones of the reference (value-equal)
 #pragma unroll
