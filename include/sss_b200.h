@@ -443,6 +443,23 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
                         int part_width, const void* xp, const uint32_t* bits, double* vk,
                         void* stream);
 
+/* sss_transfer_rbcsc: stage 2 (runtime.py:138-150; csc_apply,
+ *   _kernels_nb.py:301-313) over the row-block column-major layout of
+ *   runtime.rbcsc_layout: per block of row_block tile-major rows, segment
+ *   descriptors {column | length << 16, first entry} (desc_ptr (n_rows /
+ *   row_block + 1) into them), entries rowk (row in block | k << log2
+ *   row_block, u16) and vals (f32). Only segments of kept columns (bits =
+ *   sss_pack_x_bits's kept bitmap) are read, x fetched once per segment.
+ *   Exact 64-bit fixed-point accumulation in shared memory, scale per (k, c)
+ *   from rowabs[k] = max_row sum |T_k| and energy (3, 2) = select's (total,
+ *   kept) sums of squares; writes every vk[(k * 3 + c) * n_rows + row]
+ *   (deterministic, no memset). row_block in {32, 64, 128} for K in {4, 8};
+ *   row_block 64 for any K <= 8. */
+int sss_transfer_rbcsc(int K, int n_rows, int row_block, const void* desc,
+                       const uint32_t* desc_ptr, const uint16_t* rowk, const float* vals,
+                       const double* rowabs, const double* energy, const void* xp,
+                       const uint32_t* bits, double* vk, void* stream);
+
 /* sss_transfer_pairgroup: stage 2 (runtime.py:138-150; csc_apply,
  *   _kernels_nb.py:301-313) over the kpairs headers / pair-major values with
  *   per-row pair starts pair_ptr (n_rows + 1) and value starts val_ptr (n_rows +

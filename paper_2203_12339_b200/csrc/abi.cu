@@ -32,6 +32,7 @@
 #include "kpairs21.cu"
 #include "flat8c22.cu"
 #include "kgroup23.cu"
+#include "rbcsc24.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -1017,6 +1018,32 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
   }
 #undef SSS_V22
   return check_launch("k_transfer_flat8c");
+}
+
+int sss_transfer_rbcsc(int K, int n_rows, int row_block, const void* desc,
+                       const uint32_t* desc_ptr, const uint16_t* rowk, const float* vals,
+                       const double* rowabs, const double* energy, const void* xp,
+                       const uint32_t* bits, double* vk, void* stream) {
+  if (K <= 0 || K > 8 || n_rows <= 0 || n_rows > 65536 || !desc || !desc_ptr || !rowk ||
+      !vals || !rowabs || !energy || !xp || !bits || !vk || n_rows % row_block)
+    return fail(SSS_EINVAL, "bad transfer_rbcsc arguments");
+  if (reinterpret_cast<uintptr_t>(xp) % 32 || reinterpret_cast<uintptr_t>(desc) % 8)
+    return fail(SSS_EINVAL, "transfer_rbcsc: xp 32-B, desc 8-B aligned");
+  const unsigned grid = n_rows / row_block;
+  const auto* d2 = reinterpret_cast<const uint2*>(desc);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+#define SSS_V24(RBV, KK)                                                                         \
+  if (row_block == RBV && K == KK) {                                                             \
+    sss::k_transfer_rbcsc<RBV, KK><<<grid, sss::kV24Threads, 0, S_(stream)>>>(                   \
+        n_rows, d2, desc_ptr, rowk, vals, rowabs, energy, x4, bits, vk);                         \
+    return check_launch("k_transfer_rbcsc");                                                     \
+  }
+  SSS_V24(64, 8) SSS_V24(128, 8) SSS_V24(32, 8)
+  SSS_V24(64, 4) SSS_V24(128, 4) SSS_V24(32, 4)
+  SSS_V24(64, 1) SSS_V24(64, 2) SSS_V24(64, 3) SSS_V24(64, 5) SSS_V24(64, 6) SSS_V24(64, 7)
+#undef SSS_V24
+  return fail(SSS_EINVAL, "transfer_rbcsc: row_block in {32, 64, 128} for K in {4, 8}, 64 for "
+                          "K <= 8");
 }
 
 int sss_transfer_pairgroup(int K, int n_rows, const uint32_t* pair_ptr, const uint32_t* val_ptr,

@@ -401,6 +401,15 @@ class Scene:
             if epilogue:
                 self._launch_edit(stream)
             return epilogue
+        if self.transfer_kernel == "rbcsc":
+            sp = _lib.stream_ptr(stream)
+            if getattr(t, "rbcsc", None) is None:
+                t.rbcsc = rbcsc_layout(t)
+            self._kpairs_prep(sp, build=False)
+            self._rbcsc_core(sp)
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
         if self.transfer_kernel == "pairgroup":
             sp = _lib.stream_ptr(stream)
             if getattr(t, "pairgroup", None) is None:
@@ -643,6 +652,12 @@ class Scene:
                   _lib.ptr(cta_part), G, cw, _lib.ptr(self.xp), _lib.ptr(self.xbits),
                   _lib.ptr(self.vk), sp)
 
+    def _rbcsc_core(self, sp):
+        desc, dptr, rk16, v32, rowabs, rb, _ = self.transfer.rbcsc
+        _lib.call("sss_transfer_rbcsc", self.K, self.n, rb, _lib.ptr(desc), _lib.ptr(dptr),
+                  _lib.ptr(rk16), _lib.ptr(v32), _lib.ptr(rowabs), _lib.ptr(self.energy),
+                  _lib.ptr(self.xp), _lib.ptr(self.xbits), _lib.ptr(self.vk), sp)
+
     def _pairgroup_core(self, sp):
         pp, vp, hdr, vals, rbeg, W, _ = self.transfer.pairgroup
         _lib.call("sss_transfer_pairgroup", self.K, self.n, _lib.ptr(pp), _lib.ptr(vp),
@@ -682,6 +697,8 @@ class Scene:
             return self._flat8c_core(_lib.stream_ptr(stream))
         if self.transfer_kernel == "pairgroup":
             return self._pairgroup_core(_lib.stream_ptr(stream))
+        if self.transfer_kernel == "rbcsc":
+            return self._rbcsc_core(_lib.stream_ptr(stream))
         if self.transfer_kernel not in ("flat", "flat8"):
             return self._launch_transfer(stream)
         self._flat_core(_lib.stream_ptr(stream))
@@ -1425,6 +1442,51 @@ def flat8c_layout(t: DeviceTransfer, parts: int = None, ctas_per_sm: int = 2):
     return (c16, v32, heads.contiguous(), hpre.contiguous(), rowk.contiguous(),
             torch.tensor(wbeg, dtype=torch.int32, device=dev),
             torch.tensor(cta_part, dtype=torch.int32, device=dev), G, parts, cw, stats)
+
+
+def rbcsc_layout(t: DeviceTransfer, row_block: int = None):
+    """v24 row-block column-major layout (csrc/rbcsc24.cu): per block of
+    `row_block` tile-major rows, the entries of all K terms grouped by column
+    (segments described by column | length << 16 and first entry), entries as
+    (row in block | k << log2 row_block) u16 + f32 value; rowabs[k] = max over
+    rows of sum |T_k[row, :]| (the fixed-point scale bound)."""
+    import os
+
+    n, K = t.n, t.K
+    rb = row_block or int(os.environ.get("SSS_RBCSC_RB", "128"))
+    if n > 65536 or K > 8 or n % rb:
+        raise ValueError("rbcsc layout needs n <= 65536 (16-bit columns), K <= 8, rb | n")
+    sh = rb.bit_length() - 1
+    dev = t.rowptr.device
+    rp = t.rowptr.to(torch.int64)
+    nnz = int(rp[-1, -1])
+    kk = torch.repeat_interleave(torch.arange(K, device=dev), rp[:, -1] - rp[:, 0])
+    rows = torch.cat([torch.repeat_interleave(torch.arange(n, device=dev), torch.diff(rp[k]))
+                      for k in range(K)])
+    cols = t.cols[:nnz].to(torch.int64) & 0xFFFFFFFF
+    vals = t.vals[:nnz]
+    rowabs = torch.zeros(K * n, dtype=torch.float64, device=dev).index_add_(
+        0, kk * n + rows, vals.abs().double()).view(K, n).amax(1).contiguous()
+    key = ((rows // rb) * n + cols) * (rb * 8) + (kk * rb + rows % rb)
+    key, order = torch.sort(key)
+    rk16 = (((key % (rb * 8)) % rb) | (((key % (rb * 8)) // rb) << sh)).to(torch.int32)
+    v32 = vals[order].contiguous()
+    del order
+    seg = key // (rb * 8)
+    del key
+    useg, cnt = torch.unique_consecutive(seg, return_counts=True)
+    del seg
+    first = torch.cumsum(cnt, 0) - cnt
+    desc = torch.stack([((useg % n) | (cnt << 16)), first], 1)
+    desc = torch.where(desc >= (1 << 31), desc - (1 << 32), desc).to(torch.int32).contiguous()
+    blk = useg // n
+    dcount = torch.bincount(blk, minlength=n // rb)
+    dptr = torch.zeros(n // rb + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(dcount, 0, out=dptr[1:])
+    stats = {"segments": int(useg.numel()), "entries": nnz, "row_block": rb,
+             "bytes": nnz * 6 + int(useg.numel()) * 8}
+    return (desc, dptr.to(torch.int32).contiguous(), rk16.to(torch.int16).contiguous(), v32,
+            rowabs, rb, stats)
 
 
 def kpairs_layout(t: DeviceTransfer, warps_per_sm: int = None):
