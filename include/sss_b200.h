@@ -443,6 +443,19 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
                         int part_width, const void* xp, const uint32_t* bits, double* vk,
                         void* stream);
 
+/* sss_transfer_flat16: sss_transfer_flat8 with entries_per_lane = 16 or 32
+ *   entries per lane (segments padded to a multiple of it with column n_rows /
+ *   value 0, heads one bit per group); the kept bitmap `bits` needs
+ *   n_rows / 32 + 1 words with the bit of column n_rows clear (padding entries
+ *   then skip their gather). min_blocks = CTAs of 128 threads per SM (register
+ *   cap): 4, 6, 8 for 16 entries, 6, 8 for 32. Zeroes vk and accumulates into it. */
+int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                        unsigned long long n_entries, const uint32_t* heads,
+                        const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                        const unsigned* warp_begin, int n_warps, int min_blocks,
+                        int entries_per_lane, const void* xp, const uint32_t* bits, double* vk,
+                        void* stream);
+
 /* sss_transfer_rbcsc: stage 2 (runtime.py:138-150; csc_apply,
  *   _kernels_nb.py:301-313) over the row-block column-major layout of
  *   runtime.rbcsc_layout: per block of row_block tile-major rows, segment

@@ -33,6 +33,7 @@
 #include "flat8c22.cu"
 #include "kgroup23.cu"
 #include "rbcsc24.cu"
+#include "flat16_25.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -1018,6 +1019,40 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
   }
 #undef SSS_V22
   return check_launch("k_transfer_flat8c");
+}
+
+int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+                        unsigned long long n_entries, const uint32_t* heads,
+                        const uint32_t* head_prefix, const uint32_t* seg_rowk,
+                        const unsigned* warp_begin, int n_warps, int min_blocks,
+                        int entries_per_lane, const void* xp, const uint32_t* bits, double* vk,
+                        void* stream) {
+  const int E = entries_per_lane;
+  if (K <= 0 || K > 16 || n_rows <= 0 || !pcols || !pvals || !heads || !head_prefix ||
+      !seg_rowk || !warp_begin || !xp || !bits || !vk || n_warps <= 0 || (E != 16 && E != 32) ||
+      n_warps % (sss::kV25Threads / 32) || n_entries % E || n_entries / E >= (1ull << 32) - 64)
+    return fail(SSS_EINVAL, "bad transfer_flat16 arguments");
+  if (reinterpret_cast<uintptr_t>(pcols) % 32 || reinterpret_cast<uintptr_t>(pvals) % 32 ||
+      reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_flat16: pcols/pvals/xp must be 32-byte aligned");
+  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  const size_t smem = (size_t)((n_rows >> 5) + 1) * 4;
+  const auto* c16 = reinterpret_cast<const unsigned long long*>(pcols);
+  const auto* v16 = reinterpret_cast<const unsigned long long*>(pvals);
+  const auto* x4 = reinterpret_cast<const double4*>(xp);
+  const unsigned grid = n_warps / (sss::kV25Threads / 32);
+  const unsigned ng = (unsigned)(n_entries / E);
+#define SSS_V25(MB, EE)                                                                          \
+  if (min_blocks == MB && E == EE) {                                                             \
+    if (int r = set_smem((const void*)sss::k_transfer_flat16<MB, EE>, smem)) return r;           \
+    sss::k_transfer_flat16<MB, EE><<<grid, sss::kV25Threads, smem, S_(stream)>>>(                \
+        n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);           \
+    return check_launch("k_transfer_flat16");                                                    \
+  }
+  SSS_V25(4, 16) SSS_V25(6, 16) SSS_V25(8, 16) SSS_V25(8, 32) SSS_V25(6, 32)
+#undef SSS_V25
+  return fail(SSS_EINVAL, "transfer_flat16: (min_blocks, entries_per_lane) in {4,6,8}x16, {6,8}x32");
 }
 
 int sss_transfer_rbcsc(int K, int n_rows, int row_block, const void* desc,

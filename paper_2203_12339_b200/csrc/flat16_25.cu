@@ -1,0 +1,118 @@
+// Transfer v25 "flat16": flat8 with 16 entries per lane.
+//
+// In flat8 (v17) the segmented warp scan that closes every 256-entry warp
+// iteration (5 shuffle steps x 3 fp64 channels = 30 SHFL) costs 8.5 M of the
+// kernel's 45.8 M L1 data-pipe wavefronts at C3 (the x gathers are 28.8 M).
+// Sixteen entries per lane (segments padded to a multiple of 16 and
+// lane-interleaved the same way) halve the iterations, so the scans, the head
+// / prefix loads and the loop overhead halve, for ~3 % more padding entries.
+// Gathers run in quarters of four entries (12 live fp64 x registers).
+#include "sss_common.cuh"
+
+namespace sss {
+
+constexpr int kV25Threads = 128;
+
+struct V25Slot {
+  unsigned long long c[8];  // 16 u32 columns
+  unsigned long long v[8];  // 16 f32 values
+  uint32_t h, hp;
+};
+
+// group q = i * 32 + lane of G = E / 16 sub-slots; sub-slot j of the group is
+// the 16 entries at (q * G + j) * 16
+__device__ __forceinline__ void v25_load(V25Slot& S, size_t q, unsigned ngroups, int G, int j,
+                                         const unsigned long long* __restrict__ C16,
+                                         const unsigned long long* __restrict__ V16) {
+  if (q >= ngroups) {  // past the stream's last group (partial last word)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) S.c[t] = S.v[t] = 0ull;
+    return;
+  }
+  q = q * G + j;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(S.c[4 * h]), "=l"(S.c[4 * h + 1]), "=l"(S.c[4 * h + 2]), "=l"(S.c[4 * h + 3])
+                 : "l"(C16 + 8 * q + 4 * h));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(S.v[4 * h]), "=l"(S.v[4 * h + 1]), "=l"(S.v[4 * h + 2]), "=l"(S.v[4 * h + 3])
+                 : "l"(V16 + 8 * q + 4 * h));
+  }
+}
+
+__device__ __forceinline__ uint32_t v25_col(const V25Slot& S, int e) {
+  return (uint32_t)(S.c[e >> 1] >> (32 * (e & 1)));
+}
+__device__ __forceinline__ float v25_val(const V25Slot& S, int e) {
+  return __uint_as_float((uint32_t)(S.v[e >> 1] >> (32 * (e & 1))));
+}
+
+template <int MINB, int E = 16>
+__global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
+    int N, unsigned ngroups, const unsigned long long* __restrict__ C16,
+    const unsigned long long* __restrict__ V16,
+    const uint32_t* __restrict__ H, const uint32_t* __restrict__ hpre,
+    const uint32_t* __restrict__ rowk, const unsigned* __restrict__ warp_begin,
+    const double4* __restrict__ xp, const uint32_t* __restrict__ bits, double* __restrict__ vk) {
+  constexpr int G = E / 16;
+  extern __shared__ uint32_t v25_bits[];
+  // one word past the N columns: padding entries carry column N, never kept
+  for (int t = threadIdx.x; t <= (N >> 5); t += blockDim.x) v25_bits[t] = bits[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned i0 = warp_begin[w], i1 = warp_begin[w + 1];
+  const unsigned upto = (2u << lane) - 1u;
+#pragma unroll 1
+  for (unsigned i = i0; i < i1; ++i) {
+    V25Slot S;
+    S.h = __ldg(&H[i]);
+    S.hp = __ldg(&hpre[i]);
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < G; ++j) {
+      v25_load(S, (size_t)i * 32u + (unsigned)lane, ngroups, G, j, C16, V16);
+#pragma unroll
+      for (int qd = 0; qd < 4; ++qd) {
+        double x[4][3];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t c = v25_col(S, qd * 4 + e);
+          x[e][0] = x[e][1] = x[e][2] = 0.0;
+          if ((v25_bits[c >> 5] >> (c & 31u)) & 1u) v15_gather1(xp, c, x[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double v = (double)v25_val(S, qd * 4 + e);
+          p0 = fma(v, x[e][0], p0);
+          p1 = fma(v, x[e][1], p1);
+          p2 = fma(v, x[e][2], p2);
+        }
+      }
+    }
+    const unsigned hm = S.h & upto;
+    const int sstart = hm ? 31 - __clz(hm) : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y0 = __shfl_up_sync(0xffffffffu, p0, o);
+      const double y1 = __shfl_up_sync(0xffffffffu, p1, o);
+      const double y2 = __shfl_up_sync(0xffffffffu, p2, o);
+      if (lane >= o && lane - o >= sstart) {
+        p0 += y0;
+        p1 += y1;
+        p2 += y2;
+      }
+    }
+    const bool tail = (lane == 31) || ((S.h >> (lane + 1)) & 1u);
+    if (tail && (p0 != 0.0 || p1 != 0.0 || p2 != 0.0)) {
+      const unsigned rk = __ldg(&rowk[S.hp + __popc(hm) - 1u]);
+      double* vo = vk + (size_t)(rk & 15u) * 3 * N + (rk >> 4);
+      atomicAdd(vo, p0);
+      atomicAdd(vo + N, p1);
+      atomicAdd(vo + 2 * (size_t)N, p2);
+    }
+  }
+}
+
+}  // namespace sss

@@ -147,10 +147,10 @@ class Scene:
         self.material_buf = torch.empty(7, **f64)
         self.cam_buf = torch.empty(3, **f64)
         self._light_kind = None
-        # "flat8" (flat-stream CSR, 8 entries per lane, head flags, kept-column
-        # skip: the default) | "flat" | "csr9" | "v6" | ... (earlier layouts,
-        # kept for A/B checks)
-        self.transfer_kernel = os.environ.get("SSS_TRANSFER", "flat8")
+        # "flat16" (flat-stream CSR, 16 entries per lane, head flags, kept-column
+        # skip: the default) | "flat8" | "flat" | "csr9" | "v6" | ... (earlier
+        # layouts and measured alternatives, kept for A/B checks)
+        self.transfer_kernel = os.environ.get("SSS_TRANSFER", "flat16")
         self._have_cache = False
         self._sequence = 0
         self._graph = None
@@ -398,6 +398,27 @@ class Scene:
             _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
                       _lib.ptr(self.xbits), sp)
             self._flat8c_core(sp)
+            if epilogue:
+                self._launch_edit(stream)
+            return epilogue
+        if self.transfer_kernel == "flat16":
+            sp = _lib.stream_ptr(stream)
+            E = int(os.environ.get("SSS_FLAT16_E", "16"))
+            if getattr(t, "flat16", None) is None or t.flat16[-1].get("E") != E:
+                lay = flat_layout(t, group=E, interleave=True,
+                                  warps_per_sm=int(os.environ.get("SSS_FLAT16_WPS", "32")))
+                pcols, pvals = lay[0], lay[1]
+                # padding entries (value 0) point at column n, whose kept bit
+                # is always clear: they skip the gather instead of loading x[0]
+                pcols = torch.where(pvals == 0, torch.full_like(pcols, self.n), pcols)
+                t.flat16 = (pcols,) + tuple(lay[1:-1]) + (dict(lay[-1], E=E),)
+            if getattr(self, "xp", None) is None:
+                self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            if getattr(self, "xbits16", None) is None:  # + one always-clear word
+                self.xbits16 = torch.zeros((self.n >> 5) + 1, dtype=torch.int32, device="cuda")
+            _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
+                      _lib.ptr(self.xbits16), sp)
+            self._flat16_core(sp)
             if epilogue:
                 self._launch_edit(stream)
             return epilogue
@@ -652,6 +673,13 @@ class Scene:
                   _lib.ptr(cta_part), G, cw, _lib.ptr(self.xp), _lib.ptr(self.xbits),
                   _lib.ptr(self.vk), sp)
 
+    def _flat16_core(self, sp):
+        pcols, pvals, ne, heads, hpre, rowk, wbeg, W, st = self.transfer.flat16
+        _lib.call("sss_transfer_flat16", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
+                  _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W,
+                  int(os.environ.get("SSS_FLAT16_MINB", "8")), st["E"], _lib.ptr(self.xp),
+                  _lib.ptr(self.xbits16), _lib.ptr(self.vk), sp)
+
     def _rbcsc_core(self, sp):
         desc, dptr, rk16, v32, rowabs, rb, _ = self.transfer.rbcsc
         _lib.call("sss_transfer_rbcsc", self.K, self.n, rb, _lib.ptr(desc), _lib.ptr(dptr),
@@ -699,8 +727,10 @@ class Scene:
             return self._pairgroup_core(_lib.stream_ptr(stream))
         if self.transfer_kernel == "rbcsc":
             return self._rbcsc_core(_lib.stream_ptr(stream))
+        if self.transfer_kernel == "flat16":
+            return self._flat16_core(_lib.stream_ptr(stream))
         if self.transfer_kernel not in ("flat", "flat8"):
-            return self._launch_transfer(stream)
+            return self._launch_transfer(stream, epilogue=False)
         self._flat_core(_lib.stream_ptr(stream))
 
     def _launch_edit(self, stream=None):

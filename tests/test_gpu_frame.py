@@ -330,7 +330,7 @@ def test_stream_and_banded_kernels_agree(c1):
     sc.transfer_kernel = "banded"
     a = sc.relight()
     vk_a = sc.vk.clone()
-    for kern in ("stream", "v4", "v6", "csr7", "csr8", "csr9", "kpack", "kpackp", "kstep", "kstream", "csr9s", "kgroup", "flat", "flatp", "flat8", "kflat", "regional", "k8", "kpairs", "flat8c", "pairgroup", "rbcsc"):
+    for kern in ("stream", "v4", "v6", "csr7", "csr8", "csr9", "kpack", "kpackp", "kstep", "kstream", "csr9s", "kgroup", "flat", "flatp", "flat8", "kflat", "regional", "k8", "kpairs", "flat8c", "pairgroup", "rbcsc", "flat16"):
         sc.transfer_kernel = kern
         sc.vk.fill_(float("nan"))  # a kernel that leaves v_k untouched must fail
         sc.radiance_unclamped.fill_(float("nan"))

@@ -16,7 +16,7 @@ from collections import OrderedDict, defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-FRAME = ("k_transfer_flat8s", "k_env_irradiance_multi", "k_select_cluster", "k_env_project",
+FRAME = ("k_transfer_flat16", "k_transfer_flat8s", "k_env_irradiance_multi", "k_select_cluster", "k_env_project",
          "k_edit_finish_multi", "k_material_weights", "k_env_union", "k_pack_x_bits",
          "k_sh_irradiance_multi", "k_direct_single", "k_fold_apply_rows")
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -96,7 +96,7 @@ def main():
         launches(src / "launches.csv", a.prefix, out)
     if (src / a.rep).exists():
         full(src / a.rep, a.prefix, out, "ncu --set full --import-source on --clock-control none "
-             "-k regex:k_transfer_flat8s -c 1, C3 bench (bench.py --steps 2 --warmup 3 "
+             "-k regex:k_transfer_flat -c 1, C3 bench (bench.py --steps 2 --warmup 3 "
              "--no-cpu-baseline --no-secondary)")
 
 
