@@ -252,6 +252,10 @@ def run_ours(a, cfg):
     from paper_2203_12339_b200.runtime import EnvLight
 
     n_e2e = min(a.steps, 30)
+    # one untimed API frame first: allocates the pinned read-back buffers and
+    # warms the host conversion path (as W warm-up steps do for the device loop)
+    scene.set_light(EnvLight(faces[0]))
+    scene.set_material(scene.material)
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
