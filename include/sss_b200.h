@@ -456,6 +456,17 @@ int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* p
                         int entries_per_lane, const void* xp, const uint32_t* bits, double* vk,
                         void* stream);
 
+/* sss_flat_align: layout pass over a 16-entries-per-lane flat stream (see
+ *   sss_transfer_flat16): inside every 512-entry window (one warp iteration)
+ *   re-slot each lane's entries so that a column present in several of the
+ *   window's segments sits in the same slot of their lanes (shared gather
+ *   wavefront); lanes keep their segments, so heads / prefixes / segment ids are
+ *   unchanged. n_groups = 16-entry groups in the stream (the last word may be
+ *   partial). cols >= sentinel mark padding. Out-of-place. */
+int sss_flat_align(unsigned n_words, unsigned n_groups, const uint32_t* cols_in, const float* vals_in,
+                   const uint32_t* heads, uint32_t sentinel, uint32_t* cols_out, float* vals_out,
+                   void* stream);
+
 /* sss_transfer_rbcsc: stage 2 (runtime.py:138-150; csc_apply,
  *   _kernels_nb.py:301-313) over the row-block column-major layout of
  *   runtime.rbcsc_layout: per block of row_block tile-major rows, segment

@@ -34,6 +34,7 @@
 #include "kgroup23.cu"
 #include "rbcsc24.cu"
 #include "flat16_25.cu"
+#include "align26.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -1053,6 +1054,20 @@ int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* p
   SSS_V25(4, 16) SSS_V25(6, 16) SSS_V25(8, 16) SSS_V25(8, 32) SSS_V25(6, 32)
 #undef SSS_V25
   return fail(SSS_EINVAL, "transfer_flat16: (min_blocks, entries_per_lane) in {4,6,8}x16, {6,8}x32");
+}
+
+int sss_flat_align(unsigned n_words, unsigned n_groups, const uint32_t* cols_in, const float* vals_in,
+                   const uint32_t* heads, uint32_t sentinel, uint32_t* cols_out, float* vals_out,
+                   void* stream) {
+  if (!cols_in || !vals_in || !heads || !cols_out || !vals_out || cols_in == cols_out ||
+      vals_in == vals_out)
+    return fail(SSS_EINVAL, "bad flat_align arguments");
+  if (n_words == 0) return SSS_OK;
+  if (n_groups > 32ull * n_words || n_groups + 32 <= 32ull * n_words)
+    return fail(SSS_EINVAL, "flat_align: n_groups must cover the last word");
+  sss::k_flat_align<<<(n_words + 63) / 64, 64, 0, S_(stream)>>>(n_words, n_groups, cols_in, vals_in,
+                                                                heads, sentinel, cols_out, vals_out);
+  return check_launch("k_flat_align");
 }
 
 int sss_transfer_rbcsc(int K, int n_rows, int row_block, const void* desc,

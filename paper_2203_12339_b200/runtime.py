@@ -411,7 +411,14 @@ class Scene:
                 # padding entries (value 0) point at column n, whose kept bit
                 # is always clear: they skip the gather instead of loading x[0]
                 pcols = torch.where(pvals == 0, torch.full_like(pcols, self.n), pcols)
-                t.flat16 = (pcols,) + tuple(lay[1:-1]) + (dict(lay[-1], E=E),)
+                aligned = E == 16 and os.environ.get("SSS_FLAT16_ALIGN", "0") == "1"
+                if aligned:  # duplicate columns of a warp iteration share a slot
+                    c2, v2 = torch.empty_like(pcols), torch.empty_like(pvals)
+                    _lib.call("sss_flat_align", lay[3].numel(), lay[2] // 16, _lib.ptr(pcols),
+                              _lib.ptr(pvals),
+                              _lib.ptr(lay[3]), self.n, _lib.ptr(c2), _lib.ptr(v2), sp)
+                    pcols, pvals = c2, v2
+                t.flat16 = (pcols, pvals) + tuple(lay[2:-1]) + (dict(lay[-1], E=E, aligned=aligned),)
             if getattr(self, "xp", None) is None:
                 self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
             if getattr(self, "xbits16", None) is None:  # + one always-clear word
