@@ -629,3 +629,28 @@ def test_frame_ambient_folded_parity(c1):
     _, unc_d, _ = O.finish(vk_direct, w, cfg.side, cfg.levels, "haar", nrm, pos,
                            np.array(C.CAMERA[0]), m.eta)
     assert O.parity_error(unc_d, unc, TAU) > 1e-2
+
+
+def test_flat16_layout_variants_agree(c1, monkeypatch):
+    """flat16 with 32 entries per lane and with the window column-alignment
+    pass (csrc/align26.cu) computes the same v_k as the default flat16."""
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import SHLight
+
+    sc = _scene(c1, SHLight(LT.random_sh_light(3, 29)))
+    sc.transfer_kernel = "flat16"
+    sc.relight()
+    ref = sc.vk.clone()
+    for env in ({"SSS_FLAT16_ALIGN": "1"}, {"SSS_FLAT16_E": "32"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        sc.transfer.flat16 = None
+        sc._graph = None
+        sc.vk.fill_(float("nan"))
+        sc._launch_stage1()
+        sc._launch_transfer(epilogue=False)
+        torch.cuda.synchronize()
+        assert torch.isfinite(sc.vk).all(), env
+        assert (sc.vk - ref).abs().max().item() <= 1e-12 * ref.abs().max().item(), env
+        for k in env:
+            monkeypatch.delenv(k)
