@@ -270,7 +270,7 @@ def run_ours(a, cfg):
     e2e_s = max_over_ranks(e2e_s, ws)
     n_edit_e2e = sum(1 for i in range(n_e2e) if a.warmup + i in mats)
     h2d = faces[0].nbytes + (56 * n_edit_e2e) / n_e2e
-    d2h = (n * 3 * 4 + 48) * (1 + n_edit_e2e / n_e2e)  # unclamped f32 radiance + energy sums
+    d2h = (2 * n * 3 * 8 + 48) * (1 + n_edit_e2e / n_e2e)  # f64 radiance + unclamped + energies
     e2e = {"value": ws * n * n_e2e / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s / n_e2e,
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_e2e,
            "path": "Scene.set_light(EnvLight(host cubemap)) / set_material -> FrameResult (numpy)"}

@@ -612,6 +612,12 @@ int sss_project_vertices(const double* vertices, int n_vertices, const double* c
 int sss_vertex_colors(const float* radiance, const int32_t* source_vertex, int n, double* colors,
                       void* stream);
 
+/* sss_widen_frame: out (2, n) f64 = (radiance, radiance_unclamped) widened
+ *   from the frame's f32 device buffers: the FrameResult arrays (runtime.py:
+ *   56-62, float64) leave the device ready to use (n = points * 3). */
+int sss_widen_frame(const float* radiance, const float* radiance_unclamped, long long n,
+                    double* out, void* stream);
+
 /* sss_encode_srgb8: out[i] = uint8(linear_to_srgb(x[i] * exposure) * 255 + 0.5),
  *   the quantised frame payload of the service (service.py:181, envmap.py:74-76). */
 int sss_encode_srgb8(const double* x, long long n, double exposure, uint8_t* out, void* stream);

@@ -1357,6 +1357,16 @@ int sss_vertex_colors(const float* radiance, const int32_t* source_vertex, int n
   return check_launch("k_vertex_colors");
 }
 
+int sss_widen_frame(const float* radiance, const float* radiance_unclamped, long long n,
+                    double* out, void* stream) {
+  if (n < 0 || (n > 0 && (!radiance || !radiance_unclamped || !out)))
+    return fail(SSS_EINVAL, "bad widen_frame arguments");
+  if (n == 0) return SSS_OK;
+  sss::k_widen_frame<<<(unsigned)((n + 255) / 256), 256, 0, S_(stream)>>>(radiance,
+                                                                         radiance_unclamped, n, out);
+  return check_launch("k_widen_frame");
+}
+
 int sss_encode_srgb8(const double* x, long long n, double exposure, uint8_t* out, void* stream) {
   if (n < 0 || (n > 0 && (!x || !out))) return fail(SSS_EINVAL, "bad encode_srgb8 arguments");
   if (n == 0) return SSS_OK;

@@ -223,6 +223,18 @@ __global__ void k_vertex_colors(const float* __restrict__ radiance, const int32_
   for (int c = 0; c < 3; ++c) colors[3 * (int64_t)v + c] = (double)radiance[3 * (int64_t)i + c];
 }
 
+// FrameResult read-back: out[0] = radiance, out[1] = radiance_unclamped as
+// float64 (runtime.py:56-62 dtype), so the host receives the final arrays by
+// DMA with no host-side conversion.
+__global__ void k_widen_frame(const float* __restrict__ rad, const float* __restrict__ radu,
+                              int64_t n, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    out[i] = (double)rad[i];
+    out[n + i] = (double)radu[i];
+  }
+}
+
 // Per-element sRGB u8 encoding (service.py:181 frame payload).
 __global__ void k_encode_srgb8(const double* __restrict__ x, int64_t n, double exposure,
                                uint8_t* __restrict__ out) {

@@ -90,18 +90,47 @@ class FrameResult:
     sequence: int = 0
 
 
-_POOL = None
+class _PinnedBlock:
+    """One pinned (2, N, 3) float64 host block lent to a FrameResult: its two
+    arrays are numpy views through the buffer protocol, so the block stays
+    alive (and out of the pool) until every view of either array is gone."""
+
+    __slots__ = ("pool", "t", "__weakref__")
+
+    def __init__(self, pool, t):
+        self.pool, self.t = pool, t
+
+    def __buffer__(self, flags):
+        return memoryview(self.t.numpy())
+
+    def __release_buffer__(self, view):
+        pass
+
+    def __del__(self):
+        self.pool.give_back(self.t)
 
 
-def _host_pool():
-    """One helper thread for the second float64 conversion of a frame
-    (numpy releases the GIL in the cast loop)."""
-    global _POOL
-    if _POOL is None:
-        from concurrent.futures import ThreadPoolExecutor
+class _PinnedPool:
+    """Recycled pinned read-back blocks for FrameResult arrays. Frames the
+    caller keeps hold their blocks; past `cap` blocks outstanding the frame
+    falls back to host-converted pageable arrays."""
 
-        _POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="sss-frame")
-    return _POOL
+    def __init__(self, n, cap=64):
+        self.n, self.cap, self.free, self.out = n, cap, [], 0
+
+    def take(self):
+        if self.free:
+            t = self.free.pop()
+        elif self.out >= self.cap:
+            return None
+        else:
+            t = torch.empty((2, self.n, 3), dtype=torch.float64, pin_memory=True)
+        self.out += 1
+        return t
+
+    def give_back(self, t):
+        self.out -= 1
+        self.free.append(t)
 
 
 class Scene:
@@ -806,37 +835,47 @@ class Scene:
     # ------------------------------------------------------------------
 
     def _enqueue_readback(self):
-        """Queue the device->host copies of the frame's results (radiance,
-        unclamped radiance, kept-energy sums) into pinned buffers on the
-        current stream, behind the frame's kernels: no host round trip
-        between the frame and its read-back."""
+        """Queue the device->host read-back of the frame's results on the
+        current stream, behind the frame's kernels: the radiance and unclamped
+        radiance widened to float64 on the device (the reference FrameResult
+        dtype) straight into a pooled pinned block that becomes the returned
+        arrays, plus the kept-energy sums. No host round trip before the copy,
+        no host-side conversion after it."""
         if getattr(self, "_pin", None) is None:
-            self._pin = {"radu": torch.empty((self.n, 3), dtype=torch.float32, pin_memory=True),
-                         "energy": torch.empty((3, 2), dtype=torch.float64, pin_memory=True)}
-        pin = self._pin
-        # radiance = max(unclamped, 0) exactly (runtime.py:212), so only the
-        # unclamped f32 values cross the bus; the clamp is redone on the host
-        pin["radu"].copy_(self.radiance_unclamped, non_blocking=True)
-        pin["energy"].copy_(self.energy, non_blocking=True)
+            self._pin = {"energy": torch.empty((3, 2), dtype=torch.float64, pin_memory=True),
+                         "radu": torch.empty((self.n, 3), dtype=torch.float32, pin_memory=True)}
+            self._pool = _PinnedPool(self.n)
+            self._rad64 = torch.empty((2, self.n, 3), dtype=torch.float64, device="cuda")
+        blk = self._pool.take()
+        if blk is not None:
+            _lib.call("sss_widen_frame", _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped),
+                      self.n * 3, _lib.ptr(self._rad64), _lib.stream_ptr())
+            blk.copy_(self._rad64, non_blocking=True)
+        else:  # caller holds every pooled block: pageable arrays, host cast
+            self._pin["radu"].copy_(self.radiance_unclamped, non_blocking=True)
+        self._pin["energy"].copy_(self.energy, non_blocking=True)
+        self._blk = blk
 
     def _frame(self, timings, queued: bool = False) -> FrameResult:
-        """One device->host round trip per frame: the unclamped radiance and
-        the kept-energy sums land in pinned buffers, one synchronize; the two
-        float64 arrays of the reference's FrameResult (unclamped, and clamped
-        at 0 — bitwise the device's clamped radiance) are built on two host
-        threads."""
+        """One device->host round trip per frame (see _enqueue_readback), one
+        synchronize. radiance = max(unclamped, 0) bitwise as on the device."""
         if not queued:
             self._enqueue_readback()
-        pin = self._pin
+        pin, blk = self._pin, self._blk
+        self._blk = None
         torch.cuda.current_stream().synchronize()
         e = pin["energy"].numpy()
         total, kept = float(e[:, 0].sum()), float(e[:, 1].sum())
         self._cache_energy = kept / total if total else 1.0
         self._sequence += 1
-        u32 = pin["radu"].numpy()
-        fut = _host_pool().submit(np.maximum, u32, 0.0, dtype=np.float64)
-        radu = u32.astype(np.float64)
-        return FrameResult(radiance=fut.result(), radiance_unclamped=radu,
+        if blk is not None:
+            both = np.frombuffer(_PinnedBlock(self._pool, blk), dtype=np.float64).reshape(2, self.n, 3)
+            rad, radu = both[0], both[1]
+        else:
+            u32 = pin["radu"].numpy()
+            radu = u32.astype(np.float64)
+            rad = np.maximum(u32, 0.0, dtype=np.float64)
+        return FrameResult(radiance=rad, radiance_unclamped=radu,
                            timings_ms=timings, kept_energy_ratio=self._cache_energy,
                            sequence=self._sequence)
 

@@ -654,3 +654,30 @@ def test_flat16_layout_variants_agree(c1, monkeypatch):
         assert (sc.vk - ref).abs().max().item() <= 1e-12 * ref.abs().max().item(), env
         for k in env:
             monkeypatch.delenv(k)
+
+
+def test_frame_result_arrays_survive_later_frames(c1):
+    """FrameResult arrays live in pooled pinned blocks: a kept frame (or a
+    view of it) is never overwritten by later frames; dropped frames recycle."""
+    import gc
+
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import SHLight
+
+    sc = _scene(c1, SHLight(LT.random_sh_light(3, 41)))
+    f1 = sc.relight()
+    keep_view = f1.radiance_unclamped[:, 1]
+    snap = (f1.radiance.copy(), f1.radiance_unclamped.copy())
+    assert f1.radiance.dtype == np.float64 and f1.radiance.shape == (sc.n, 3)
+    assert np.array_equal(f1.radiance, np.maximum(f1.radiance_unclamped, 0.0))
+    assert np.array_equal(f1.radiance_unclamped,
+                          sc.radiance_unclamped.cpu().numpy().astype(np.float64))
+    del f1
+    gc.collect()
+    for s in range(20):  # later frames with other lights
+        sc.set_light(SHLight(LT.random_sh_light(3, 100 + s)))
+    assert np.array_equal(keep_view, snap[1][:, 1])
+    out0 = sc._pool.out
+    del keep_view
+    gc.collect()
+    assert sc._pool.out == out0 - 1
