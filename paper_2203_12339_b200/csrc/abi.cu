@@ -159,8 +159,11 @@ int sss_env_irradiance(const float* W2, int D, const uint32_t* union_idx, const 
   const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
   // one point per thread with a sequential (bitwise-pinned) sum: balance the
   // grid across the SMs with small CTAs (>= 64 threads)
-  int tpb = 64 / T2 < 1 ? 1 : 64 / T2;
-  while (tpb > 1 && tiles % tpb) tpb >>= 1;
+  // TPB horizontally adjacent tiles per CTA (a warp then reads whole 128-B
+  // lines of W^{w2}); SSS_ENV_TPB overrides for experiments
+  const char* tpb_env = getenv("SSS_ENV_TPB");
+  int tpb = tpb_env ? atoi(tpb_env) : (T * 4 <= side ? 4 : 1);
+  if (tpb < 1 || (side / T) % tpb) tpb = 1;
   const size_t smem = 6 * (size_t)tpb * T2 * sizeof(double) + 12 * (size_t)n_keep * sizeof(double) +
                       3 * (size_t)n_keep * sizeof(int);
   if (int r = set_smem((const void*)sss::k_env_irradiance_multi, smem)) return r;

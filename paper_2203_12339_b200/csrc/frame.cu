@@ -380,7 +380,10 @@ __global__ void k_env_irradiance_multi(const float* __restrict__ W2,
   __syncthreads();
   const int tile0 = blockIdx.x * TPB;
   for (int q = threadIdx.x; q < TPB * T2; q += blockDim.x) {
-    const int j = q / T2, e = q % T2;
+    // the CTA's TPB tiles are horizontally adjacent: consecutive threads walk
+    // one image row across them, so a warp's W^{w2} loads are whole lines
+    const int rr = q / (TPB * T), cc = q % (TPB * T);
+    const int j = cc / T, e = rr * T + cc % T;
     const int tile = tile0 + j, tr = tile / tpr, tc = tile % tpr;
     const int i = (tr * T + e / T) * S + tc * T + e % T;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
