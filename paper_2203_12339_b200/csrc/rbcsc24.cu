@@ -15,8 +15,9 @@
 // segments' entries (only touched coefficients are read: 6 bytes each).
 //
 // The entries of a segment scatter into (row, k) outputs of the block; the
-// CTA accumulates them in shared memory as 64-bit fixed-point integers with
-// native shared-memory atomics: q = rn(v * x * S_kc), S_kc = 2^(61 - e),
+// CTA accumulates them in shared memory as 64-bit fixed-point integers, each
+// kept as two 32-bit words updated with native 32-bit shared atomics (carry
+// from the returned old low word): q = rn(v * x * S_kc), S_kc = 2^(61 - e),
 // 2^e > B_kc = max_row sum |T_k| * max |x_c| (max |x_c| bounded by the square
 // root of the kept energy of channel c). Integer sums are exact and order
 // independent, so the result is deterministic; each product is rounded once
@@ -39,12 +40,20 @@ __global__ void __launch_bounds__(kV24Threads) k_transfer_rbcsc(
     double* __restrict__ vk) {
   constexpr int kSh = RB == 32 ? 5 : RB == 64 ? 6 : 7;  // row-in-block bits
   static_assert(RB == 32 || RB == 64 || RB == 128, "RB in {32, 64, 128}");
-  __shared__ unsigned long long acc[K * 3 * RB];
+  // exact 64-bit fixed-point sums as two 32-bit halves: native shared-memory
+  // ATOMS.ADD on the low word returns the old value, so the carry of every
+  // single addition is known and added to the high word (64-bit shared
+  // atomics compile to CAS loops on sm_100a)
+  // (k, c) planes of RB + 1 words: entries of one segment share rows, so a
+  // plain RB stride would put (row, k) and (row, k') in the same bank
+  constexpr int PL = RB + 1;
+  __shared__ uint32_t acc_lo[K * 3 * PL], acc_hi[K * 3 * PL];
   __shared__ double scale[K * 3], inv_scale[K * 3];
   __shared__ double xs[kV24Warps][32][3];
   __shared__ uint32_t sst[kV24Warps][33], soff[kV24Warps][32];
+  __shared__ uint32_t smask[kV24Warps][32], wpre[kV24Warps][32];
   const int rb = blockIdx.x;
-  for (int t = threadIdx.x; t < K * 3 * RB; t += blockDim.x) acc[t] = 0ull;
+  for (int t = threadIdx.x; t < K * 3 * PL; t += blockDim.x) acc_lo[t] = acc_hi[t] = 0u;
   if (threadIdx.x < K * 3) {
     const int k = threadIdx.x / 3, c = threadIdx.x % 3;
     const double B = rowabs[k] * sqrt(fmax(energy[c * 2 + 1], 0.0));
@@ -73,6 +82,9 @@ __global__ void __launch_bounds__(kV24Threads) k_transfer_rbcsc(
       if (lane >= o) inc += y;
     }
     const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    const uint32_t start = inc - cnt;
+    smask[wid][lane] = 0u;
+    __syncwarp();
     if (kept) {
       const int s = __popc(m & lt);
       double x3;
@@ -80,38 +92,64 @@ __global__ void __launch_bounds__(kV24Threads) k_transfer_rbcsc(
                    : "=d"(xs[wid][s][0]), "=d"(xs[wid][s][1]), "=d"(xs[wid][s][2]), "=d"(x3)
                    : "l"(xp + col));
       (void)x3;
-      sst[wid][s] = inc - cnt;
+      sst[wid][s] = start;
       soff[wid][s] = ds.y;
+      // segment-start bitmap over the first 1024 virtual entries
+      if (start < 1024u) atomicOr(&smask[wid][start >> 5], 1u << (start & 31u));
     }
     const int nk = __popc(m);
     if (lane == 0) sst[wid][nk] = total;
     __syncwarp();
+    {
+      const uint32_t pc = __popc(smask[wid][lane]);
+      uint32_t ps = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, ps, o);
+        if (lane >= o) ps += y;
+      }
+      wpre[wid][lane] = ps - pc;
+    }
+    __syncwarp();
 #pragma unroll 1
     for (uint32_t e = lane; e < total; e += 32) {
-      // segment of virtual entry e: the last s with sst[s] <= e (nk <= 32)
-      int lo = 0, hi = nk - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sst[wid][mid] <= e) lo = mid; else hi = mid - 1;
+      int sg;  // the segment of virtual entry e: starts at or below e, minus one
+      if (e < 1024u) {
+        const uint32_t wd = smask[wid][e >> 5];
+        sg = (int)(wpre[wid][e >> 5] + __popc(wd & ((2u << (e & 31u)) - 1u))) - 1;
+      } else {  // long batches: binary search over the (<= 32) starts
+        int a0 = 0, a1 = nk - 1;
+        while (a0 < a1) {
+          const int mid = (a0 + a1 + 1) >> 1;
+          if (sst[wid][mid] <= e) a0 = mid; else a1 = mid - 1;
+        }
+        sg = a0;
       }
-      const uint32_t idx = soff[wid][lo] + (e - sst[wid][lo]);
+      const uint32_t idx = soff[wid][sg] + (e - sst[wid][sg]);
       const uint32_t q = __ldcs(rk + idx);
       const double v = (double)__ldcs(vals + idx);
       const int r = q & (RB - 1), k = q >> kSh;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double p = dmul(v, xs[wid][lo][c]);
-        const long long iq = __double2ll_rn(dmul(p, scale[k * 3 + c]));
-        if (iq) atomicAdd(acc + (k * 3 + c) * RB + r, (unsigned long long)iq);
+        const double p = dmul(v, xs[wid][sg][c]);
+        const unsigned long long uq =
+            (unsigned long long)__double2ll_rn(dmul(p, scale[k * 3 + c]));
+        if (uq) {
+          const int a = (k * 3 + c) * PL + r;
+          const uint32_t wlo = (uint32_t)uq, whi = (uint32_t)(uq >> 32);
+          const uint32_t old = atomicAdd(acc_lo + a, wlo);
+          const uint32_t h = whi + (uint32_t)(old + wlo < old);  // + carry of the low word
+          if (h) atomicAdd(acc_hi + a, h);
+        }
       }
     }
     __syncwarp();
   }
   __syncthreads();
   for (int t = threadIdx.x; t < K * 3 * RB; t += blockDim.x) {
-    const int kc = t / RB, r = t % RB;
-    vk[(size_t)kc * N + (size_t)rb * RB + r] =
-        dmul(__ll2double_rn((long long)acc[t]), inv_scale[kc]);
+    const int kc = t / RB, r = t % RB, a = kc * PL + r;
+    const long long q = (long long)(((unsigned long long)acc_hi[a] << 32) | acc_lo[a]);
+    vk[(size_t)kc * N + (size_t)rb * RB + r] = dmul(__ll2double_rn(q), inv_scale[kc]);
   }
 }
 
