@@ -129,18 +129,16 @@ __global__ void __launch_bounds__(kV24Threads) k_transfer_rbcsc(
       const uint32_t q = __ldcs(rk + idx);
       const double v = (double)__ldcs(vals + idx);
       const int r = q & (RB - 1), k = q >> kSh;
+      // branch-free: every product does both word updates (zeros included)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double p = dmul(v, xs[wid][sg][c]);
         const unsigned long long uq =
             (unsigned long long)__double2ll_rn(dmul(p, scale[k * 3 + c]));
-        if (uq) {
-          const int a = (k * 3 + c) * PL + r;
-          const uint32_t wlo = (uint32_t)uq, whi = (uint32_t)(uq >> 32);
-          const uint32_t old = atomicAdd(acc_lo + a, wlo);
-          const uint32_t h = whi + (uint32_t)(old + wlo < old);  // + carry of the low word
-          if (h) atomicAdd(acc_hi + a, h);
-        }
+        const int a = (k * 3 + c) * PL + r;
+        const uint32_t wlo = (uint32_t)uq, whi = (uint32_t)(uq >> 32);
+        const uint32_t old = atomicAdd(acc_lo + a, wlo);
+        atomicAdd(acc_hi + a, whi + (uint32_t)(old + wlo < old));  // + carry of the low word
       }
     }
     __syncwarp();
