@@ -448,13 +448,15 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
  *   value 0, heads one bit per group); the kept bitmap `bits` needs
  *   n_rows / 32 + 1 words with the bit of column n_rows clear (padding entries
  *   then skip their gather). min_blocks = CTAs of 128 threads per SM (register
- *   cap): 4, 6, 8 for 16 entries, 6, 8 for 32. Zeroes vk and accumulates into it. */
+ *   cap): 4, 6, 8 for 16 entries, 6, 8 for 32. Accumulates into vk, zeroing it
+ *   first when zero_vk (else the caller has zeroed it, e.g. on a side stream
+ *   overlapping stage 1). */
 int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* pvals,
                         unsigned long long n_entries, const uint32_t* heads,
                         const uint32_t* head_prefix, const uint32_t* seg_rowk,
                         const unsigned* warp_begin, int n_warps, int min_blocks,
-                        int entries_per_lane, const void* xp, const uint32_t* bits, double* vk,
-                        void* stream);
+                        int entries_per_lane, int zero_vk, const void* xp, const uint32_t* bits,
+                        double* vk, void* stream);
 
 /* sss_flat_align: layout pass over a 16-entries-per-lane flat stream (see
  *   sss_transfer_flat16): inside every 512-entry window (one warp iteration)
@@ -611,6 +613,10 @@ int sss_project_vertices(const double* vertices, int n_vertices, const double* c
  *   caller-zeroed (V, 3). */
 int sss_vertex_colors(const float* radiance, const int32_t* source_vertex, int n, double* colors,
                       void* stream);
+
+/* sss_zero: cudaMemsetAsync(ptr, 0, bytes) on the stream (v_k before an
+ *   accumulating transfer, issued on a side stream that overlaps stage 1). */
+int sss_zero(void* ptr, unsigned long long bytes, void* stream);
 
 /* sss_widen_frame: out (2, n) f64 = (radiance, radiance_unclamped) widened
  *   from the frame's f32 device buffers: the FrameResult arrays (runtime.py:

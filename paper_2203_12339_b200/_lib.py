@@ -50,8 +50,8 @@ _SIGS = {
     "sss_fold_emit": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_transfer_flat8c": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P,
                             _P],
-    "sss_transfer_flat16": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P,
-                            _P],
+    "sss_transfer_flat16": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P,
+                            _P, _P],
     "sss_flat_align": [C.c_uint, C.c_uint, _P, _P, _P, C.c_uint, _P, _P, _P],
     "sss_transfer_rbcsc": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_transfer_pairgroup": [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P],
@@ -89,6 +89,7 @@ _SIGS = {
     "sss_raster_clear": [_I, _I, _D, _D, _D, _P, _P, _P],
     "sss_project_vertices": [_P, _I, _P, _D, _D, _I, _I, _P, _P, _P, _P, _P],
     "sss_vertex_colors": [_P, _P, _I, _P, _P],
+    "sss_zero": [_P, C.c_ulonglong, _P],
     "sss_widen_frame": [_P, _P, C.c_longlong, _P, _P],
     "sss_encode_srgb8": [_P, C.c_longlong, _D, _P, _P],
 }

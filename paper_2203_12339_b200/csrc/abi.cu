@@ -1029,8 +1029,8 @@ int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* p
                         unsigned long long n_entries, const uint32_t* heads,
                         const uint32_t* head_prefix, const uint32_t* seg_rowk,
                         const unsigned* warp_begin, int n_warps, int min_blocks,
-                        int entries_per_lane, const void* xp, const uint32_t* bits, double* vk,
-                        void* stream) {
+                        int entries_per_lane, int zero_vk, const void* xp, const uint32_t* bits,
+                        double* vk, void* stream) {
   const int E = entries_per_lane;
   if (K <= 0 || K > 16 || n_rows <= 0 || !pcols || !pvals || !heads || !head_prefix ||
       !seg_rowk || !warp_begin || !xp || !bits || !vk || n_warps <= 0 || (E != 16 && E != 32) ||
@@ -1039,8 +1039,10 @@ int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* p
   if (reinterpret_cast<uintptr_t>(pcols) % 32 || reinterpret_cast<uintptr_t>(pvals) % 32 ||
       reinterpret_cast<uintptr_t>(xp) % 32)
     return fail(SSS_EINVAL, "transfer_flat16: pcols/pvals/xp must be 32-byte aligned");
-  cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
-  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  if (zero_vk) {
+    cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+    if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  }
   const size_t smem = (size_t)((n_rows >> 5) + 1) * 4;
   const auto* c16 = reinterpret_cast<const unsigned long long*>(pcols);
   const auto* v16 = reinterpret_cast<const unsigned long long*>(pvals);
@@ -1358,6 +1360,13 @@ int sss_vertex_colors(const float* radiance, const int32_t* source_vertex, int n
   if (n == 0) return SSS_OK;
   sss::k_vertex_colors<<<(n + 255) / 256, 256, 0, S_(stream)>>>(radiance, source_vertex, n, colors);
   return check_launch("k_vertex_colors");
+}
+
+int sss_zero(void* ptr, unsigned long long bytes, void* stream) {
+  if (!ptr && bytes) return fail(SSS_EINVAL, "bad zero arguments");
+  cudaError_t e = cudaMemsetAsync(ptr, 0, bytes, S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  return SSS_OK;
 }
 
 int sss_widen_frame(const float* radiance, const float* radiance_unclamped, long long n,

@@ -713,7 +713,8 @@ class Scene:
         pcols, pvals, ne, heads, hpre, rowk, wbeg, W, st = self.transfer.flat16
         _lib.call("sss_transfer_flat16", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
                   _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W,
-                  int(os.environ.get("SSS_FLAT16_MINB", "8")), st["E"], _lib.ptr(self.xp),
+                  int(os.environ.get("SSS_FLAT16_MINB", "8")), st["E"],
+                  0 if getattr(self, "_vk_zeroed", False) else 1, _lib.ptr(self.xp),
                   _lib.ptr(self.xbits16), _lib.ptr(self.vk), sp)
 
     def _rbcsc_core(self, sp):
@@ -787,6 +788,11 @@ class Scene:
         fork.record(cur)
         self._side.wait_event(fork)
         self._launch_weights(self._side)
+        # the default transfer accumulates into a zeroed v_k: zero it here,
+        # overlapping stage 1, instead of on the critical path
+        self._vk_zeroed = self.transfer_kernel == "flat16"
+        if self._vk_zeroed:
+            _lib.call("sss_zero", _lib.ptr(self.vk), self.vk.numel() * 8, _lib.stream_ptr(self._side))
         join.record(self._side)
         self._launch_stage1(cur)
         cur.wait_event(join)
@@ -799,6 +805,7 @@ class Scene:
             self._launch_edit(cur)
         else:
             self._launch_transfer(cur)
+        self._vk_zeroed = False
         self._have_cache = True
 
     def _ambient_active(self) -> bool:
