@@ -297,17 +297,24 @@ def run_ours(a, cfg):
         cpu = cpu_baseline(cfg, scene, dt, g, b, faces, mats, a.cpu_sample_rows, steps=2, warmup=0)
     secondary = None
     if rank == 0 and not a.no_secondary and a.side is None:
-        # the other §8 rows, measured in the same run on the same GPU: C4 sweep
+        # the other §8 rows, measured in the same run on the same GPU: the C2
+        # medium interactive sequence (BASELINE configs[1]), the C4 sweep
         # (HBM-write roofline) and the C5 pair pass (FP32/SFU), one term each mode
         del scene
         torch.cuda.empty_cache()
         sys.path.insert(0, str(ROOT / "tools"))
+        import c2_bench
         import precompute_bench
         import sweep_bench
 
+        c2 = c2_bench.measure(100)
+        torch.cuda.empty_cache()
         c4 = sweep_bench.measure(256, 20)
         c5 = precompute_bench.measure(256, skip_full=True, ks=1)
         secondary = {
+            "c2_medium_interactive": {k: c2[k] for k in (
+                "points", "frames", "operator_nnz", "device_ms_per_frame", "device_points_per_s",
+                "api_ms_per_frame", "api_points_per_s", "frame")},
             "c4_batched_sweep": {"kernel": "k_sweep_umma (tcgen05 bf16 UMMA, fp32 TMEM accum)",
                                  "us": c4["sweep_gemm_us"], "achieved_GBps": c4["achieved_GBps"],
                                  "peak_GBps": c4["peak_GBps"], "frac": c4["frac"],
