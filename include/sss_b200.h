@@ -444,19 +444,21 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
                         void* stream);
 
 /* sss_transfer_flat16: sss_transfer_flat8 with entries_per_lane = 16 or 32
- *   entries per lane (segments padded to a multiple of it with column n_rows /
- *   value 0, heads one bit per group); the kept bitmap `bits` needs
- *   n_rows / 32 + 1 words with the bit of column n_rows clear (padding entries
- *   then skip their gather). min_blocks = CTAs of 128 threads per SM (register
- *   cap): 4, 6, 8 for 16 entries, 6, 8 for 32. Accumulates into vk, zeroing it
- *   first when zero_vk (else the caller has zeroed it, e.g. on a side stream
- *   overlapping stage 1). */
-int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+ *   entries per lane (segments padded to a multiple of it, heads one bit per
+ *   group). col_bits 32: u32 columns, padding entries carry column n_rows /
+ *   value 0 and the kept bitmap `bits` needs n_rows / 32 + 1 words with the bit
+ *   of column n_rows clear (padding skips its gather). col_bits 16 (n_rows <=
+ *   65536, 16 entries per lane): u16 columns, padding keeps column 0 and is
+ *   skipped by its zero value. min_blocks = CTAs of 128 threads per SM (register
+ *   cap): 4, 6, 8 for 16 entries, 6, 8 for 32, 8 for 16-bit columns.
+ *   Accumulates into vk, zeroing it first when zero_vk (else the caller has
+ *   zeroed it, e.g. on a side stream overlapping stage 1). */
+int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals,
                         unsigned long long n_entries, const uint32_t* heads,
                         const uint32_t* head_prefix, const uint32_t* seg_rowk,
                         const unsigned* warp_begin, int n_warps, int min_blocks,
-                        int entries_per_lane, int zero_vk, const void* xp, const uint32_t* bits,
-                        double* vk, void* stream);
+                        int entries_per_lane, int col_bits, int zero_vk, const void* xp,
+                        const uint32_t* bits, double* vk, void* stream);
 
 /* sss_flat_align: layout pass over a 16-entries-per-lane flat stream (see
  *   sss_transfer_flat16): inside every 512-entry window (one warp iteration)

@@ -1025,13 +1025,15 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
   return check_launch("k_transfer_flat8c");
 }
 
-int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* pvals,
+int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals,
                         unsigned long long n_entries, const uint32_t* heads,
                         const uint32_t* head_prefix, const uint32_t* seg_rowk,
                         const unsigned* warp_begin, int n_warps, int min_blocks,
-                        int entries_per_lane, int zero_vk, const void* xp, const uint32_t* bits,
-                        double* vk, void* stream) {
+                        int entries_per_lane, int col_bits, int zero_vk, const void* xp,
+                        const uint32_t* bits, double* vk, void* stream) {
   const int E = entries_per_lane;
+  if ((col_bits != 16 && col_bits != 32) || (col_bits == 16 && (n_rows > 65536 || E != 16)))
+    return fail(SSS_EINVAL, "transfer_flat16: col_bits 32, or 16 with n_rows <= 65536 and E 16");
   if (K <= 0 || K > 16 || n_rows <= 0 || !pcols || !pvals || !heads || !head_prefix ||
       !seg_rowk || !warp_begin || !xp || !bits || !vk || n_warps <= 0 || (E != 16 && E != 32) ||
       n_warps % (sss::kV25Threads / 32) || n_entries % E || n_entries / E >= (1ull << 32) - 64)
@@ -1055,6 +1057,13 @@ int sss_transfer_flat16(int K, int n_rows, const uint32_t* pcols, const float* p
     sss::k_transfer_flat16<MB, EE><<<grid, sss::kV25Threads, smem, S_(stream)>>>(                \
         n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);           \
     return check_launch("k_transfer_flat16");                                                    \
+  }
+  if (col_bits == 16) {
+    if (min_blocks != 8) return fail(SSS_EINVAL, "transfer_flat16: 16-bit columns use min_blocks 8");
+    if (int r = set_smem((const void*)sss::k_transfer_flat16<8, 16, true>, smem)) return r;
+    sss::k_transfer_flat16<8, 16, true><<<grid, sss::kV25Threads, smem, S_(stream)>>>(
+        n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);
+    return check_launch("k_transfer_flat16");
   }
   SSS_V25(4, 16) SSS_V25(6, 16) SSS_V25(8, 16) SSS_V25(8, 32) SSS_V25(6, 32)
 #undef SSS_V25

@@ -13,42 +13,53 @@ namespace sss {
 
 constexpr int kV25Threads = 128;
 
+template <bool COL16>
 struct V25Slot {
-  unsigned long long c[8];  // 16 u32 columns
-  unsigned long long v[8];  // 16 f32 values
+  unsigned long long c[COL16 ? 4 : 8];  // 16 u16 or u32 columns
+  unsigned long long v[8];              // 16 f32 values
   uint32_t h, hp;
 };
 
 // group q = i * 32 + lane of G = E / 16 sub-slots; sub-slot j of the group is
 // the 16 entries at (q * G + j) * 16
-__device__ __forceinline__ void v25_load(V25Slot& S, size_t q, unsigned ngroups, int G, int j,
-                                         const unsigned long long* __restrict__ C16,
+template <bool COL16>
+__device__ __forceinline__ void v25_load(V25Slot<COL16>& S, size_t q, unsigned ngroups, int G,
+                                         int j, const unsigned long long* __restrict__ C16,
                                          const unsigned long long* __restrict__ V16) {
+  constexpr int NC = COL16 ? 4 : 8;
   if (q >= ngroups) {  // past the stream's last group (partial last word)
 #pragma unroll
-    for (int t = 0; t < 8; ++t) S.c[t] = S.v[t] = 0ull;
+    for (int t = 0; t < NC; ++t) S.c[t] = 0ull;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) S.v[t] = 0ull;
     return;
   }
   q = q * G + j;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NC / 4; ++h)
     asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
                  : "=l"(S.c[4 * h]), "=l"(S.c[4 * h + 1]), "=l"(S.c[4 * h + 2]), "=l"(S.c[4 * h + 3])
-                 : "l"(C16 + 8 * q + 4 * h));
+                 : "l"(C16 + NC * q + 4 * h));
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
     asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
                  : "=l"(S.v[4 * h]), "=l"(S.v[4 * h + 1]), "=l"(S.v[4 * h + 2]), "=l"(S.v[4 * h + 3])
                  : "l"(V16 + 8 * q + 4 * h));
-  }
 }
 
-__device__ __forceinline__ uint32_t v25_col(const V25Slot& S, int e) {
+template <bool COL16>
+__device__ __forceinline__ uint32_t v25_col(const V25Slot<COL16>& S, int e) {
+  if (COL16) return (uint32_t)(S.c[e >> 2] >> (16 * (e & 3))) & 0xffffu;
   return (uint32_t)(S.c[e >> 1] >> (32 * (e & 1)));
 }
-__device__ __forceinline__ float v25_val(const V25Slot& S, int e) {
+template <bool COL16>
+__device__ __forceinline__ float v25_val(const V25Slot<COL16>& S, int e) {
   return __uint_as_float((uint32_t)(S.v[e >> 1] >> (32 * (e & 1))));
 }
 
-template <int MINB, int E = 16>
+// COL16: 16-bit columns (n <= 65536; 6 bytes per entry instead of 8);
+// padding entries then keep column 0 and are skipped by their zero value
+template <int MINB, int E = 16, bool COL16 = false>
 __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
     int N, unsigned ngroups, const unsigned long long* __restrict__ C16,
     const unsigned long long* __restrict__ V16,
@@ -66,25 +77,26 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
   const unsigned upto = (2u << lane) - 1u;
 #pragma unroll 1
   for (unsigned i = i0; i < i1; ++i) {
-    V25Slot S;
+    V25Slot<COL16> S;
     S.h = __ldg(&H[i]);
     S.hp = __ldg(&hpre[i]);
     double p0 = 0.0, p1 = 0.0, p2 = 0.0;
 #pragma unroll 1
     for (int j = 0; j < G; ++j) {
-      v25_load(S, (size_t)i * 32u + (unsigned)lane, ngroups, G, j, C16, V16);
+      v25_load<COL16>(S, (size_t)i * 32u + (unsigned)lane, ngroups, G, j, C16, V16);
 #pragma unroll
       for (int qd = 0; qd < 4; ++qd) {
         double x[4][3];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint32_t c = v25_col(S, qd * 4 + e);
+          const uint32_t c = v25_col<COL16>(S, qd * 4 + e);
           x[e][0] = x[e][1] = x[e][2] = 0.0;
-          if ((v25_bits[c >> 5] >> (c & 31u)) & 1u) v15_gather1(xp, c, x[e]);
+          const bool live = COL16 ? v25_val<COL16>(S, qd * 4 + e) != 0.0f : true;
+          if (live && ((v25_bits[c >> 5] >> (c & 31u)) & 1u)) v15_gather1(xp, c, x[e]);
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const double v = (double)v25_val(S, qd * 4 + e);
+          const double v = (double)v25_val<COL16>(S, qd * 4 + e);
           p0 = fma(v, x[e][0], p0);
           p1 = fma(v, x[e][1], p1);
           p2 = fma(v, x[e][2], p2);

@@ -439,15 +439,23 @@ class Scene:
                 pcols, pvals = lay[0], lay[1]
                 # padding entries (value 0) point at column n, whose kept bit
                 # is always clear: they skip the gather instead of loading x[0]
-                pcols = torch.where(pvals == 0, torch.full_like(pcols, self.n), pcols)
-                aligned = E == 16 and os.environ.get("SSS_FLAT16_ALIGN", "0") == "1"
+                col16 = (E == 16 and self.n <= 65536 and
+                         os.environ.get("SSS_FLAT16_COL16", "1") == "1")
+                if not col16:
+                    pcols = torch.where(pvals == 0, torch.full_like(pcols, self.n), pcols)
+                aligned = (not col16 and E == 16 and
+                           os.environ.get("SSS_FLAT16_ALIGN", "0") == "1")
                 if aligned:  # duplicate columns of a warp iteration share a slot
                     c2, v2 = torch.empty_like(pcols), torch.empty_like(pvals)
                     _lib.call("sss_flat_align", lay[3].numel(), lay[2] // 16, _lib.ptr(pcols),
                               _lib.ptr(pvals),
                               _lib.ptr(lay[3]), self.n, _lib.ptr(c2), _lib.ptr(v2), sp)
                     pcols, pvals = c2, v2
-                t.flat16 = (pcols, pvals) + tuple(lay[2:-1]) + (dict(lay[-1], E=E, aligned=aligned),)
+                if col16:  # 16-bit columns: 6 bytes per entry (padding stays column 0)
+                    pcols = (pcols.to(torch.int32) & 0xFFFF).to(torch.int32)
+                    pcols = torch.where(pcols >= 32768, pcols - 65536, pcols).to(torch.int16)
+                t.flat16 = (pcols, pvals) + tuple(lay[2:-1]) + (
+                    dict(lay[-1], E=E, aligned=aligned, col_bits=16 if col16 else 32),)
             if getattr(self, "xp", None) is None:
                 self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
             if getattr(self, "xbits16", None) is None:  # + one always-clear word
@@ -713,7 +721,7 @@ class Scene:
         pcols, pvals, ne, heads, hpre, rowk, wbeg, W, st = self.transfer.flat16
         _lib.call("sss_transfer_flat16", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
                   _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W,
-                  int(os.environ.get("SSS_FLAT16_MINB", "8")), st["E"],
+                  int(os.environ.get("SSS_FLAT16_MINB", "8")), st["E"], st["col_bits"],
                   0 if getattr(self, "_vk_zeroed", False) else 1, _lib.ptr(self.xp),
                   _lib.ptr(self.xbits16), _lib.ptr(self.vk), sp)
 
