@@ -251,7 +251,7 @@ def run_ours(a, cfg):
     # ---- e2e: public API, host cubemap in, host radiance out
     from paper_2203_12339_b200.runtime import EnvLight
 
-    n_e2e = min(a.steps, 30)
+    n_e2e = min(a.steps, 100)
     # one untimed API frame first: allocates the pinned read-back buffers and
     # warms the host conversion path (as W warm-up steps do for the device loop)
     scene.set_light(EnvLight(faces[0]))
