@@ -354,7 +354,7 @@ def run_ours(a, cfg):
             "e2e": e2e,
             # per relight: env_project, env_union, env_irradiance, select, weights,
             # pack_x_bits, transfer, edit_finish; per edit: weights, edit_finish
-            "gpu_launches": 8 * a.steps + 2 * n_edit,
+            "gpu_launches": 7 * a.steps + 2 * n_edit,
             "clocks": clk,
             "relight_ms": relight_ms, "edit_ms": edit_ms,
             "cpu_baseline": cpu,

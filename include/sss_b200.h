@@ -71,6 +71,14 @@ int sss_env_irradiance(const float* W2, int D, const uint32_t* union_idx,
                        const double* union_lc, const int* n_union, int n_keep, int side,
                        int levels, double* E_out, double* ehat, void* stream);
 
+/* sss_env_irradiance_sel: sss_env_irradiance with the union built inside
+ *   every CTA from sss_env_project's per-channel kept lists (sel_idx (3, n_keep)
+ *   u32, 0xffffffff-padded; sel_val (3, n_keep) f64) instead of k_env_union's
+ *   output: same E and spectrum bits, one launch less per frame. D = 6 s^2 <= 6144. */
+int sss_env_irradiance_sel(const float* W2, int D, const uint32_t* sel_idx, const double* sel_val,
+                           int n_keep, int side, int levels, double* E_out, double* ehat,
+                           void* stream);
+
 /* ---- env transfer precompute: W[i, d] = V F_t cos+ d_omega with V = 1,
  *      eta = 1 (visibility_weights, lighting.py:318-329), per-face full Haar
  *      (fold_visibility's w2, transfer.py:407-411), stored float32 (D, N).

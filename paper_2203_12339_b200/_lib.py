@@ -25,6 +25,7 @@ _SIGS = {
     "sss_sh_irradiance": [_P, _P, _I, _I, _I, _P, _P, _P],
     "sss_env_project": [_P, _I, _I, _P, _P, _P, _P, _P, _P],
     "sss_env_irradiance": [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P, _P],
+    "sss_env_irradiance_sel": [_P, _I, _P, _P, _I, _I, _I, _P, _P, _P],
     "sss_env_transfer": [_P, _I, _P, _P, _I, _P, _P],
     "sss_material_weights": [_P, _P, _I, _I, _P, _P, _P],
     "sss_transfer_relight": [_I, _I, _I, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],

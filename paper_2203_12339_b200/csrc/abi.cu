@@ -173,6 +173,26 @@ int sss_env_irradiance(const float* W2, int D, const uint32_t* union_idx, const 
   return check_launch("k_env_irradiance_multi");
 }
 
+int sss_env_irradiance_sel(const float* W2, int D, const uint32_t* sel_idx, const double* sel_val,
+                           int n_keep, int side, int levels, double* E_out, double* ehat,
+                           void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (!W2 || !sel_idx || !sel_val || !ehat || n_keep <= 0 || D <= 0 || D > 6 * 32 * 32)
+    return fail(SSS_EINVAL, "bad env_irradiance_sel arguments");
+  const int T = 1 << levels, T2 = T * T;
+  const char* tpb_env = getenv("SSS_ENV_TPB");
+  int tpb = tpb_env ? atoi(tpb_env) : (T * 4 <= side ? 4 : 1);
+  if (tpb < 1 || (side / T) % tpb) tpb = 1;
+  const int tiles = (side / T) * (side / T);
+  const size_t nw = (size_t)(D + 31) / 32;
+  const size_t smem = 6 * (size_t)tpb * T2 * sizeof(double) + 12 * (size_t)n_keep * sizeof(double) +
+                      3 * (size_t)n_keep * sizeof(int) + 2 * nw * sizeof(uint32_t);
+  if (int r = set_smem((const void*)sss::k_env_irradiance_multi, smem)) return r;
+  sss::k_env_irradiance_multi<<<tiles / tpb, tpb * T2 < 32 ? 32 : tpb * T2, smem, S_(stream)>>>(
+      W2, nullptr, nullptr, nullptr, n_keep, side, levels, tpb, E_out, ehat, sel_idx, sel_val, D);
+  return check_launch("k_env_irradiance_multi");
+}
+
 int sss_env_transfer(const float* normals, int n_points, const double* dirs, const double* dom,
                      int env_side, float* W2, void* stream) {
   if (!pow2(env_side) || env_side > 64 || n_points <= 0 || !normals || !dirs || !dom || !W2)

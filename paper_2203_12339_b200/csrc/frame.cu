@@ -359,25 +359,74 @@ __device__ __forceinline__ void scatter_ehat(const double* a, int T, int TPB, in
   }
 }
 
+// union_idx != nullptr: the ascending union of the three channels' kept w2
+// ids and their per-channel values come from k_env_union. union_idx ==
+// nullptr: every CTA builds the same union itself from the per-channel kept
+// lists sel_idx / sel_val (3 x n_keep, k_env_project's output): flags over the
+// D ids, a word prefix, each kept id's rank = its union position (ascending),
+// the value of a channel that dropped the id = 0 (k_env_union's rule).
 __global__ void k_env_irradiance_multi(const float* __restrict__ W2,
                                        const uint32_t* __restrict__ union_idx,
                                        const double* __restrict__ union_lc,
                                        const int* __restrict__ n_union, int n_keep, int S, int L,
                                        int TPB, double* __restrict__ E_out,
-                                       double* __restrict__ ehat) {
+                                       double* __restrict__ ehat,
+                                       const uint32_t* __restrict__ sel_idx = nullptr,
+                                       const double* __restrict__ sel_val = nullptr, int D = 0) {
   extern __shared__ double sm[];
+  __shared__ int s_m;
   const int T = 1 << L, T2 = T * T, N = S * S, tpr = S / T;
   double* a = sm;                       // TPB * 3 * T2
   double* tmp = a + TPB * 3 * T2;       // TPB * 3 * T2
   double* lc = tmp + TPB * 3 * T2;      // 3 n_keep x 4 (l0, l1, l2, 0): one 16-B + one 8-B LDS
   int* ul = reinterpret_cast<int*>(lc + 12 * n_keep);
-  const int m = *n_union;
-  for (int q = threadIdx.x; q < m; q += blockDim.x) {
-    ul[q] = (int)union_idx[q];
-    lc[q * 4] = union_lc[q * 3]; lc[q * 4 + 1] = union_lc[q * 3 + 1];
-    lc[q * 4 + 2] = union_lc[q * 3 + 2]; lc[q * 4 + 3] = 0.0;
+  if (union_idx) {
+    const int mm = *n_union;
+    for (int q = threadIdx.x; q < mm; q += blockDim.x) {
+      ul[q] = (int)union_idx[q];
+      lc[q * 4] = union_lc[q * 3]; lc[q * 4 + 1] = union_lc[q * 3 + 1];
+      lc[q * 4 + 2] = union_lc[q * 3 + 2]; lc[q * 4 + 3] = 0.0;
+    }
+    if (threadIdx.x == 0) s_m = mm;
+  } else {
+    const int nw = (D + 31) >> 5;
+    uint32_t* flag = reinterpret_cast<uint32_t*>(ul + 3 * n_keep);
+    uint32_t* wpre = flag + nw;
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) flag[w] = 0u;
+    for (int q = threadIdx.x; q < 12 * n_keep; q += blockDim.x) lc[q] = 0.0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < 3 * n_keep; e += blockDim.x) {
+      const uint32_t id = sel_idx[e];
+      if (id < (uint32_t)D) atomicOr(&flag[id >> 5], 1u << (id & 31u));
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive word prefix (<= 32 words per lane)
+      const int lane = threadIdx.x, per = (nw + 31) >> 5;
+      const int w0 = lane * per, w1 = min(w0 + per, nw);
+      int cnt = 0;
+      for (int w = w0; w < w1; ++w) cnt += __popc(flag[w]);
+      int inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      int run = inc - cnt;
+      for (int w = w0; w < w1; ++w) { wpre[w] = (uint32_t)run; run += __popc(flag[w]); }
+      if (lane == 31) s_m = inc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 3 * n_keep; e += blockDim.x) {
+      const uint32_t id = sel_idx[e];
+      if (id >= (uint32_t)D) continue;
+      const int c = e / n_keep;
+      const int pos = (int)(wpre[id >> 5] + __popc(flag[id >> 5] & ((1u << (id & 31u)) - 1u)));
+      ul[pos] = (int)id;
+      lc[pos * 4 + c] = sel_val[e];
+    }
   }
   __syncthreads();
+  const int m = s_m;
   const int tile0 = blockIdx.x * TPB;
   for (int q = threadIdx.x; q < TPB * T2; q += blockDim.x) {
     // the CTA's TPB tiles are horizontally adjacent: consecutive threads walk

@@ -327,12 +327,19 @@ class Scene:
                       _lib.ptr(self.ehat), sp)
         else:
             s, kk = self._light_kind[1], self.env_keep
-            _lib.call("sss_env_project", _lib.ptr(self.light_buf), s, kk, _lib.ptr(self.env_idx),
-                      _lib.ptr(self.env_val), _lib.ptr(self.env_uidx), _lib.ptr(self.env_ulc),
-                      _lib.ptr(self.env_nu), sp)
-            _lib.call("sss_env_irradiance", _lib.ptr(self.W2), 6 * s * s, _lib.ptr(self.env_uidx),
-                      _lib.ptr(self.env_ulc), _lib.ptr(self.env_nu), kk, self.side, self.levels,
-                      _lib.ptr(E), _lib.ptr(self.ehat), sp)
+            if os.environ.get("SSS_ENV_UNION_KERNEL", "0") == "1":  # separate union launch
+                _lib.call("sss_env_project", _lib.ptr(self.light_buf), s, kk,
+                          _lib.ptr(self.env_idx), _lib.ptr(self.env_val), _lib.ptr(self.env_uidx),
+                          _lib.ptr(self.env_ulc), _lib.ptr(self.env_nu), sp)
+                _lib.call("sss_env_irradiance", _lib.ptr(self.W2), 6 * s * s,
+                          _lib.ptr(self.env_uidx), _lib.ptr(self.env_ulc), _lib.ptr(self.env_nu),
+                          kk, self.side, self.levels, _lib.ptr(E), _lib.ptr(self.ehat), sp)
+            else:  # the union is rebuilt inside every irradiance CTA: one launch less
+                _lib.call("sss_env_project", _lib.ptr(self.light_buf), s, kk,
+                          _lib.ptr(self.env_idx), _lib.ptr(self.env_val), None, None, None, sp)
+                _lib.call("sss_env_irradiance_sel", _lib.ptr(self.W2), 6 * s * s,
+                          _lib.ptr(self.env_idx), _lib.ptr(self.env_val), kk, self.side,
+                          self.levels, _lib.ptr(E), _lib.ptr(self.ehat), sp)
         keep = max(1, int(round(self.e_keep * self.n)))  # runtime.py:112
         _lib.call("sss_select_topn", _lib.ptr(self.ehat), 3, self.n, keep, _lib.ptr(self.f2t),
                   _lib.ptr(self.x), _lib.ptr(self.mask), _lib.ptr(self.energy), sp)

@@ -681,3 +681,21 @@ def test_frame_result_arrays_survive_later_frames(c1):
     del keep_view
     gc.collect()
     assert sc._pool.out == out0 - 1
+
+
+def test_env_union_fused_equals_union_kernel(c1, monkeypatch):
+    """The environment union rebuilt inside every irradiance CTA
+    (sss_env_irradiance_sel, default) gives the same E spectrum bits as the
+    separate k_env_union launch."""
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import EnvLight
+
+    env = LT.Environment(side=16, seed=12)
+    sc = _scene(c1, EnvLight(env.faces(21.0)))
+    sc._launch_stage1(want_E=True)
+    torch.cuda.synchronize()
+    e_fused, h_fused = sc.E.clone(), sc.ehat.clone()
+    monkeypatch.setenv("SSS_ENV_UNION_KERNEL", "1")
+    sc._launch_stage1(want_E=True)
+    torch.cuda.synchronize()
+    assert torch.equal(sc.E, e_fused) and torch.equal(sc.ehat, h_fused)

@@ -51,6 +51,9 @@ def main():
     out["env_project+union"] = timed(lambda: _lib.call(
         "sss_env_project", _lib.ptr(sc.light_buf), s, kk, _lib.ptr(sc.env_idx), _lib.ptr(sc.env_val),
         _lib.ptr(sc.env_uidx), _lib.ptr(sc.env_ulc), _lib.ptr(sc.env_nu), sp), a.reps)
+    out["env_irradiance_sel+haar"] = timed(lambda: _lib.call(
+        "sss_env_irradiance_sel", _lib.ptr(sc.W2), 6 * s * s, _lib.ptr(sc.env_idx),
+        _lib.ptr(sc.env_val), kk, sc.side, sc.levels, None, _lib.ptr(sc.ehat), sp), a.reps)
     out["env_irradiance+haar"] = timed(lambda: _lib.call(
         "sss_env_irradiance", _lib.ptr(sc.W2), 6 * s * s, _lib.ptr(sc.env_uidx), _lib.ptr(sc.env_ulc),
         _lib.ptr(sc.env_nu), kk, sc.side, sc.levels, None, _lib.ptr(sc.ehat), sp), a.reps)
