@@ -456,8 +456,8 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
  *   group). col_bits 32: u32 columns, padding entries carry column n_rows /
  *   value 0 and the kept bitmap `bits` needs n_rows / 32 + 1 words with the bit
  *   of column n_rows clear (padding skips its gather). col_bits 16 (n_rows <=
- *   65536, 16 entries per lane): u16 columns, padding keeps column 0 and is
- *   skipped by its zero value. min_blocks = CTAs of 128 threads per SM (register
+ *   65536, 16 entries per lane): u16 columns, padding keeps column 0 with
+ *   value 0 (its gather, if column 0 is kept, shares one address per instruction). min_blocks = CTAs of 128 threads per SM (register
  *   cap): 4, 6, 8 for 16 entries, 6, 8 for 32, 8 for 16-bit columns.
  *   Accumulates into vk, zeroing it first when zero_vk (else the caller has
  *   zeroed it, e.g. on a side stream overlapping stage 1). */

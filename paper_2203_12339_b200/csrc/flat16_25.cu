@@ -58,7 +58,7 @@ __device__ __forceinline__ float v25_val(const V25Slot<COL16>& S, int e) {
 }
 
 // COL16: 16-bit columns (n <= 65536; 6 bytes per entry instead of 8);
-// padding entries then keep column 0 and are skipped by their zero value
+// padding entries then keep column 0 with value 0
 template <int MINB, int E = 16, bool COL16 = false>
 __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
     int N, unsigned ngroups, const unsigned long long* __restrict__ C16,
@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
         for (int e = 0; e < 4; ++e) {
           const uint32_t c = v25_col<COL16>(S, qd * 4 + e);
           x[e][0] = x[e][1] = x[e][2] = 0.0;
-          const bool live = COL16 ? v25_val<COL16>(S, qd * 4 + e) != 0.0f : true;
-          if (live && ((v25_bits[c >> 5] >> (c & 31u)) & 1u)) v15_gather1(xp, c, x[e]);
+          // padding entries (value 0, column 0 with u16 columns) may gather
+          // x[0]: all such lanes of an instruction share that one address
+          if ((v25_bits[c >> 5] >> (c & 31u)) & 1u) v15_gather1(xp, c, x[e]);
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
