@@ -780,7 +780,13 @@ class Scene:
         if self.transfer_kernel == "rbcsc":
             return self._rbcsc_core(_lib.stream_ptr(stream))
         if self.transfer_kernel == "flat16":
-            return self._flat16_core(_lib.stream_ptr(stream))
+            # the kernel alone: in a frame v_k is zeroed on the side stream,
+            # overlapping stage 1, so the memset is not part of its launch
+            self._vk_zeroed = True
+            try:
+                return self._flat16_core(_lib.stream_ptr(stream))
+            finally:
+                self._vk_zeroed = False
         if self.transfer_kernel not in ("flat", "flat8"):
             return self._launch_transfer(stream, epilogue=False)
         self._flat_core(_lib.stream_ptr(stream))
