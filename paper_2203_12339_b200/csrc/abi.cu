@@ -109,6 +109,9 @@ int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, const uint
     // one 8-CTA cluster per vector, slices resident in shared memory
     const size_t smem = ((sizeof(sss::ClusterSelShared) + 15) & ~size_t(15)) + chunk * sizeof(double);
     if (int r = set_smem((const void*)sss::k_select_cluster, smem)) return r;
+    if (sss::kSelCluster > 8)
+      cudaFuncSetAttribute((const void*)sss::k_select_cluster,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     sss::k_select_cluster<<<nvec * sss::kSelCluster, 1024, smem, S_(stream)>>>(
         v, n_dom, n_keep, chunk, f2t, x_out, mask, energy);
     return check_launch("k_select_cluster");
