@@ -167,6 +167,61 @@ __device__ unsigned long long g_env_trace[16];
   } while (0)
 #endif
 
+// batch_tile_haar_fwd for the cubemap faces with the small levels (s <= 8)
+// done by one warp per face under __syncwarp: the same arithmetic, six block
+// barriers fewer (the pass count, not the work, bounds this transform)
+__device__ inline void env_faces_haar_fwd(double* a, double* tmp, int T, int B) {
+  constexpr int kTail = 8;
+  const int T2 = T * T, nt = blockDim.x, tid = threadIdx.x;
+  int s = T;
+  for (; s > kTail; s >>= 1) {
+    const int h = s >> 1, lh = ilog2i(h), lsh = ilog2i(s * h);
+    for (int q = tid; q < (B << lsh); q += nt) {
+      const int b = q >> lsh, e = q & ((1 << lsh) - 1);
+      const int i = e >> lh, j = e & (h - 1);
+      const double* g = a + b * T2;
+      double* o = tmp + b * T2;
+      const double ev = g[i * T + 2 * j], od = g[i * T + 2 * j + 1];
+      o[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+      o[i * T + h + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+    }
+    __syncthreads();
+    for (int q = tid; q < (B << lsh); q += nt) {
+      const int b = q >> lsh, e = q & ((1 << lsh) - 1);
+      const int i = e >> (lh + 1), j = e & (2 * h - 1);  // j (of s) fastest: no bank conflicts
+      const double* g = tmp + b * T2;
+      double* o = a + b * T2;
+      const double ev = g[(2 * i) * T + j], od = g[(2 * i + 1) * T + j];
+      o[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+      o[(h + i) * T + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+    }
+    __syncthreads();
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  if (warp < B) {
+    double* g = a + warp * T2;
+    double* o = tmp + warp * T2;
+    for (; s >= 2; s >>= 1) {
+      const int h = s >> 1;
+      for (int q = lane; q < s * h; q += 32) {
+        const int i = q / h, j = q % h;
+        const double ev = g[i * T + 2 * j], od = g[i * T + 2 * j + 1];
+        o[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+        o[i * T + h + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+      }
+      __syncwarp();
+      for (int q = lane; q < s * h; q += 32) {
+        const int i = q / s, j = q % s;
+        const double ev = o[(2 * i) * T + j], od = o[(2 * i + 1) * T + j];
+        g[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
+        g[(h + i) * T + j] = dmul(dsub(ev, od), SSS_ISQRT2);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void k_env_project(const double* __restrict__ faces, int s, int n_keep,
                               uint32_t* __restrict__ idx_out, double* __restrict__ val_out,
                               double* __restrict__ energy) {
@@ -179,7 +234,7 @@ __global__ void k_env_project(const double* __restrict__ faces, int s, int n_kee
   for (int e = threadIdx.x; e < D; e += blockDim.x) a[e] = faces[(size_t)e * 3 + c];
   __syncthreads();
   ENV_TRACE(1);
-  batch_tile_haar_fwd(a, tmp, s, 6);
+  env_faces_haar_fwd(a, tmp, s, 6);
   ENV_TRACE(2);
   const int n = min(n_keep, D);
   SelectResult sel;

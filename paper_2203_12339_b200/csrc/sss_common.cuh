@@ -75,7 +75,7 @@ __device__ inline void tile_haar_fwd(double* a, double* tmp, int T, int nthreads
     }
     __syncthreads();
     for (int e = tid; e < s * h; e += nthreads) {  // columns tmp -> a
-      const int j = e >> lh, i = e & (h - 1);
+      const int i = e >> (lh + 1), j = e & (2 * h - 1);  // j (of s) fastest: no bank conflicts
       const double ev = tmp[(2 * i) * T + j], od = tmp[(2 * i + 1) * T + j];
       a[i * T + j] = dmul(dadd(ev, od), SSS_ISQRT2);
       a[(h + i) * T + j] = dmul(dsub(ev, od), SSS_ISQRT2);
@@ -90,7 +90,7 @@ __device__ inline void tile_haar_inv(double* a, double* tmp, int T, int nthreads
   for (int s = 2; s <= T; s <<= 1) {
     const int h = s >> 1, lh = ilog2i(h);
     for (int e = tid; e < s * h; e += nthreads) {  // columns a -> tmp
-      const int j = e >> lh, i = e & (h - 1);
+      const int i = e >> (lh + 1), j = e & (2 * h - 1);  // j (of s) fastest: no bank conflicts
       const double lo = a[i * T + j], hi = a[(h + i) * T + j];
       tmp[(2 * i) * T + j] = dmul(dadd(lo, hi), SSS_ISQRT2);
       tmp[(2 * i + 1) * T + j] = dmul(dsub(lo, hi), SSS_ISQRT2);
@@ -124,7 +124,7 @@ __device__ inline void batch_tile_haar_fwd(double* a, double* tmp, int T, int B)
     __syncthreads();
     for (int q = tid; q < (B << lsh); q += nt) {
       const int b = q >> lsh, e = q & ((1 << lsh) - 1);
-      const int j = e >> lh, i = e & (h - 1);
+      const int i = e >> (lh + 1), j = e & (2 * h - 1);  // j (of s) fastest: no bank conflicts
       const double* g = tmp + b * T2;
       double* o = a + b * T2;
       const double ev = g[(2 * i) * T + j], od = g[(2 * i + 1) * T + j];
@@ -143,7 +143,7 @@ __device__ inline void batch_tile_haar_inv(double* a, double* tmp, int T, int B)
     const int h = s >> 1, lh = ilog2i(h), lsh = ilog2i(s * h);
     for (int q = tid; q < (B << lsh); q += nt) {
       const int b = q >> lsh, e = q & ((1 << lsh) - 1);
-      const int j = e >> lh, i = e & (h - 1);
+      const int i = e >> (lh + 1), j = e & (2 * h - 1);  // j (of s) fastest: no bank conflicts
       const double* g = a + b * T2;
       double* o = tmp + b * T2;
       const double lo = g[i * T + j], hi = g[(h + i) * T + j];
