@@ -7,6 +7,8 @@ extern "C" int select_trace(const double* v, int nvec, int n_dom, int n_keep, co
   const int chunk = (((n_dom + sss::kSelCluster - 1) / sss::kSelCluster) + 31) / 32 * 32;
   const size_t smem = ((sizeof(sss::ClusterSelShared) + 15) & ~size_t(15)) + chunk * sizeof(double);
   cudaFuncSetAttribute(sss::k_select_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (sss::kSelCluster > 8)
+    cudaFuncSetAttribute(sss::k_select_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaMemset(mask, 0, (size_t)nvec * ((n_dom + 31) / 32) * 4);
   unsigned long long zero[32] = {0};
   cudaMemcpyToSymbol(sss::g_sel_trace, zero, sizeof(zero));
