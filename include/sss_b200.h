@@ -460,13 +460,17 @@ int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals
  *   value 0 (its gather, if column 0 is kept, shares one address per instruction). min_blocks = CTAs of 128 threads per SM (register
  *   cap): 4, 6, 8 for 16 entries, 6, 8 for 32, 8 for 16-bit columns.
  *   Accumulates into vk, zeroing it first when zero_vk (else the caller has
- *   zeroed it, e.g. on a side stream overlapping stage 1). */
+ *   zeroed it, e.g. on a side stream overlapping stage 1). work_counter (u32,
+ *   nullable): warps claim `chunk` words at a time from it instead of their
+ *   static ranges (load balance); it must be zero at launch (zeroed here with
+ *   vk when zero_vk). */
 int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals,
                         unsigned long long n_entries, const uint32_t* heads,
                         const uint32_t* head_prefix, const uint32_t* seg_rowk,
                         const unsigned* warp_begin, int n_warps, int min_blocks,
                         int entries_per_lane, int col_bits, int zero_vk, const void* xp,
-                        const uint32_t* bits, double* vk, void* stream);
+                        const uint32_t* bits, double* vk, uint32_t* work_counter, int chunk,
+                        void* stream);
 
 /* sss_flat_align: layout pass over a 16-entries-per-lane flat stream (see
  *   sss_transfer_flat16): inside every 512-entry window (one warp iteration)

@@ -52,7 +52,7 @@ _SIGS = {
     "sss_transfer_flat8c": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P,
                             _P],
     "sss_transfer_flat16": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P,
-                            _P, _P, _P],
+                            _P, _P, _P, _I, _P],
     "sss_flat_align": [C.c_uint, C.c_uint, _P, _P, _P, C.c_uint, _P, _P, _P],
     "sss_transfer_rbcsc": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_transfer_pairgroup": [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P],

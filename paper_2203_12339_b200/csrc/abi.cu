@@ -1053,7 +1053,8 @@ int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals
                         const uint32_t* head_prefix, const uint32_t* seg_rowk,
                         const unsigned* warp_begin, int n_warps, int min_blocks,
                         int entries_per_lane, int col_bits, int zero_vk, const void* xp,
-                        const uint32_t* bits, double* vk, void* stream) {
+                        const uint32_t* bits, double* vk, uint32_t* work_counter, int chunk,
+                        void* stream) {
   const int E = entries_per_lane;
   if ((col_bits != 16 && col_bits != 32) || (col_bits == 16 && (n_rows > 65536 || E != 16)))
     return fail(SSS_EINVAL, "transfer_flat16: col_bits 32, or 16 with n_rows <= 65536 and E 16");
@@ -1066,8 +1067,11 @@ int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals
     return fail(SSS_EINVAL, "transfer_flat16: pcols/pvals/xp must be 32-byte aligned");
   if (zero_vk) {
     cudaError_t e = cudaMemsetAsync(vk, 0, (size_t)K * 3 * n_rows * sizeof(double), S_(stream));
+    if (e == cudaSuccess && work_counter)
+      e = cudaMemsetAsync(work_counter, 0, sizeof(uint32_t), S_(stream));
     if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
   }
+  if (chunk < 1) chunk = 1;
   const size_t smem = (size_t)((n_rows >> 5) + 1) * 4;
   const auto* c16 = reinterpret_cast<const unsigned long long*>(pcols);
   const auto* v16 = reinterpret_cast<const unsigned long long*>(pvals);
@@ -1078,14 +1082,16 @@ int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals
   if (min_blocks == MB && E == EE) {                                                             \
     if (int r = set_smem((const void*)sss::k_transfer_flat16<MB, EE>, smem)) return r;           \
     sss::k_transfer_flat16<MB, EE><<<grid, sss::kV25Threads, smem, S_(stream)>>>(                \
-        n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);           \
+        n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk,            \
+        work_counter, chunk);                                                                    \
     return check_launch("k_transfer_flat16");                                                    \
   }
   if (col_bits == 16) {
     if (min_blocks != 8) return fail(SSS_EINVAL, "transfer_flat16: 16-bit columns use min_blocks 8");
     if (int r = set_smem((const void*)sss::k_transfer_flat16<8, 16, true>, smem)) return r;
     sss::k_transfer_flat16<8, 16, true><<<grid, sss::kV25Threads, smem, S_(stream)>>>(
-        n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk);
+        n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk,
+        work_counter, chunk);
     return check_launch("k_transfer_flat16");
   }
   SSS_V25(4, 16) SSS_V25(6, 16) SSS_V25(8, 16) SSS_V25(8, 32) SSS_V25(6, 32)

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
     const unsigned long long* __restrict__ V16,
     const uint32_t* __restrict__ H, const uint32_t* __restrict__ hpre,
     const uint32_t* __restrict__ rowk, const unsigned* __restrict__ warp_begin,
-    const double4* __restrict__ xp, const uint32_t* __restrict__ bits, double* __restrict__ vk) {
+    const double4* __restrict__ xp, const uint32_t* __restrict__ bits, double* __restrict__ vk,
+    unsigned* __restrict__ work = nullptr, int chunk = 4) {
   constexpr int G = E / 16;
   extern __shared__ uint32_t v25_bits[];
   // one word past the N columns: padding entries carry column N, never kept
@@ -73,10 +74,8 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned i0 = warp_begin[w], i1 = warp_begin[w + 1];
   const unsigned upto = (2u << lane) - 1u;
-#pragma unroll 1
-  for (unsigned i = i0; i < i1; ++i) {
+  auto word = [&](unsigned i) {
     V25Slot<COL16> S;
     S.h = __ldg(&H[i]);
     S.hp = __ldg(&hpre[i]);
@@ -125,6 +124,26 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
       atomicAdd(vo + N, p1);
       atomicAdd(vo + 2 * (size_t)N, p2);
     }
+  };
+  if (!work) {  // static equal word ranges
+    const unsigned i0 = warp_begin[w], i1 = warp_begin[w + 1];
+#pragma unroll 1
+    for (unsigned i = i0; i < i1; ++i) word(i);
+    return;
+  }
+  // dynamic: warps claim chunks of words from a zeroed counter (the equal
+  // static ranges differ in gather count: SM busy times spread by +-10 %)
+  const unsigned nwords = warp_begin[(gridDim.x * blockDim.x) >> 5];
+#pragma unroll 1
+  for (;;) {
+    unsigned c = 0;
+    if (lane == 0) c = atomicAdd(work, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    const unsigned i0 = c * (unsigned)chunk;
+    if (i0 >= nwords) break;
+    const unsigned i1 = min(i0 + (unsigned)chunk, nwords);
+#pragma unroll 1
+    for (unsigned i = i0; i < i1; ++i) word(i);
   }
 }
 

@@ -730,7 +730,16 @@ class Scene:
                   _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W,
                   int(os.environ.get("SSS_FLAT16_MINB", "8")), st["E"], st["col_bits"],
                   0 if getattr(self, "_vk_zeroed", False) else 1, _lib.ptr(self.xp),
-                  _lib.ptr(self.xbits16), _lib.ptr(self.vk), sp)
+                  _lib.ptr(self.xbits16), _lib.ptr(self.vk), _lib.ptr(self._work_counter()),
+                  int(os.environ.get("SSS_FLAT16_CHUNK", "4")), sp)
+
+    def _work_counter(self):
+        """The flat16 kernel's dynamic word counter (None: static ranges)."""
+        if os.environ.get("SSS_FLAT16_DYN", "1") != "1":
+            return None
+        if getattr(self, "_wctr", None) is None:
+            self._wctr = torch.zeros(1, dtype=torch.int32, device="cuda")
+        return self._wctr
 
     def _rbcsc_core(self, sp):
         desc, dptr, rk16, v32, rowabs, rb, _ = self.transfer.rbcsc
@@ -784,6 +793,9 @@ class Scene:
             # overlapping stage 1, so the memset is not part of its launch
             self._vk_zeroed = True
             try:
+                wc = self._work_counter()
+                if wc is not None:
+                    _lib.call("sss_zero", _lib.ptr(wc), 4, _lib.stream_ptr(stream))
                 return self._flat16_core(_lib.stream_ptr(stream))
             finally:
                 self._vk_zeroed = False
@@ -814,6 +826,9 @@ class Scene:
         self._vk_zeroed = self.transfer_kernel == "flat16"
         if self._vk_zeroed:
             _lib.call("sss_zero", _lib.ptr(self.vk), self.vk.numel() * 8, _lib.stream_ptr(self._side))
+            wc = self._work_counter()
+            if wc is not None:
+                _lib.call("sss_zero", _lib.ptr(wc), 4, _lib.stream_ptr(self._side))
         join.record(self._side)
         self._launch_stage1(cur)
         cur.wait_event(join)
