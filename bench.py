@@ -252,27 +252,36 @@ def run_ours(a, cfg):
     from paper_2203_12339_b200.runtime import EnvLight
 
     n_e2e = min(a.steps, 100)
-    # one untimed API frame first: allocates the pinned read-back buffers and
-    # warms the host conversion path (as W warm-up steps do for the device loop)
-    scene.set_light(EnvLight(faces[0]))
-    scene.set_material(scene.material)
+    # untimed API frames first: allocate the pinned read-back blocks and warm
+    # the host path (as the W warm-up steps do for the device loop)
+    for f in range(min(a.warmup, 5) or 1):  # the read-back block pool reaches steady state
+        fr = scene.set_light(EnvLight(faces[f]))
+        fr = scene.set_material(scene.material)
+    del fr
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for i in range(n_e2e):
-        f = a.warmup + i
-        fr = scene.set_light(EnvLight(faces[f]))
-        if f in mats:
-            fr = scene.set_material(mats[f])
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    # three blocks of the same n_e2e-frame sequence; the median block (the
+    # host shares the box: single blocks occasionally stall by 30-50 %)
+    blocks = []
+    for _blk in range(3):
+        t0 = time.perf_counter()
+        for i in range(n_e2e):
+            f = a.warmup + i
+            fr = scene.set_light(EnvLight(faces[f]))
+            if f in mats:
+                fr = scene.set_material(mats[f])
+        torch.cuda.synchronize()
+        blocks.append(time.perf_counter() - t0)
+    e2e_s = float(np.median(blocks))
     e2e_s = max_over_ranks(e2e_s, ws)
     n_edit_e2e = sum(1 for i in range(n_e2e) if a.warmup + i in mats)
     h2d = faces[0].nbytes + (56 * n_edit_e2e) / n_e2e
     d2h = (2 * n * 3 * 8 + 48) * (1 + n_edit_e2e / n_e2e)  # f64 radiance + unclamped + energies
     e2e = {"value": ws * n * n_e2e / e2e_s, "unit": UNIT, "ms_per_step": 1e3 * e2e_s / n_e2e,
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": n_e2e,
+           "timing": "median of 3 blocks of the sequence (wall clock, synchronize at block end)",
+           "block_ms_per_step": [round(1e3 * b_ / n_e2e, 4) for b_ in blocks],
            "path": "Scene.set_light(EnvLight(host cubemap)) / set_material -> FrameResult (numpy)"}
 
     # ---- edit-path latency alone (launch-bound; reported separately)
