@@ -632,8 +632,9 @@ def test_frame_ambient_folded_parity(c1):
 
 
 def test_flat16_layout_variants_agree(c1, monkeypatch):
-    """flat16 with 32 entries per lane and with the window column-alignment
-    pass (csrc/align26.cu) computes the same v_k as the default flat16."""
+    """flat16 variants (32 entries per lane, u32 columns, the window
+    column-alignment pass csrc/align26.cu, static warp ranges) and rbcsc with
+    32-row blocks compute the same v_k as the default flat16."""
     from paper_2203_12339_b200 import lighting as LT
     from paper_2203_12339_b200.runtime import SHLight
 
@@ -641,10 +642,13 @@ def test_flat16_layout_variants_agree(c1, monkeypatch):
     sc.transfer_kernel = "flat16"
     sc.relight()
     ref = sc.vk.clone()
-    for env in ({"SSS_FLAT16_ALIGN": "1"}, {"SSS_FLAT16_E": "32"}):
+    for env in ({"SSS_FLAT16_ALIGN": "1", "SSS_FLAT16_COL16": "0"}, {"SSS_FLAT16_E": "32"},
+                {"SSS_FLAT16_DYN": "0"}, {"SSS_FLAT16_COL16": "0"}, {"SSS_RBCSC_RB": "32"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         sc.transfer.flat16 = None
+        sc.transfer.rbcsc = None
+        sc.transfer_kernel = "rbcsc" if "SSS_RBCSC_RB" in env else "flat16"
         sc._graph = None
         sc.vk.fill_(float("nan"))
         sc._launch_stage1()
