@@ -107,6 +107,8 @@ def exported_symbols():
 def load(require_cuda: bool = True):
     """Load the library (and bind signatures). Raises if it is missing."""
     global _lib
+    if require_cuda and not torch.cuda.is_available():
+        raise SSSError("CUDA device required: the relight path runs only on sm_100a")
     if _lib is not None:
         return _lib
     if not _SO.exists():
@@ -120,8 +122,6 @@ def load(require_cuda: bool = True):
         fn.argtypes = args
         fn.restype = C.c_int
     _lib = lib
-    if require_cuda and not torch.cuda.is_available():
-        raise SSSError("CUDA device required: the relight path runs only on sm_100a")
     return lib
 
 

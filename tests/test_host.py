@@ -5,6 +5,7 @@ import re
 from pathlib import Path
 
 import numpy as np
+import torch
 import pytest
 
 from oracle import sss_oracle as O
@@ -180,6 +181,24 @@ def test_library_rejects_bad_arguments_without_gpu():
     assert rc == -1 and b"power of two" in lib.sss_last_error()
     rc = lib.sss_select_topn(None, 1, 16, 4, None, None, None, None, None)
     assert rc == -1
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_product_path_fails_loudly_without_gpu_or_library(monkeypatch, tmp_path):
+    """No CPU fallback: without a GPU the API raises (even after a CPU-side
+    load of the library for symbol checks), and a missing .so raises too."""
+    from paper_2203_12339_b200 import _lib
+    from paper_2203_12339_b200.runtime import Scene
+
+    _lib.load(require_cuda=False)
+    with pytest.raises(_lib.SSSError, match="CUDA device required"):
+        _lib.load()
+    with pytest.raises(_lib.SSSError, match="CUDA device required"):
+        Scene(None, None, None, None, None)
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "_SO", tmp_path / "missing.so")
+    with pytest.raises(_lib.SSSError, match="no CPU fallback"):
+        _lib.load(require_cuda=False)
 
 
 def test_geometry_image_properties():
