@@ -78,6 +78,15 @@ class Clocks:
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # nvidia-smi's start-up (NVML init) stalls GPU work submission for
+        # milliseconds: let it finish (first sample written) before the timed
+        # region, which the 100 ms samples then span
+        t0 = time.time()
+        while time.time() - t0 < 3.0 and self.proc.poll() is None:
+            if self.path.stat().st_size > 0:
+                break
+            time.sleep(0.005)
 
     def stop(self):
         if self.proc is None:
