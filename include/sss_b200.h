@@ -93,234 +93,6 @@ int sss_env_transfer(const float* normals, int n_points, const double* dirs,
 int sss_material_weights(const double* bw, const double* r_nodes, int K, int nr,
                          const double* material, double* g, void* stream);
 
-/* ---- (b)+(c) relight: K-fused transfer (TransferOperator.apply x K x 3,
- *      transfer.py:66-71 / csc_apply _kernels_nb.py:301-313) with the
- *      recombine + inverse-Haar + Fresnel shade epilogue (runtime.py:155-216).
- *      Frame layout: per k a tile-major CSR (rowptr (K, N+1) u64 absolute
- *      offsets; cols = TILE-MAJOR w0 ids, ascending within a row; vals f32),
- *      split into column bands of band_width ids (bandoff (K, N, n_bands+1)
- *      u32 offsets relative to the row start). A CTA owns unit_tiles tiles
- *      (unit_tiles * 4^levels rows, a multiple of 32, <= 256) visited in
- *      rowperm order (N global row ids, unit-major). x (3, N) = masked E
- *      spectrum in tile-major column order; g (3, K) material weights; vk
- *      (K, 3, N) tile-major cache out; scatter (N, 3) may be NULL;
- *      radiance / radiance_unclamped (N, 3) float32; cam (3); material
- *      {sp[3], sa[3], eta}. K <= 16. */
-int sss_transfer_relight(int K, int side, int levels, int unit_tiles, const uint64_t* rowptr,
-                         const uint32_t* bandoff, int band_width, int n_bands, const int* rowperm,
-                         const uint32_t* cols, const float* vals, const double* x, const double* g,
-                         const float* positions, const float* normals, const double* cam,
-                         const double* material, double* vk, double* scatter, float* radiance,
-                         float* radiance_unclamped, void* stream);
-
-/* ---- frame layout v3 ("stream"): each CTA unit's entries as one contiguous
- *      TMA-streamable range, item = (band, k), rows in rowperm order inside
- *      an item, entry = {u32 band-local column, f32 value}, items padded to
- *      even length. pass 0: item_len (units*n_bands*K) + exclusive scan
- *      item_off (+ total entries); pass 1: rowoff (items x (unit_rows+1))
- *      and the entries (8 B each, 16-byte aligned buffer). */
-int sss_stream_build(int pass, const uint64_t* rowptr, const uint32_t* cols, const float* vals,
-                     const uint32_t* bandoff, const int* rowperm, int K, int n_rows, int n_bands,
-                     int unit_rows, int band_width, uint32_t* item_len, uint64_t* item_off,
-                     uint64_t* block_sums, uint64_t* total, uint32_t* rowoff, void* entries,
-                     void* stream);
-
-/* ---- relight on the stream layout: cp.async.bulk + mbarrier double-buffered
- *      pipeline into shared memory; otherwise identical contract to
- *      sss_transfer_relight. */
-int sss_transfer_stream(int K, int side, int levels, int unit_tiles, int band_width, int n_bands,
-                        const uint64_t* item_off, const uint32_t* item_len, const uint32_t* rowoff,
-                        const void* entries, const int* rowperm, const double* x, const double* g,
-                        const float* positions, const float* normals, const double* cam,
-                        const double* material, double* vk, double* scatter, float* radiance,
-                        float* radiance_unclamped, void* stream);
-
-/* ---- relight on frame layout v4 (persistent, warp-specialized): one CTA per
- *      unit (a contiguous tile range, ~one per SM); a producer warp streams
- *      self-describing (band, k) items {u16 warp bases, u8 per-thread counts,
- *      entries} into a 4-slot ring with cp.async.bulk and the x bands into a
- *      double buffer; 16 consumer warps (512 virtual threads, long rows split
- *      over several) accumulate in fp64 registers; mbarrier full/empty
- *      hand-off only. Layout built by paper_2203_12339_b200/stream4.py;
- *      contract otherwise as sss_transfer_relight. */
-int sss_transfer_v4(int K, int side, int levels, int band_width, int slot_bytes, int units,
-                    int max_unit_items,
-                    const int* unit_tile0, const int* unit_ntiles, const int* unit_item0,
-                    const int* unit_nitems, const void* items, const void* stream_bytes,
-                    const void* vrow_first, const double* x, const double* g,
-                    const float* positions, const float* normals, const double* cam,
-                    const double* material, double* vk, double* scatter, float* radiance,
-                    float* radiance_unclamped, void* stream);
-
-/* ---- relight on frame layout v6 (persistent, warp-specialized, merge-path):
- *      items = (unit, column band[, split]) of entries {u32 (row_local << 4 | k)
- *      << 11 | band-local col, f32 val} sorted by (row, k, col); every item is
- *      split evenly over 512 consumer threads; segment partials merge by warp
- *      affine scans + 16 boundary records into a shared-memory accumulator.
- *      Layout built by paper_2203_12339_b200/stream6.py. */
-int sss_transfer_v6(int K, int side, int levels, int band_width, int slot_bytes, int units,
-                    int max_unit_items, int max_unit_rows, const int* unit_tile0,
-                    const int* unit_ntiles, const int* unit_item0, const int* unit_nitems,
-                    const void* items, const void* stream_bytes, const double* x, const double* g,
-                    const float* positions, const float* normals, const double* cam,
-                    const double* material, double* vk, double* scatter, float* radiance,
-                    float* radiance_unclamped, void* stream);
-
-/* ---- x (3, N) -> packed (N, 4) {x0, x1, x2, 0} doubles (32-byte aligned) */
-int sss_pack_x(const double* x, int n, void* xp, void* stream);
-
-/* ---- relight, v7: warp-per-(row, k) CSR SpMV on the canonical tile-major CSR
- *      (rowptr / cols / vals as in sss_transfer_relight), CTA = unit_tiles
- *      tiles with an in-CTA longest-first work list `order` (per CTA,
- *      R*K u16 = row_local << 4 | k), x packed (sss_pack_x) and gathered
- *      through L1. Same outputs as sss_transfer_relight. */
-int sss_transfer_csr7(int K, int side, int levels, int unit_tiles, const uint64_t* rowptr,
-                      const uint32_t* cols, const float* vals, const void* order, const void* xp,
-                      const double* g, const float* positions, const float* normals,
-                      const double* cam, const double* material, double* vk, double* scatter,
-                      float* radiance, float* radiance_unclamped, void* stream);
-
-/* ---- transfer, v8: persistent merge-path CSR SpMV. pieces = {u32 start, u32
- *      len, u32 row*16+k, pad} cut from the (row, k)-ordered segments of the
- *      canonical CSR; warp w processes pieces [warp_begin[w], warp_begin[w+1]).
- *      Zeroes vk (K, 3, n_rows) and accumulates it with red.global.add.f64;
- *      follow with sss_edit_finish for recombine + inverse + shade. n_warps is
- *      a multiple of 8. */
-int sss_transfer_csr8(int K, int n_rows, const uint32_t* cols, const float* vals,
-                      const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
-                      double* vk, void* stream);
-
-/* ---- padded copy of the canonical CSR for v9: segment i (seg_src[i],
- *      seg_len[i]) copied to seg_dst[i] (multiple of 4) and padded to a
- *      multiple of 4 entries with (col 0, val 0). */
-int sss_pad_segments(const uint64_t* seg_src, const uint32_t* seg_len, const uint64_t* seg_dst,
-                     long long nseg, const uint32_t* cols, const float* vals, uint32_t* pcols,
-                     float* pvals, void* stream);
-
-/* ---- transfer, v9: as sss_transfer_csr8 on the padded arrays, pieces {u32
- *      start (multiple of 4), u32 len (multiple of 4), u32 row*16+k, pad};
- *      4 pieces per warp in flight (8-lane groups, 16-byte vector loads). */
-int sss_transfer_csr9(int K, int n_rows, const uint32_t* pcols, const float* pvals,
-                      const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
-                      double* vk, void* stream);
-
-/* ---- transfer v10: K-packed (row, column) pairs. meta[p] = column (24 bits)
- * | k-mask (8 bits) << 24; vals holds the f32 coefficients of the terms in
- * the mask (k ascending), pair after pair. pieces = {pair0, npair, val0, row}
- * (uint32 x4), warp_begin (n_warps + 1) balanced ranges. Requires K <= 8 and
- * n_rows <= 2^24. Zeroes and fills vk; shade with sss_edit_finish. Same
- * contract as sss_transfer_csr9 (runtime.py:148-153). */
-int sss_transfer_kpack(int K, int n_rows, const uint32_t* meta, const float* vals,
-                       const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
-                       double* vk, void* stream);
-
-/* ---- transfer v11: the v10 layout with a cp.async software pipeline (meta two
- * steps ahead, values one step ahead, x gathers one step ahead); pairs_per_lane
- * 2 or 4. n_warps a multiple of 4. Same contract as sss_transfer_kpack. */
-int sss_transfer_kpack_pipe(int K, int n_rows, const uint32_t* meta, const float* vals,
-                            const void* pieces, const unsigned* warp_begin, int n_warps,
-                            int pairs_per_lane, const void* xp, double* vk, void* stream);
-
-/* ---- transfer v12: mask-sorted K-fused warp steps. steps (uint32 x4 each):
- * {pair0, val0, row, kmask | count << 8 | row_end << 16}; cols[pair0 + l]
- * (l < count) = tile-major columns; for every k in kmask (ascending) 32 f32
- * values at vals[val0 + j * 32 + l] (j = rank of k in kmask, 0 where pair l
- * lacks term k). Steps of a row are consecutive; warp_begin (n_warps + 1)
- * gives each warp a contiguous step range. K <= 8, n_warps a multiple of 4.
- * Zeroes and fills vk; shade with sss_edit_finish (runtime.py:148-153). */
-int sss_transfer_kstep(int K, int n_rows, const uint32_t* cols, const float* vals,
-                       const void* steps, const unsigned* warp_begin, int n_warps, const void* xp,
-                       double* vk, void* stream);
-
-/* ---- transfer v13: the v12 warp steps as contiguous blobs, TMA-streamed.
- * blob: per step [32 u32 tile-major columns (0-padded) | popc(kmask) x 32 f32
- * values, k ascending, lane order], 16-byte aligned; recs (uint32 x4 per step)
- * {blob offset in 16-byte units, row, kmask | count << 8 | row_end << 16, 0};
- * steps of a row consecutive, warp_begin (n_warps + 1) contiguous per-warp
- * ranges. depth = steps in flight per warp (4, 8 or 12). K <= 8, n_warps a
- * multiple of 8. Zeroes and fills vk; shade with sss_edit_finish. */
-int sss_transfer_kstream(int K, int n_rows, const void* blob, const void* recs,
-                         const unsigned* warp_begin, int n_warps, int depth, const void* xp,
-                         double* vk, void* stream);
-
-/* ---- packed x (n, 4) doubles {x0, x1, x2, 0} + kept-column bitmap: bit c of
- * bits ((n + 31) / 32 words) set iff any channel of x[:, c] is nonzero. */
-int sss_pack_x_bits(const double* x, int n, void* xp, uint32_t* bits, void* stream);
-
-/* ---- sss_transfer_csr9 visiting only kept columns (bits from
- * sss_pack_x_bits): entries whose column is not kept issue no x gather and
- * no FMA, like the reference's csc_apply over the kept columns
- * (transfer.py:66-71). Same v_k bit for bit. */
-int sss_transfer_csr9s(int K, int n_rows, const uint32_t* pcols, const float* pvals,
-                       const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
-                       const uint32_t* bits, double* vk, void* stream);
-
-/* ---- transfer v14: K-packed pairs (meta = column | k-mask << 24, values of
- * the present terms, k ascending) with every row padded to a multiple of 32
- * pairs (meta 0 = empty); pieces (uint32 x4 each) = {pair0, npair, val0, row}
- * runs of <= split pairs of one row (multiples of 32); warp_begin
- * (n_warps + 1) contiguous per-warp piece ranges; bits = kept-column bitmap
- * from sss_pack_x_bits. Zeroes and fills vk; shade with sss_edit_finish
- * (runtime.py:148-153). K <= 8. */
-int sss_transfer_kgroup(int K, int n_rows, const uint32_t* meta, const float* vals,
-                        const void* pieces, const unsigned* warp_begin, int n_warps, const void* xp,
-                        const uint32_t* bits, double* vk, void* stream);
-
-/* ---- transfer v15: flat stream over csr9's padded operator copy (every
- * (row, k) segment padded to a multiple of 4 entries; n_entries total).
- * heads: bit l of word i set iff 4-entry group 32 i + l starts a segment;
- * head_prefix[i] = segments started before word i; seg_rowk[s] = row * 16 + k
- * of segment s (segments in stream order); warp_begin (n_warps + 1) = word
- * ranges per warp. n_warps a multiple of 8. bits (may be NULL) = kept-column
- * bitmap from sss_pack_x_bits: entries over unkept columns skip their x
- * gather (exact zeros). Zeroes and fills vk; shade with sss_edit_finish
- * (runtime.py:148-153). */
-int sss_transfer_flat(int K, int n_rows, const uint32_t* pcols, const float* pvals,
-                      unsigned long long n_entries, const uint32_t* heads,
-                      const uint32_t* head_prefix, const uint32_t* seg_rowk,
-                      const unsigned* warp_begin, int n_warps, const void* xp,
-                      const uint32_t* bits, double* vk, void* stream);
-
-/* ---- transfer v16: sss_transfer_flat with a depth-iteration cp.async
- * prefetch ring per warp (depth 4, 8 or 12); n_warps a multiple of 4. */
-int sss_transfer_flatp(int K, int n_rows, const uint32_t* pcols, const float* pvals,
-                       unsigned long long n_entries, const uint32_t* heads,
-                       const uint32_t* head_prefix, const uint32_t* seg_rowk,
-                       const unsigned* warp_begin, int n_warps, int depth, const void* xp,
-                       double* vk, void* stream);
-
-/* ---- transfer v17: sss_transfer_flat over a copy with every (row, k)
- * segment padded to a multiple of 8 entries (pcols/pvals 32-byte aligned);
- * heads bit l of word i marks 8-entry group 32 i + l. variant: 0 = gather and
- * consume per iteration, 1 = x gathers one iteration ahead, 4..8 = gathers in
- * two halves of 4 entries with a register cap for `variant` resident CTAs per
- * SM; 14 / 16 / 18 = the same with a single stream slot and 6 / 8 / 10 CTAs
- * per SM (16 = default: 32 warps / SM); x_f32 != 0: xp is the packed (N, 4)
- * float array of sss_pack_x_f32_bits (fp64 products and sums of f32 operator
- * values x f32 spectrum). n_warps a multiple of 4. Same contract. */
-int sss_transfer_flat8(int K, int n_rows, const uint32_t* pcols, const float* pvals,
-                       unsigned long long n_entries, const uint32_t* heads,
-                       const uint32_t* head_prefix, const uint32_t* seg_rowk,
-                       const unsigned* warp_begin, int n_warps, const void* xp,
-                       const uint32_t* bits, int variant, int x_f32, double* vk,
-                       void* stream);
-
-/* ---- packed x in a permuted column order: xp[j] = {x0, x1, x2, 0}[perm[j]],
- * bits over j (the flat8 layout's block-local column space). */
-int sss_pack_x_perm_bits(const double* x, int n, const int* perm, void* xp, uint32_t* bits,
-                         void* stream);
-
-/* ---- packed fp32 x (n, 4) floats {x0, x1, x2, 0} + kept-column bitmap. */
-int sss_pack_x_f32_bits(const double* x, int n, void* xp, uint32_t* bits, void* stream);
-
-/* ---- transfer v18: the v12 mask-sorted warp steps (same cols / vals / steps
- * arrays as sss_transfer_kstep) streamed with batched step records and a
- * two-step prefetch; bits (may be NULL) = kept-column bitmap. K <= 8, n_warps
- * a multiple of 4. Zeroes and fills vk; shade with sss_edit_finish. */
-int sss_transfer_kflat(int K, int n_rows, const uint32_t* cols, const float* vals,
-                       const void* steps, const unsigned* warp_begin, int n_warps, const void* xp,
-                       const uint32_t* bits, double* vk, void* stream);
-
 /* ---- C4 batched material sweep (BASELINE configs[3]; runtime.py:202-216 for
  * a batch of materials). B operand: Bq (3, N, 16) bf16 = w1^-1 of the cached
  * v_k (K <= 16 terms, zero padded), points in flat (spatial) order. */
@@ -341,30 +113,6 @@ int sss_material_weights_batch(const double* bw, const double* r_nodes, int K, i
 int sss_sweep_gemm(int n_points, int M, const void* Bq, const void* Gq, const float* eta,
                    float eta_lo, float eta_hi, const float* positions, const float* normals,
                    const double* cam, float* out, void* stream);
-
-/* ---- transfer v19: receiver regions (2^L tiles) with the kept x working set
- * in shared memory. ucols / uoff (n_regions + 1): each region's sorted union
- * of columns; pcols / pvals: the flat8 stream whose column fields are
- * region-local slots (< umax < 32768), every region padded to whole 256-entry
- * iterations (rit, n_regions + 1, iteration offsets); heads / head_prefix /
- * seg_rowk as sss_transfer_flat8; xp / bits from sss_pack_x_bits. Zeroes and
- * fills vk; shade with sss_edit_finish. */
-int sss_transfer_regional(int K, int n_rows, const uint32_t* ucols, const int* uoff,
-                          const int* rit, int n_regions, int umax, const uint32_t* pcols,
-                          const float* pvals, unsigned long long n_entries,
-                          const uint32_t* heads, const uint32_t* head_prefix,
-                          const uint32_t* seg_rowk, const void* xp, const uint32_t* bits,
-                          double* vk, void* stream);
-
-/* ---- transfer v20: dense K-fused pairs. cols (npairs) = tile-major column
- * per (row, column) pair (N = padding); vals (npairs, 8) f32 = the pair's
- * terms 0..K-1 (0 where absent); rows padded to 32 pairs; pieces (uint32 x4)
- * {pair0, npair (multiples of 32), row, 0}; warp_begin (n_warps + 1);
- * min_ctas = occupancy target (1..3 CTAs of 256 threads per SM); bits / xp
- * from sss_pack_x_bits. Zeroes and fills vk; shade with sss_edit_finish. */
-int sss_transfer_k8(int K, int n_rows, const uint32_t* cols, const float* vals, const void* pieces,
-                    const unsigned* warp_begin, int n_warps, int min_ctas, const void* xp,
-                    const uint32_t* bits, double* vk, void* stream);
 
 /* ---- (a) direct lights with shadow rays: irradiance_direct
  * (lighting.py:208-290) with BVH any-hit visibility (lighting.py:101-176,
@@ -435,35 +183,47 @@ int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const 
                    const float* vals, const uint32_t* union_idx, const double* union_lc,
                    const int* n_union, const uint32_t* flat2tm, double* vk, void* stream);
 
-/* sss_transfer_flat8c: stage 2 (runtime.py:138-150; csc_apply,
- *   _kernels_nb.py:301-313) over the column-partitioned flat8 stream of
- *   runtime.flat8c_layout: entries (u16 partition-local column, f32 value)
- *   partition-major, (partition, row, k) sub-segments padded to 8 entries,
- *   head bits / word prefixes / segment ids (row * 16 + k) as
- *   sss_transfer_flat8; CTA b serves partition cta_part[b] with that
- *   partition's x (from xp, (n_rows, 4) f64) and kept bits staged in shared
- *   memory; warp w streams words [warp_begin[w], warp_begin[w + 1]). Zeroes vk
- *   (K, 3, n_rows) f64 and accumulates into it. part_width in {1024, 2048, 4096}. */
-int sss_transfer_flat8c(int K, int n_rows, const void* cols16, const float* vals,
-                        unsigned long long n_entries, const uint32_t* heads,
-                        const uint32_t* head_prefix, const uint32_t* seg_rowk,
-                        const unsigned* warp_begin, const int* cta_part, int n_ctas,
-                        int part_width, const void* xp, const uint32_t* bits, double* vk,
-                        void* stream);
+/* ---- (b) scattering transfer, stage 2 of the frame: replaces the K x 3
+ *      TransferOperator.apply -> _k.csc_apply calls of _stage2_transfer
+ *      (runtime.py:138-150, transfer.py:50-71, _kernels_nb.py:301-313):
+ *      vk (K, 3, n_rows) f64 tile-major = T_k x_c for every term k and channel c.
+ *      xp (n_rows, 4) f64 and bits (n_rows / 32 + 1 words, last word clear) are
+ *      sss_pack_x_bits's packing of the kept spectrum x (3, n_rows).
+ *
+ * sss_transfer_kfr ("K-fused rows", default): the operator as a stream of
+ *   (column, term-mask) pairs per receiver-row chunk (layout.kfr_layout):
+ *   items (n_items x {first batch, steps}), lane_len / lane_dst (32 per item:
+ *   chunk length; row, 0x80000000 | partial slot, or 0xffffffff), batch_off
+ *   ({word, value} offsets of every 4-step batch + a sentinel), cm (col | mask
+ *   << 16 words), vals (f32, term planes), partials ((3K, n_partials) f64
+ *   scratch), partial_row (multi-chunk row index of each slot), multi_info
+ *   ({row, first slot, count, 0} per multi-chunk row), multi_count (zeroed u32
+ *   per multi-chunk row; left zero on return). Writes every row of vk (no
+ *   memset), bitwise reproducible. K <= 16, n_rows <= 65536. n_warps: warps
+ *   launched (multiple of 4), min_blocks: CTAs of 128 threads per SM. */
+int sss_transfer_kfr(int K, int n_rows, unsigned n_items, unsigned n_partials, const void* items,
+                     const uint32_t* lane_len, const uint32_t* lane_dst, const void* batch_off,
+                     const uint32_t* cm, const float* vals, const void* xp, const uint32_t* bits,
+                     double* vk, double* partials, const uint32_t* partial_row,
+                     const void* multi_info, uint32_t* multi_count, int n_warps, int min_blocks,
+                     void* stream);
 
-/* sss_transfer_flat16: sss_transfer_flat8 with entries_per_lane = 16 or 32
- *   entries per lane (segments padded to a multiple of it, heads one bit per
- *   group). col_bits 32: u32 columns, padding entries carry column n_rows /
- *   value 0 and the kept bitmap `bits` needs n_rows / 32 + 1 words with the bit
- *   of column n_rows clear (padding skips its gather). col_bits 16 (n_rows <=
- *   65536, 16 entries per lane): u16 columns, padding keeps column 0 with
- *   value 0 (its gather, if column 0 is kept, shares one address per instruction). min_blocks = CTAs of 128 threads per SM (register
- *   cap): 4, 6, 8 for 16 entries, 6, 8 for 32, 8 for 16-bit columns.
- *   Accumulates into vk, zeroing it first when zero_vk (else the caller has
- *   zeroed it, e.g. on a side stream overlapping stage 1). work_counter (u32,
- *   nullable): warps claim `chunk` words at a time from it instead of their
- *   static ranges (load balance); it must be zero at launch (zeroed here with
- *   vk when zero_vk). */
+/* sss_pack_x_bits: xp (n, 4) f64 = {x0, x1, x2, 0} of the kept spectrum
+ *   x (3, n) and the kept-column bitmap (bit c set iff any channel is kept). */
+int sss_pack_x_bits(const double* x, int n, void* xp, uint32_t* bits, void* stream);
+
+/* sss_transfer_flat16 (A/B alternative): the operator as a flat stream of
+ *   (row, k) segments, each padded to a multiple of entries_per_lane (16 or 32)
+ *   entries and lane-interleaved, head bits one per group, per-word head prefix
+ *   and segment (row << 4 | k) ids (layout.flat16_layout). col_bits 32: u32
+ *   columns, padding entries carry column n_rows / value 0 and the kept bitmap
+ *   `bits` needs n_rows / 32 + 1 words with the bit of column n_rows clear.
+ *   col_bits 16 (n_rows <= 65536, 16 entries per lane): u16 columns, padding
+ *   keeps column 0 with value 0. min_blocks = CTAs of 128 threads per SM: 4, 6,
+ *   8 for 16 entries, 6, 8 for 32, 8 for 16-bit columns. Accumulates into vk
+ *   with fp64 atomics (order not fixed), zeroing it first when zero_vk.
+ *   work_counter (u32, nullable): warps claim `chunk` words at a time from it;
+ *   it must be zero at launch (zeroed here with vk when zero_vk). */
 int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals,
                         unsigned long long n_entries, const uint32_t* heads,
                         const uint32_t* head_prefix, const uint32_t* seg_rowk,
@@ -471,59 +231,6 @@ int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals
                         int entries_per_lane, int col_bits, int zero_vk, const void* xp,
                         const uint32_t* bits, double* vk, uint32_t* work_counter, int chunk,
                         void* stream);
-
-/* sss_flat_align: layout pass over a 16-entries-per-lane flat stream (see
- *   sss_transfer_flat16): inside every 512-entry window (one warp iteration)
- *   re-slot each lane's entries so that a column present in several of the
- *   window's segments sits in the same slot of their lanes (shared gather
- *   wavefront); lanes keep their segments, so heads / prefixes / segment ids are
- *   unchanged. n_groups = 16-entry groups in the stream (the last word may be
- *   partial). cols >= sentinel mark padding. Out-of-place. */
-int sss_flat_align(unsigned n_words, unsigned n_groups, const uint32_t* cols_in, const float* vals_in,
-                   const uint32_t* heads, uint32_t sentinel, uint32_t* cols_out, float* vals_out,
-                   void* stream);
-
-/* sss_transfer_rbcsc: stage 2 (runtime.py:138-150; csc_apply,
- *   _kernels_nb.py:301-313) over the row-block column-major layout of
- *   runtime.rbcsc_layout: per block of row_block tile-major rows, segment
- *   descriptors {column | length << 16, first entry} (desc_ptr (n_rows /
- *   row_block + 1) into them), entries rowk (row in block | k << log2
- *   row_block, u16) and vals (f32). Only segments of kept columns (bits =
- *   sss_pack_x_bits's kept bitmap) are read, x fetched once per segment.
- *   Exact 64-bit fixed-point accumulation in shared memory, scale per (k, c)
- *   from rowabs[k] = max_row sum |T_k| and energy (3, 2) = select's (total,
- *   kept) sums of squares; writes every vk[(k * 3 + c) * n_rows + row]
- *   (deterministic, no memset). row_block in {32, 64, 128} for K in {4, 8};
- *   row_block 64 for any K <= 8. */
-int sss_transfer_rbcsc(int K, int n_rows, int row_block, const void* desc,
-                       const uint32_t* desc_ptr, const uint16_t* rowk, const float* vals,
-                       const double* rowabs, const double* energy, const void* xp,
-                       const uint32_t* bits, double* vk, void* stream);
-
-/* sss_transfer_pairgroup: stage 2 (runtime.py:138-150; csc_apply,
- *   _kernels_nb.py:301-313) over the kpairs headers / pair-major values with
- *   per-row pair starts pair_ptr (n_rows + 1) and value starts val_ptr (n_rows +
- *   1), warps owning rows [row_begin[w], row_begin[w + 1]). Four lanes per (row,
- *   column) pair (lane g: terms g, g + 4), one x gather per kept pair; writes
- *   every vk[(k * 3 + c) * n_rows + row] (no memset, deterministic). K <= 8,
- *   n_rows <= 65536, n_warps % 8 == 0. */
-int sss_transfer_pairgroup(int K, int n_rows, const uint32_t* pair_ptr, const uint32_t* val_ptr,
-                           const uint32_t* hdr, const float* vals, const uint32_t* row_begin,
-                           int n_warps, const void* xp, const uint32_t* bits, double* vk,
-                           void* stream);
-
-/* sss_transfer_kpairs: stage 2 of the frame (runtime.py:138-150, the K x 3
- *   csc_apply calls of _kernels_nb.py:301-313) over the pair layout of
- *   transfer.kpairs_layout: per (row, column) pair one header (column | term
- *   mask << 16), the pair's values pair-major (terms ascending), chunk
- *   descriptors {row, first pair, count <= 32, first value} (uint4, every row
- *   >= 1 chunk) and per-warp chunk ranges covering whole rows. One x gather
- *   per kept pair for all K terms; writes every vk[(k * 3 + c) * n_rows + row]
- *   (no memset needed, deterministic). xp (n_rows, 4) f64 = sss_pack_x_bits's,
- *   bits its kept bitmap. K <= 8, n_rows <= 65536, n_warps % 8 == 0. */
-int sss_transfer_kpairs(int K, int n_rows, const void* chunks, const uint32_t* hdr,
-                        const float* vals, const uint32_t* chunk_begin, int n_warps,
-                        const void* xp, const uint32_t* bits, double* vk, void* stream);
 
 /* sss_fold_apply_rows: the same v_k update as sss_fold_apply from a row-major
  *   copy of the folded operators, ELL-interleaved per 32-row group: group g =
@@ -536,10 +243,6 @@ int sss_fold_apply_rows(int K, int n_rows, int n_dirs, const uint64_t* gbase,
                         const uint32_t* entries, const uint32_t* union_idx,
                         const double* union_lc, const int* n_union, const uint32_t* flat2tm,
                         double* vk, void* stream);
-
-/* ---- band offsets of a frame-layout operator (see sss_transfer_relight) */
-int sss_band_offsets(const uint64_t* rowptr, const uint32_t* cols, int K, int n_rows,
-                     int band_width, int n_bands, uint32_t* bandoff, void* stream);
 
 /* ---- edit path: stages 3-5 against the cached vk (Scene.set_material,
  *      runtime.py:189-216). */

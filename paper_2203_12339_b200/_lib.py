@@ -28,57 +28,23 @@ _SIGS = {
     "sss_env_irradiance_sel": [_P, _I, _P, _P, _I, _I, _I, _P, _P, _P],
     "sss_env_transfer": [_P, _I, _P, _P, _I, _P, _P],
     "sss_material_weights": [_P, _P, _I, _I, _P, _P, _P],
-    "sss_transfer_relight": [_I, _I, _I, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
-    "sss_band_offsets": [_P, _P, _I, _I, _I, _I, _P, _P],
-    "sss_pack_x": [_P, _I, _P, _P],
-    "sss_transfer_csr8": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
-    "sss_pad_segments": [_P, _P, _P, C.c_longlong, _P, _P, _P, _P, _P],
-    "sss_transfer_csr9": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
-    "sss_transfer_kpack": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
-    "sss_transfer_kstep": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P],
     "sss_pack_x_bits": [_P, _I, _P, _P, _P],
-    "sss_transfer_flat": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "sss_sweep_basis": [_I, _I, _I, _P, _P, _P],
     "sss_material_weights_batch": [_P, _P, _I, _I, _I, _P, _P, _P, _P, _P],
     "sss_sweep_gemm": [_I, _I, _P, _P, _P, C.c_float, C.c_float, _P, _P, _P, _P, _P],
-    "sss_transfer_regional": [_I, _I, _P, _P, _P, _I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P,
-                              _P, _P, _P],
     "sss_visibility": [_I, _P, _P, _I, _P, C.c_double, C.c_double, _P, _P, _P, _P],
     "sss_fold_weights": [_P, _I, _P, _P, _I, _P, C.c_double, _P, _P],
     "sss_transpose_f64": [_P, _I, _I, _P, _P, _P],
     "sss_fold_spmm": [_I, _I, _P, _P, _P, _P, _P, _P],
     "sss_fold_select": [_P, _I, _I, C.c_double, _P, _P, _P, _P, _P, _P, _P],
     "sss_fold_emit": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
-    "sss_transfer_flat8c": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P,
-                            _P],
+    "sss_transfer_kfr": [_I, _I, C.c_uint, C.c_uint, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                         _P, _P, _I, _I, _P],
     "sss_transfer_flat16": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P,
                             _P, _P, _P, _I, _P],
-    "sss_flat_align": [C.c_uint, C.c_uint, _P, _P, _P, C.c_uint, _P, _P, _P],
-    "sss_transfer_rbcsc": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
-    "sss_transfer_pairgroup": [_I, _I, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P],
-    "sss_transfer_kpairs": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
     "sss_fold_apply_rows": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_fold_apply": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_direct_irradiance": [_I, _P, _P, _I, _P, _P, _P, C.c_double, C.c_double, _P, _P, _P, _P],
-    "sss_transfer_k8": [_I, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P],
-    "sss_transfer_kflat": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
-    "sss_transfer_flat8": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _P, _P, _I, _I, _P, _P],
-    "sss_pack_x_f32_bits": [_P, _I, _P, _P, _P],
-    "sss_pack_x_perm_bits": [_P, _I, _P, _P, _P, _P],
-    "sss_transfer_flatp": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _I, _P, _P, _P],
-    "sss_transfer_kgroup": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
-    "sss_transfer_csr9s": [_I, _I, _P, _P, _P, _P, _I, _P, _P, _P, _P],
-    "sss_transfer_kstream": [_I, _I, _P, _P, _P, _I, _I, _P, _P, _P],
-    "sss_transfer_kpack_pipe": [_I, _I, _P, _P, _P, _P, _I, _I, _P, _P, _P],
-    "sss_transfer_csr7": [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                          _P, _P],
-    "sss_transfer_v6": [_I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                        _P, _P, _P, _P, _P, _P, _P],
-    "sss_transfer_v4": [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                        _P, _P, _P, _P, _P, _P, _P],
-    "sss_stream_build": [_I, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
-    "sss_transfer_stream": [_I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                            _P, _P, _P, _P, _P],
     "sss_edit_finish": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_pair_block": [_I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _I, C.c_float, _P, _P, _P],
     "sss_step1_select": [_P, _I, _I, _I, _P, _P, _P],

@@ -1,22 +1,19 @@
-"""Scattering-transfer operators (path b): data model and device layout.
+"""Scattering-transfer operators (path b): data model.
 
 Reference data model (transfer.py:50-93): per PCA term k a
 ``TransferOperator`` in CSC over retained w0 columns (cols, colptr, rowidx
 into the w1 flat domain, vals), grouped in a ``CompressedTransfer``.
 
-Device layout (this framework, "frame layout v2"): one tile-major CSR per k
-so a CTA that owns 2^L x 2^L spatial tiles owns the 4^L w1 rows their
-inverse Haar needs (SURVEY §7 hard parts 4/5): ``rowptr`` (K, N+1) u64
-absolute offsets, ``cols`` u32 TILE-MAJOR w0 ids ascending within a row,
-``vals`` f32 — 8 bytes per stored coefficient, the reference container's
-width (container.py:87-88). Each row is split into column bands of
-``band_width`` ids (``bandoff`` (K, N, n_bands+1) u32 offsets relative to
-the row start) so the transfer kernel can stage one band of the E spectrum
-in shared memory at a time; ``rowperm`` orders each CTA unit's rows
-longest-first so a warp's rows have similar lengths.
+Device form (``DeviceTransfer``): one tile-major CSR per k — ``rowptr``
+(K, N+1) absolute offsets, ``cols`` u32 TILE-MAJOR w0 ids ascending within a
+row, ``vals`` f32, 8 bytes per stored coefficient as in the reference
+container (container.py:87-88). Tile-major = tile * 4^L + local, so every
+2^L x 2^L spatial tile owns a contiguous block of 4^L rows (the L-level
+inverse Haar is tile-local). The frame kernels read rearranged copies built
+from it (layout.py).
 
 ``DeviceTransfer.from_reference`` is the bridge from reference-format
-operators (e.g. a PRTS1 container) to the device layout;
+operators (e.g. a PRTS1 container) to the device form;
 ``precompute.precompute_compressed`` builds it on the GPU directly.
 """
 
@@ -76,13 +73,9 @@ def tile_major_to_flat(side: int, levels: int) -> np.ndarray:
     return perm
 
 
-BAND_WIDTH = 2048  # w0 ids per shared-memory band (3 x 2048 doubles = 48 KB)
-UNIT_ROWS = 256  # rows per CTA of the transfer kernel
-
-
 @dataclass
 class DeviceTransfer:
-    """K operators resident in HBM in the banded tile-major CSR frame layout."""
+    """K operators resident in HBM as tile-major CSR (canonical form)."""
 
     K: int
     side: int
@@ -96,79 +89,6 @@ class DeviceTransfer:
     kept_energy: list = None
     total_energy: list = None
     step1_entries: list = None
-    band_width: int = 0
-    n_bands: int = 0
-    bandoff: torch.Tensor = None  # int32 (K, N, n_bands+1)
-    rowperm: torch.Tensor = None  # int32 (N,)
-    unit_tiles: int = 0
-    # stream layout (v3), built on CUDA devices
-    item_len: torch.Tensor = None
-    item_off: torch.Tensor = None
-    rowoff: torch.Tensor = None
-    entries: torch.Tensor = None
-    stream_entries: int = 0
-
-    def __post_init__(self):
-        if self.bandoff is None:
-            self._finalize()
-
-    def _finalize(self):
-        n, K = self.n, self.K
-        T2 = (1 << self.levels) ** 2
-        self.band_width = min(BAND_WIDTH, n)
-        self.n_bands = (n + self.band_width - 1) // self.band_width
-        rows = min(UNIT_ROWS, n)
-        self.unit_tiles = max(1, rows // T2)
-        rp = self.rowptr.cpu().numpy()
-        if self.rowptr.is_cuda:
-            from . import _lib
-
-            self.bandoff = torch.empty((K, n, self.n_bands + 1), dtype=torch.int32,
-                                       device=self.rowptr.device)
-            _lib.call("sss_band_offsets", _lib.ptr(self.rowptr), _lib.ptr(self.cols), K, n,
-                      self.band_width, self.n_bands, _lib.ptr(self.bandoff), _lib.stream_ptr())
-        else:
-            cols = self.cols.numpy().view(np.uint32).astype(np.int64)
-            bo = np.zeros((K, n, self.n_bands + 1), np.int64)
-            for k in range(K):
-                counts = np.diff(rp[k])
-                rid = np.repeat(np.arange(n), counts)
-                band = cols[rp[k, 0]:rp[k, -1]] // self.band_width
-                h = np.bincount(rid * self.n_bands + band, minlength=n * self.n_bands)
-                bo[k, :, 1:] = np.cumsum(h.reshape(n, self.n_bands), axis=1)
-            self.bandoff = torch.as_tensor(bo.astype(np.int32))
-        lengths = (rp[:, 1:] - rp[:, :-1]).sum(axis=0)
-        R = self.unit_tiles * T2
-        perm = np.empty(n, np.int64)
-        for u in range(n // R):
-            seg = lengths[u * R:(u + 1) * R]
-            perm[u * R:(u + 1) * R] = u * R + np.argsort(-seg, kind="stable")
-        self.rowperm = torch.as_tensor(perm.astype(np.int32), device=self.rowptr.device)
-        if self.rowptr.is_cuda and R % 32 == 0:
-            self._build_stream(R)
-
-    def _build_stream(self, R):
-        """Frame layout v3: per-unit contiguous (band, k) items for the TMA
-        pipeline (csrc/stream.cu)."""
-        from . import _lib
-
-        n, K, dev = self.n, self.K, self.rowptr.device
-        nitems = (n // R) * self.n_bands * K
-        self.item_len = torch.empty(nitems, dtype=torch.int32, device=dev)
-        self.item_off = torch.empty(nitems, dtype=torch.int64, device=dev)
-        bs = torch.empty((nitems + 1023) // 1024 + 1, dtype=torch.int64, device=dev)
-        total = torch.empty(1, dtype=torch.int64, device=dev)
-        sp = _lib.stream_ptr()
-        args = (_lib.ptr(self.rowptr), _lib.ptr(self.cols), _lib.ptr(self.vals),
-                _lib.ptr(self.bandoff), _lib.ptr(self.rowperm), K, n, self.n_bands, R,
-                self.band_width, _lib.ptr(self.item_len), _lib.ptr(self.item_off))
-        _lib.call("sss_stream_build", 0, *args, _lib.ptr(bs), _lib.ptr(total), None, None, sp)
-        ne = int(total.item())
-        self.rowoff = torch.empty(nitems * (R + 1), dtype=torch.int32, device=dev)
-        self.entries = torch.empty(max(ne, 2), dtype=torch.int64, device=dev)  # 8 B each
-        _lib.call("sss_stream_build", 1, *args, _lib.ptr(bs), _lib.ptr(total),
-                  _lib.ptr(self.rowoff), _lib.ptr(self.entries), sp)
-        self.stream_entries = ne
 
     @property
     def n(self) -> int:
@@ -184,15 +104,15 @@ class DeviceTransfer:
 
     @property
     def nbytes(self) -> int:
-        """Stored bytes of the operator the frame streams (8 B / coefficient
-        + row pointers + band offsets)."""
-        return self.nnz * 8 + self.rowptr.numel() * 8 + self.bandoff.numel() * 4
+        """Stored bytes of the canonical operator (8 B / coefficient + row
+        pointers)."""
+        return self.nnz * 8 + self.rowptr.numel() * 8
 
     @classmethod
     def from_reference(cls, operators, side: int, levels: int, device="cuda",
                        step1_keep=0.0, step2_fraction=0.0) -> "DeviceTransfer":
         """CSC (reference TransferOperator list, flat w0 cols / w1 rows) ->
-        banded tile-major CSR (the PRTS1 bridge direction reference -> B200)."""
+        tile-major CSR (the PRTS1 bridge direction reference -> B200)."""
         n = side * side
         f2t = flat_to_tile_major(np.arange(n), side, levels)
         rowptrs, cols_all, vals_all, nnz = [], [], [], []

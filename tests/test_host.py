@@ -72,7 +72,6 @@ def test_operator_layout_round_trip():
     rp = dt.rowptr.numpy()
     cols = dt.cols.numpy().view(np.uint32)
     vals = dt.vals.numpy().astype(np.float64)
-    bo = dt.bandoff.numpy()
     for k, op in enumerate(ops):
         want = O.csc_apply(op.cols, op.colptr, op.rowidx, op.vals, np.arange(n, dtype=np.uint32), x, n)
         got = np.zeros(n)
@@ -80,17 +79,7 @@ def test_operator_layout_round_trip():
             sl = slice(rp[k, r], rp[k, r + 1])
             assert np.all(np.diff(cols[sl].astype(np.int64)) > 0)  # ascending within a row
             got[perm[r]] = np.dot(vals[sl], x_tm[cols[sl]])
-            # band offsets partition the row by column band
-            for b in range(dt.n_bands):
-                seg = cols[rp[k, r] + bo[k, r, b]: rp[k, r] + bo[k, r, b + 1]]
-                assert np.all(seg // dt.band_width == b)
-            assert bo[k, r, dt.n_bands] == rp[k, r + 1] - rp[k, r]
         assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
-    # rowperm: a permutation within each unit, longest rows first
-    R = dt.unit_tiles * (1 << L) ** 2
-    pr = dt.rowperm.numpy()
-    assert np.array_equal(np.sort(pr), np.arange(n))
-    assert np.all(pr // R == np.arange(n) // R)
 
 
 def _random_device_transfer(rng, side, L, K, per_col):
@@ -122,42 +111,6 @@ def _csr_vk(dt, x_tm):
             sl = slice(rp[k, r], rp[k, r + 1])
             vk[k, :, r] = vals[sl] @ x_tm[cols[sl]]
     return vk
-
-
-def test_kstep_layout_reproduces_csr_product():
-    """The mask-sorted K-fused warp-step layout (sss_transfer_kstep) computes
-    the same v_k as the per-term CSR: emulate the kernel over the layout."""
-    from paper_2203_12339_b200.runtime import kstep_layout
-
-    rng = np.random.default_rng(12)
-    dt = _random_device_transfer(rng, 32, 2, 5, 24)
-    x_tm = rng.standard_normal((dt.n, 3))
-    want = _csr_vk(dt, x_tm)
-    cols, vals, steps, wbeg, W, stats = kstep_layout(dt, warps_per_sm=1)
-    cols = cols.numpy().view(np.uint32)
-    vals = vals.numpy().astype(np.float64)
-    steps = steps.numpy().view(np.uint32)
-    wbeg = wbeg.numpy()
-    assert wbeg[0] == 0 and wbeg[-1] == steps.shape[0] and np.all(np.diff(wbeg) >= 0)
-    assert stats["pairs"] <= int(dt.rowptr[:, -1].max() - dt.rowptr[0, 0])
-    got = np.zeros_like(want)
-    rows_seen = []
-    for s in range(steps.shape[0]):
-        p0, v0, row, info = (int(v) for v in steps[s])
-        mask, cnt, end = info & 0xFF, (info >> 8) & 0xFF, (info >> 16) & 1
-        assert 1 <= cnt <= 32 and v0 % 32 == 0
-        xs = x_tm[cols[p0:p0 + cnt]]
-        j = 0
-        for k in range(8):
-            if mask >> k & 1:
-                v = vals[v0 + 32 * j: v0 + 32 * j + 32]
-                assert np.all(v[cnt:] == 0)
-                got[k, :, row] += v[:cnt] @ xs
-                j += 1
-        if end:
-            rows_seen.append(row)
-    assert len(rows_seen) == len(set(rows_seen))
-    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
 
 
 def test_library_exports_every_header_symbol():
@@ -263,179 +216,54 @@ def test_configs_frozen():
     assert C.STEP2_FRACTION == 0.95 and C.E_KEEP == 0.25
 
 
-def test_kstream_blobs_reproduce_csr_product():
-    """sss_transfer_kstream's per-step blobs [32 columns | popc x 32 values]
-    carry the same v_k as the per-term CSR (kernel emulated on the host)."""
-    from paper_2203_12339_b200.runtime import kstream_layout
+def test_kfr_layout_reproduces_csr_product():
+    """The K-fused row-chunk stream of sss_transfer_kfr (layout.kfr_layout),
+    decoded the way the kernel reads it (compacted words per step, term
+    planes, partial sums of multi-chunk rows), computes the per-term CSR
+    product; every coefficient appears exactly once."""
+    from paper_2203_12339_b200.layout import kfr_layout, kfr_reference_apply
+
+    rng = np.random.default_rng(12)
+    dt = _random_device_transfer(rng, 32, 2, 5, 24)
+    x_tm = rng.standard_normal((dt.n, 3))
+    want = _csr_vk(dt, x_tm)
+    for chunk in (512, 8):  # 8: most rows span several chunks (partial sums)
+        lay = kfr_layout(dt, chunk=chunk)
+        assert lay.stats["entries"] == dt.nnz
+        assert int((lay.lane_len.long() & 0xFFFFFFFF).sum()) == lay.stats["pairs"]
+        if chunk == 8:
+            assert lay.n_partials > 0
+        bo = lay.batch_off.long()
+        assert int(bo[-1, 0]) == lay.stats["pairs"] and int(bo[-1, 1]) == dt.nnz
+        got = kfr_reference_apply(lay, torch.as_tensor(x_tm.T.copy())).numpy()
+        assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("col16", [True, False])
+def test_flat16_layout_reproduces_csr_product(col16):
+    """The flat16 stream (layout.flat16_layout): (row, k) segments padded to 16
+    entries and lane-interleaved, head bits at segment starts."""
+    from paper_2203_12339_b200.layout import flat16_layout
 
     rng = np.random.default_rng(13)
-    dt = _random_device_transfer(rng, 32, 2, 6, 20)
+    dt = _random_device_transfer(rng, 32, 2, 5, 24)
     x_tm = rng.standard_normal((dt.n, 3))
     want = _csr_vk(dt, x_tm)
-    blob, recs, wbeg, W, stats = kstream_layout(dt, warps_per_sm=1)
-    blob = blob.numpy()
-    recs = recs.numpy().view(np.uint32)
-    wbeg = wbeg.numpy()
-    assert wbeg[0] == 0 and wbeg[-1] == recs.shape[0] and W % 8 == 0
-    bcols = blob.view(np.uint32)
-    bvals = blob.view(np.float32).astype(np.float64)
+    pcols, pvals, ne, heads, hpre, rowk, wbeg, W, st = flat16_layout(dt, warps_per_sm=1, col16=col16)
+    cols = pcols.numpy().astype(np.int64) & (0xFFFF if col16 else 0xFFFFFFFF)
+    vals = pvals.numpy().astype(np.float64)
+    hb = heads.numpy().view(np.uint32)
+    rowk = rowk.numpy()
+    ng = ne // 16
+    starts = [g for g in range(ng) if (hb[g // 32] >> (g % 32)) & 1]
+    assert len(starts) == rowk.size and starts[0] == 0
+    xpad = np.vstack([x_tm, np.zeros((1, 3))])
     got = np.zeros_like(want)
-    for s in range(recs.shape[0]):
-        off, row, info = int(recs[s, 0]) * 4, int(recs[s, 1]), int(recs[s, 2])
-        mask, cnt = info & 0xFF, (info >> 8) & 0xFF
-        assert np.all(bcols[off + cnt: off + 32] == 0)
-        xs = x_tm[bcols[off: off + 32]]
-        j = 0
-        for k in range(8):
-            if mask >> k & 1:
-                got[k, :, row] += bvals[off + 32 + 32 * j: off + 64 + 32 * j] @ xs
-                j += 1
-        if s + 1 < recs.shape[0]:
-            assert int(recs[s + 1, 0]) * 4 == off + 32 * (1 + j)  # contiguous blobs
-    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
-
-
-def test_kgroup_layout_reproduces_csr_product():
-    """sss_transfer_kgroup's K-packed, 32-padded row pieces carry the same v_k
-    as the per-term CSR (kernel emulated on the host, unkept columns skipped)."""
-    from paper_2203_12339_b200.runtime import kgroup_layout
-
-    rng = np.random.default_rng(14)
-    dt = _random_device_transfer(rng, 32, 2, 7, 40)
-    x_tm = rng.standard_normal((dt.n, 3))
-    x_tm[rng.random(dt.n) < 0.6] = 0.0  # unkept columns
-    want = _csr_vk(dt, x_tm)
-    meta, vals, pieces, wbeg, W, stats = kgroup_layout(dt, warps_per_sm=1, split=64)
-    assert stats["pieces"] > dt.n - np.count_nonzero(
-        (dt.rowptr[:, 1:] - dt.rowptr[:, :-1]).sum(0).numpy() == 0)  # some rows split
-    meta = meta.numpy().view(np.uint32)
-    vals = vals.numpy().astype(np.float64)
-    pieces = pieces.numpy().view(np.uint32)
-    wbeg = wbeg.numpy()
-    assert wbeg[0] == 0 and wbeg[-1] == pieces.shape[0] and np.all(np.diff(wbeg) >= 0)
-    kept = np.any(x_tm != 0, axis=1)
-    got = np.zeros_like(want)
-    for p0, npair, v0, row in pieces:
-        assert p0 % 32 == 0 and npair % 32 == 0 and 0 < npair <= 64
-        off = v0
-        for m in meta[p0:p0 + npair]:
-            mask, col = int(m) >> 24, int(m) & 0xFFFFFF
-            for k in range(8):
-                if mask >> k & 1:
-                    if kept[col]:
-                        got[k, :, row] += vals[off] * x_tm[col]
-                    off += 1
-    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
-
-
-@pytest.mark.parametrize("group,perm", [(4, False), (8, False), (8, True)])
-def test_flat_stream_layout_reproduces_csr_product(group, perm):
-    """sss_transfer_flat's head-flag bitmap / segment prefix over the padded
-    operator copy recover every segment's (row, k): emulate the segmented
-    warp-stream on the host, including warp ranges that cut segments."""
-    from paper_2203_12339_b200.runtime import flat_layout
-
-    rng = np.random.default_rng(15)
-    dt = _random_device_transfer(rng, 32, 2, 5, 30)
-    x_tm = rng.standard_normal((dt.n, 3))
-    want = _csr_vk(dt, x_tm)
-    from paper_2203_12339_b200.runtime import block_column_order
-
-    order = None
-    if perm:
-        new_of, tm_of = block_column_order(32, 2)
-        assert np.array_equal(np.sort(new_of), np.arange(dt.n))
-        order = new_of
-        x_tm = x_tm[tm_of]  # the kernel reads x in the permuted column order
-    pcols, pvals, ne, heads, hpre, rowk, wbeg, W, stats = flat_layout(dt, warps_per_sm=1,
-                                                                       group=group, col_order=order)
-    c4 = pcols.numpy().view(np.uint32).reshape(-1, group)
-    v4 = pvals.numpy().astype(np.float64).reshape(-1, group)
-    heads = heads.numpy().view(np.uint32)
-    hpre = hpre.numpy().view(np.uint32)
-    rowk = rowk.numpy().view(np.uint32)
-    wbeg = wbeg.numpy()
-    assert ne == c4.size and wbeg[0] == 0 and wbeg[-1] == heads.size
-    got = np.zeros_like(want)
-    n4 = c4.shape[0]
-    for w in range(W):
-        for i in range(wbeg[w], wbeg[w + 1]):
-            for lane in range(32):
-                q = 32 * i + lane
-                if q >= n4:
-                    continue
-                hm = int(heads[i]) & ((2 << lane) - 1)
-                pid = int(hpre[i]) + bin(hm).count("1") - 1
-                rk = int(rowk[pid])
-                got[rk & 15, :, rk >> 4] += v4[q] @ x_tm[c4[q]]
-    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
-
-
-def test_regional_layout_reproduces_csr_product():
-    """v19 regional layout: region-local slots map back to columns through
-    each region's union list; regions span whole 256-entry iterations; the
-    head-flag stream gives every segment's (row, k) (host emulation)."""
-    from paper_2203_12339_b200.runtime import regional_layout
-
-    rng = np.random.default_rng(19)
-    dt = _random_device_transfer(rng, 32, 2, 4, 30)
-    x_tm = rng.standard_normal((dt.n, 3))
-    x_tm[rng.random(dt.n) < 0.5] = 0.0
-    want = _csr_vk(dt, x_tm)
-    R = regional_layout(dt)
-    c8 = R["pcols"].numpy().view(np.uint32).reshape(-1, 8)
-    v8 = R["pvals"].numpy().astype(np.float64).reshape(-1, 8)
-    heads = R["heads"].numpy().view(np.uint32)
-    hpre = R["hpre"].numpy().view(np.uint32)
-    rowk = R["rowk"].numpy().view(np.uint32)
-    ucols = R["ucols"].numpy().view(np.uint32)
-    uoff = R["uoff"].numpy()
-    rit = R["rit"].numpy()
-    T2 = 16
-    assert rit[-1] * 32 == c8.shape[0] or rit[-1] * 32 >= c8.shape[0] - 31
-    got = np.zeros_like(want)
-    for r in range(R["n_regions"]):
-        u = ucols[uoff[r]:uoff[r + 1]]
-        assert np.all(np.diff(u.astype(np.int64)) > 0)
-        for i in range(rit[r], rit[r + 1]):
-            for lane in range(32):
-                q = 32 * i + lane
-                if q >= c8.shape[0]:
-                    continue
-                hm = int(heads[i]) & ((2 << lane) - 1)
-                pid = int(hpre[i]) + bin(hm).count("1") - 1
-                rk = int(rowk[pid])
-                assert (rk >> 4) // T2 == r  # the segment belongs to this region
-                got[rk & 15, :, rk >> 4] += v8[q] @ x_tm[u[c8[q]]]
-    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
-
-
-def test_k8_dense_pairs_layout_reproduces_csr_product():
-    """v20 dense K-fused pairs: one lane per (row, column) pair with its K
-    values at slots 0..K-1; padding pairs carry column N (host emulation)."""
-    from paper_2203_12339_b200.runtime import k8_layout
-
-    rng = np.random.default_rng(20)
-    dt = _random_device_transfer(rng, 32, 2, 6, 30)
-    x_tm = rng.standard_normal((dt.n, 3))
-    x_tm[rng.random(dt.n) < 0.5] = 0.0
-    want = _csr_vk(dt, x_tm)
-    cols, vals, pieces, wbeg, W, stats = k8_layout(dt, warps_per_sm=1, split=64)
-    cols = cols.numpy().view(np.uint32)
-    vals = vals.numpy().astype(np.float64)
-    pieces = pieces.numpy()
-    wbeg = wbeg.numpy()
-    assert wbeg[0] == 0 and wbeg[-1] == pieces.shape[0]
-    got = np.zeros_like(want)
-    for p0, pn, row, _ in pieces:
-        assert p0 % 32 == 0 and pn % 32 == 0 and 0 < pn <= 64
-        for p in range(p0, p0 + pn):
-            c = int(cols[p])
-            if c >= dt.n:
-                assert np.all(vals[p] == 0)
-                continue
-            for k in range(dt.K):
-                got[k, :, row] += vals[p, k] * x_tm[c]
+    for i, g0 in enumerate(starts):
+        g1 = starts[i + 1] if i + 1 < len(starts) else ng
+        sl = slice(g0 * 16, g1 * 16)
+        r, k = rowk[i] >> 4, rowk[i] & 15
+        got[k, :, r] += vals[sl] @ xpad[cols[sl]]
     assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
 
 

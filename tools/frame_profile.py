@@ -63,7 +63,7 @@ def main():
         _lib.ptr(sc.mask), _lib.ptr(sc.energy), sp), a.reps)
     out["material_weights"] = timed(sc._launch_weights, a.reps)
     ref_vk = None
-    for kern in ("flat8", "k8"):
+    for kern in ("kfr", "flat16"):
         sc.transfer_kernel = kern
         sc.vk.fill_(float("nan"))
         sc._launch_transfer()
@@ -74,9 +74,8 @@ def main():
             ref_vk = sc.vk.clone()
         else:
             out[f"relerr_{kern}"] = float((sc.vk - ref_vk).abs().max() / ref_vk.abs().max())
-    out["flat8_MB"] = dt.flat8[8]["bytes"] / 1e6
-    out.update({f"k8_{k}": v for k, v in dt.k8[5].items()})
-    sc.transfer_kernel = "flat8"
+    out.update({f"kfr_{k}": v for k, v in dt.kfr.stats.items()})
+    sc.transfer_kernel = "kfr"
     out["edit_finish"] = timed(sc._launch_edit, a.reps)
     sc.capture()
     out["relight_graph"] = timed(lambda: sc.replay(False), a.reps)

@@ -1,8 +1,9 @@
-"""A/B of transfer kernels on the C3 operator: per kernel, the core launch
+"""A/B of the transfer kernels on the C3 operator: per kernel, the core launch
 timed alone with CUDA events (inputs prepared by a relight), v_k agreement
-with flat8, and layout stats.
+with kfr, and layout stats. Environment knobs (SSS_KFR_CHUNK, SSS_KFR_MINB)
+apply to every Scene the tool builds.
 
-    python tools/transfer_ab.py [kpairs flat8 ...]
+    python tools/transfer_ab.py [kfr flat16]
 """
 import json
 import sys
@@ -21,13 +22,13 @@ def main():
     from paper_2203_12339_b200.runtime import EnvLight
 
     _lib.load()
-    kerns = sys.argv[1:] or ["flat8", "kpairs"]
+    kerns = sys.argv[1:] or ["kfr", "flat16"]
     cfg = CONFIGS["env_large_256"]
     g, b, dt, env, sc = B.setup_scene(cfg, 0, torch, {})
     sc.set_light(EnvLight(env.faces(3.0)))
     ref = None
     out = {}
-    for kern in ["flat8"] + [k for k in kerns if k != "flat8"]:
+    for kern in ["kfr"] + [k for k in kerns if k != "kfr"]:
         sc.transfer_kernel = kern
         sc._graph = None
         sc.relight()
@@ -46,8 +47,8 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         st = getattr(dt, kern, None)
-        out[kern] = {"us": 1e3 * e0.elapsed_time(e1) / reps, "rel_err_vs_flat8": err,
-                     "stats": st[-1] if isinstance(st, tuple) and isinstance(st[-1], dict) else None}
+        stats = st.stats if hasattr(st, "stats") else (st[-1] if isinstance(st, tuple) else None)
+        out[kern] = {"us": 1e3 * e0.elapsed_time(e1) / reps, "rel_err_vs_kfr": err, "stats": stats}
         print(json.dumps({kern: out[kern]}), flush=True)
 
 
