@@ -191,22 +191,27 @@ int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const 
  *      sss_pack_x_bits's packing of the kept spectrum x (3, n_rows).
  *
  * sss_transfer_kfr ("K-fused rows", default): the operator as a stream of
- *   (column, term-mask) pairs per receiver-row chunk (layout.kfr_layout):
- *   items (n_items x {first batch, steps}), lane_len / lane_dst (32 per item:
- *   chunk length; row, 0x80000000 | partial slot, or 0xffffffff), batch_off
- *   ({word, value} offsets of every 4-step batch + a sentinel), cm (col | mask
- *   << 16 words), vals (f32, term planes), partials ((3K, n_partials) f64
- *   scratch), partial_row (multi-chunk row index of each slot), multi_info
- *   ({row, first slot, count, 0} per multi-chunk row), multi_count (zeroed u32
- *   per multi-chunk row; left zero on return). Writes every row of vk (no
- *   memset), bitwise reproducible. K <= 16, n_rows <= 65536. n_warps: warps
- *   launched (multiple of 4), min_blocks: CTAs of 128 threads per SM. */
+ *   (column, term-mask) pairs per (receiver row, group of 4 terms) chunk
+ *   (layout.kfr_layout): items (n_items x {first batch, steps}), lane_len /
+ *   lane_dst (32 per item: chunk length; row | group << 16, 0x80000000 |
+ *   partial slot, or 0xffffffff), batch_off (byte offset of every batch in
+ *   stream_bytes + a sentinel, multiples of 16), stream_bytes (per batch of
+ *   steps_per_batch (4 or 8) steps: 32 words per step {col | mask << 16 |
+ *   value offset << 20, 0 = no pair}, then the f32 values lane-major per
+ *   step, padded to 16 bytes), partials ((12, n_partials) f64 scratch),
+ *   partial_row (multi-chunk index of each slot), multi_info ({row, first
+ *   slot, count, group} per multi-chunk (row, group)), multi_count (zeroed
+ *   u32 per multi-chunk (row, group); left zero on return), work (two zeroed
+ *   u32: item claim and CTA exit counters; left zero on return). Writes every
+ *   row of vk (no memset), bitwise reproducible. K <= 16, n_rows <= 65536.
+ *   n_warps: warps launched (multiple of 8), min_blocks: CTAs of 256 threads
+ *   per SM (3 for 4-step batches, 2 for 8-step batches). */
 int sss_transfer_kfr(int K, int n_rows, unsigned n_items, unsigned n_partials, const void* items,
-                     const uint32_t* lane_len, const uint32_t* lane_dst, const void* batch_off,
-                     const uint32_t* cm, const float* vals, const void* xp, const uint32_t* bits,
+                     const uint32_t* lane_len, const uint32_t* lane_dst, const uint32_t* batch_off,
+                     const void* stream_bytes, const void* xp, const uint32_t* bits,
                      double* vk, double* partials, const uint32_t* partial_row,
-                     const void* multi_info, uint32_t* multi_count, int n_warps, int min_blocks,
-                     void* stream);
+                     const void* multi_info, uint32_t* multi_count, uint32_t* work,
+                     int steps_per_batch, int n_warps, int min_blocks, void* stream);
 
 /* sss_pack_x_bits: xp (n, 4) f64 = {x0, x1, x2, 0} of the kept spectrum
  *   x (3, n) and the kept-column bitmap (bit c set iff any channel is kept). */

@@ -410,40 +410,38 @@ int sss_fold_emit(const double* FT, int n_rows, int n_dirs, const uint32_t* flat
 
 // stage 2, K-fused rows (csrc/transfer.cu; layout built by layout.kfr_layout)
 int sss_transfer_kfr(int K, int n_rows, unsigned n_items, unsigned n_partials, const void* items,
-                     const uint32_t* lane_len, const uint32_t* lane_dst, const void* batch_off,
-                     const uint32_t* cm, const float* vals, const void* xp, const uint32_t* bits,
+                     const uint32_t* lane_len, const uint32_t* lane_dst, const uint32_t* batch_off,
+                     const void* stream_bytes, const void* xp, const uint32_t* bits,
                      double* vk, double* partials, const uint32_t* partial_row,
-                     const void* multi_info, uint32_t* multi_count, int n_warps, int min_blocks,
-                     void* stream) {
-  if (K <= 0 || K > 16 || n_rows <= 0 || n_rows > 65536 || !items || !lane_len || !lane_dst ||
-      !batch_off || !cm || !vals || !xp || !bits || !vk || n_warps <= 0 ||
+                     const void* multi_info, uint32_t* multi_count, uint32_t* work,
+                     int steps_per_batch, int n_warps, int min_blocks, void* stream) {
+  if ((steps_per_batch != 4 && steps_per_batch != 8) || K <= 0 || K > 4 * sss::kKfrG || n_rows <= 0 || n_rows > 65536 || !items || !lane_len ||
+      !lane_dst || !batch_off || !stream_bytes || !xp || !bits || !vk || !work || n_warps <= 0 ||
       n_warps % sss::kKfrWarps)
     return fail(SSS_EINVAL, "bad transfer_kfr arguments");
   if (n_partials && (!partials || !partial_row || !multi_info || !multi_count))
     return fail(SSS_EINVAL, "transfer_kfr: partial buffers required");
-  if (reinterpret_cast<uintptr_t>(cm) % 16 || reinterpret_cast<uintptr_t>(vals) % 16 ||
-      reinterpret_cast<uintptr_t>(xp) % 32)
-    return fail(SSS_EINVAL, "transfer_kfr: cm / vals 16-byte and xp 32-byte aligned");
+  if (reinterpret_cast<uintptr_t>(stream_bytes) % 16 || reinterpret_cast<uintptr_t>(xp) % 32)
+    return fail(SSS_EINVAL, "transfer_kfr: stream 16- and xp 32-byte aligned");
   if (n_items == 0) return SSS_OK;
-  const int KS = K <= 4 ? 4 : K <= 8 ? 8 : K <= 12 ? 12 : 16;
-  const size_t smem = sss::kfr_smem_bytes(KS, n_rows);
+  const int ns = getenv("SSS_KFR_SLOTS") ? atoi(getenv("SSS_KFR_SLOTS")) : 3;  // A/B knob
   unsigned grid = (unsigned)(n_warps / sss::kKfrWarps);
   const unsigned need = (n_items + sss::kKfrWarps - 1) / sss::kKfrWarps;
   if (grid > need) grid = need;
-#define SSS_KFR(KK, MB)                                                                          \
-  if (K <= KK && min_blocks == MB) {                                                             \
-    if (int r = set_smem((const void*)sss::k_transfer_kfr<KK, MB>, smem)) return r;              \
-    sss::k_transfer_kfr<KK, MB><<<grid, sss::kKfrWarps * 32, smem, S_(stream)>>>(                \
+#define SSS_KFR(UU, NS, MB)                                                                      \
+  if (steps_per_batch == UU && ns == NS && min_blocks == MB) {                                   \
+    const size_t smem = sss::kfr_smem_bytes(n_rows, sss::KfrSmem<UU, NS>::WARP);                 \
+    if (int r = set_smem((const void*)sss::k_transfer_kfr<UU, NS, MB>, smem)) return r;          \
+    sss::k_transfer_kfr<UU, NS, MB><<<grid, sss::kKfrWarps * 32, smem, S_(stream)>>>(            \
         n_rows, K, n_items, n_partials, reinterpret_cast<const uint2*>(items), lane_len,         \
-        lane_dst,                                                                                 \
-        reinterpret_cast<const uint2*>(batch_off), cm, vals,                                     \
+        lane_dst, batch_off, reinterpret_cast<const unsigned char*>(stream_bytes),               \
         reinterpret_cast<const double4*>(xp), bits, vk, partials, partial_row,                   \
-        reinterpret_cast<const uint4*>(multi_info), multi_count);                                \
+        reinterpret_cast<const uint4*>(multi_info), multi_count, work);                          \
     return check_launch("k_transfer_kfr");                                                       \
   }
-  SSS_KFR(4, 4) SSS_KFR(8, 4) SSS_KFR(8, 3) SSS_KFR(12, 3) SSS_KFR(16, 2)
+  SSS_KFR(4, 3, 3) SSS_KFR(4, 2, 3) SSS_KFR(4, 4, 2) SSS_KFR(8, 3, 2) SSS_KFR(4, 3, 2)
 #undef SSS_KFR
-  return fail(SSS_EINVAL, "transfer_kfr: (K <= 4, min_blocks 4), (K <= 8, 3 or 4), (K <= 12, 3), (K <= 16, 2)");
+  return fail(SSS_EINVAL, "transfer_kfr: (steps_per_batch, slots, min_blocks) in {(4,3,3), (4,2,3), (4,4,2), (8,3,2), (4,3,2)}");
 }
 
 int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const uint32_t* rows,

@@ -66,36 +66,42 @@ __device__ __forceinline__ void v15_gather1(const double4* __restrict__ xp, uint
   (void)x3;
 }
 
-constexpr int kKfrWarps = 4;  // warps per CTA (independent; each owns its smem ring)
-constexpr int kKfrU = 4;      // steps per staged batch
+constexpr int kKfrWarps = 8;  // warps per CTA (independent; each owns its smem ring)
+constexpr int kKfrG = 4;      // terms per group: a chunk accumulates G terms x 3 channels
+constexpr int kKfrMaxBatches = 128;  // batches per item (chunk length <= 128 * steps per batch)
 
-template <int K>
+template <int U, int NS>  // steps per staged batch, ring slots per warp
 struct KfrSmem {
-  // one batch: <= U*32 words and <= U*32*K values, + 32 bytes of alignment
-  // slack each (the bulk copies start and end on 16-byte boundaries)
-  static constexpr int CMB = kKfrU * 32 * 4 + 32;
-  static constexpr int VB = kKfrU * 32 * K * 4 + 32;
-  static constexpr int SLOT = CMB + VB;
-  static constexpr int WARP = 2 * SLOT + 16;  // two slots + two mbarriers
+  // one batch of the stream: U*32 pair words (dense per step), then <= U*32*G
+  // values, padded to 16 bytes (one bulk copy per batch)
+  static constexpr int WB = U * 32 * 4;
+  static constexpr int VB = U * 32 * kKfrG * 4;
+  static constexpr int SLOT = (WB + VB + 15) / 16 * 16;
+  static_assert(WB % 16 == 0, "word block must keep 16-byte alignment");
+  // the item's batch offsets (<= kKfrMaxBatches + 1 u32)
+  static constexpr int BOFF = (kKfrMaxBatches + 1) * 4;
+  // NS slots + NS mbarriers + offsets, 128-byte aligned (bulk copies need 16)
+  static constexpr int WARP = ((NS * SLOT + 8 * NS + BOFF) + 127) / 128 * 128;
 };
 
-inline size_t kfr_smem_bytes(int K, int N) {
+inline size_t kfr_smem_bytes(int N, size_t warp_bytes) {
   const size_t bits = (((size_t)((N >> 5) + 1) * 4 + 127) / 128) * 128;
-  const size_t slot = (size_t)(kKfrU * 32 * 4 + 32) + (size_t)(kKfrU * 32 * K * 4 + 32);
-  return bits + (size_t)kKfrWarps * (2 * slot + 16);
+  return bits + (size_t)kKfrWarps * warp_bytes;
 }
 
-// K = accumulator slots (>= the operator's term count Kr; mask bits >= Kr are
-// never set)
-template <int K, int MINB>
+// Pair word: col (bits 0-15) | term mask within the group (16-19) | offset of
+// the lane's first value in the step's value block (20-26); 0 = no pair.
+template <int U, int NS, int MINB>
 __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
     int N, int Kr, unsigned n_items, unsigned n_partials, const uint2* __restrict__ items,
     const uint32_t* __restrict__ lane_len, const uint32_t* __restrict__ lane_dst,
-    const uint2* __restrict__ boff, const uint32_t* __restrict__ cm, const float* __restrict__ vals,
-    const double4* __restrict__ xp, const uint32_t* __restrict__ bits, double* __restrict__ vk,
-    double* __restrict__ part, const uint32_t* __restrict__ part_row,
-    const uint4* __restrict__ minfo, unsigned* __restrict__ mcount) {
-  using SM = KfrSmem<K>;
+    const uint32_t* __restrict__ boff, const unsigned char* __restrict__ stream,
+    const double4* __restrict__ xp,
+    const uint32_t* __restrict__ bits, double* __restrict__ vk, double* __restrict__ part,
+    const uint32_t* __restrict__ part_row, const uint4* __restrict__ minfo,
+    unsigned* __restrict__ mcount, unsigned* __restrict__ work) {
+  using SM = KfrSmem<U, NS>;
+  constexpr int G = kKfrG;
   extern __shared__ __align__(128) unsigned char kfr_smem[];
   const int nbw = (N >> 5) + 1;
   const int bits_bytes = ((nbw * 4 + 127) / 128) * 128;
@@ -103,115 +109,151 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
   for (int t = threadIdx.x; t < nbw; t += blockDim.x) sbits[t] = bits[t];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wb = kfr_smem + bits_bytes + wid * SM::WARP;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wb + 2 * SM::SLOT);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wb + NS * SM::SLOT);
+  uint32_t* sboff = reinterpret_cast<uint32_t*>(wb + NS * SM::SLOT + 8 * NS);
   if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int j = 0; j < NS; ++j) mbar_init(&bar[j], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
-  unsigned seq = 0;  // batches consumed by this warp: slot seq & 1, parity (seq >> 1) & 1
-  const unsigned nwarps = gridDim.x * kKfrWarps;
+  // batches consumed by this warp: slot seq % NS, parity (seq / NS) & 1; the
+  // ring runs NS - 1 batches ahead of the consumer
+  unsigned seq = 0;
 
-  auto issue = [&](unsigned b, unsigned slot) {
+  // batch b = stream bytes [boff[b], boff[b + 1]), 16-byte aligned. The slot
+  // was last read by this warp (its loads completed before the __syncwarp
+  // that ended that batch): no proxy fence is needed for the write-after-read
+  auto issue = [&](unsigned b, unsigned slot) {  // b: batch of the current item
     if (lane == 0) {
-      const uint2 o0 = __ldg(&boff[b]), o1 = __ldg(&boff[b + 1]);
-      const unsigned ca = (o0.x * 4u) & ~15u, ce = (o1.x * 4u + 15u) & ~15u;
-      const unsigned va = (o0.y * 4u) & ~15u, ve = (o1.y * 4u + 15u) & ~15u;
-      unsigned char* s = wb + slot * SM::SLOT;
-      fence_proxy_async();
-      mbar_expect_tx(&bar[slot], (ce - ca) + (ve - va));
-      bulk_g2s(s, reinterpret_cast<const unsigned char*>(cm) + ca, ce - ca, &bar[slot]);
-      bulk_g2s(s + SM::CMB, reinterpret_cast<const unsigned char*>(vals) + va, ve - va, &bar[slot]);
+      const unsigned a0 = sboff[b], a1 = sboff[b + 1];
+      mbar_expect_tx(&bar[slot], a1 - a0);
+      bulk_g2s(wb + slot * SM::SLOT, stream + a0, a1 - a0, &bar[slot]);
     }
   };
 
-  for (unsigned item = blockIdx.x * kKfrWarps + wid; item < n_items; item += nwarps) {
+  for (;;) {
+    // items are ordered longest first; warps claim them dynamically (the
+    // counters are reset by the last CTA out, so graph replays work)
+    unsigned item = 0;
+    if (lane == 0) item = atomicAdd(&work[0], 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
     const uint2 it = __ldg(&items[item]);
-    const unsigned b0 = it.x, S = it.y, nb = (S + kKfrU - 1) / kKfrU;
-    const unsigned len = __ldg(&lane_len[item * 32 + lane]);
-    double acc[K][3];
+    const unsigned b0 = it.x, S = it.y, nb = (S + U - 1) / U;
+    // the item's batch offsets, staged once (the issuing lane reads them from
+    // shared memory instead of an L2 round trip per batch)
+    for (unsigned j = lane; j <= nb; j += 32) sboff[j] = __ldg(&boff[b0 + j]);
+    __syncwarp();
+    double acc[G][3];
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
-    if (nb) issue(b0, seq & 1u);
+    for (int k = 0; k < G; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
+    // x of the last gathered pair per step slot: finite, so an absent or
+    // unkept term's 0 * x leaves the accumulators exactly unchanged
+    double xa[U][3];
+#pragma unroll
+    for (int t = 0; t < U; ++t) xa[t][0] = xa[t][1] = xa[t][2] = 0.0;
+#pragma unroll
+    for (int j = 0; j < NS - 1; ++j)
+      if ((unsigned)j < nb) issue(j, (seq + j) % NS);
 #pragma unroll 1
     for (unsigned b = 0; b < nb; ++b) {
-      const unsigned slot = seq & 1u, par = (seq >> 1) & 1u;
-      if (b + 1 < nb) issue(b0 + b + 1, slot ^ 1u);
-      const uint2 o0 = __ldg(&boff[b0 + b]);
-      mbar_wait_warp(&bar[slot], par);
+      const unsigned slot = seq % NS, par = (seq / NS) & 1u;
+      if (b + NS - 1 < nb) issue(b + NS - 1, (seq + NS - 1) % NS);
+      mbar_wait_warp_spin(&bar[slot], par);
       ++seq;
-      const uint32_t* scm = reinterpret_cast<const uint32_t*>(wb + slot * SM::SLOT) + (o0.x & 3u);
-      const float* sv = reinterpret_cast<const float*>(wb + slot * SM::SLOT + SM::CMB) + (o0.y & 3u);
-      // phase A: this batch's pair words, kept test, x gathers (U in flight)
-      uint32_t w[kKfrU];
-      bool kp[kKfrU];
-      double xa[kKfrU][3];
-      unsigned co = 0;
+      const uint32_t* sw = reinterpret_cast<const uint32_t*>(wb + slot * SM::SLOT);
+      const float* sv = reinterpret_cast<const float*>(wb + slot * SM::SLOT + SM::WB);
+      // phase A: pair words (0 past the chunk's end), kept test, x gathers
+      // (U in flight per lane)
+      uint32_t w[U];
+      bool kp[U];
 #pragma unroll
-      for (int t = 0; t < kKfrU; ++t) {
-        const bool act = b * kKfrU + t < len;
-        const unsigned am = __ballot_sync(0xffffffffu, act);
-        w[t] = act ? scm[co + __popc(am & lt)] : 0u;
-        co += __popc(am);
+      for (int t = 0; t < U; ++t) {
+        w[t] = sw[t * 32 + lane];
         const uint32_t c = w[t] & 0xffffu;
-        kp[t] = act && ((sbits[c >> 5] >> (c & 31u)) & 1u);
-        xa[t][0] = xa[t][1] = xa[t][2] = 0.0;
+        kp[t] = (w[t] >> 16) != 0u && ((sbits[c >> 5] >> (c & 31u)) & 1u);
         if (kp[t]) gather_x(xp, c, xa[t][0], xa[t][1], xa[t][2]);
       }
-      // phase B: term planes, fp64 accumulation in (step, term) order
-      unsigned vo = 0;
+      // phase B: the lane's values (lane-major in the step block), fp64
+      // accumulation in (step, term) order; absent / unkept terms add 0 * x
+      unsigned vbase = 0;
 #pragma unroll
-      for (int t = 0; t < kKfrU; ++t) {
-        const uint32_t m = w[t] >> 16;  // 0 on inactive lanes
+      for (int t = 0; t < U; ++t) {
+        const uint32_t m = (w[t] >> 16) & 0xfu;
+        const float* sl = sv + vbase + ((w[t] >> 20) & 0x7fu);
+        const uint32_t mk = kp[t] ? m : 0u;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const unsigned bk = __ballot_sync(0xffffffffu, (m >> k) & 1u);
-          if (bk) {
-            if (kp[t] && ((m >> k) & 1u)) {
-              const double v = (double)sv[vo + __popc(bk & lt)];
-              acc[k][0] = fma(v, xa[t][0], acc[k][0]);
-              acc[k][1] = fma(v, xa[t][1], acc[k][1]);
-              acc[k][2] = fma(v, xa[t][2], acc[k][2]);
-            }
-            vo += __popc(bk);
-          }
+        for (int k = 0; k < G; ++k) {
+          const float vf = ((mk >> k) & 1u) ? sl[__popc(m & ((1u << k) - 1u))] : 0.0f;
+          const double v = (double)vf;
+          acc[k][0] = fma(v, xa[t][0], acc[k][0]);
+          acc[k][1] = fma(v, xa[t][1], acc[k][1]);
+          acc[k][2] = fma(v, xa[t][2], acc[k][2]);
         }
+        vbase += __reduce_add_sync(0xffffffffu, __popc(m));
       }
       __syncwarp();  // every lane is done with this slot before it is refilled
     }
     const unsigned dst = __ldg(&lane_dst[item * 32 + lane]);
-    if (dst == 0xffffffffu) continue;  // padding lane of the last item
-    if (!(dst & 0x80000000u)) {
+    if (dst != 0xffffffffu && !(dst & 0x80000000u)) {  // a whole (row, term group)
+      const unsigned row = dst & 0xffffu, k0 = (dst >> 16) * G;
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (k < Kr)
+      for (int k = 0; k < G; ++k)
+        if (k0 + k < (unsigned)Kr)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) vk[((size_t)k * 3 + c) * N + dst] = acc[k][c];
-      continue;
-    }
-    // one chunk of a long row: partial sums; the last arriving chunk of the
-    // row adds all of them in chunk order (the sum order is fixed)
-    const unsigned p = dst & 0x7fffffffu;
+          for (int c = 0; c < 3; ++c) vk[((size_t)(k0 + k) * 3 + c) * N + row] = acc[k][c];
+    } else if (dst != 0xffffffffu) {
+      // one chunk of a long (row, group): partial sums; the last arriving
+      // chunk adds all of them in chunk order (the sum order is fixed)
+      const unsigned p = dst & 0x7fffffffu;
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-      if (k < Kr)
+      for (int k = 0; k < G; ++k)
 #pragma unroll
         for (int c = 0; c < 3; ++c) part[((size_t)k * 3 + c) * n_partials + p] = acc[k][c];
-    __threadfence();
-    const unsigned m = __ldg(&part_row[p]);
-    const uint4 mi = __ldg(&minfo[m]);  // (row, first partial, count, -)
-    const unsigned old = atomicAdd(&mcount[m], 1u);
-    if (old == mi.z - 1u) {
       __threadfence();
+      const unsigned m = __ldg(&part_row[p]);
+      const uint4 mi = __ldg(&minfo[m]);  // (row, first partial, count, group)
+      const unsigned old = atomicAdd(&mcount[m], 1u);
+      if (old == mi.z - 1u) {
+        __threadfence();
+        // fixed order: i ascending per component; the loads of 8 chunks x 3
+        // channels are issued together (the adds stay in order)
 #pragma unroll 1
-      for (int j = 0; j < 3 * Kr; ++j) {
-        double s = 0.0;
-        for (unsigned i = 0; i < mi.z; ++i) s += __ldcg(&part[(size_t)j * n_partials + mi.y + i]);
-        vk[(size_t)j * N + mi.x] = s;
+        for (int k = 0; k < G; ++k) {
+          if (mi.w * G + k >= (unsigned)Kr) break;
+          double sum[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
+          for (unsigned i0 = 0; i0 < mi.z; i0 += 8) {
+            double q[3][8];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                q[c][i] = (i0 + i < mi.z)
+                              ? __ldcg(&part[(size_t)(k * 3 + c) * n_partials + mi.y + i0 + i]) : 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (i0 + i < mi.z) sum[c] += q[c][i];
+          }
+#pragma unroll
+          for (int c = 0; c < 3; ++c) vk[((size_t)(mi.w * G + k) * 3 + c) * N + mi.x] = sum[c];
+        }
+        mcount[m] = 0u;  // ready for the next frame
       }
-      mcount[m] = 0u;  // ready for the next frame
+    }
+    __syncwarp();
+  }
+  // the last CTA out resets the claim counters for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&work[1], 1u) == gridDim.x - 1u) {
+      work[0] = 0u;
+      work[1] = 0u;
+      __threadfence();
     }
   }
 }

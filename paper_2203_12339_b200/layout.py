@@ -7,10 +7,10 @@ ascending within a row) and f32 ``vals`` — the reference's
 columns). The per-frame kernels read copies of it rearranged for the GPU:
 
 * ``kfr_layout`` — the K-fused row-chunk stream of ``sss_transfer_kfr``
-  (csrc/transfer.cu, the default): the K terms of a receiver row merged into
-  (column, term-mask) pairs, rows cut into chunks of <= ``chunk`` pairs, 32
-  chunks per warp item, one pair per lane per step, the f32 values in term
-  planes. Built on the device with torch in a few hundred milliseconds.
+  (csrc/transfer.cu, the default): the terms of a receiver row merged, in
+  groups of 4, into (column, term-mask) pairs, (row, group)s cut into chunks
+  of <= ``chunk`` pairs, 32 chunks per warp item, one pair per lane per step.
+  Built on the device with torch in well under a second.
 * ``flat16_layout`` — the flat (row, k)-segment stream of
   ``sss_transfer_flat16`` (csrc/flat16_25.cu), kept as the A/B alternative
   and for operators with more than 65536 rows or 16 terms.
@@ -25,7 +25,8 @@ from dataclasses import dataclass, field
 
 import torch
 
-KFR_STEPS_PER_BATCH = 4  # csrc/transfer.cu kKfrU
+KFR_GROUP = 4  # csrc/transfer.cu kKfrG: terms accumulated per chunk
+KFR_MAX_BATCHES = 128  # csrc/transfer.cu kKfrMaxBatches
 
 
 def _level_class(idx: torch.Tensor, levels: int) -> torch.Tensor:
@@ -60,15 +61,15 @@ class KfrLayout:
     n_items: int
     n_partials: int
     items: torch.Tensor      # (n_items, 2) int32 {first batch, steps}
-    lane_len: torch.Tensor   # (n_items * 32,) int32
-    lane_dst: torch.Tensor   # (n_items * 32,) int32 (u32 bit patterns)
-    batch_off: torch.Tensor  # (n_batches + 1, 2) int32 {word, value}
-    cm: torch.Tensor         # (n_pairs + pad,) int32: col | mask << 16
-    vals: torch.Tensor       # (nnz + pad,) float32, term planes
-    partials: torch.Tensor   # (3K, max(n_partials, 1)) float64 scratch
+    lane_len: torch.Tensor   # (n_items * 32,) int32 chunk lengths (pairs)
+    lane_dst: torch.Tensor   # (n_items * 32,) int32: row | group << 16, 1 << 31 | slot, or -1
+    batch_off: torch.Tensor  # (n_batches + 1,) int32 (u32) byte offsets into stream
+    stream: torch.Tensor     # int32 words: per batch U * 32 pair words, then f32 values
+    partials: torch.Tensor   # (3 G, max(n_partials, 1)) float64 scratch
     partial_row: torch.Tensor
-    multi_info: torch.Tensor  # (n_multi, 4) int32 {row, first slot, count, 0}
+    multi_info: torch.Tensor  # (n_multi, 4) int32 {row, first slot, count, group}
     multi_count: torch.Tensor  # (n_multi,) int32, zero between frames
+    work: torch.Tensor = None  # (2,) int32 claim / exit counters, zero between frames
     stats: dict = field(default_factory=dict)
 
 
@@ -79,57 +80,69 @@ def _bitrev(mask: torch.Tensor, K: int) -> torch.Tensor:
     return r
 
 
-def kfr_layout(t, chunk: int = 512, bucket: int = 16) -> KfrLayout:
+def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4) -> KfrLayout:
     """K-fused row-chunk layout of sss_transfer_kfr (see csrc/transfer.cu).
 
-    Pairs of a row are ordered by term mask (highest terms first: the masks
-    of one step across the warp's lanes then share most of their planes),
-    then column. Chunks are grouped 32 to a warp item by (row level class,
-    length bucket, row) so a warp's lanes have similar lengths (idle lanes
-    cost issue slots) and neighbouring rows (coalesced v_k stores); items are
-    ordered longest first for the static round-robin assignment."""
+    The K terms are split in groups of G = KFR_GROUP; the terms of one
+    (receiver row, group) merge into (column, G-bit term mask) pairs, ordered
+    by mask (highest terms first) then column and cut into chunks of <=
+    `chunk` pairs (every (row, group) has at least one, possibly empty,
+    chunk: its v_k rows are written even when zero). A warp item is 32
+    chunks, one per lane; step s of an item holds the s-th pair of every
+    lane: 32 dense words {col | mask << 16 | offset << 20} (0 where the lane's
+    chunk has ended) and the lanes' values lane-major (offset = the lane's
+    first value in the step). Chunks are grouped by (row level class, length
+    bucket, row, group) so an item's lanes have similar lengths and
+    neighbouring rows; items are ordered longest first (dynamic claiming)."""
+    G = KFR_GROUP
     K, n, L = t.K, t.n, t.levels
-    if K > 16 or n > 65536:
+    NG = (K + G - 1) // G
+    if K > 4 * G or n > 65536:
         raise ValueError("kfr layout: K <= 16 terms and n <= 65536 rows (16-bit columns)")
+    if chunk > KFR_MAX_BATCHES * steps_per_batch:
+        raise ValueError(f"kfr layout: chunk <= {KFR_MAX_BATCHES} x steps_per_batch")
     dev = t.rowptr.device
-    U = KFR_STEPS_PER_BATCH
+    U = steps_per_batch
     row, k, col, val = canonical_entries(t)
     nnz = row.numel()
-    key = row * n + col
-    o = torch.argsort(key * 16 + k)
-    key, k, val = key[o], k[o], val[o]
-    del o, row, col
+    grp, kl = k // G, k % G
+    key = (row * NG + grp) * n + col
+    o = torch.argsort(key * G + kl)
+    key, kl, val = key[o], kl[o], val[o]
+    del o, row, col, k, grp
     newp = torch.ones(nnz, dtype=torch.bool, device=dev)
     if nnz:
         newp[1:] = key[1:] != key[:-1]
     pid = torch.cumsum(newp.to(torch.int64), 0) - 1
     P = int(newp.sum())
     pkey = key[newp]
-    prow, pcol = pkey // n, pkey % n
+    prg, pcol = pkey // n, pkey % n  # prg = row * NG + group
     pmask = torch.zeros(P, dtype=torch.int64, device=dev).scatter_add_(
-        0, pid, torch.bitwise_left_shift(torch.ones_like(k), k))
-    del pkey, newp
-    # pair order inside a row: masks with high terms first, then column
-    okey = (prow << 33) | (((1 << 16) - 1 - _bitrev(pmask, K)) << 16) | pcol
+        0, pid, torch.bitwise_left_shift(torch.ones_like(kl), kl))
+    del pkey, newp, key
+    # pair order inside a (row, group): masks with high terms first, then column
+    okey = (prg << 24) | (((1 << G) - 1 - _bitrev(pmask, G)) << 16) | pcol
     po = torch.argsort(okey)
     del okey
     rank_of_pair = torch.empty_like(po)
     rank_of_pair[po] = torch.arange(P, device=dev)
-    prow, pcol, pmask = prow[po], pcol[po], pmask[po]
-    cnt = torch.bincount(prow, minlength=n)
+    prg, pcol, pmask = prg[po], pcol[po], pmask[po]
+    RG = n * NG
+    cnt = torch.bincount(prg, minlength=RG)
     start = torch.cumsum(cnt, 0) - cnt
-    pos = torch.arange(P, device=dev) - start[prow]
+    pos = torch.arange(P, device=dev) - start[prg]
     nch = torch.clamp((cnt + chunk - 1) // chunk, min=1)
     chbase = torch.cumsum(nch, 0) - nch
-    pchunk = chbase[prow] + pos // chunk
+    pchunk = chbase[prg] + pos // chunk
     pstep = pos % chunk
     NC = int(nch.sum())
     clen = torch.bincount(pchunk, minlength=NC)
-    crow = torch.repeat_interleave(torch.arange(n, device=dev), nch)
-    cidx = torch.arange(NC, device=dev) - chbase[crow]
+    crg = torch.repeat_interleave(torch.arange(RG, device=dev), nch)
+    crow, cgrp = crg // NG, crg % NG
+    cidx = torch.arange(NC, device=dev) - chbase[crg]
     lvl = _level_class(crow, L)
     nb = max(1, (chunk + bucket - 1) // bucket)
-    ckey = (lvl << 44) | ((nb - clen // bucket) << 30) | (crow << 12) | cidx
+    ckey = (lvl << 48) | ((nb - clen // bucket) << 36) | (crow << 20) | (cgrp << 16) | cidx
     corder = torch.argsort(ckey)
     NI = (NC + 31) // 32
     slot_len = torch.zeros(NI * 32, dtype=torch.int64, device=dev)
@@ -143,20 +156,21 @@ def kfr_layout(t, chunk: int = 512, bucket: int = 16) -> KfrLayout:
     citem = inew[cpos // 32]
     clane = cpos % 32
     S = S[iorder]
-    # partial slots for rows cut into several chunks, consecutive per row
+    # partial slots for (row, group)s cut into several chunks, consecutive
     multi = nch > 1
-    mrows = torch.nonzero(multi).flatten()
-    M = mrows.numel()
-    mcnt = nch[mrows]
+    mrg = torch.nonzero(multi).flatten()
+    M = mrg.numel()
+    mcnt = nch[mrg]
     mfirst = torch.cumsum(mcnt, 0) - mcnt
-    m_of_row = torch.full((n,), -1, dtype=torch.int64, device=dev)
-    m_of_row[mrows] = torch.arange(M, device=dev)
-    cm_of = m_of_row[crow]
+    m_of = torch.full((RG,), -1, dtype=torch.int64, device=dev)
+    m_of[mrg] = torch.arange(M, device=dev)
+    cm_of = m_of[crg]
     n_partials = int(mcnt.sum()) if M else 0
+    direct = crow | (cgrp << 16)
     if M:
-        cdst = torch.where(cm_of >= 0, (1 << 31) | (mfirst[cm_of.clamp(min=0)] + cidx), crow)
+        cdst = torch.where(cm_of >= 0, (1 << 31) | (mfirst[cm_of.clamp(min=0)] + cidx), direct)
     else:
-        cdst = crow.clone()
+        cdst = direct
     lane_len = torch.zeros(NI * 32, dtype=torch.int64, device=dev)
     lane_dst = torch.full((NI * 32,), 0xFFFFFFFF, dtype=torch.int64, device=dev)
     lane_len[citem * 32 + clane] = clen
@@ -165,107 +179,125 @@ def kfr_layout(t, chunk: int = 512, bucket: int = 16) -> KfrLayout:
         torch.zeros(1, dtype=torch.int64, device=dev)
     multi_info = torch.zeros((max(M, 1), 4), dtype=torch.int64, device=dev)
     if M:
-        multi_info[:, 0] = mrows
+        multi_info[:, 0] = mrg // NG
         multi_info[:, 1] = mfirst
         multi_info[:, 2] = mcnt
-    # word stream: pairs ordered (item, step, lane)
+        multi_info[:, 3] = mrg % NG
+    # batches of U steps per item; batch = [U * 32 words | values], 16-byte padded
     item_p = citem[pchunk]
     lane_p = clane[pchunk]
-    skey = (item_p << 25) | (pstep << 5) | lane_p
-    so = torch.argsort(skey)
-    skey_sorted = skey[so]
-    cm = (pcol | (pmask << 16))[so]
-    # value stream: entries ordered (item, step, term, lane)
-    ent_pair = rank_of_pair[pid]  # pair index (new order) of every sorted entry
-    vkey = (item_p[ent_pair] << 30) | (pstep[ent_pair] << 14) | (k << 5) | lane_p[ent_pair]
-    vo = torch.argsort(vkey)
-    vkey_sorted = vkey[vo]
-    vals = val[vo]
-    del vkey, vo, ent_pair
-    # batches of U steps per item: first word / value of step b*U
     nbat = (S + U - 1) // U
     bbase = torch.cumsum(nbat, 0) - nbat
     NB = int(nbat.sum())
+    pbatch = bbase[item_p] + pstep // U
+    # values ordered (item, step, lane, term) = (batch, step, lane, term)
+    ent_pair = rank_of_pair[pid]
+    vkey = (item_p[ent_pair] << 30) | (pstep[ent_pair] << 14) | (lane_p[ent_pair] << 4) | kl
+    vo = torch.argsort(vkey)
+    vkey_sorted = vkey[vo]
+    vals = val[vo]
+    vpos = torch.empty(nnz, dtype=torch.int64, device=dev)
+    vpos[vo] = torch.arange(nnz, device=dev)
+    del vkey, vo
+    # first value of every pair, of every step and of every batch (global order)
+    pfirst = torch.full((P,), nnz, dtype=torch.int64, device=dev).scatter_reduce_(
+        0, ent_pair, vpos, "amin")
+    step_first = torch.searchsorted(vkey_sorted, (item_p << 30) | (pstep << 14))
+    poff = pfirst - step_first
+    if P and int(poff.max()) >= 128:
+        raise AssertionError("kfr layout: step value offset overflow")
     bitem = torch.repeat_interleave(torch.arange(NI, device=dev), nbat)
     bstep = (torch.arange(NB, device=dev) - bbase[bitem]) * U
-    q_w = (bitem << 25) | (bstep << 5)
-    q_v = (bitem << 30) | (bstep << 14)
-    boff = torch.zeros((NB + 1, 2), dtype=torch.int64, device=dev)
-    boff[:NB, 0] = torch.searchsorted(skey_sorted, q_w)
-    boff[:NB, 1] = torch.searchsorted(vkey_sorted, q_v)
-    boff[NB, 0] = P
-    boff[NB, 1] = nnz
+    bv0 = torch.searchsorted(vkey_sorted, (bitem << 30) | (bstep << 14))
+    bv1 = torch.cat([bv0[1:], torch.tensor([nnz], device=dev)]) if NB else bv0
+    bwords = (U * 32 * 4) // 4
+    bsize = bwords + ((bv1 - bv0) + 3) // 4 * 4  # in 4-byte units, 16-byte multiples
+    bstart = torch.cumsum(bsize, 0) - bsize
+    total = int(bsize.sum()) if NB else 0
+    stream = torch.zeros(total + 4, dtype=torch.int32, device=dev)
+    wv = (pcol | (pmask << 16) | (poff << 20)).to(torch.int64)
+    wv = torch.where(wv >= (1 << 31), wv - (1 << 32), wv).to(torch.int32)
+    stream[bstart[pbatch] + (pstep % U) * 32 + lane_p] = wv
+    vb = bbase[item_p[ent_pair]] + pstep[ent_pair] // U  # batch of every entry
+    stream[bstart[vb] + bwords + (vpos - bv0[vb])] = val.view(torch.int32)
+    del ent_pair, vpos, vb, wv
+    boff = torch.zeros(NB + 1, dtype=torch.int64, device=dev)
+    boff[:NB] = bstart * 4
+    boff[NB] = total * 4
+    if total * 4 >= (1 << 32):
+        raise ValueError("kfr layout: stream larger than 4 GB")
     items = torch.stack([bbase, S], dim=1)
-    pad = 8  # bulk copies round the last batch up to 16 bytes
-    cm_t = torch.zeros(P + pad, dtype=torch.int32, device=dev)
-    cm_t[:P] = cm.to(torch.int32)
-    vals_t = torch.zeros(nnz + pad, dtype=torch.float32, device=dev)
-    vals_t[:nnz] = vals
 
     def u32(x):
         return torch.where(x >= (1 << 31), x - (1 << 32), x).to(torch.int32).contiguous()
 
     steps = int(S.sum())
-    stats = {"pairs": P, "entries": nnz, "chunks": NC, "items": NI, "steps": steps,
-             "batches": NB, "lane_util": round(P / max(32 * steps, 1), 4),
-             "multi_rows": M, "partials": n_partials,
-             "bytes": (P + pad) * 4 + (nnz + pad) * 4 + NI * 8 + NI * 256 + (NB + 1) * 8}
+    stats = {"steps_per_batch": U, "groups": NG, "pairs": P, "entries": nnz, "chunks": NC,
+             "items": NI, "steps": steps, "batches": NB,
+             "lane_util": round(P / max(32 * steps, 1), 4), "multi": M, "partials": n_partials,
+             "bytes": total * 4 + NI * 8 + NI * 256 + (NB + 1) * 4}
     return KfrLayout(
         K=K, n=n, n_items=NI, n_partials=n_partials, items=u32(items), lane_len=u32(lane_len),
-        lane_dst=u32(lane_dst), batch_off=u32(boff), cm=cm_t, vals=vals_t,
-        partials=torch.zeros((3 * K, max(n_partials, 1)), dtype=torch.float64, device=dev),
+        lane_dst=u32(lane_dst), batch_off=u32(boff), stream=stream,
+        partials=torch.zeros((3 * G, max(n_partials, 1)), dtype=torch.float64, device=dev),
         partial_row=u32(partial_row), multi_info=u32(multi_info),
-        multi_count=torch.zeros(max(M, 1), dtype=torch.int32, device=dev), stats=stats)
+        multi_count=torch.zeros(max(M, 1), dtype=torch.int32, device=dev),
+        work=torch.zeros(2, dtype=torch.int32, device=dev), stats=stats)
 
 
 def kfr_reference_apply(lay: KfrLayout, x: torch.Tensor) -> torch.Tensor:
-    """Decode the kfr stream on the host side of torch (any device) and apply
-    it: v (K, 3, n) = T_k x_c. For layout tests; mirrors the kernel's
-    indexing (compacted words per step, term planes)."""
+    """Decode the kfr stream with torch (any device) and apply it: v (K, 3, n)
+    = T_k x_c. For layout tests; mirrors the kernel's indexing (per batch U x
+    32 words then the values, lane-major per step at the word's offset,
+    partial sums of long (row, group)s summed in chunk order)."""
+    G = KFR_GROUP
     K, n = lay.K, lay.n
-    dev = lay.cm.device
+    dev = lay.stream.device
     items = lay.items.long()
-    lane_len = lay.lane_len.long().view(-1, 32)
     dst = lay.lane_dst.long() & 0xFFFFFFFF
-    boff = lay.batch_off.long()
-    cm = lay.cm.long() & 0xFFFFFFFF
-    vals = lay.vals.double()
+    boff = lay.batch_off.long() & 0xFFFFFFFF
+    words = lay.stream.long() & 0xFFFFFFFF
+    vals = lay.stream.view(torch.float32).double()
     v = torch.zeros((K, 3, n), dtype=torch.float64, device=dev)
-    part = torch.zeros((3 * K, max(lay.n_partials, 1)), dtype=torch.float64, device=dev)
+    part = torch.zeros((3 * G, max(lay.n_partials, 1)), dtype=torch.float64, device=dev)
     x = x.double()
-    lanes = torch.arange(32, device=dev)
+    U = lay.stats["steps_per_batch"]
     for i in range(lay.n_items):
         b0, S = int(items[i, 0]), int(items[i, 1])
-        w = int(boff[b0, 0]) if S else 0
-        vo = int(boff[b0, 1]) if S else 0
-        acc = torch.zeros((32, K, 3), dtype=torch.float64, device=dev)
+        acc = torch.zeros((32, G, 3), dtype=torch.float64, device=dev)
         for s in range(S):
-            act = s < lane_len[i]
-            na = int(act.sum())
-            words = torch.zeros(32, dtype=torch.int64, device=dev)
-            words[act] = cm[w:w + na]
-            w += na
-            col, mask = words & 0xFFFF, words >> 16
+            b = b0 + s // U
+            base = int(boff[b]) // 4
+            w = words[base + (s % U) * 32: base + (s % U) * 32 + 32]
+            if s % U == 0:
+                vbase = base + U * 32
+            col, mask, off = w & 0xFFFF, (w >> 16) & 0xF, (w >> 20) & 0x7F
             xs = x[:, col].T  # (32, 3)
-            for k in range(K):
-                has = ((mask >> k) & 1).bool() & act
-                m = int(has.sum())
-                if m:
-                    acc[has, k, :] += vals[vo:vo + m, None] * xs[has]
-                    vo += m
-        d = dst[i * 32:(i + 1) * 32]
-        for ln in lanes.tolist():
-            dd = int(d[ln])
+            for ln in range(32):
+                a = vbase + int(off[ln])
+                for k in range(G):
+                    if (int(mask[ln]) >> k) & 1:
+                        acc[ln, k] += vals[a] * xs[ln]
+                        a += 1
+            vbase += int(sum(bin(int(m)).count("1") for m in mask))
+        for ln in range(32):
+            dd = int(dst[i * 32 + ln])
             if dd == 0xFFFFFFFF:
                 continue
             if dd & 0x80000000:
                 part[:, dd & 0x7FFFFFFF] = acc[ln].reshape(-1)
             else:
-                v[:, :, dd] = acc[ln]
+                row, k0 = dd & 0xFFFF, (dd >> 16) * G
+                for k in range(G):
+                    if k0 + k < K:
+                        v[k0 + k, :, row] = acc[ln, k]
     info = lay.multi_info.long()
     for m in range(info.shape[0] if lay.n_partials else 0):
-        r, f, c = int(info[m, 0]), int(info[m, 1]), int(info[m, 2])
-        v[:, :, r] = part[:, f:f + c].sum(dim=1).view(K, 3)
+        r, f, c, g = (int(z) for z in info[m])
+        s = part[:, f:f + c].sum(dim=1).view(G, 3)
+        for k in range(G):
+            if g * G + k < K:
+                v[g * G + k, :, r] = s[k]
     return v
 
 

@@ -189,9 +189,9 @@ class Scene:
         if self.transfer_kernel not in ("kfr", "flat16") or (self.transfer_kernel == "kfr" and not kfr_ok):
             raise ValueError(f"unsupported transfer kernel {self.transfer_kernel!r}")
         self._knobs = {
-            "kfr_chunk": int(os.environ.get("SSS_KFR_CHUNK", "512")),
-            "kfr_minb": int(os.environ.get("SSS_KFR_MINB",
-                                           "4" if self.K <= 8 else "3" if self.K <= 12 else "2")),
+            "kfr_chunk": int(os.environ.get("SSS_KFR_CHUNK", "256")),
+            "kfr_steps": int(os.environ.get("SSS_KFR_STEPS", "4")),
+            "kfr_minb": int(os.environ.get("SSS_KFR_MINB", "3")),
             "env_union_kernel": os.environ.get("SSS_ENV_UNION_KERNEL", "0") == "1",
         }
         self._have_cache = False
@@ -374,7 +374,8 @@ class Scene:
         t = self.transfer
         if self.transfer_kernel == "kfr":
             if getattr(t, "kfr", None) is None:
-                t.kfr = kfr_layout(t, chunk=self._knobs["kfr_chunk"])
+                t.kfr = kfr_layout(t, chunk=self._knobs["kfr_chunk"],
+                                   steps_per_batch=self._knobs["kfr_steps"])
             return t.kfr
         if getattr(t, "flat16", None) is None:
             t.flat16 = flat16_layout(t)
@@ -395,10 +396,11 @@ class Scene:
             mb = self._knobs["kfr_minb"]
             _lib.call("sss_transfer_kfr", self.K, self.n, lay.n_items, lay.n_partials,
                       _lib.ptr(lay.items), _lib.ptr(lay.lane_len), _lib.ptr(lay.lane_dst),
-                      _lib.ptr(lay.batch_off), _lib.ptr(lay.cm), _lib.ptr(lay.vals),
+                      _lib.ptr(lay.batch_off), _lib.ptr(lay.stream),
                       _lib.ptr(self.xp), _lib.ptr(self.xbits), _lib.ptr(self.vk),
                       _lib.ptr(lay.partials), _lib.ptr(lay.partial_row), _lib.ptr(lay.multi_info),
-                      _lib.ptr(lay.multi_count), nsm * mb * 4, mb, sp)
+                      _lib.ptr(lay.multi_count), _lib.ptr(lay.work), lay.stats["steps_per_batch"],
+                      nsm * mb * 8, mb, sp)
             return
         pcols, pvals, ne, heads, hpre, rowk, wbeg, W, st = lay
         if getattr(self, "_wctr", None) is None:
