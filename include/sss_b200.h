@@ -279,6 +279,12 @@ int sss_pair_block(int levels, int exact, int side, const float* pos, const floa
 int sss_step1_select(const double* D, int n_dom, int n_rows, int n_keep, const uint32_t* tm2flat,
                      uint32_t* union_bits, void* stream);
 
+/* sss_step1_rows: the same per-row top-n for the listed rows of D only (tile-
+ * major row ids), each row's kept flat ids written as a bitmap (n_sel x
+ * N/32 words): the sampled-row parity hook of step 1. */
+int sss_step1_rows(const double* D, int n_dom, const int* rows, int n_sel, int n_keep,
+                   const uint32_t* tm2flat, uint32_t* row_bits, void* stream);
+
 /* Step 2 (_threshold_columns, transfer.py:303-333 with compress_energy): for
  * each union column, the energy-fraction cut. Per tm column: threshold key
  * col_t (~0 = column dropped), tie bound col_fmax (flat row), kept count,

@@ -48,6 +48,7 @@ _SIGS = {
     "sss_edit_finish": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_pair_block": [_I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _I, C.c_float, _P, _P, _P],
     "sss_step1_select": [_P, _I, _I, _I, _P, _P, _P],
+    "sss_step1_rows": [_P, _I, _P, _I, _I, _P, _P, _P],
     "sss_step2_select": [_P, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_emit": [_I, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_scan_u32": [_P, _P, C.c_size_t, _P, _P, _P],

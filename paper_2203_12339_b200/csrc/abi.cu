@@ -424,24 +424,28 @@ int sss_transfer_kfr(int K, int n_rows, unsigned n_items, unsigned n_partials, c
   if (reinterpret_cast<uintptr_t>(stream_bytes) % 16 || reinterpret_cast<uintptr_t>(xp) % 32)
     return fail(SSS_EINVAL, "transfer_kfr: stream 16- and xp 32-byte aligned");
   if (n_items == 0) return SSS_OK;
-  const int ns = getenv("SSS_KFR_SLOTS") ? atoi(getenv("SSS_KFR_SLOTS")) : 3;  // A/B knob
+  const int ns = 2;  // ring slots per warp (3 measured slower: less L1 for the x gathers)
   unsigned grid = (unsigned)(n_warps / sss::kKfrWarps);
   const unsigned need = (n_items + sss::kKfrWarps - 1) / sss::kKfrWarps;
   if (grid > need) grid = need;
 #define SSS_KFR(UU, NS, MB)                                                                      \
   if (steps_per_batch == UU && ns == NS && min_blocks == MB) {                                   \
     const size_t smem = sss::kfr_smem_bytes(n_rows, sss::KfrSmem<UU, NS>::WARP);                 \
-    if (int r = set_smem((const void*)sss::k_transfer_kfr<UU, NS, MB>, smem)) return r;          \
-    sss::k_transfer_kfr<UU, NS, MB><<<grid, sss::kKfrWarps * 32, smem, S_(stream)>>>(            \
+    auto fn = sss::k_transfer_kfr<UU, NS, MB>;                                                   \
+    /* the static bitmap counts against the default 48 KB: always raise */                     \
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                             (int)smem) != cudaSuccess)                                          \
+      return fail(SSS_ECUDA, "transfer_kfr: shared memory attribute");                          \
+    fn<<<grid, sss::kKfrWarps * 32, smem, S_(stream)>>>(                                         \
         n_rows, K, n_items, n_partials, reinterpret_cast<const uint2*>(items), lane_len,         \
         lane_dst, batch_off, reinterpret_cast<const unsigned char*>(stream_bytes),               \
         reinterpret_cast<const double4*>(xp), bits, vk, partials, partial_row,                   \
         reinterpret_cast<const uint4*>(multi_info), multi_count, work);                          \
     return check_launch("k_transfer_kfr");                                                       \
   }
-  SSS_KFR(4, 3, 3) SSS_KFR(4, 2, 3) SSS_KFR(4, 4, 2) SSS_KFR(8, 3, 2) SSS_KFR(4, 3, 2)
+  SSS_KFR(4, 2, 3) SSS_KFR(8, 2, 2)
 #undef SSS_KFR
-  return fail(SSS_EINVAL, "transfer_kfr: (steps_per_batch, slots, min_blocks) in {(4,3,3), (4,2,3), (4,4,2), (8,3,2), (4,3,2)}");
+  return fail(SSS_EINVAL, "transfer_kfr: (steps_per_batch, min_blocks) in {(4, 3), (8, 2)}");
 }
 
 int sss_fold_apply(int K, int n_rows, int n_dirs, const uint64_t* colptr, const uint32_t* rows,
@@ -609,6 +613,18 @@ int sss_step1_select(const double* D, int n_dom, int n_rows, int n_keep, const u
   if (int r = set_smem((const void*)sss::k_step1_select, smem)) return r;
   sss::k_step1_select<<<n_rows, sss::kSelThreads, smem, S_(stream)>>>(D, n_dom, n_keep, tm2flat,
                                                                       union_bits);
+  return check_launch("k_step1_select");
+}
+
+int sss_step1_rows(const double* D, int n_dom, const int* rows, int n_sel, int n_keep,
+                   const uint32_t* tm2flat, uint32_t* row_bits, void* stream) {
+  if (!D || !rows || !tm2flat || !row_bits || n_dom <= 0 || n_sel < 0 || n_keep < 1)
+    return fail(SSS_EINVAL, "bad step1_rows arguments");
+  if (n_sel == 0) return SSS_OK;
+  const size_t smem = sizeof(sss::SelShared) + 2 * (size_t)((n_dom + 31) / 32) * 4;
+  if (int r = set_smem((const void*)sss::k_step1_select, smem)) return r;
+  sss::k_step1_select<<<n_sel, sss::kSelThreads, smem, S_(stream)>>>(D, n_dom, n_keep, tm2flat,
+                                                                     nullptr, rows, row_bits);
   return check_launch("k_step1_select");
 }
 

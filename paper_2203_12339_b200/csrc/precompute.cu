@@ -180,17 +180,22 @@ __global__ void __launch_bounds__(128) k_pair_block(PairParams p, double* __rest
 
 // step 1: one CTA per receiver row of D (tile-major), top-n with flat-index
 // tie-break, OR the kept flat column ids into the per-k union bitmap
+// rows (nullable): the CTA's row of D is rows[blockIdx.x]; row_bits (nullable):
+// write the row's kept bitmap (flat ids, nw words per CTA) instead of OR-ing
+// it into the union (the sampled-row parity hook)
 __global__ void __launch_bounds__(kSelThreads) k_step1_select(const double* __restrict__ D, int N,
                                                               int n_keep,
                                                               const uint32_t* __restrict__ tm2flat,
-                                                              uint32_t* __restrict__ union_bits) {
+                                                              uint32_t* __restrict__ union_bits,
+                                                              const int* __restrict__ rows = nullptr,
+                                                              uint32_t* __restrict__ row_bits = nullptr) {
   extern __shared__ __align__(16) unsigned char dsm[];
   SelShared& sh = *reinterpret_cast<SelShared*>(dsm);
   uint32_t* smb = reinterpret_cast<uint32_t*>(dsm + sizeof(SelShared));  // keep + tie bits
   const int nw = (N + 31) / 32;
   uint32_t* keep = smb;
   uint32_t* tie = smb + nw;
-  const double* v = D + (size_t)blockIdx.x * N;
+  const double* v = D + (size_t)(rows ? rows[blockIdx.x] : (int)blockIdx.x) * N;
   for (int w = threadIdx.x; w < 2 * nw; w += blockDim.x) smb[w] = 0;
   uint64_t t;
   long long take, tiecnt;
@@ -211,7 +216,8 @@ __global__ void __launch_bounds__(kSelThreads) k_step1_select(const double* __re
       else if (fmax - lo < 31) tb &= (2u << (fmax - lo)) - 1u;
     }
     const uint32_t kept = keep[w] | tb;
-    if (kept && (union_bits[w] & kept) != kept) atomicOr(&union_bits[w], kept);
+    if (row_bits) row_bits[(size_t)blockIdx.x * nw + w] = kept;
+    else if (kept && (union_bits[w] & kept) != kept) atomicOr(&union_bits[w], kept);
   }
 }
 

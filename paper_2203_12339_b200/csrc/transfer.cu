@@ -68,6 +68,7 @@ __device__ __forceinline__ void v15_gather1(const double4* __restrict__ xp, uint
 
 constexpr int kKfrWarps = 8;  // warps per CTA (independent; each owns its smem ring)
 constexpr int kKfrG = 4;      // terms per group: a chunk accumulates G terms x 3 channels
+static_assert(kKfrG == 4, "phase B's slot selects are written for groups of 4 terms");
 constexpr int kKfrMaxBatches = 128;  // batches per item (chunk length <= 128 * steps per batch)
 
 template <int U, int NS>  // steps per staged batch, ring slots per warp
@@ -75,7 +76,7 @@ struct KfrSmem {
   // one batch of the stream: U*32 pair words (dense per step), then <= U*32*G
   // values, padded to 16 bytes (one bulk copy per batch)
   static constexpr int WB = U * 32 * 4;
-  static constexpr int VB = U * 32 * kKfrG * 4;
+  static constexpr int VB = U * 32 * kKfrG * 4 + 16;  // + slack: lanes read 4 values unconditionally
   static constexpr int SLOT = (WB + VB + 15) / 16 * 16;
   static_assert(WB % 16 == 0, "word block must keep 16-byte alignment");
   // the item's batch offsets (<= kKfrMaxBatches + 1 u32)
@@ -84,9 +85,11 @@ struct KfrSmem {
   static constexpr int WARP = ((NS * SLOT + 8 * NS + BOFF) + 127) / 128 * 128;
 };
 
+constexpr int kKfrBitWords = 65536 / 32 + 1;  // kept-column bitmap, static shared
+
 inline size_t kfr_smem_bytes(int N, size_t warp_bytes) {
-  const size_t bits = (((size_t)((N >> 5) + 1) * 4 + 127) / 128) * 128;
-  return bits + (size_t)kKfrWarps * warp_bytes;
+  (void)N;
+  return (size_t)kKfrWarps * warp_bytes;  // dynamic part (the bitmap is static)
 }
 
 // Pair word: col (bits 0-15) | term mask within the group (16-19) | offset of
@@ -103,12 +106,11 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
   using SM = KfrSmem<U, NS>;
   constexpr int G = kKfrG;
   extern __shared__ __align__(128) unsigned char kfr_smem[];
+  __shared__ uint32_t sbits[kKfrBitWords];
   const int nbw = (N >> 5) + 1;
-  const int bits_bytes = ((nbw * 4 + 127) / 128) * 128;
-  uint32_t* sbits = reinterpret_cast<uint32_t*>(kfr_smem);
   for (int t = threadIdx.x; t < nbw; t += blockDim.x) sbits[t] = bits[t];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wb = kfr_smem + bits_bytes + wid * SM::WARP;
+  unsigned char* wb = kfr_smem + wid * SM::WARP;
   uint64_t* bar = reinterpret_cast<uint64_t*>(wb + NS * SM::SLOT);
   uint32_t* sboff = reinterpret_cast<uint32_t*>(wb + NS * SM::SLOT + 8 * NS);
   if (lane == 0) {
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
   // was last read by this warp (its loads completed before the __syncwarp
   // that ended that batch): no proxy fence is needed for the write-after-read
   auto issue = [&](unsigned b, unsigned slot) {  // b: batch of the current item
-    if (lane == 0) {
+    if (lane == 0) {  // one TMA bulk copy, completion counted on the slot's mbarrier
       const unsigned a0 = sboff[b], a1 = sboff[b + 1];
       mbar_expect_tx(&bar[slot], a1 - a0);
       bulk_g2s(wb + slot * SM::SLOT, stream + a0, a1 - a0, &bar[slot]);
@@ -148,53 +150,67 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
     double acc[G][3];
 #pragma unroll
     for (int k = 0; k < G; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
-    // x of the last gathered pair per step slot: finite, so an absent or
-    // unkept term's 0 * x leaves the accumulators exactly unchanged
-    double xa[U][3];
-#pragma unroll
-    for (int t = 0; t < U; ++t) xa[t][0] = xa[t][1] = xa[t][2] = 0.0;
-#pragma unroll
-    for (int j = 0; j < NS - 1; ++j)
-      if ((unsigned)j < nb) issue(j, (seq + j) % NS);
-#pragma unroll 1
-    for (unsigned b = 0; b < nb; ++b) {
-      const unsigned slot = seq % NS, par = (seq / NS) & 1u;
-      if (b + NS - 1 < nb) issue(b + NS - 1, (seq + NS - 1) % NS);
-      mbar_wait_warp_spin(&bar[slot], par);
-      ++seq;
-      const uint32_t* sw = reinterpret_cast<const uint32_t*>(wb + slot * SM::SLOT);
-      const float* sv = reinterpret_cast<const float*>(wb + slot * SM::SLOT + SM::WB);
-      // phase A: pair words (0 past the chunk's end), kept test, x gathers
-      // (U in flight per lane)
-      uint32_t w[U];
-      bool kp[U];
+    // phase A of a batch: pair words (0 past the chunk's end), kept test, x
+    // gathers (U in flight per lane). x of a skipped step keeps the last
+    // gathered (finite) value, so an absent or unkept term's 0 * x adds
+    // exactly nothing
+    auto phaseA = [&](const unsigned char* slot_p, uint32_t (&w)[U], bool (&kp)[U],
+                      double (&xa)[U][3]) {
+      const uint32_t* sw = reinterpret_cast<const uint32_t*>(slot_p);
 #pragma unroll
       for (int t = 0; t < U; ++t) {
         w[t] = sw[t * 32 + lane];
         const uint32_t c = w[t] & 0xffffu;
-        kp[t] = (w[t] >> 16) != 0u && ((sbits[c >> 5] >> (c & 31u)) & 1u);
+        kp[t] = ((sbits[c >> 5] >> (c & 31u)) & (w[t] >> 16 != 0u ? 1u : 0u)) != 0u;
         if (kp[t]) gather_x(xp, c, xa[t][0], xa[t][1], xa[t][2]);
       }
-      // phase B: the lane's values (lane-major in the step block), fp64
-      // accumulation in (step, term) order; absent / unkept terms add 0 * x
+    };
+    // phase B: the lane's values (lane-major in the step block; the term of
+    // each is the next set bit of the mask), fp64 accumulation in (step,
+    // term) order
+    auto phaseB = [&](const unsigned char* slot_p, const uint32_t (&w)[U], const bool (&kp)[U],
+                      const double (&xa)[U][3]) {
+      const float* sv = reinterpret_cast<const float*>(slot_p + SM::WB);
       unsigned vbase = 0;
 #pragma unroll
       for (int t = 0; t < U; ++t) {
         const uint32_t m = (w[t] >> 16) & 0xfu;
         const float* sl = sv + vbase + ((w[t] >> 20) & 0x7fu);
         const uint32_t mk = kp[t] ? m : 0u;
+        float vf[G];  // one predicated load per present term
+#pragma unroll
+        for (int k = 0; k < G; ++k)
+          vf[k] = ((mk >> k) & 1u) ? sl[__popc(m & ((1u << k) - 1u))] : 0.0f;
 #pragma unroll
         for (int k = 0; k < G; ++k) {
-          const float vf = ((mk >> k) & 1u) ? sl[__popc(m & ((1u << k) - 1u))] : 0.0f;
-          const double v = (double)vf;
+          const double v = (double)vf[k];
           acc[k][0] = fma(v, xa[t][0], acc[k][0]);
           acc[k][1] = fma(v, xa[t][1], acc[k][1]);
           acc[k][2] = fma(v, xa[t][2], acc[k][2]);
         }
         vbase += __reduce_add_sync(0xffffffffu, __popc(m));
       }
+    };
+    auto slot_of = [&](unsigned q) { return wb + (q % NS) * SM::SLOT; };
+    uint32_t w[U];
+    bool kp[U];
+    double xa[U][3];
+#pragma unroll
+    for (int t = 0; t < U; ++t) xa[t][0] = xa[t][1] = xa[t][2] = 0.0;
+    const unsigned q0 = seq;  // ring position of batch 0 of this item
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+      if ((unsigned)j < nb) issue(j, (q0 + j) % NS);
+#pragma unroll 1
+    for (unsigned b = 0; b < nb; ++b) {
+      const unsigned q = q0 + b;
+      mbar_wait_warp_spin(&bar[q % NS], (q / NS) & 1u);
+      phaseA(slot_of(q), w, kp, xa);
+      phaseB(slot_of(q), w, kp, xa);
       __syncwarp();  // every lane is done with this slot before it is refilled
+      if (b + NS < nb) issue(b + NS, q % NS);
     }
+    seq = q0 + nb;
     const unsigned dst = __ldg(&lane_dst[item * 32 + lane]);
     if (dst != 0xffffffffu && !(dst & 0x80000000u)) {  // a whole (row, term group)
       const unsigned row = dst & 0xffffu, k0 = (dst >> 16) * G;

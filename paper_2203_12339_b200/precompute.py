@@ -122,7 +122,7 @@ def precompute_compressed(geometry: GeometryImage, basis: DiffusionBasis, levels
     bsums = torch.empty((n * nchunks + 1023) // 1024 + 1, dtype=torch.int64, device=dev)
     total = torch.empty(1, dtype=torch.int64, device=dev)
     rowptr = torch.empty((K, n + 1), dtype=torch.int64, device=dev)
-    cols_k, vals_k, nnz, kept_e, total_e, union_sizes = [], [], [], [], [], []
+    cols_k, vals_k, nnz, kept_e, total_e, union_sizes, unions = [], [], [], [], [], [], []
     t_start = time.perf_counter()
     base = 0
     for k in range(K):
@@ -146,8 +146,8 @@ def precompute_compressed(geometry: GeometryImage, basis: DiffusionBasis, levels
         e = col_e.sum(dim=0).cpu().numpy()
         kept_e.append(float(e[0]))
         total_e.append(float(e[1]))
-        union_sizes.append(int(torch.bitwise_count(union).sum().item()) if hasattr(torch, "bitwise_count")
-                           else int(np.unpackbits(union.cpu().numpy().view(np.uint8)).sum()))
+        union_sizes.append(int(np.unpackbits(union.cpu().numpy().view(np.uint8)).sum()))
+        unions.append(union.clone())
         cols_k.append(cols[:nk])
         vals_k.append(vals[:nk])
         nnz.append(nk)
@@ -160,7 +160,8 @@ def precompute_compressed(geometry: GeometryImage, basis: DiffusionBasis, levels
         cols=torch.cat(cols_k) if cols_k else torch.empty(0, dtype=torch.int32, device=dev),
         vals=torch.cat(vals_k) if vals_k else torch.empty(0, dtype=torch.float32, device=dev),
         nnz_per_k=nnz, step1_keep=step1_keep, step2_fraction=step2_fraction,
-        kept_energy=kept_e, total_energy=total_e, step1_entries=[n * min(n_keep, n)] * K)
+        kept_energy=kept_e, total_energy=total_e, step1_entries=[n * min(n_keep, n)] * K,
+        unions=torch.stack(unions) if unions else None)
     if stats is not None:
         stats.update(seconds=t_total, union_sizes=union_sizes, nnz=nnz, n_keep=n_keep,
                      pairs=pp.pairs * K)

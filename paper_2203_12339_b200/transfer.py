@@ -89,6 +89,10 @@ class DeviceTransfer:
     kept_energy: list = None
     total_energy: list = None
     step1_entries: list = None
+    # (K, ceil(N / 32)) int32 bitmaps of each term's step-1 union over flat w0
+    # ids (transfer.py:233-246), when known: union columns whose step-2 energy
+    # cut kept nothing are still columns of the reference operator
+    unions: torch.Tensor = None
 
     @property
     def n(self) -> int:
@@ -148,19 +152,41 @@ class DeviceTransfer:
         for the PRTS1 bridge and parity checks."""
         perm = tile_major_to_flat(self.side, self.levels)
         rp = self.rowptr.cpu().numpy()
-        cols = perm[self.cols.cpu().numpy().view(np.uint32).astype(np.int64)]
-        vals = self.vals.cpu().numpy()
-        ops = []
         n = self.n
+        dev = self.rowptr.device
+        ops = []
+        if dev.type == "cuda":  # the CSR -> CSC transpose on the device (torch sort)
+            perm_d = torch.as_tensor(perm, device=dev)
+            cols_d = perm_d[self.cols.long() & 0xFFFFFFFF]
+        else:
+            cols = perm[self.cols.cpu().numpy().view(np.uint32).astype(np.int64)]
+            vals = self.vals.cpu().numpy()
         for k in range(self.K):
             lo, hi = int(rp[k, 0]), int(rp[k, -1])
-            counts = np.diff(rp[k])
-            rows_tm = np.repeat(np.arange(n), counts)
-            c, v, r = cols[lo:hi], vals[lo:hi], perm[rows_tm]
-            order = np.lexsort((r, c))
-            c, v, r = c[order], v[order], r[order]
-            ucols, start = np.unique(c, return_index=True)
-            colptr = np.append(start, c.size).astype(np.int64)
+            if dev.type == "cuda":
+                counts = self.rowptr[k, 1:] - self.rowptr[k, :-1]
+                r_d = perm_d[torch.repeat_interleave(torch.arange(n, device=dev), counts)]
+                c_d = cols_d[lo:hi]
+                order = torch.argsort(c_d * n + r_d)
+                c = c_d[order].cpu().numpy()
+                r = r_d[order].cpu().numpy()
+                v = self.vals[lo:hi][order].cpu().numpy()
+                del counts, r_d, c_d, order
+            else:
+                counts = np.diff(rp[k])
+                rows_tm = np.repeat(np.arange(n), counts)
+                c, v, r = cols[lo:hi], vals[lo:hi], perm[rows_tm]
+                order = np.lexsort((r, c))
+                c, v, r = c[order], v[order], r[order]
+            if self.unions is not None:  # every union column, empty spans included
+                bits = np.unpackbits(self.unions[k].cpu().numpy().view(np.uint8),
+                                     bitorder="little")[:n]
+                ucols = np.flatnonzero(bits)
+                colptr = np.searchsorted(c, np.append(ucols, n), side="left").astype(np.int64)
+                colptr[-1] = c.size
+            else:
+                ucols, start = np.unique(c, return_index=True)
+                colptr = np.append(start, c.size).astype(np.int64)
             ops.append(TransferOperator(
                 cols=ucols.astype(np.uint32), colptr=colptr, rowidx=r.astype(np.uint32),
                 vals=v.astype(np.float64),

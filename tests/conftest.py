@@ -24,3 +24,8 @@ def golden():
         return np.load(GOLDEN / f"{name}.npz")
 
     return load
+
+
+@pytest.fixture(scope="session")
+def golden_dir():
+    return GOLDEN

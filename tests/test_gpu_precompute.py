@@ -72,6 +72,21 @@ def test_pair_pass_lerp_bitwise(lib, side, L):
         assert np.array_equal(gotM, wantM)
 
 
+def _assert_operators_equal(dt, ops, stats=None):
+    got = dt.to_reference()
+    for k, (a, o) in enumerate(zip(got, ops)):
+        assert np.array_equal(a.cols, o.cols), k  # the step-1 union (step1_unions)
+        assert np.array_equal(a.colptr, o.colptr), k
+        assert np.array_equal(a.rowidx, o.rowidx), k  # per-column kept row sets, identical
+        assert np.array_equal(a.vals, o.vals.astype(np.float32).astype(np.float64))
+        assert dt.nnz_per_k[k] == o.nnz
+        assert dt.kept_energy[k] == pytest.approx(o.kept_energy, rel=1e-12)
+        assert dt.total_energy[k] == pytest.approx(o.total_energy, rel=1e-12)
+        if stats is not None:
+            assert stats["union_sizes"][k] == o.cols.size
+        assert dt.step1_entries[k] == o.step1_entries
+
+
 @pytest.mark.parametrize("side,L,keep,K", [(32, 2, 0.10, 4), (64, 3, 0.05, 8)])
 def test_precompute_matches_oracle(lib, side, L, keep, K):
     from paper_2203_12339_b200.basis import build_basis
@@ -84,18 +99,63 @@ def test_precompute_matches_oracle(lib, side, L, keep, K):
     dt = precompute_compressed(g, b, L, keep, C.STEP2_FRACTION, stats=stats)
     ops = O.precompute_compressed(g.positions.astype(np.float64), g.area.astype(np.float64), side,
                                   b.r_nodes, b.bases, keep, C.STEP2_FRACTION, levels=L, w1="haar")
-    got = dt.to_reference()
-    for k, (a, o) in enumerate(zip(got, ops)):
-        nz = np.diff(o.colptr) > 0
-        assert np.array_equal(a.cols, o.cols[nz]), k  # kept column set
-        assert np.array_equal(a.colptr, np.concatenate([[0], np.cumsum(np.diff(o.colptr)[nz])]))
-        assert np.array_equal(a.rowidx, o.rowidx), k  # per-column kept row sets, identical
-        assert np.array_equal(a.vals, o.vals.astype(np.float32).astype(np.float64))
-        assert dt.nnz_per_k[k] == o.nnz
-        assert dt.kept_energy[k] == pytest.approx(o.kept_energy, rel=1e-12)
-        assert dt.total_energy[k] == pytest.approx(o.total_energy, rel=1e-12)
-        assert stats["union_sizes"][k] == o.cols.size
-        assert dt.step1_entries[k] == o.step1_entries
+    _assert_operators_equal(dt, ops, stats)
+
+
+@pytest.mark.parametrize("chunk", [512, 1000])
+def test_precompute_multi_chunk_emission_matches_oracle(lib, monkeypatch, chunk):
+    """The emit -> scan -> rowptr path with several column chunks per row
+    (the path every BASELINE operator is built through: C2 has 4 chunks, C3
+    16): force 8 (512) and 5 uneven (1000) chunks at 64^2 and compare the whole
+    operator with the oracle."""
+    from paper_2203_12339_b200 import precompute as P
+    from paper_2203_12339_b200.basis import build_basis
+    from paper_2203_12339_b200.geometry import make_geometry_image
+
+    monkeypatch.setattr(P, "EMIT_CHUNK", chunk)
+    side, L, keep, K = 64, 3, 0.05, 8
+    g = make_geometry_image(side, 10.0, 0.05, 8, 2203)
+    b = build_basis(K, (8, 4))
+    dt = P.precompute_compressed(g, b, L, keep, C.STEP2_FRACTION)
+    ops = O.precompute_compressed(g.positions.astype(np.float64), g.area.astype(np.float64), side,
+                                  b.r_nodes, b.bases, keep, C.STEP2_FRACTION, levels=L, w1="haar")
+    _assert_operators_equal(dt, ops)
+
+
+def test_c2_operator_matches_oracle_digests(lib, golden_dir):
+    """BASELINE configs[1] (C2: 128^2, K = 8, 32 materials, L = 3, 5 %, 0.95):
+    the GPU-built operator equals the oracle's, term by term: SHA-256 of
+    cols / colptr / rowidx / f32 vals and the energy ledger
+    (tests/golden/make_c2_digests.py ran the oracle here, ~11 min on a CPU
+    core; the geometry image and basis travel as data)."""
+    import hashlib
+    import json
+
+    from paper_2203_12339_b200.basis import DiffusionBasis
+    from paper_2203_12339_b200.geometry import GeometryImage
+    from paper_2203_12339_b200.precompute import precompute_compressed
+
+    z = np.load(golden_dir / "c2_inputs.npz")
+    want = json.loads((golden_dir / "c2_digests.json").read_text())
+    side = int(z["side"])
+    g = GeometryImage(side=side, positions=z["positions"], normals=z["normals"], area=z["area"])
+    b = DiffusionBasis(r_nodes=z["r_nodes"], bases=z["bases"], singular_values=z["singular_values"],
+                       sigma_nodes=z["sigma_nodes"], U=z["U"], eta=float(z["eta"]))
+    dt = precompute_compressed(g, b, int(z["levels"]), float(z["step1_keep"]),
+                               float(z["step2_fraction"]))
+
+    def digest(a, dtype):
+        return hashlib.sha256(np.ascontiguousarray(a, dtype=dtype).tobytes()).hexdigest()
+
+    for k, (op, w) in enumerate(zip(dt.to_reference(), want["operators"])):
+        assert op.nnz == w["nnz"] and op.cols.size == w["n_cols"], k
+        assert digest(op.cols, "<u4") == w["cols"], k
+        assert digest(op.colptr, "<i8") == w["colptr"], k
+        assert digest(op.rowidx, "<u4") == w["rowidx"], k
+        assert digest(op.vals.astype(np.float32), "<f4") == w["vals_f32"], k
+        assert op.kept_energy == pytest.approx(w["kept_energy"], rel=1e-12)
+        assert op.total_energy == pytest.approx(w["total_energy"], rel=1e-12)
+        assert op.step1_entries == w["step1_entries"]
 
 
 def test_step1_ties_flat_index(lib):

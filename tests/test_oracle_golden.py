@@ -6,6 +6,9 @@ import numpy as np
 import pytest
 
 from oracle import sss_oracle as O
+from pathlib import Path
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
 def test_haar_full_pyramid_bitwise(golden):
@@ -254,3 +257,24 @@ def test_raster_oracle_matches_reference(golden):
         assert np.array_equal(img, g[f"c{ci}_img"]) and np.array_equal(zb, g[f"c{ci}_zbuf"])
         assert np.array_equal(O.encode_srgb8(img, 2.0), g[f"c{ci}_u8"])
         assert np.isfinite(zb).mean() > 0.2  # the object covers the frame
+
+
+def test_c2_digest_inputs_are_the_config():
+    """tests/golden/c2_inputs.npz holds exactly the C2 geometry image and PCA
+    basis this container builds from the frozen config (the GPU digest test
+    uses the stored copy so the box's numpy cannot change a bit)."""
+    import json
+
+    from paper_2203_12339_b200 import config as C
+    from paper_2203_12339_b200.basis import build_basis
+    from paper_2203_12339_b200.geometry import make_geometry_image
+
+    z = np.load(GOLDEN / "c2_inputs.npz")
+    cfg = C.C2
+    g = make_geometry_image(cfg.side, cfg.radius, cfg.bump_amp, cfg.bump_terms, cfg.seed)
+    b = build_basis(cfg.K, cfg.lattice)
+    assert np.array_equal(z["positions"], g.positions) and np.array_equal(z["area"], g.area)
+    assert np.array_equal(z["bases"], b.bases) and np.array_equal(z["r_nodes"], b.r_nodes)
+    d = json.loads((GOLDEN / "c2_digests.json").read_text())
+    assert d["config"] == cfg.name and d["K"] == cfg.K and d["levels"] == cfg.levels
+    assert len(d["operators"]) == cfg.K
