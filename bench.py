@@ -12,9 +12,12 @@ Scene API with host cubemaps in and host radiance out. Under torchrun every
 rank renders its own independent object (weak scaling, no data-path
 collective); timing is the max over ranks.
 
-``--impl reference`` times the CPU oracle port of the same frame on the host
-cores (rank 0 only), on a bounded sample (stage 2 on a subset of operator
-rows, scaled), using an operator built by the GPU precompute in setup.
+``--impl reference`` times the reference's own implementation of the same
+frames on the host cores (rank 0 only): whole frames of the same sequence
+through sssrelight from baseline/_ref (oracle/reference_frame.py), on an
+operator exported by a separate GPU process as a PRTS1 file and loaded with
+the reference's own loader (the timing process never maps this framework's
+library).
 """
 
 from __future__ import annotations
@@ -43,7 +46,10 @@ def _args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="env_large_256")
-    ap.add_argument("--cpu-sample-rows", type=int, default=32, help="1/x of tiles in the CPU sample")
+    ap.add_argument("--cpu-frames", type=int, default=3,
+                    help="frames of the reference path timed for cpu_baseline")
+    ap.add_argument("--export-operator", default=None,
+                    help=argparse.SUPPRESS)  # internal: the reference arm's GPU export step
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--side", type=int, default=None, help="override the geometry-image side (testing)")
     ap.add_argument("--no-secondary", action="store_true",
@@ -244,12 +250,18 @@ def run_ours(a, cfg):
     # radiance writes + geometry reads
     sel = (scene.x != 0).any(dim=0)
     touched = int(sel[dt.cols.long()].sum().item())
+    n_kept = int(sel.sum().item())
     K = dt.K
-    alg_bytes = 8 * touched + 8 * K * (n + 1) + 24 * K * n + 24 * n + 24 * n
-    all_bytes = 8 * dt.nnz + 8 * K * (n + 1) + 24 * K * n + 24 * n + 24 * n
+    # algorithmic bytes of the timed launch (SURVEY §8d B_T): 8 B per touched
+    # coefficient (u32 column + f32 value, the reference container's width),
+    # 8 B per selected column and term (+1), and the v_k write (K x 3 x N fp64,
+    # the stage-2 cache). The kernel's own packing of x / the kept bitmap and
+    # the radiance / geometry of the edit epilogue are not part of this launch
+    alg_bytes = 8 * touched + 8 * K * (n_kept + 1) + 24 * K * n
+    all_bytes = 8 * dt.nnz + 8 * K * (n + 1) + 24 * K * n
     peak, peak_kind = _peaks()
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
-    traffic_path = ROOT / "profiles" / "r01_transfer_dram_bytes.json"
+    traffic_path = ROOT / "profiles" / f"r02_transfer_{scene.transfer_kernel}_dram_bytes.json"
     traffic = None
     if traffic_path.exists():
         try:
@@ -312,7 +324,7 @@ def run_ours(a, cfg):
 
     cpu = None
     if rank == 0 and ws == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, scene, dt, g, b, faces, mats, a.cpu_sample_rows, steps=2, warmup=0)
+        cpu = cpu_baseline(cfg, scene, dt, g, b, faces, mats, a.cpu_frames)
     secondary = None
     if rank == 0 and not a.no_secondary and a.side is None:
         # the other §8 rows, measured in the same run on the same GPU: the C2
@@ -383,86 +395,159 @@ def run_ours(a, cfg):
         torch.distributed.destroy_process_group()
 
 
-def cpu_baseline(cfg, scene, dt, g, b, faces, mats, sample, steps=2, warmup=0):
-    """Oracle port of the C3 frame on the host (numpy; stage 2 split over all
-    host cores with a thread pool): stage 1 in full, stage 2 on every
-    `sample`-th tile's rows (scaled), stages 3-5 in full. Returns the
+def _reference_ops(ops):
+    """Reference-format operators (ours) -> the reference's own TransferOperator."""
+    from oracle.reference_frame import import_reference
+
+    R = import_reference()
+    return [R["transfer"].TransferOperator(cols=o.cols, colptr=o.colptr, rowidx=o.rowidx,
+                                           vals=o.vals, kept_energy=o.kept_energy,
+                                           total_energy=o.total_energy,
+                                           step1_entries=o.step1_entries) for o in ops]
+
+
+def _reference_basis(b):
+    from oracle.reference_frame import import_reference
+
+    R = import_reference()
+    return R["basisgen"].DiffusionBasis(r_nodes=b.r_nodes, bases=b.bases,
+                                        singular_values=b.singular_values, eta=b.eta, g=b.g,
+                                        sigma_box=tuple(b.sigma_box))
+
+
+def _material_tuple(m):
+    return (np.asarray(m.sigma_s_prime, np.float64), np.asarray(m.sigma_a, np.float64), float(m.eta))
+
+
+def cpu_baseline(cfg, scene, dt, g, b, faces, mats, frames):
+    """The reference's own frame (oracle/reference_frame.py: sssrelight from
+    baseline/_ref, numba csc_apply on every host core) on `frames` frames of
+    the bench sequence, operator from this run's GPU precompute. Returns the
     cpu_baseline object."""
-    import torch
-
-    from oracle import sss_oracle as O
-
-    n, side, L, K = g.count, g.side, cfg.levels, dt.K
-    T2 = (1 << L) ** 2
-    rp = dt.rowptr.cpu().numpy()
-    cols = dt.cols.cpu().numpy().view(np.uint32)
-    vals = dt.vals.cpu().numpy()
-    W2 = scene.W2.cpu().numpy().T  # (N, D) float32 table (precompute output)
-    from paper_2203_12339_b200.transfer import tile_major_to_flat
-
-    tm2flat = tile_major_to_flat(side, L)
-    tiles = np.arange(0, n // T2, sample)
-    rows = (tiles[:, None] * T2 + np.arange(T2)[None, :]).reshape(-1)
-    cam = np.array(scene.camera.position)
-    import concurrent.futures as cf
+    from oracle.reference_frame import ReferenceFrame, time_sequence
 
     cores = os.cpu_count() or 1
-    chunks = np.array_split(rows, cores)
-    pool = cf.ThreadPoolExecutor(max_workers=cores)
-    times = []
-    for i in range(warmup + steps):
-        f = i
-        t0 = time.perf_counter()
-        spectra = O.project_environment(faces[f], 128)
-        E = O.env_irradiance(W2, spectra)
-        sel = O.select_irradiance(E, side, L, cfg.e_keep)
-        x = np.zeros((3, n))
-        for c in range(3):
-            x[c, sel[c].indices] = sel[c].values
-        x = x[:, tm2flat]  # the operator's columns are tile-major ids
-        t1 = time.perf_counter()
-        # stage 2 on every host core: (k, row chunk) tasks in a thread pool
-        # (numpy's gather / bincount release the GIL)
-        list(pool.map(lambda kc: O.csr_rows_apply(rp[kc[0]], cols, vals, kc[1], x),
-                      [(k, ch) for k in range(K) for ch in chunks]))
-        t2 = time.perf_counter()
-        m = scene.material
-        w = O.project_material(b.bases, b.r_nodes, m.sigma_s_prime, m.sigma_a, m.eta)
-        vk = np.zeros((K, 3, n))
-        O.finish(vk, w, side, L, "haar", g.normals.astype(np.float64),
-                 g.positions.astype(np.float64), cam, m.eta)
-        t3 = time.perf_counter()
-        if i >= warmup:
-            times.append((t1 - t0) + (t2 - t1) * (n / rows.size) + (t3 - t2))
-    pool.shutdown()
+    t0 = time.perf_counter()
+    ops = _reference_ops(dt.to_reference())
+    fr = ReferenceFrame(ops, _reference_basis(b), g.positions, g.normals, cfg.side, cfg.levels,
+                        cfg.e_keep, cfg.env_side, scene.camera.position, workers=cores)
+    setup_s = time.perf_counter() - t0
+    try:
+        times = time_sequence(fr, faces, {f: _material_tuple(m) for f, m in mats.items()},
+                              warmup=1, steps=frames, material0=_material_tuple(scene.material))
+    finally:
+        fr.close()
     per_frame = float(np.mean(times))
-    return {"value": n / per_frame, "unit": UNIT, "cores": cores, "kind": "port",
+    return {"value": g.count / per_frame, "unit": UNIT, "cores": cores, "kind": "reference",
             "ms_per_step": per_frame * 1e3,
-            "sample": f"C3 frame, oracle (numpy) port on {cores} host threads: stage 1 + stages 3-5 "
-                      f"in full, stage 2 on "
-                      f"1/{sample} of the tiles ({rows.size} of {n} rows, scaled linearly), "
-                      f"{steps} frames, operator from the GPU precompute"}
+            "sample": f"{frames} whole C3 frames (after 1 warm-up) of the bench sequence through "
+                      f"the reference's own code (baseline/_ref sssrelight: TransferOperator.apply "
+                      f"= numba csc_apply, K x 3 calls over {cores} processes; compress_top_n, "
+                      f"project_material, fresnel_transmittance) with the oracle's L-level Haar "
+                      f"and environment-irradiance restatements; operator from this run's GPU "
+                      f"precompute; setup {setup_s:.1f} s untimed"}
+
+
+def export_operator(a, cfg, path):
+    """Reference arm, step 1 (its own process, on the GPU): build the C3
+    operator with this framework and write it as a PRTS1 container (the
+    reference's on-disk format) + the frame inputs, so the timing process
+    never maps this framework's library."""
+    import torch
+
+    from paper_2203_12339_b200 import _lib
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.basis import build_basis
+    from paper_2203_12339_b200.geometry import make_geometry_image
+    from paper_2203_12339_b200.precompute import precompute_compressed
+    from paper_2203_12339_b200.prts1 import save_prts1
+
+    _lib.load()
+    g = make_geometry_image(cfg.side, cfg.radius, cfg.bump_amp, cfg.bump_terms, cfg.seed)
+    b = build_basis(cfg.K, cfg.lattice)
+    dt = precompute_compressed(g, b, cfg.levels, cfg.step1_keep, cfg.step2_fraction)
+    torch.cuda.synchronize()
+    save_prts1(path, b, dt.to_reference(), cfg.step1_keep, cfg.step2_fraction, cfg.side,
+               mesh_hash=bytes(32), metadata={"config": cfg.name, "levels": cfg.levels})
+    env = LT.Environment(side=cfg.env_side, seed=7)
+    faces, mats = frame_inputs(cfg, env, a.warmup + a.steps, 100)
+    from paper_2203_12339_b200.basis import OpticalMaterial
+    from paper_2203_12339_b200.config import CAMERA
+
+    m0 = OpticalMaterial(sigma_s_prime=cfg.material[0], sigma_a=cfg.material[1], eta=cfg.material[2])
+    edit_frames = sorted(mats)
+    np.savez(str(path) + ".inputs.npz", positions=g.positions, normals=g.normals,
+             faces=np.stack(faces), edit_frames=np.array(edit_frames, np.int64),
+             edit_mats=np.array([np.concatenate([mats[f].sigma_s_prime, mats[f].sigma_a,
+                                                 [mats[f].eta]]) for f in edit_frames]).reshape(-1, 7),
+             material0=np.concatenate([m0.sigma_s_prime, m0.sigma_a, [m0.eta]]),
+             camera=np.array(CAMERA[0]), nnz=dt.nnz)
 
 
 def run_reference(a, cfg):
+    """--impl reference: the reference's own implementation of the C3 frame
+    on this box's host cores (oracle/reference_frame.py), whole frames of the
+    same sequence as ours. Step 1 (a separate GPU process) exports this run's
+    operator as PRTS1; this process loads it with the reference's own loader
+    and never imports the framework or maps its library."""
     ws, rank, local = _dist()
     if rank != 0:
         return
-    import torch
+    from oracle.reference_frame import (ReferenceFrame, import_reference, load_reference_container,
+                                        time_sequence)
 
-    torch.cuda.set_device(local)
-    stats = {}
-    g, b, dt, env, scene = setup_scene(cfg, 0, torch, stats)
-    faces, mats = frame_inputs(cfg, env, a.warmup + a.steps, 100)
-    cpu = cpu_baseline(cfg, scene, dt, g, b, faces, mats, a.cpu_sample_rows, steps=a.steps,
-                       warmup=a.warmup)
+    path = Path("/tmp") / f"sss_ref_{cfg.name}_{os.getpid()}.prts"
+    t0 = time.perf_counter()
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(local)))
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", a.config,
+                          "--steps", str(a.steps), "--warmup", str(a.warmup),
+                          "--export-operator", str(path)], env=env, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("reference arm: operator export failed")
+    export_s = time.perf_counter() - t0
+    R = import_reference()
+    c = load_reference_container(path)
+    z = np.load(str(path) + ".inputs.npz")
+    cores = os.cpu_count() or 1
+    fr = ReferenceFrame(c.compressed.operators, c.basis, z["positions"], z["normals"], cfg.side,
+                        cfg.levels, cfg.e_keep, cfg.env_side, z["camera"], workers=cores)
+    setup_s = time.perf_counter() - t0
+    mats = {int(f): (m[0:3], m[3:6], float(m[6])) for f, m in zip(z["edit_frames"], z["edit_mats"])}
+    m0 = z["material0"]
+    try:
+        times = time_sequence(fr, list(z["faces"]), mats, a.warmup, a.steps,
+                              (m0[0:3], m0[3:6], float(m0[6])))
+    finally:
+        fr.close()
+    for p in (path, Path(str(path) + ".inputs.npz")):
+        try:
+            p.unlink()
+        except OSError:
+            pass
+    per_frame = float(np.mean(times))
+    n = cfg.n
+    loaded = sorted({Path(m.__file__).name for m in list(sys.modules.values())
+                     if getattr(m, "__file__", None) and "paper_2203_12339_b200" in m.__file__})
+    cpu = {"value": n / per_frame, "unit": UNIT, "cores": cores, "kind": "reference",
+           "ms_per_step": per_frame * 1e3,
+           "sample": f"{a.steps} whole C3 frames of the bench sequence (relight every frame, "
+                     f"material edit every {cfg.extra.get('edit_every', 10)}) through the "
+                     f"reference's own code ({R['backend']}: TransferOperator.apply = csc_apply, "
+                     f"K x 3 calls over {cores} processes; compress_top_n, project_material, "
+                     f"fresnel_transmittance) + the oracle's L-level Haar and environment "
+                     f"irradiance restatements; operator loaded from a PRTS1 file by the "
+                     f"reference's load_container (export {export_s:.1f} s, setup "
+                     f"{setup_s:.1f} s, untimed)"}
     line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": cpu["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-            "data": "synthetic (BASELINE C3 shapes)",
-            "config": {"workload": f"{cfg.name} (BASELINE configs[2], C3)", "side": cfg.side,
-                       "points": g.count, "K": cfg.K, "operator_nnz": dt.nnz},
+            "data": "synthetic (seeded geometry image + log-normal/lobe cubemap; BASELINE C3 shapes)",
+            "config": {"workload": f"{cfg.name} (BASELINE configs[2], C3): relight per frame, edit "
+                                   f"every {cfg.extra.get('edit_every', 10)}",
+                       "side": cfg.side, "points": n, "K": cfg.K, "operator_nnz": int(z["nnz"])},
             "cpu_baseline": cpu,
+            "framework_modules_imported": loaded,
             "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -475,7 +560,9 @@ def main():
     cfg = CONFIGS[a.config]
     if a.side:
         cfg = cfg.with_(side=a.side)
-    if a.impl == "reference":
+    if a.export_operator:
+        export_operator(a, cfg, a.export_operator)
+    elif a.impl == "reference":
         run_reference(a, cfg)
     else:
         run_ours(a, cfg)
