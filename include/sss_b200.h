@@ -132,6 +132,13 @@ int sss_direct_irradiance(int n_points, const float* positions, const float* nor
                           const double* material, double ray_offset, double bbox_diagonal,
                           const double* nodes, const double* tris, double* E, void* stream);
 
+/* sss_direct_irradiance64: the same with fp64 positions / normals (the
+ *   reference's SurfaceSamples of an arbitrary mesh, api.Scene). */
+int sss_direct_irradiance64(int n_points, const double* positions, const double* normals,
+                            int n_lights, const int* kinds, const double* lights,
+                            const double* material, double ray_offset, double bbox_diagonal,
+                            const double* nodes, const double* tris, double* E, void* stream);
+
 /* ---- visibility precompute + ambient folding (
  * transfer.py:368-451). D = 6 face_side^2 cubemap texel directions.
  *
@@ -355,6 +362,77 @@ int sss_widen_frame(const float* radiance, const float* radiance_unclamped, long
 /* sss_encode_srgb8: out[i] = uint8(linear_to_srgb(x[i] * exposure) * 255 + 0.5),
  *   the quantised frame payload of the service (service.py:181, envmap.py:74-76). */
 int sss_encode_srgb8(const double* x, long long n, double exposure, uint8_t* out, void* stream);
+
+/* ---- kernel seam: device twins of _kernels_nb (bound with numpy in / out
+ *      by paper_2203_12339_b200/kernels_b200.py, the module a maintainer puts
+ *      behind _accel.get_kernels(), _accel.py:35-43). Bitwise the reference's
+ *      arithmetic (no FMA contraction). ------------------------------------ */
+
+/* sss_wavelet2d: replaces haar2d_fwd_batch / haar2d_inv_batch (kind 0,
+ *   _kernels_nb.py:22-77) and cdf97_fwd_batch / cdf97_inv_batch (kind 1,
+ *   _kernels_nb.py:80-163, used by w1_inverse transfer.py:147-151 and
+ *   _threshold_columns transfer.py:303-316). (batch, side, side) f64, any
+ *   power-of-two side; levels <= 0 = the full pyramid (the reference's only
+ *   mode), else the first `levels` levels. in may alias out. */
+int sss_wavelet2d(const double* in, double* out, int batch, int side, int levels, int kind,
+                  int inverse, void* stream);
+
+/* sss_csr_apply: replaces csc_apply (_kernels_nb.py:301-313, called by
+ *   TransferOperator.apply, transfer.py:66-71). The operator as a row-major
+ *   copy whose entries keep ascending column order (rowptr (n_rows+1) i64,
+ *   cpos = column position, vals f64); xcol (n_cols) the spectrum value per
+ *   column position, present (n_cols) u8 = the column is in x_idx. out[r] =
+ *   the reference's fp64 sum in its order; rows without entries are 0. */
+int sss_csr_apply(int n_rows, const int64_t* rowptr, const int32_t* cpos, const double* vals,
+                  const double* xcol, const uint8_t* present, double* out, void* stream);
+
+/* sss_transfer_rows: replaces transfer_block (_kernels_nb.py:179-205):
+ *   out (nblk, K, n) f64. block_pos (nblk, 3) and positions (n, 3) in one
+ *   dtype (f64pos = 1: double, 0: float; the distance is evaluated in it as
+ *   numba does), areas (n) f64, r_nodes (nr), bases (K, nr), slopes (K, nr-1) f64. */
+int sss_transfer_rows(int nblk, int n, int K, int nr, int f64pos, const void* block_pos,
+                      const void* positions, const double* areas, const double* r_nodes,
+                      const double* bases, const double* slopes, double* out, void* stream);
+
+/* sss_bvh_any_hit: replaces bvh_any_hit (_kernels_nb.py:265-298) on the
+ *   reference's RayAccelerator arrays (lighting.py:101-170): node_min/max
+ *   (n_nodes, 3) f64, left/right/start/count i32, v0/e1/e2 (T, 3) f64;
+ *   origins/dirs (n_rays, 3), tmax (n_rays). hit (n_rays) u8. *overflow is
+ *   set to 1 if a traversal needed more than the reference's 64-entry stack. */
+int sss_bvh_any_hit(int n_rays, const double* origins, const double* dirs, const double* tmax,
+                    int n_nodes, const double* node_min, const double* node_max,
+                    const int32_t* node_left, const int32_t* node_right, const int32_t* node_start,
+                    const int32_t* node_count, const double* v0, const double* e1, const double* e2,
+                    uint8_t* hit, int32_t* overflow, void* stream);
+
+/* ---- the frame of an arbitrary QuadtreeAtlas (api.Scene; runtime.py:109-216)
+ *      D = part_count * grid_side^2 (the w0 / w1 domain), flat_cells (N) i32 =
+ *      part * side^2 + cell (atlas_flat_cells, transfer.py:122-125). */
+
+/* sss_atlas_scatter: scatter_to_grids (transfer.py:128-132): dst (nch, D)
+ *   zeroed (PAD cells), then dst[c, flat_cells[i]] = src[c, i]. */
+int sss_atlas_scatter(const double* src, int nch, int N, const int32_t* flat_cells, int D,
+                      double* dst, void* stream);
+
+/* sss_atlas_recombine: out (3, D) = sum_k g[c, k] (vk[k, c] + vk2[k, c])
+ *   (runtime.py:204; vk2 = the folded ambient term, may be NULL). */
+int sss_atlas_recombine(int K, int D, const double* vk, const double* vk2, const double* g,
+                        double* out, void* stream);
+
+/* sss_atlas_shade: gather_from_grids (transfer.py:135-137) of the inverse-9/7
+ *   grids (3, D) + _shade (runtime.py:162-168): radiance / radiance_unclamped
+ *   (N, 3) f64; cam (3) f64 device, material {sp[3], sa[3], eta}. */
+int sss_atlas_shade(int N, int D, const double* grids, const int32_t* flat_cells,
+                    const double* positions, const double* normals, const double* cam,
+                    const double* material, double* radiance, double* radiance_unclamped,
+                    void* stream);
+
+/* sss_energy_cut: the kept count of compress_energy (wavelets.py:139-153)
+ *   for nvec vectors: sqT (D, nvec) = squared coefficients in descending-|v|
+ *   order (stable), transposed; the reference's sequential cumsum and
+ *   searchsorted(.., fraction * total, "left") + 1, capped at nnz[v]. */
+int sss_energy_cut(const double* sqT, int nvec, int D, double fraction, const int32_t* nnz,
+                   int32_t* kept, void* stream);
 
 #ifdef __cplusplus
 }

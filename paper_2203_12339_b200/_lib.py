@@ -45,6 +45,8 @@ _SIGS = {
     "sss_fold_apply_rows": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_fold_apply": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_direct_irradiance": [_I, _P, _P, _I, _P, _P, _P, C.c_double, C.c_double, _P, _P, _P, _P],
+    "sss_direct_irradiance64": [_I, _P, _P, _I, _P, _P, _P, C.c_double, C.c_double, _P, _P, _P,
+                                _P],
     "sss_edit_finish": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_pair_block": [_I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _I, C.c_float, _P, _P, _P],
     "sss_step1_select": [_P, _I, _I, _I, _P, _P, _P],
@@ -60,6 +62,14 @@ _SIGS = {
     "sss_zero": [_P, C.c_ulonglong, _P],
     "sss_widen_frame": [_P, _P, C.c_longlong, _P, _P],
     "sss_encode_srgb8": [_P, C.c_longlong, _D, _P, _P],
+    "sss_wavelet2d": [_P, _P, _I, _I, _I, _I, _I, _P],
+    "sss_csr_apply": [_I, _P, _P, _P, _P, _P, _P, _P],
+    "sss_transfer_rows": [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_atlas_scatter": [_P, _I, _I, _P, _I, _P, _P],
+    "sss_atlas_recombine": [_I, _I, _P, _P, _P, _P, _P],
+    "sss_atlas_shade": [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_energy_cut": [_P, _I, _I, _D, _P, _P, _P],
+    "sss_bvh_any_hit": [_I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
 }
 
 

@@ -17,6 +17,7 @@
 #include "direct.cu"
 #include "fold.cu"
 #include "raster.cu"
+#include "seam.cu"
 
 namespace {
 thread_local std::string g_err;
@@ -289,10 +290,16 @@ int sss_sweep_gemm(int n_points, int M, const void* Bq, const void* Gq, const fl
 
 
 
-int sss_direct_irradiance(int n_points, const float* positions, const float* normals,
-                          int n_lights, const int* kinds, const double* lights,
-                          const double* material, double ray_offset, double bbox_diagonal,
-                          const double* nodes, const double* tris, double* E, void* stream) {
+}  // extern "C"
+
+namespace {
+// positions / normals in PT (float: geometry images; double: the reference's
+// SurfaceSamples, sss_direct_irradiance64)
+template <typename PT>
+int direct_irradiance(int n_points, const PT* positions, const PT* normals, int n_lights,
+                      const int* kinds, const double* lights, const double* material,
+                      double ray_offset, double bbox_diagonal, const double* nodes,
+                      const double* tris, double* E, void* stream) {
   if (n_points <= 0 || n_lights < 0 || !positions || !normals || !material || !E || !nodes ||
       !tris || (n_lights > 0 && (!lights || !kinds)))
     return fail(SSS_EINVAL, "bad direct_irradiance arguments");
@@ -303,35 +310,45 @@ int sss_direct_irradiance(int n_points, const float* positions, const float* nor
     return fail(SSS_ECUDA, "memset E");
   const sss::BvhView B{reinterpret_cast<const double2*>(nodes),
                        reinterpret_cast<const double2*>(tris)};
-  const char* sv = getenv("SSS_DIRECT_SPLIT");
-  const int split = sv ? atoi(sv) : 3;
+  constexpr int S = 3;  // 8 threads share a ray (one subtree each)
   for (int l = 0; l < n_lights; ++l) {
     const double* L = lights + 12 * (size_t)l;
     if (kinds[l] < 2) {
-#define SSS_DS(K, S)                                                                        \
-  do {                                                                                      \
-    const int grid = (n_points + (sss::kDirectThreads >> S) - 1) / (sss::kDirectThreads >> S); \
-    sss::k_direct_single<K, S><<<grid, sss::kDirectThreads, 0, st>>>(                       \
-        n_points, positions, normals, L, material, ray_offset, bbox_diagonal, B, E);         \
-  } while (0)
-#define SSS_DSK(K)        \
-  if (split <= 0) SSS_DS(K, 0); \
-  else if (split == 1) SSS_DS(K, 1); \
-  else if (split == 2) SSS_DS(K, 2); \
-  else if (split == 3) SSS_DS(K, 3); \
-  else SSS_DS(K, 4)
-      if (kinds[l] == 0) { SSS_DSK(0); } else { SSS_DSK(1); }
-#undef SSS_DSK
-#undef SSS_DS
+      const int grid = (n_points + (sss::kDirectThreads >> S) - 1) / (sss::kDirectThreads >> S);
+      if (kinds[l] == 0)
+        sss::k_direct_single<0, S, PT><<<grid, sss::kDirectThreads, 0, st>>>(
+            n_points, positions, normals, L, material, ray_offset, bbox_diagonal, B, E);
+      else
+        sss::k_direct_single<1, S, PT><<<grid, sss::kDirectThreads, 0, st>>>(
+            n_points, positions, normals, L, material, ray_offset, bbox_diagonal, B, E);
     } else {
-      sss::k_direct_sphere<<<(n_points + sss::kSpherePts - 1) / sss::kSpherePts,
-                             64 * sss::kSpherePts, 0, st>>>(n_points, positions, normals, L,
-                                                            material, ray_offset, B, E);
+      sss::k_direct_sphere<PT><<<(n_points + sss::kSpherePts - 1) / sss::kSpherePts,
+                                 64 * sss::kSpherePts, 0, st>>>(n_points, positions, normals, L,
+                                                                material, ray_offset, B, E);
     }
     const int rc = check_launch("k_direct_light");
     if (rc) return rc;
   }
   return SSS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int sss_direct_irradiance(int n_points, const float* positions, const float* normals,
+                          int n_lights, const int* kinds, const double* lights,
+                          const double* material, double ray_offset, double bbox_diagonal,
+                          const double* nodes, const double* tris, double* E, void* stream) {
+  return direct_irradiance<float>(n_points, positions, normals, n_lights, kinds, lights, material,
+                                  ray_offset, bbox_diagonal, nodes, tris, E, stream);
+}
+
+int sss_direct_irradiance64(int n_points, const double* positions, const double* normals,
+                            int n_lights, const int* kinds, const double* lights,
+                            const double* material, double ray_offset, double bbox_diagonal,
+                            const double* nodes, const double* tris, double* E, void* stream) {
+  return direct_irradiance<double>(n_points, positions, normals, n_lights, kinds, lights,
+                                   material, ray_offset, bbox_diagonal, nodes, tris, E, stream);
 }
 
 int sss_visibility(int n_points, const float* positions, const float* normals, int n_dirs,
@@ -756,6 +773,148 @@ int sss_encode_srgb8(const double* x, long long n, double exposure, uint8_t* out
   if (n == 0) return SSS_OK;
   sss::k_encode_srgb8<<<(unsigned)((n + 255) / 256), 256, 0, S_(stream)>>>(x, n, exposure, out);
   return check_launch("k_encode_srgb8");
+}
+
+// ---- kernel seam (_accel.get_kernels(), _kernels_nb.py) -------------------
+
+int sss_wavelet2d(const double* in, double* out, int batch, int side, int levels, int kind,
+                  int inverse, void* stream) {
+  if (!pow2(side) || side < 2) return fail(SSS_EINVAL, "side must be a power of two >= 2");
+  int full = 0;
+  while ((1 << full) < side) ++full;
+  if (levels <= 0) levels = full;
+  if (levels > full) return fail(SSS_EINVAL, "levels exceeds log2 side");
+  if (kind != 0 && kind != 1) return fail(SSS_EINVAL, "kind must be 0 (Haar) or 1 (CDF 9/7)");
+  if (batch < 0 || (batch > 0 && (!in || !out))) return fail(SSS_EINVAL, "bad batch or pointer");
+  if (batch == 0) return SSS_OK;
+  if (in != out) {
+    cudaError_t e = cudaMemcpyAsync(out, in, (size_t)batch * side * side * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, S_(stream));
+    if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  }
+  // forward: s = side .. side >> (levels-1), rows then columns;
+  // inverse: s ascending, columns then rows (_kernels_nb.py:22-77, 124-163)
+  const int s_lo = side >> (levels - 1);
+  for (int step = 0; step < levels; ++step) {
+    const int s = inverse ? (s_lo << step) : (side >> step);
+    const int tpl = std::min(std::max(s / 2, 1), 256);
+    const int lpc = 256 / tpl;
+    const size_t smem = 2 * (size_t)lpc * (s + 1) * sizeof(double);
+    const long long lines = (long long)batch * s;
+    const long long grid = (lines + lpc - 1) / lpc;
+    if (grid > 2147483647LL) return fail(SSS_EINVAL, "batch too large");
+    for (int pass = 0; pass < 2; ++pass) {
+      const int axis = inverse ? 1 - pass : pass;
+      const void* fn = kind == 0 ? (inverse ? (const void*)sss::k_wline<0, true>
+                                            : (const void*)sss::k_wline<0, false>)
+                                 : (inverse ? (const void*)sss::k_wline<1, true>
+                                            : (const void*)sss::k_wline<1, false>);
+      if (int r = set_smem(fn, smem)) return r;
+      if (kind == 0) {
+        if (inverse) sss::k_wline<0, true><<<(unsigned)grid, 256, smem, S_(stream)>>>(out, batch, side, s, axis, tpl);
+        else sss::k_wline<0, false><<<(unsigned)grid, 256, smem, S_(stream)>>>(out, batch, side, s, axis, tpl);
+      } else {
+        if (inverse) sss::k_wline<1, true><<<(unsigned)grid, 256, smem, S_(stream)>>>(out, batch, side, s, axis, tpl);
+        else sss::k_wline<1, false><<<(unsigned)grid, 256, smem, S_(stream)>>>(out, batch, side, s, axis, tpl);
+      }
+      if (int r = check_launch("k_wline")) return r;
+    }
+  }
+  return SSS_OK;
+}
+
+int sss_csr_apply(int n_rows, const int64_t* rowptr, const int32_t* cpos, const double* vals,
+                  const double* xcol, const uint8_t* present, double* out, void* stream) {
+  if (n_rows < 0 || (n_rows > 0 && (!rowptr || !out || !xcol || !present)))
+    return fail(SSS_EINVAL, "bad csr_apply arguments");
+  if (n_rows == 0) return SSS_OK;
+  sss::k_csr_apply<<<(n_rows + 127) / 128, 128, 0, S_(stream)>>>(
+      n_rows, reinterpret_cast<const long long*>(rowptr), cpos, vals, xcol, present, out);
+  return check_launch("k_csr_apply");
+}
+
+int sss_transfer_rows(int nblk, int n, int K, int nr, int f64pos, const void* block_pos,
+                      const void* positions, const double* areas, const double* r_nodes,
+                      const double* bases, const double* slopes, double* out, void* stream) {
+  if (nblk < 0 || n < 0 || K < 1 || nr < 2 || !areas || !r_nodes || !bases || !slopes ||
+      ((long long)nblk * n > 0 && (!block_pos || !positions || !out)))
+    return fail(SSS_EINVAL, "bad transfer_rows arguments");
+  const long long total = (long long)nblk * n;
+  if (total == 0) return SSS_OK;
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  if (f64pos)
+    sss::k_transfer_rows<double><<<grid, 256, 0, S_(stream)>>>(
+        nblk, n, K, nr, (const double*)block_pos, (const double*)positions, areas, r_nodes, bases,
+        slopes, out);
+  else
+    sss::k_transfer_rows<float><<<grid, 256, 0, S_(stream)>>>(
+        nblk, n, K, nr, (const float*)block_pos, (const float*)positions, areas, r_nodes, bases,
+        slopes, out);
+  return check_launch("k_transfer_rows");
+}
+
+int sss_bvh_any_hit(int n_rays, const double* origins, const double* dirs, const double* tmax,
+                    int n_nodes, const double* node_min, const double* node_max,
+                    const int32_t* node_left, const int32_t* node_right, const int32_t* node_start,
+                    const int32_t* node_count, const double* v0, const double* e1, const double* e2,
+                    uint8_t* hit, int32_t* overflow, void* stream) {
+  if (n_rays < 0 || n_nodes < 0 || (n_rays > 0 && (!origins || !dirs || !tmax || !hit)))
+    return fail(SSS_EINVAL, "bad bvh_any_hit arguments");
+  if (n_rays == 0) return SSS_OK;
+  if (n_nodes == 0) {  // empty BVH: nothing is hit (_kernels_nb.py:269-270)
+    cudaError_t e = cudaMemsetAsync(hit, 0, (size_t)n_rays, S_(stream));
+    return e == cudaSuccess ? SSS_OK : fail(SSS_ECUDA, cudaGetErrorString(e));
+  }
+  if (!overflow) return fail(SSS_EINVAL, "overflow flag required");
+  sss::RefBvh B{node_min, node_max, node_left, node_right, node_start, node_count, v0, e1, e2};
+  sss::k_bvh_any_hit<<<(n_rays + 127) / 128, 128, 0, S_(stream)>>>(n_rays, origins, dirs, tmax, B,
+                                                                   hit, overflow);
+  return check_launch("k_bvh_any_hit");
+}
+
+int sss_atlas_scatter(const double* src, int nch, int N, const int32_t* flat_cells, int D,
+                      double* dst, void* stream) {
+  if (nch < 1 || N < 0 || D < N || !dst || (N > 0 && (!src || !flat_cells)))
+    return fail(SSS_EINVAL, "bad atlas_scatter arguments");
+  cudaError_t e = cudaMemsetAsync(dst, 0, (size_t)nch * D * sizeof(double), S_(stream));
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  if (N == 0) return SSS_OK;
+  const long long t = (long long)nch * N;
+  sss::k_atlas_scatter<<<(unsigned)((t + 255) / 256), 256, 0, S_(stream)>>>(src, nch, N, flat_cells,
+                                                                          D, dst);
+  return check_launch("k_atlas_scatter");
+}
+
+int sss_atlas_recombine(int K, int D, const double* vk, const double* vk2, const double* g,
+                        double* out, void* stream) {
+  if (K < 1 || D < 1 || !vk || !g || !out) return fail(SSS_EINVAL, "bad atlas_recombine arguments");
+  const long long t = 3LL * D;
+  sss::k_atlas_recombine<<<(unsigned)((t + 255) / 256), 256, 0, S_(stream)>>>(K, D, vk, vk2, g, out);
+  return check_launch("k_atlas_recombine");
+}
+
+int sss_atlas_shade(int N, int D, const double* grids, const int32_t* flat_cells,
+                    const double* positions, const double* normals, const double* cam,
+                    const double* material, double* radiance, double* radiance_unclamped,
+                    void* stream) {
+  if (N < 0 || (N > 0 && (!grids || !flat_cells || !positions || !normals || !cam || !material ||
+                          !radiance || !radiance_unclamped)))
+    return fail(SSS_EINVAL, "bad atlas_shade arguments");
+  if (N == 0) return SSS_OK;
+  sss::k_atlas_shade<<<(N + 127) / 128, 128, 0, S_(stream)>>>(N, D, grids, flat_cells, positions,
+                                                             normals, cam, material, radiance,
+                                                             radiance_unclamped);
+  return check_launch("k_atlas_shade");
+}
+
+int sss_energy_cut(const double* sqT, int nvec, int D, double fraction, const int32_t* nnz,
+                   int32_t* kept, void* stream) {
+  if (nvec < 0 || D < 0 || fraction < 0.0 || fraction > 1.0 ||
+      (nvec > 0 && (!sqT || !nnz || !kept)))
+    return fail(SSS_EINVAL, "bad energy_cut arguments");
+  if (nvec == 0) return SSS_OK;
+  sss::k_energy_cut<<<(nvec + 127) / 128, 128, 0, S_(stream)>>>(sqT, nvec, D, fraction, nnz, kept);
+  return check_launch("k_energy_cut");
 }
 
 }  // extern "C"

@@ -181,8 +181,9 @@ __device__ __forceinline__ double dot3(const double* a, const double* b) {
   return dadd(dadd(dmul(a[0], b[0]), dmul(a[1], b[1])), dmul(a[2], b[2]));
 }
 
-__device__ __forceinline__ void load_point(int i, const float* __restrict__ positions,
-                                           const float* __restrict__ normals, double ray_offset,
+template <typename PT>
+__device__ __forceinline__ void load_point(int i, const PT* __restrict__ positions,
+                                           const PT* __restrict__ normals, double ray_offset,
                                            double* p, double* n, double* o) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -207,9 +208,9 @@ __device__ __forceinline__ void add_light(double* E, int N, int i, double w, con
 // per sample, so this is where the parallelism comes from.
 constexpr int kDirectThreads = 128;
 
-template <int KIND, int SPLIT>
+template <int KIND, int SPLIT, typename PT = float>
 __global__ void __launch_bounds__(kDirectThreads) k_direct_single(
-    int N, const float* __restrict__ positions, const float* __restrict__ normals,
+    int N, const PT* __restrict__ positions, const PT* __restrict__ normals,
     const double* __restrict__ Lp, const double* __restrict__ material, double ray_offset,
     double bbox_diag, BvhView B, double* __restrict__ E) {
   constexpr int P = 1 << SPLIT;
@@ -265,8 +266,9 @@ __global__ void __launch_bounds__(kDirectThreads) k_direct_single(
 // them in stratum order (the reference's sequential mean).
 constexpr int kSpherePts = 4;
 
+template <typename PT = float>
 __global__ void __launch_bounds__(64 * kSpherePts) k_direct_sphere(
-    int N, const float* __restrict__ positions, const float* __restrict__ normals,
+    int N, const PT* __restrict__ positions, const PT* __restrict__ normals,
     const double* __restrict__ Lp, const double* __restrict__ material, double ray_offset,
     BvhView B, double* __restrict__ E) {
   __shared__ double term[kSpherePts][64];

@@ -41,6 +41,15 @@ class TransferOperator:
     def nnz(self) -> int:
         return int(self.rowidx.size)
 
+    def apply(self, x_idx: np.ndarray, x_val: np.ndarray, out_len: int) -> np.ndarray:
+        """transfer.py:66-71: the operator applied to a sparse spectrum, on the
+        GPU (kernels_b200.csc_apply: bitwise the reference's csc_apply)."""
+        from .kernels_b200 import csc_apply
+
+        return csc_apply(self.cols, self.colptr, self.rowidx, self.vals,
+                         np.ascontiguousarray(x_idx, np.uint32),
+                         np.ascontiguousarray(x_val, np.float64), out_len)
+
 
 def flat_to_tile_major(flat, side: int, levels: int) -> np.ndarray:
     """Global Mallat flat index -> tile-major index (vectorised mirror of
