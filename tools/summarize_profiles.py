@@ -16,7 +16,7 @@ from collections import OrderedDict, defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-FRAME = ("k_transfer_flat16", "k_transfer_flat8s", "k_env_irradiance_multi", "k_select_cluster", "k_env_project",
+FRAME = ("k_transfer_kfr", "k_transfer_flat16", "k_transfer_flat8s", "k_env_irradiance_multi", "k_select_cluster", "k_env_project",
          "k_edit_finish_multi", "k_material_weights", "k_env_union", "k_pack_x_bits",
          "k_sh_irradiance_multi", "k_direct_single", "k_fold_apply_rows")
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -47,8 +47,8 @@ def launches(src: Path, prefix: str, out: Path):
     relight += sum(sum(v) / len(v) for k, v in frame.items() if "k_edit_finish" in k)
     lines = [f"# {prefix} ncu launch list summary (gpu__time_duration.sum, --clock-control none; "
              "cold-cache, serialized)",
-             f"# source: profiles/{prefix}_launches.csv (python bench.py --steps 2 --warmup 3 "
-             "--no-cpu-baseline --no-secondary under ncu)",
+             f"# source: profiles/{prefix}_launches.csv (ncu --nvtx --nvtx-include timed/ python "
+             "bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-secondary: the timed frames only)",
              "# --- per-frame kernels (relight; edit frames: k_material_weights + k_edit_finish_multi)",
              "kernel,launches,mean_us,share_of_relight_pct"]
     for k, v in frame.items():
@@ -81,7 +81,9 @@ def full(rep: Path, prefix: str, out: Path, command: str):
     js = {"kernel": kname[:90], "capture": command, "dram_bytes_per_launch": rd + wr,
           "dram_read_bytes": rd, "dram_write_bytes": wr, "metrics": met,
           "top_stalls_per_issue": stalls}
-    (out / f"{prefix}_transfer_dram_bytes.json").write_text(json.dumps(js, indent=1) + "\n")
+    kk = "kfr" if "kfr" in kname else ("flat16" if "flat16" in kname else "")
+    name = f"{prefix}_transfer_{kk}_dram_bytes.json" if kk else f"{prefix}_transfer_dram_bytes.json"
+    (out / name).write_text(json.dumps(js, indent=1) + "\n")
 
 
 def main():
@@ -96,7 +98,7 @@ def main():
         launches(src / "launches.csv", a.prefix, out)
     if (src / a.rep).exists():
         full(src / a.rep, a.prefix, out, "ncu --set full --import-source on --clock-control none "
-             "-k regex:k_transfer_flat -c 1, C3 bench (bench.py --steps 2 --warmup 3 "
+             "-k regex:k_transfer_kfr -s 3 -c 1, C3 bench (bench.py --steps 3 --warmup 3 "
              "--no-cpu-baseline --no-secondary)")
 
 
