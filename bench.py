@@ -331,18 +331,18 @@ def run_ours(a, cfg):
     if rank == 0 and not a.no_secondary and a.side is None:
         # the other §8 rows, measured in the same run on the same GPU: the C2
         # medium interactive sequence (BASELINE configs[1]), the C4 sweep
-        # (HBM-write roofline) and the C5 pair pass (FP32/SFU), one term each mode
+        # (HBM-write roofline) and the C5 exact dipole precompute (FP32/SFU)
         del scene
         torch.cuda.empty_cache()
         sys.path.insert(0, str(ROOT / "tools"))
         import c2_bench
-        import precompute_bench
+        import c5_bench
         import sweep_bench
 
         c2 = c2_bench.measure(100)
         torch.cuda.empty_cache()
         c4 = sweep_bench.measure(256, 20)
-        c5 = precompute_bench.measure(256, skip_full=True, ks=1)
+        c5 = c5_bench.measure(256)
         secondary = {
             "c2_medium_interactive": {k: c2[k] for k in (
                 "points", "frames", "operator_nnz", "device_ms_per_frame", "device_points_per_s",
@@ -352,12 +352,15 @@ def run_ours(a, cfg):
                                  "peak_GBps": c4["peak_GBps"], "frac": c4["frac"],
                                  "bound": "hbm (fp32 output write)", "materials": c4["materials"],
                                  "K": c4["K"]},
-            "c5_pair_pass": {"lerp_s_per_term": c5["pair_pass_lerp_s_per_k"],
-                             "exact_s_per_term": c5["pair_pass_exact_s_per_k"],
-                             "lerp_pairs_per_s_all_K": c5["pair_pass_lerp_pairs_per_s_all_K"],
-                             "exact_pairs_per_s_all_K": c5["pair_pass_exact_pairs_per_s_all_K"],
-                             "exact_mufu_per_s": c5["exact_mufu_per_s_per_k"],
-                             "pairs": c5["pairs"], "bound": "SFU/FP32 (exact), FP64 (lerp)"}}
+            "c5_dipole_precompute": {
+                "kernel": "k_pair_rows_exact (K-fused: R_d once per pair for all 8 terms, "
+                          "receiver-tile blocks, + per-row top-2 % step 1)",
+                "pairs": c5["pairs"], "materials": c5["materials"], "K": c5["K"],
+                "pair_pass_s": c5["pair_pass_s"], "step1_select_s": c5["step1_select_s"],
+                "pairs_per_s": c5["pairs_per_s"],
+                "algorithmic_tflops": c5["algorithmic_tflops"],
+                "fp32_peak_tflops": c5["fp32_peak_tflops"], "fp32_frac": c5["fp32_frac"],
+                "flop_per_pair": 2000, "bound": "MUFU (4 per pair and material) / FP32"}}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,

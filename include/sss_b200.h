@@ -280,6 +280,18 @@ int sss_pair_block(int levels, int exact, int side, const float* pos, const floa
                    const float* Pkm, const float* mat, int n_mat, float r_max, double* D,
                    double* Mout, void* stream);
 
+/* sss_pair_rows_exact: the exact pair pass K-fused and streamed (BASELINE
+ * C5): for receiver tiles [rt0, rt0 + nrt) against every source tile, each
+ * pair's fp32 R_d at the n_mat training materials is evaluated once and
+ * projected on all K terms, x area, w0 Haar along sources. Pkm (K, n_mat)
+ * and mat (n_mat, 4) {sigma_tr, z_r, z_v, alpha'/(4 pi)} are HOST arrays
+ * (copied into the kernel's parameter bank; n_mat <= 64, K <= 16). D (K,
+ * nrt * 4^L, N) fp64 = the step-1 rows of the block for every term
+ * (tile-major rows and columns). */
+int sss_pair_rows_exact(int levels, int side, const float* pos, const float* area, int K,
+                        const float* Pkm, const float* mat, int n_mat, float r_max, int rt0,
+                        int nrt, double* D, void* stream);
+
 /* Step 1 (run_step1 + step1_unions, transfer.py:216-246): per row of D keep
  * the n_keep largest |v| (flat-index tie-break) and OR the kept flat column
  * ids into union_bits (N/32 words, caller-zeroed). */

@@ -49,6 +49,7 @@ _SIGS = {
                                 _P],
     "sss_edit_finish": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_pair_block": [_I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _I, C.c_float, _P, _P, _P],
+    "sss_pair_rows_exact": [_I, _I, _P, _P, _I, _P, _P, _I, C.c_float, _I, _I, _P, _P],
     "sss_step1_select": [_P, _I, _I, _I, _P, _P, _P],
     "sss_step1_rows": [_P, _I, _P, _I, _I, _P, _P, _P],
     "sss_step2_select": [_P, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -621,6 +621,48 @@ int sss_pair_block(int levels, int exact, int side, const float* pos, const floa
   return check_launch("k_pair_block");
 }
 
+int sss_pair_rows_exact(int levels, int side, const float* pos, const float* area, int K,
+                        const float* Pkm, const float* mat, int n_mat, float r_max, int rt0,
+                        int nrt, double* D, void* stream) {
+  if (int r = check_geom(side, levels)) return r;
+  if (levels > 3) return fail(SSS_EINVAL, "pair pass supports levels <= 3");
+  if (!pos || !area || !Pkm || !mat || !D) return fail(SSS_EINVAL, "bad pair_rows pointers");
+  if (K < 1 || K > sss::kExactMaxK) return fail(SSS_EINVAL, "K must lie in [1, 16]");
+  if (n_mat < 1 || n_mat > sss::kExactMaxM) return fail(SSS_EINVAL, "n_mat must lie in [1, 64]");
+  const int MM = n_mat <= 16 ? 16 : (n_mat <= 32 ? 32 : 64);
+  const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
+  if (rt0 < 0 || nrt <= 0 || rt0 + nrt > tiles) return fail(SSS_EINVAL, "receiver tile block out of range");
+  const int KT = K <= 4 ? 4 : (K <= 8 ? 8 : (K <= 12 ? 12 : 16));
+  // host tables -> the kernel's parameter bank (Pkm / mat are host arrays:
+  // Pkm (K, n_mat) row-major, mat (n_mat, 4) {sigma_tr, z_r, z_v, c}); the
+  // padded materials and terms have zero weight
+  sss::ExactTables tb;
+  std::memset(&tb, 0, sizeof(tb));
+  for (int k = 0; k < K; ++k)
+    for (int m = 0; m < n_mat; ++m) tb.P[k * MM + m] = Pkm[k * n_mat + m];
+  for (int m = 0; m < MM; ++m) {
+    const bool real = m < n_mat;
+    const float s = real ? mat[m * 4] : 1.0f, zr = real ? mat[m * 4 + 1] : 1.0f,
+                zv = real ? mat[m * 4 + 2] : 1.0f, c = real ? mat[m * 4 + 3] : 0.0f;
+    tb.m0[m] = make_float4(zr * zr, zv * zv, -s * 1.4426950408889634f, s);
+    tb.m1[m] = make_float4(c * zr, c * zv, 0.0f, 0.0f);
+  }
+  dim3 grid(tiles, nrt);
+  const int rpp = 512 / T2 > 0 ? (512 / T2 < 8 ? 512 / T2 : 8) : 1;
+  const size_t smem = (size_t)KT * rpp * (T2 + 1) * sizeof(double);
+#define SSS_PR(LV, KK, M_)                                                                      \
+  if (levels == LV && KT == KK && MM == M_) {                                                   \
+    if (int r = set_smem((const void*)sss::k_pair_rows_exact<LV, KK, M_>, smem)) return r;      \
+    sss::k_pair_rows_exact<LV, KK, M_><<<grid, 256, smem, S_(stream)>>>(tb, pos, area, side,    \
+                                                                       r_max, rt0, nrt, D);     \
+    return check_launch("k_pair_rows_exact");                                                   \
+  }
+  SSS_PR(3, 8, 64) SSS_PR(3, 4, 16) SSS_PR(3, 8, 32) SSS_PR(3, 4, 64) SSS_PR(3, 12, 64)
+  SSS_PR(3, 16, 64) SSS_PR(2, 4, 16) SSS_PR(2, 8, 32) SSS_PR(2, 8, 64)
+#undef SSS_PR
+  return fail(SSS_EINVAL, "pair_rows: unsupported (levels, K, n_mat)");
+}
+
 int sss_step1_select(const double* D, int n_dom, int n_rows, int n_keep, const uint32_t* tm2flat,
                      uint32_t* union_bits, void* stream) {
   if (!D || !tm2flat || !union_bits || n_dom <= 0 || n_rows < 0 || n_keep < 1)

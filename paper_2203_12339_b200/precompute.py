@@ -13,7 +13,10 @@ atlas) with L-level Haar on w0 and w1 (L <= 3), per PCA term k:
      CSR frame layout.
 
 D and M are materialised per k (2 N^2 doubles: 69 GB at 256^2) — the B200's
-180 GB replaces the reference's spill file and per-group re-evaluation.
+180 GB replaces the reference's spill file and per-group re-evaluation. Exact
+mode (per-pair R_d at every training material) runs step 1 K-fused and
+streamed instead (``sss_pair_rows_exact``: R_d once per pair for all terms,
+receiver-tile blocks of step-1 rows, no N^2 D).
 """
 
 from __future__ import annotations
@@ -83,6 +86,17 @@ class PairPass:
         self.mat = torch.as_tensor(mat, device=dev)
         self.n_mat = mat.shape[0]
         self.r_max = float(basis.r_max)
+        self.Pkm_host = self.mat_host = None
+
+    def run_rows_exact(self, rt0: int, nrt: int, D, stream=None):
+        """K-fused exact pass for receiver tiles [rt0, rt0 + nrt): D (K, nrt *
+        4^L, N) = the step-1 rows of every term (sss_pair_rows_exact)."""
+        if self.Pkm_host is None:  # host tables: the library copies them into the launch
+            self.Pkm_host = self.Pkm.cpu().contiguous()
+            self.mat_host = self.mat.cpu().contiguous()
+        _lib.call("sss_pair_rows_exact", self.levels, self.side, _lib.ptr(self.pos),
+                  _lib.ptr(self.area), self.K, _lib.ptr(self.Pkm_host), _lib.ptr(self.mat_host),
+                  self.n_mat, self.r_max, rt0, nrt, _lib.ptr(D), _lib.stream_ptr(stream))
 
     def run(self, k: int, D=None, M=None, stream=None):
         _lib.call("sss_pair_block", self.levels, int(self.exact), self.side, _lib.ptr(self.pos),
@@ -110,7 +124,11 @@ def precompute_compressed(geometry: GeometryImage, basis: DiffusionBasis, levels
     T2 = (1 << levels) ** 2
     nchunks = (n + EMIT_CHUNK - 1) // EMIT_CHUNK
     sp = _lib.stream_ptr()
-    D = torch.empty((n, n), dtype=torch.float64, device=dev)
+    t_start = time.perf_counter()
+    # exact mode: step 1 K-fused and streamed by receiver blocks (R_d once
+    # per pair for all terms); lerp mode: per term from the full D below
+    exact_unions = step1_unions_exact(pp, n_keep, t2f)[0] if exact else None
+    D = None if exact else torch.empty((n, n), dtype=torch.float64, device=dev)
     M = torch.empty((n, n), dtype=torch.float64, device=dev)
     union = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
     col_t = torch.empty(n, dtype=torch.int64, device=dev)
@@ -123,12 +141,15 @@ def precompute_compressed(geometry: GeometryImage, basis: DiffusionBasis, levels
     total = torch.empty(1, dtype=torch.int64, device=dev)
     rowptr = torch.empty((K, n + 1), dtype=torch.int64, device=dev)
     cols_k, vals_k, nnz, kept_e, total_e, union_sizes, unions = [], [], [], [], [], [], []
-    t_start = time.perf_counter()
     base = 0
     for k in range(K):
         pp.run(k, D, M)
-        union.zero_()
-        _lib.call("sss_step1_select", _lib.ptr(D), n, n, n_keep, _lib.ptr(t2f), _lib.ptr(union), sp)
+        if exact:
+            union.copy_(exact_unions[k])
+        else:
+            union.zero_()
+            _lib.call("sss_step1_select", _lib.ptr(D), n, n, n_keep, _lib.ptr(t2f), _lib.ptr(union),
+                      sp)
         _lib.call("sss_step2_select", _lib.ptr(M), n, float(step2_fraction), _lib.ptr(f2t),
                   _lib.ptr(t2f), _lib.ptr(union), _lib.ptr(col_t), _lib.ptr(col_fmax),
                   _lib.ptr(col_cnt), _lib.ptr(col_e), sp)
@@ -168,15 +189,54 @@ def precompute_compressed(geometry: GeometryImage, basis: DiffusionBasis, levels
     return dt
 
 
+def step1_unions_exact(pp: "PairPass", n_keep: int, t2f: torch.Tensor, block_bytes: int = 4 << 30,
+                       stats: dict = None):
+    """Step 1 of the exact mode, K-fused and streamed (BASELINE C5): receiver
+    tiles in blocks whose (K, rows, N) fp64 step-1 rows fit `block_bytes`;
+    per block one sss_pair_rows_exact launch (R_d once per pair, all K terms)
+    and per term one sss_step1_select over the block's rows. Returns the
+    per-term union bitmaps (flat w0 ids)."""
+    n, K = pp.n, pp.K
+    T2 = (1 << pp.levels) ** 2
+    tiles = n // T2
+    dev = pp.pos.device
+    nrt = max(1, min(tiles, block_bytes // (K * T2 * n * 8)))
+    D = torch.empty((K, nrt * T2, n), dtype=torch.float64, device=dev)
+    unions = [torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev) for _ in range(K)]
+    sp = _lib.stream_ptr()
+    t_pair = t_sel = 0.0
+    for rt0 in range(0, tiles, nrt):
+        nb = min(nrt, tiles - rt0)
+        Db = D.view(-1)[: K * nb * T2 * n].view(K, nb * T2, n)  # a short last block packs tighter
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        pp.run_rows_exact(rt0, nb, Db)
+        e[1].record()
+        for k in range(K):
+            _lib.call("sss_step1_select", _lib.ptr(Db[k]), n, nb * T2, n_keep, _lib.ptr(t2f),
+                      _lib.ptr(unions[k]), sp)
+        e[2].record()
+        if stats is not None:
+            e[2].synchronize()
+            t_pair += e[0].elapsed_time(e[1]) / 1e3
+            t_sel += e[1].elapsed_time(e[2]) / 1e3
+    if stats is not None:
+        stats.update(pair_s=t_pair, select_s=t_sel, block_tiles=nrt, pairs=n * n)
+    return unions, D
+
+
 def step1_only(geometry: GeometryImage, basis: DiffusionBasis, levels: int, step1_keep: float,
-               exact: bool = True, ks=None, device="cuda"):
+               exact: bool = True, ks=None, device="cuda", stats: dict = None):
     """The C5 workload: pair pass (+ w0 Haar) and per-row top-n for each k;
-    returns per-k union bitmaps (flat w0 ids)."""
+    returns per-k union bitmaps (flat w0 ids). Exact mode runs K-fused and
+    streamed (step1_unions_exact); lerp mode one term at a time."""
     side, n = geometry.side, geometry.count
     dev = torch.device(device)
     pp = PairPass(geometry, basis, levels, exact, device)
     _, t2f = _tables(side, levels, dev)
     n_keep = max(int(round(step1_keep * n)), 1)
+    if exact and ks is None:
+        return step1_unions_exact(pp, n_keep, t2f, stats=stats)
     D = torch.empty((n, n), dtype=torch.float64, device=dev)
     unions = []
     for k in (range(basis.K) if ks is None else ks):

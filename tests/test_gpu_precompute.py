@@ -205,3 +205,52 @@ def test_exact_mode_matches_projection_oracle(lib):
         got = D.cpu().numpy()[_rows_tm(pts, side, L)][:, f2t]
         scale = np.abs(b.bases[k]).max() * area.max()
         assert np.abs(got - want).max() <= 1e-3 * scale, k
+
+
+def test_kfused_exact_rows_equal_per_term_pass(lib):
+    """The K-fused streamed exact pass (sss_pair_rows_exact: R_d once per pair,
+    all K terms, constants folded per material) reproduces the per-term
+    pass's step-1 rows (sss_pair_block exact mode) to fp32 rounding, block by
+    block; its per-term unions agree up to near-tie columns; sampled rows are
+    within 1e-3 of the fp64 projection oracle."""
+    from paper_2203_12339_b200.precompute import PairPass, _tables, step1_unions_exact
+
+    cfg = C.C5
+    side, L = 32, 3
+    g, b = _setup(cfg, side, amp=0.1)
+    n, T2 = side * side, 64
+    pp = PairPass(g, b, L, exact=True)
+    f2t, t2f = _tables(side, L, "cuda")
+    Dfull = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    nrt = 3
+    Dblk = torch.empty((b.K, nrt * T2, n), dtype=torch.float64, device="cuda")
+    rt0 = 5
+    pp.run_rows_exact(rt0, nrt, Dblk)
+    for k in range(b.K):
+        pp.run(k, Dfull, None)
+        want = Dfull[rt0 * T2:(rt0 + nrt) * T2]
+        scale = want.abs().max().item()
+        assert (Dblk[k] - want).abs().max().item() <= 1e-4 * scale, k
+    keep = max(int(round(cfg.step1_keep * n)), 1)
+    unions, _ = step1_unions_exact(pp, keep, t2f, block_bytes=8 * b.K * T2 * n * 5)  # 5-tile blocks
+    for k in range(b.K):
+        pp.run(k, Dfull, None)
+        u = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+        lib.sss_step1_select(Dfull.data_ptr(), n, n, keep, t2f.data_ptr(), u.data_ptr(), None)
+        torch.cuda.synchronize()
+        diff = (unions[k] ^ u).cpu().numpy().view(np.uint32)
+        a = int(np.unpackbits(u.cpu().numpy().view(np.uint8)).sum())
+        assert int(np.unpackbits(diff.view(np.uint8)).sum()) <= max(2, a // 200), k
+    # against the fp64 projection oracle on sampled rows of one block
+    pos, area = g.positions.astype(np.float64), g.area.astype(np.float64)
+    P = O.exact_projection_coeffs(b.U, b.singular_values, b.r_nodes, b.K)
+    f2t_h = f2t.cpu().numpy()
+    rows_tm = np.arange(rt0 * T2, (rt0 + nrt) * T2)[::17]
+    T, tpr = 1 << L, side >> L  # tile-major receiver row -> its grid point
+    tile, loc = rows_tm // T2, rows_tm % T2
+    pts = ((tile // tpr) * T + loc // T) * side + (tile % tpr) * T + loc % T
+    ref = O.transfer_block_exact(pos[pts], pos, area, b.r_max, b.sigma_nodes, C.ETA, P)
+    for k in range(b.K):
+        want = O.haar2d_fwd(ref[:, k].reshape(-1, side, side), L).reshape(len(pts), n)
+        got = Dblk[k].cpu().numpy()[rows_tm - rt0 * T2][:, f2t_h]
+        assert np.abs(got - want).max() <= 1e-3 * np.abs(b.bases[k]).max() * area.max(), k
