@@ -146,6 +146,22 @@ def whole_job_rate(points_per_rank: int, ws: int, steps: int, ms: float) -> floa
     return ws * points_per_rank * steps / (ms / 1e3)
 
 
+def workload_config(cfg, n, nnz, ws):
+    """The `config` object of the JSON line: identical for both arms."""
+    return {
+        "workload": f"{cfg.name} (BASELINE configs[2], C3): relight per frame, edit every "
+                    f"{cfg.extra.get('edit_every', 10)}",
+        "side": cfg.side, "points": n, "K": cfg.K, "training_materials": cfg.n_materials,
+        "levels": cfg.levels, "step1_keep": cfg.step1_keep, "step2_fraction": cfg.step2_fraction,
+        "e_keep": cfg.e_keep,
+        "env": f"6x{cfg.env_side}x{cfg.env_side} cubemap, top-128 per channel, "
+               f"{cfg.extra.get('rotate_deg', 1.0)} deg/frame about +y",
+        "operator_nnz": int(nnz),
+        "l2": "inputs larger than L2 (operator > 0.5 GB vs 126 MB L2)",
+        "parallelism": f"{ws} independent objects (1 per GPU)" if ws > 1 else "1 GPU",
+    }
+
+
 def setup_scene(cfg, rank, torch, stats):
     from paper_2203_12339_b200 import lighting as LT
     from paper_2203_12339_b200.basis import OpticalMaterial, build_basis
@@ -367,19 +383,9 @@ def run_ours(a, cfg):
             "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded geometry image + log-normal/lobe cubemap; BASELINE C3 shapes)",
-            "config": {
-                "workload": f"{cfg.name} (BASELINE configs[2], C3): relight per frame, edit every "
-                            f"{cfg.extra.get('edit_every', 10)}",
-                "side": cfg.side, "points": n, "K": cfg.K, "training_materials": cfg.n_materials,
-                "levels": cfg.levels, "step1_keep": cfg.step1_keep,
-                "step2_fraction": cfg.step2_fraction, "e_keep": cfg.e_keep,
-                "env": f"6x{cfg.env_side}x{cfg.env_side} cubemap, top-128 per channel, "
-                       f"{cfg.extra.get('rotate_deg', 1.0)} deg/frame about +y",
-                "operator_nnz": dt.nnz, "operator_bytes": dt.nbytes,
-                "l2": f"inputs larger than L2 (operator {dt.nbytes / 1e9:.2f} GB > 126 MB)",
-                "parallelism": f"{ws} independent objects (1 per GPU)" if ws > 1 else "1 GPU",
-                "precompute_s": stats.get("precompute_s"), "precompute_pairs": stats.get("pairs"),
-            },
+            "config": workload_config(cfg, n, dt.nnz, ws),
+            "setup": {"operator_bytes": dt.nbytes, "precompute_s": stats.get("precompute_s"),
+                      "precompute_pairs": stats.get("pairs")},
             "roofline": {"bound": "hbm", "kernel": f"transfer[{kname}]",
                          "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
@@ -548,9 +554,7 @@ def run_reference(a, cfg):
             "warmup": a.warmup, "ms_per_step": cpu["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
             "data": "synthetic (seeded geometry image + log-normal/lobe cubemap; BASELINE C3 shapes)",
-            "config": {"workload": f"{cfg.name} (BASELINE configs[2], C3): relight per frame, edit "
-                                   f"every {cfg.extra.get('edit_every', 10)}",
-                       "side": cfg.side, "points": n, "K": cfg.K, "operator_nnz": int(z["nnz"])},
+            "config": workload_config(cfg, n, z["nnz"], ws),
             "cpu_baseline": cpu,
             "framework_modules_imported": loaded,
             "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
