@@ -114,17 +114,25 @@ def _operator_bytes(op: TransferOperator, k: int, keep: float, frac: float) -> b
 
 
 def save_prts1(path, basis, operators, step1_keep: float, step2_fraction: float,
-               side: int, mesh_hash: bytes = None, positions=None, metadata: dict = None) -> None:
+               side: int, mesh_hash: bytes = None, positions=None, metadata: dict = None,
+               normals=None) -> None:
     """Write a PRTS1 container for a geometry image (identity single-part
     atlas of side x side cells). `basis` is any object with the BASIS fields
     (r_nodes, bases, singular_values, eta, g, sigma_box); `operators` are
     reference-format TransferOperators (e.g. DeviceTransfer.to_reference()).
-    mesh_hash defaults to sha256 of the float64 positions."""
+    mesh_hash defaults to the reference's TriangleMesh.content_hash
+    (surface.py:42-50) of the geometry image's grid mesh (vertices =
+    positions, normals, grid triangles), so the reference's Scene accepts the
+    container for that mesh."""
     n = side * side
     if mesh_hash is None:
-        if positions is None:
-            raise PRTS1Error("need mesh_hash or positions")
-        mesh_hash = hashlib.sha256(np.ascontiguousarray(positions, np.float64).tobytes()).digest()
+        if positions is None or normals is None:
+            raise PRTS1Error("need mesh_hash, or positions and normals of the geometry image")
+        from .raster import TriangleMesh
+        from .shadows import grid_triangles
+
+        mesh_hash = TriangleMesh(np.asarray(positions, np.float64), np.asarray(normals, np.float64),
+                                 grid_triangles(side)).content_hash()
     if len(mesh_hash) != 32:
         raise PRTS1Error("mesh hash must be 32 bytes (sha256)")
     level = int(np.log2(side)) if side > 1 else 0

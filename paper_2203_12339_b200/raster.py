@@ -35,6 +35,17 @@ class TriangleMesh:
     normals: np.ndarray  # (V, 3)
     triangles: np.ndarray  # (T, 3)
 
+    def content_hash(self) -> bytes:
+        """surface.py:42-50: sha256 of float64 vertices, float64 normals and
+        int32 triangles (what a container's mesh_hash records)."""
+        import hashlib
+
+        h = hashlib.sha256()
+        h.update(np.ascontiguousarray(self.vertices, np.float64).tobytes())
+        h.update(np.ascontiguousarray(self.normals, np.float64).tobytes())
+        h.update(np.ascontiguousarray(self.triangles, np.int32).tobytes())
+        return h.digest()
+
 
 def mesh_of(geometry: GeometryImage) -> TriangleMesh:
     """The geometry image's grid triangulation; vertex i is surface sample i

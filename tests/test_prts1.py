@@ -76,3 +76,32 @@ def test_rejects_bad_containers(tmp_path):
         prts1.load_prts1(bad)
     with pytest.raises(prts1.PRTS1Error, match="different mesh"):
         prts1.load_prts1(GOLD / "ref16.prts", expected_mesh_hash=b"\0" * 32)
+
+
+def test_default_mesh_hash_is_the_reference_content_hash(tmp_path):
+    """save_prts1 without an explicit hash records TriangleMesh.content_hash
+    (surface.py:42-50) of the geometry image's grid mesh, so the reference's
+    Scene accepts the container for that mesh (runtime.py:72-73)."""
+    import sys
+    from pathlib import Path
+
+    from paper_2203_12339_b200.geometry import make_geometry_image
+    from paper_2203_12339_b200.shadows import grid_triangles
+
+    c = prts1.load_prts1(GOLD / "ref16.prts")
+    gi = make_geometry_image(16, amp=0.05, seed=11)
+    out = tmp_path / "h.prts"
+    prts1.save_prts1(out, c.basis, c.operators, c.step1_keep, c.step2_fraction, 16,
+                     positions=gi.positions, normals=gi.normals)
+    got = prts1.load_prts1(out).mesh_hash
+    ref = Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+    if not (ref / "sssrelight").exists():
+        pytest.skip("baseline/_ref not installed")
+    sys.path.insert(0, str(ref))
+    try:
+        from sssrelight.surface import TriangleMesh
+    finally:
+        sys.path.remove(str(ref))
+    mesh = TriangleMesh(vertices=gi.positions.astype(np.float64),
+                        normals=gi.normals.astype(np.float64), triangles=grid_triangles(16))
+    assert got == mesh.content_hash()
