@@ -391,7 +391,8 @@ def run_ours(a, cfg):
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes, "stored_bytes_per_launch": all_bytes,
-                         "touched_nnz": touched, "kernel_ms": k_ms},
+                         "touched_nnz": touched, "kernel_ms": k_ms,
+                         "kernel_choice_us": scene.transfer_timings_us},
             "e2e": e2e,
             # per relight: env_project, env_union, env_irradiance, select, weights,
             # pack_x_bits, transfer, edit_finish; per edit: weights, edit_finish

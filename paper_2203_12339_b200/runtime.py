@@ -184,10 +184,16 @@ class Scene:
         # csrc/flat16_25.cu: the A/B alternative and the fallback layout for
         # larger operators). Knobs are read once, here: a captured graph keeps
         # the launch parameters it was recorded with.
+        # SSS_TRANSFER=auto (default): both are timed on this operator at the
+        # first eager relight and the faster kept (kfr wins on C3-size
+        # operators, flat16 on C2's), see _autotune_transfer
         kfr_ok = self.K <= 16 and n <= 65536
-        self.transfer_kernel = os.environ.get("SSS_TRANSFER", "kfr" if kfr_ok else "flat16")
-        if self.transfer_kernel not in ("kfr", "flat16") or (self.transfer_kernel == "kfr" and not kfr_ok):
-            raise ValueError(f"unsupported transfer kernel {self.transfer_kernel!r}")
+        choice = os.environ.get("SSS_TRANSFER", "auto")
+        if choice not in ("auto", "kfr", "flat16") or (choice == "kfr" and not kfr_ok):
+            raise ValueError(f"unsupported transfer kernel {choice!r}")
+        self.transfer_kernel = ("kfr" if kfr_ok else "flat16") if choice == "auto" else choice
+        self._autotune = choice == "auto" and kfr_ok
+        self.transfer_timings_us = {}
         self._knobs = {
             "kfr_chunk": int(os.environ.get("SSS_KFR_CHUNK", "256")),
             "kfr_steps": int(os.environ.get("SSS_KFR_STEPS", "4")),
@@ -410,11 +416,39 @@ class Scene:
                   st["col_bits"], int(zero_vk), _lib.ptr(self.xp), _lib.ptr(self.xbits),
                   _lib.ptr(self.vk), _lib.ptr(self._wctr), 4, sp)
 
+    def _autotune_transfer(self, stream=None):
+        """Time the core transfer launch of every candidate kernel on this
+        operator and this frame's x (CUDA events, 3 launches each after a
+        warm-up) and keep the fastest; the other layout is freed. Runs once,
+        eagerly (never inside a graph capture)."""
+        cands = ["kfr", "flat16"]
+        times = {}
+        for kern in cands:
+            self.transfer_kernel = kern
+            self._transfer_layout()
+            self.launch_transfer_core(stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(3):
+                self.launch_transfer_core(stream)
+            e1.record(stream)
+            e1.synchronize()
+            times[kern] = 1e3 * e0.elapsed_time(e1) / 3
+        best = min(times, key=times.get)
+        self.transfer_kernel = best
+        for kern in cands:
+            if kern != best:
+                setattr(self.transfer, kern, None)
+        self.transfer_timings_us = times
+        self._autotune = False
+
     def _launch_transfer(self, stream=None, epilogue=True):
         """Stage 2 (+ stages 3-5 when `epilogue`): v_k = T_k x for every term
         and channel. Returns False: the transfer never fuses the epilogue."""
         sp = _lib.stream_ptr(stream)
         self._pack_x(sp)
+        if self._autotune and not torch.cuda.is_current_stream_capturing():
+            self._autotune_transfer(stream)
         # flat16 accumulates with atomics into a zeroed v_k (zeroed on the side
         # stream by launch_relight when _vk_zeroed); kfr writes every row
         self._transfer_core(sp, zero_vk=not getattr(self, "_vk_zeroed", False))
@@ -427,6 +461,8 @@ class Scene:
         (x packed): for roofline timing."""
         sp = _lib.stream_ptr(stream)
         if self.transfer_kernel == "flat16":
+            if getattr(self, "_wctr", None) is None:
+                self._wctr = torch.zeros(1, dtype=torch.int32, device="cuda")
             _lib.call("sss_zero", _lib.ptr(self._wctr), 4, sp)
             _lib.call("sss_zero", _lib.ptr(self.vk), self.vk.numel() * 8, sp)
         self._transfer_core(sp, zero_vk=False)

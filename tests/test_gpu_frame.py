@@ -335,13 +335,14 @@ def _csr_vk_device(sc):
     return out
 
 
-def test_kfr_and_flat16_agree_with_csr_product(c1):
+def test_kfr_and_flat16_agree_with_csr_product(c1, monkeypatch):
     """The default transfer (kfr: K-fused row chunks) and the flat16 A/B
     alternative both compute v_k = T_k x of the canonical CSR (fp64 sums in
     different orders)."""
     from paper_2203_12339_b200 import lighting as LT
     from paper_2203_12339_b200.runtime import SHLight
 
+    monkeypatch.setenv("SSS_TRANSFER", "kfr")
     sc = _scene(c1, SHLight(LT.random_sh_light(3, 23)))
     assert sc.transfer_kernel == "kfr"
     sc.vk.fill_(float("nan"))  # every row must be written
@@ -360,12 +361,13 @@ def test_kfr_and_flat16_agree_with_csr_product(c1):
     assert O.parity_error(a.radiance_unclamped, b.radiance_unclamped, TAU) <= 1e-9
 
 
-def test_kfr_relight_is_bitwise_reproducible(c1):
+def test_kfr_relight_is_bitwise_reproducible(c1, monkeypatch):
     """kfr sums every row in a fixed order (no atomics): two relights of the
     same light are bitwise equal, eager and graph-replayed."""
     from paper_2203_12339_b200 import lighting as LT
     from paper_2203_12339_b200.runtime import SHLight
 
+    monkeypatch.setenv("SSS_TRANSFER", "kfr")
     sc = _scene(c1, SHLight(LT.random_sh_light(3, 31)))
     f1 = sc.relight()
     v1 = sc.vk.clone()
@@ -387,6 +389,7 @@ def test_kfr_multi_chunk_rows(c1, monkeypatch, chunk):
     from paper_2203_12339_b200.runtime import SHLight
 
     monkeypatch.setenv("SSS_KFR_CHUNK", chunk)
+    monkeypatch.setenv("SSS_TRANSFER", "kfr")
     sc = _scene(c1, SHLight(LT.random_sh_light(3, 37)))
     sc.vk.fill_(float("nan"))
     sc.relight()
@@ -401,10 +404,11 @@ def test_kfr_multi_chunk_rows(c1, monkeypatch, chunk):
     assert torch.equal(sc.vk, v1)
 
 
-def test_cuda_graph_replay_matches_eager(c1):
+def test_cuda_graph_replay_matches_eager(c1, monkeypatch):
     from paper_2203_12339_b200 import lighting as LT
     from paper_2203_12339_b200.runtime import SHLight
 
+    monkeypatch.setenv("SSS_TRANSFER", "kfr")  # bitwise: kfr's fixed summation order
     sc = _scene(c1, SHLight(LT.random_sh_light(3, 21)))
     eager = sc.relight().radiance_unclamped
     sc.capture()
@@ -735,3 +739,24 @@ def test_env_union_fused_equals_union_kernel(c1):
     sc._launch_stage1(want_E=True)
     torch.cuda.synchronize()
     assert torch.equal(sc.E, e_fused) and torch.equal(sc.ehat, h_fused)
+
+
+def test_transfer_autotune_picks_a_kernel_and_keeps_parity(c1, monkeypatch):
+    """SSS_TRANSFER=auto (default): the first eager relight times kfr and
+    flat16 on the operator, keeps the faster, frees the other layout; the
+    frame is unchanged (both agree to 1e-12 of the CSR product)."""
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import SHLight
+
+    monkeypatch.delenv("SSS_TRANSFER", raising=False)
+    sc = _scene(c1, SHLight(LT.random_sh_light(3, 41)))
+    f = sc.relight()
+    assert set(sc.transfer_timings_us) == {"kfr", "flat16"}
+    assert sc.transfer_kernel == min(sc.transfer_timings_us, key=sc.transfer_timings_us.get)
+    other = "flat16" if sc.transfer_kernel == "kfr" else "kfr"
+    assert getattr(sc.transfer, other, None) is None
+    want = _csr_vk_device(sc)
+    assert (sc.vk - want).abs().max().item() <= 1e-12 * want.abs().max().item()
+    for _ in range(3):
+        g = sc.relight()  # graph replays with the chosen kernel
+    assert O.parity_error(g.radiance_unclamped, f.radiance_unclamped, TAU) <= 1e-12
