@@ -446,6 +446,18 @@ int sss_atlas_shade(int N, int D, const double* grids, const int32_t* flat_cells
 int sss_energy_cut(const double* sqT, int nvec, int D, double fraction, const int32_t* nnz,
                    int32_t* kept, void* stream);
 
+/* sss_frame_replay: one API frame's stream work in a single call (the Python
+ *   per-call overhead of the relight / edit frames): n_h2d host->device copies
+ *   from pinned staging (the new light / material / camera), an event, the
+ *   frame's CUDA graph (cudaGraphExec_t), an event, the float64 widening of
+ *   the radiance (as sss_widen_frame) and its device->host copy into pinned
+ *   memory, the kept-energy copy. Any part may be NULL / 0. */
+int sss_frame_replay(void* graph_exec, int n_h2d, void* const* h2d_dst, const void* const* h2d_src,
+                     const unsigned long long* h2d_bytes, void* ev_start, void* ev_end,
+                     const float* radiance, const float* radiance_unclamped, long long n3,
+                     double* rad64, void* host_rad64, const void* energy, void* host_energy,
+                     unsigned long long energy_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,8 @@ _SIGS = {
     "sss_zero": [_P, C.c_ulonglong, _P],
     "sss_widen_frame": [_P, _P, C.c_longlong, _P, _P],
     "sss_encode_srgb8": [_P, C.c_longlong, _D, _P, _P],
+    "sss_frame_replay": [_P, _I, _P, _P, _P, _P, _P, _P, _P, C.c_longlong, _P, _P, _P, _P,
+                         C.c_ulonglong, _P],
     "sss_wavelet2d": [_P, _P, _I, _I, _I, _I, _I, _P],
     "sss_csr_apply": [_I, _P, _P, _P, _P, _P, _P, _P],
     "sss_transfer_rows": [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -959,4 +959,38 @@ int sss_energy_cut(const double* sqT, int nvec, int D, double fraction, const in
   return check_launch("k_energy_cut");
 }
 
+// ---- one API frame's stream work in one call (runtime.Scene relight / edit)
+
+int sss_frame_replay(void* graph_exec, int n_h2d, void* const* h2d_dst, const void* const* h2d_src,
+                     const unsigned long long* h2d_bytes, void* ev_start, void* ev_end,
+                     const float* radiance, const float* radiance_unclamped, long long n3,
+                     double* rad64, void* host_rad64, const void* energy, void* host_energy,
+                     unsigned long long energy_bytes, void* stream) {
+  if (!graph_exec || n_h2d < 0 || (n_h2d > 0 && (!h2d_dst || !h2d_src || !h2d_bytes)))
+    return fail(SSS_EINVAL, "bad frame_replay arguments");
+  cudaStream_t st = S_(stream);
+  for (int i = 0; i < n_h2d; ++i) {
+    const cudaError_t e = cudaMemcpyAsync(h2d_dst[i], h2d_src[i], (size_t)h2d_bytes[i],
+                                          cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  }
+  if (ev_start && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_start), st) != cudaSuccess)
+    return fail(SSS_ECUDA, "frame_replay: event record");
+  cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(graph_exec), st);
+  if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  if (ev_end && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
+    return fail(SSS_ECUDA, "frame_replay: event record");
+  if (rad64 && host_rad64) {  // the float64 FrameResult arrays, widened on the device, one D2H
+    if (int r = sss_widen_frame(radiance, radiance_unclamped, n3, rad64, stream)) return r;
+    e = cudaMemcpyAsync(host_rad64, rad64, (size_t)(2 * n3) * sizeof(double),
+                        cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  }
+  if (energy && host_energy && energy_bytes) {
+    e = cudaMemcpyAsync(host_energy, energy, (size_t)energy_bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
+  }
+  return SSS_OK;
+}
+
 }  // extern "C"

@@ -231,8 +231,11 @@ class Scene:
         self._stage_copy(self.cam_buf, self.camera.position)
 
     def _stage_copy(self, dst: torch.Tensor, host: np.ndarray):
-        """Host array -> device buffer through a reused pinned staging tensor."""
-        key = ("stage", tuple(dst.shape))
+        """Host array -> device buffer through a reused pinned staging tensor.
+        The host->device copy is deferred to the next frame submission (one
+        call with the frame's graph, sss_frame_replay) or the next eager
+        launch (_flush_pending)."""
+        key = ("stage", dst.data_ptr())
         pin = getattr(self, "_stage", {}).get(key)
         if pin is None:
             pin = torch.empty(tuple(dst.shape), dtype=dst.dtype, pin_memory=True)
@@ -240,7 +243,18 @@ class Scene:
         # every API frame ends with a synchronize (_frame), so the previous
         # upload from this staging buffer has completed
         pin.numpy()[...] = np.asarray(host, dtype=np.float64).reshape(pin.shape)
-        dst.copy_(pin, non_blocking=True)
+        if not hasattr(self, "_pending"):
+            self._pending = {}
+        self._pending[dst.data_ptr()] = (dst, pin)
+
+    def _flush_pending(self, stream=None):
+        """Issue the deferred staging copies on `stream` (eager paths)."""
+        pend = getattr(self, "_pending", None)
+        if pend:
+            with torch.cuda.stream(stream or torch.cuda.current_stream()):
+                for dst, pin in pend.values():
+                    dst.copy_(pin, non_blocking=True)
+            pend.clear()
 
     def _install_light(self, light):
         dev = torch.device("cuda")
@@ -479,6 +493,8 @@ class Scene:
         depend on the light: they run on a forked stream, joined before the
         transfer (whose epilogue consumes them), off the stage-1 critical path."""
         cur = stream or torch.cuda.current_stream()
+        if not torch.cuda.is_current_stream_capturing():
+            self._flush_pending(cur)
         if getattr(self, "_side", None) is None:
             self._side = torch.cuda.Stream()
         fork, join = torch.cuda.Event(), torch.cuda.Event()
@@ -511,6 +527,8 @@ class Scene:
 
     def launch_edit(self, stream=None):
         """Enqueue the edit path (no host sync)."""
+        if not torch.cuda.is_current_stream_capturing():
+            self._flush_pending(stream)
         self._launch_weights(stream)
         self._launch_edit(stream)
 
@@ -532,6 +550,7 @@ class Scene:
     def replay(self, edit=False):
         if self._graph is None:
             self.capture()
+        self._flush_pending()
         (self._graph_edit if edit else self._graph).replay()
         self._have_cache = True
 
@@ -539,7 +558,13 @@ class Scene:
     # reference API (runtime.py:174-227)
     # ------------------------------------------------------------------
 
-    def _enqueue_readback(self):
+    def _enqueue_readback_init(self):
+        self._pin = {"energy": torch.empty((3, 2), dtype=torch.float64, pin_memory=True),
+                     "radu": torch.empty((self.n, 3), dtype=torch.float32, pin_memory=True)}
+        self._pool = _PinnedPool(self.n)
+        self._rad64 = torch.empty((2, self.n, 3), dtype=torch.float64, device="cuda")
+
+    def _enqueue_readback(self, blk_taken: bool = False):
         """Queue the device->host read-back of the frame's results on the
         current stream, behind the frame's kernels: the radiance and unclamped
         radiance widened to float64 on the device (the reference FrameResult
@@ -547,11 +572,8 @@ class Scene:
         arrays, plus the kept-energy sums. No host round trip before the copy,
         no host-side conversion after it."""
         if getattr(self, "_pin", None) is None:
-            self._pin = {"energy": torch.empty((3, 2), dtype=torch.float64, pin_memory=True),
-                         "radu": torch.empty((self.n, 3), dtype=torch.float32, pin_memory=True)}
-            self._pool = _PinnedPool(self.n)
-            self._rad64 = torch.empty((2, self.n, 3), dtype=torch.float64, device="cuda")
-        blk = self._pool.take()
+            self._enqueue_readback_init()
+        blk = None if blk_taken else self._pool.take()
         if blk is not None:
             _lib.call("sss_widen_frame", _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped),
                       self.n * 3, _lib.ptr(self._rad64), _lib.stream_ptr())
@@ -587,7 +609,42 @@ class Scene:
     def _replay_events(self):
         if getattr(self, "_ev_pair", None) is None:
             self._ev_pair = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            for e in self._ev_pair:  # create the CUDA events (sss_frame_replay records them)
+                e.record()
         return self._ev_pair
+
+    def _submit(self, graph):
+        """One API frame's stream work in one library call (sss_frame_replay):
+        the deferred staging copies, the start event, the frame's graph, the
+        end event, the float64 widening and read-back into a pooled pinned
+        block, the kept-energy copy. Returns the start / end events."""
+        import ctypes as C
+
+        ev = self._replay_events()
+        if getattr(self, "_pin", None) is None:
+            self._enqueue_readback_init()
+        blk = self._pool.take()
+        if blk is None:  # the caller holds every pooled block: the torch path
+            self._flush_pending()
+            ev[0].record()
+            graph.replay()
+            ev[1].record()
+            self._enqueue_readback(blk_taken=True)
+            return ev
+        pend = list(self._pending.values()) if getattr(self, "_pending", None) else []
+        if pend:
+            self._pending.clear()
+        n = len(pend)
+        dsts = (C.c_void_p * max(n, 1))(*[d.data_ptr() for d, _ in pend])
+        srcs = (C.c_void_p * max(n, 1))(*[p_.data_ptr() for _, p_ in pend])
+        sizes = (C.c_ulonglong * max(n, 1))(*[d.numel() * d.element_size() for d, _ in pend])
+        _lib.call("sss_frame_replay", C.c_void_p(graph.raw_cuda_graph_exec()), n, dsts, srcs, sizes,
+                  C.c_void_p(ev[0].cuda_event), C.c_void_p(ev[1].cuda_event),
+                  _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped), self.n * 3,
+                  _lib.ptr(self._rad64), C.c_void_p(blk.data_ptr()), _lib.ptr(self.energy),
+                  C.c_void_p(self._pin["energy"].data_ptr()), 48, _lib.stream_ptr())
+        self._blk = blk
+        return ev
 
     def relight(self) -> FrameResult:
         """Full pipeline; repopulates the stage-2 cache (runtime.py:174-187).
@@ -601,11 +658,7 @@ class Scene:
         if self._graph is None and getattr(self, "_eager_relights", 0) >= 2:
             self.capture()
         if self._graph is not None and getattr(self, "_stage_frac", None):
-            ev = self._replay_events()
-            ev[0].record()
-            self._graph.replay()
-            ev[1].record()
-            self._enqueue_readback()
+            ev = self._submit(self._graph)
             self._have_cache = True
             fr = self._frame(timings, queued=True)  # synchronizes: ev[1] is complete
             total = ev[0].elapsed_time(ev[1])
@@ -613,6 +666,7 @@ class Scene:
                 timings[k] = total * f
             return fr
         self._eager_relights = getattr(self, "_eager_relights", 0) + 1
+        self._flush_pending()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
         self._launch_stage1()
@@ -639,14 +693,11 @@ class Scene:
     def _edit_frame(self) -> FrameResult:
         timings = dict.fromkeys(STAGES, 0.0)
         if getattr(self, "_graph_edit", None) is not None and self._graph is not None:
-            ev = self._replay_events()
-            ev[0].record()
-            self._graph_edit.replay()
-            ev[1].record()
-            self._enqueue_readback()
+            ev = self._submit(self._graph_edit)
             fr = self._frame(timings, queued=True)
             timings["inverse_wavelet"] = ev[0].elapsed_time(ev[1])
             return fr
+        self._flush_pending()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
         self._launch_weights()
@@ -721,6 +772,7 @@ class Scene:
 
     def sweep_launch(self, ops, out, stream=None):
         """out (3, M, N) float32 = clamped exit radiance of every material."""
+        self._flush_pending(stream)
         lo, hi = ops["eta_range"]
         _lib.call("sss_sweep_gemm", self.n, ops["Gq"].shape[1], _lib.ptr(ops["Bq"]),
                   _lib.ptr(ops["Gq"]), _lib.ptr(ops["eta"]), lo, hi, _lib.ptr(self.positions),

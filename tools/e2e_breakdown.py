@@ -26,24 +26,18 @@ def main():
     faces = [env.faces(float(f)) for f in range(60)]
     for f in range(5):
         sc.set_light(EnvLight(faces[f]))
-    ph = {k: [] for k in ("install", "launch", "enqueue", "sync", "convert", "total")}
+    ph = {k: [] for k in ("install", "submit", "sync_and_result", "total")}
     for f in range(5, 55):
         t0 = time.perf_counter()
-        sc._install_light(EnvLight(faces[f]))
+        sc._install_light(EnvLight(faces[f]))   # host staging (pinned), H2D deferred
         t1 = time.perf_counter()
-        ev = sc._replay_events()
-        ev[0].record()
-        sc._graph.replay()
-        ev[1].record()
+        ev = sc._submit(sc._graph)              # sss_frame_replay: H2D, graph, widen, D2H
         t2 = time.perf_counter()
-        sc._enqueue_readback()
-        t3 = time.perf_counter()
-        t4 = time.perf_counter()
-        fr = sc._frame({}, queued=True)
+        fr = sc._frame({}, queued=True)         # synchronize + FrameResult arrays
         rad = fr.radiance
-        t5 = time.perf_counter()
-        for k, a_, b_ in (("install", t0, t1), ("launch", t1, t2), ("enqueue", t2, t3),
-                          ("sync", t3, t4), ("convert", t4, t5), ("total", t0, t5)):
+        t3 = time.perf_counter()
+        for k, a_, b_ in (("install", t0, t1), ("submit", t1, t2), ("sync_and_result", t2, t3),
+                          ("total", t0, t3)):
             ph[k].append((b_ - a_) * 1e3)
     out = {k: round(float(np.median(v)), 4) for k, v in ph.items()}
     out["gpu_graph_ms"] = round(ev[0].elapsed_time(ev[1]), 4)
