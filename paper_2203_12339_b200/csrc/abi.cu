@@ -647,14 +647,33 @@ int sss_pair_rows_exact(int levels, int side, const float* pos, const float* are
     tb.m0[m] = make_float4(zr * zr, zv * zv, -s * 1.4426950408889634f, s);
     tb.m1[m] = make_float4(c * zr, c * zv, 0.0f, 0.0f);
   }
+  for (int j = 0; j < MM / 2; ++j) {  // the packed material pairs
+    const float4 a = tb.m0[2 * j], b = tb.m0[2 * j + 1], c = tb.m1[2 * j], d = tb.m1[2 * j + 1];
+    tb.pA[j] = make_float2(a.x, b.x);
+    tb.pB[j] = make_float2(a.y, b.y);
+    tb.pS[j] = make_float2(a.z, b.z);
+    tb.ps[j] = make_float2(a.w, b.w);
+    tb.pCr[j] = make_float2(c.x, d.x);
+    tb.pCv[j] = make_float2(c.y, d.y);
+    for (int k = 0; k < sss::kExactMaxK; ++k)
+      tb.pP[k * (MM / 2) + j] = make_float2(tb.P[k * MM + 2 * j], tb.P[k * MM + 2 * j + 1]);
+  }
+  const char* x2e = getenv("SSS_C5_X2");
+  const bool x2 = !x2e || atoi(x2e) != 0;
   dim3 grid(tiles, nrt);
   const int rpp = 512 / T2 > 0 ? (512 / T2 < 8 ? 512 / T2 : 8) : 1;
   const size_t smem = (size_t)KT * rpp * (T2 + 1) * sizeof(double);
 #define SSS_PR(LV, KK, M_)                                                                      \
   if (levels == LV && KT == KK && MM == M_) {                                                   \
-    if (int r = set_smem((const void*)sss::k_pair_rows_exact<LV, KK, M_>, smem)) return r;      \
-    sss::k_pair_rows_exact<LV, KK, M_><<<grid, 256, smem, S_(stream)>>>(tb, pos, area, side,    \
-                                                                       r_max, rt0, nrt, D);     \
+    if (x2) {                                                                                   \
+      if (int r = set_smem((const void*)sss::k_pair_rows_exact<LV, KK, M_, true>, smem)) return r; \
+      sss::k_pair_rows_exact<LV, KK, M_, true><<<grid, 256, smem, S_(stream)>>>(                \
+          tb, pos, area, side, r_max, rt0, nrt, D);                                             \
+    } else {                                                                                    \
+      if (int r = set_smem((const void*)sss::k_pair_rows_exact<LV, KK, M_>, smem)) return r;    \
+      sss::k_pair_rows_exact<LV, KK, M_><<<grid, 256, smem, S_(stream)>>>(tb, pos, area, side,  \
+                                                                         r_max, rt0, nrt, D);   \
+    }                                                                                           \
     return check_launch("k_pair_rows_exact");                                                   \
   }
   SSS_PR(3, 8, 64) SSS_PR(3, 4, 16) SSS_PR(3, 8, 32) SSS_PR(3, 4, 64) SSS_PR(3, 12, 64)

@@ -429,6 +429,10 @@ __global__ void k_band_offsets(const uint64_t* __restrict__ rowptr, const uint32
 constexpr int kExactMaxK = 16, kExactMaxM = 64;
 
 struct ExactTables {
+  // material pairs for the packed-FP32x2 loop: entry j = materials (2j, 2j+1)
+  float2 pA[kExactMaxM / 2], pB[kExactMaxM / 2], pS[kExactMaxM / 2], ps[kExactMaxM / 2];
+  float2 pCr[kExactMaxM / 2], pCv[kExactMaxM / 2];
+  float2 pP[kExactMaxK * kExactMaxM / 2];  // pP[k * MM / 2 + j]
   float P[kExactMaxK * kExactMaxM];  // P[k * MM + m] = U/S projection (zero rows past K)
   // per material, with S = -sigma_tr log2(e), c = alpha' / (4 pi):
   float4 m0[kExactMaxM];  // {z_r^2, z_v^2, S, sigma_tr}
@@ -441,13 +445,41 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// packed FP32x2 (Blackwell FFMA2 / FMUL2 / FADD2): two fp32 lanes per 64-bit
+// register pair, one issue slot
+typedef unsigned long long f32x2_t;
+__device__ __forceinline__ f32x2_t pk2(float lo, float hi) {
+  f32x2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f32x2_t pk2(float2 v) { return pk2(v.x, v.y); }
+__device__ __forceinline__ void upk2(f32x2_t r, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ f32x2_t add2(f32x2_t a, f32x2_t b) {
+  f32x2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2_t mul2(f32x2_t a, f32x2_t b) {
+  f32x2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2_t fma2(f32x2_t a, f32x2_t b, f32x2_t c) {
+  f32x2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-template <int L, int KT, int MM>
+template <int L, int KT, int MM, bool X2 = false>
 __global__ void __launch_bounds__(256) k_pair_rows_exact(const __grid_constant__ ExactTables tb,
                                                          const float* __restrict__ pos,
                                                          const float* __restrict__ area, int S,
@@ -473,7 +505,40 @@ __global__ void __launch_bounds__(256) k_pair_rows_exact(const __grid_constant__
       float acc[KT];
 #pragma unroll
       for (int k = 0; k < KT; ++k) acc[k] = 0.0f;
-      if (sqrtf(r2) <= r_max) {
+      if (X2 && sqrtf(r2) <= r_max) {
+        // two materials per step in packed FP32x2 (the 4 MUFU ops per
+        // material stay scalar); per term even / odd materials accumulate
+        // separately and are added at the end
+        const f32x2_t r22 = pk2(r2, r2);
+        f32x2_t acc2[KT];
+#pragma unroll
+        for (int k = 0; k < KT; ++k) acc2[k] = 0ull;
+#pragma unroll
+        for (int j = 0; j < MM / 2; ++j) {
+          const f32x2_t ar2 = add2(r22, pk2(tb.pA[j])), av2 = add2(r22, pk2(tb.pB[j]));
+          float ar0, ar1, av0, av1;
+          upk2(ar2, ar0, ar1);
+          upk2(av2, av0, av1);
+          const f32x2_t ir2 = pk2(rsqrt_approx(ar0), rsqrt_approx(ar1));
+          const f32x2_t iv2 = pk2(rsqrt_approx(av0), rsqrt_approx(av1));
+          float xr0, xr1, xv0, xv1;
+          upk2(mul2(mul2(ar2, pk2(tb.pS[j])), ir2), xr0, xr1);
+          upk2(mul2(mul2(av2, pk2(tb.pS[j])), iv2), xv0, xv1);
+          const f32x2_t er2 = pk2(ex2_approx(xr0), ex2_approx(xr1));
+          const f32x2_t ev2 = pk2(ex2_approx(xv0), ex2_approx(xv1));
+          const f32x2_t tr2 = mul2(mul2(mul2(mul2(add2(ir2, pk2(tb.ps[j])), pk2(tb.pCr[j])), er2), ir2), ir2);
+          const f32x2_t tv2 = mul2(mul2(mul2(mul2(add2(iv2, pk2(tb.ps[j])), pk2(tb.pCv[j])), ev2), iv2), iv2);
+          const f32x2_t rd2 = add2(tr2, tv2);
+#pragma unroll
+          for (int k = 0; k < KT; ++k) acc2[k] = fma2(pk2(tb.pP[k * (MM / 2) + j]), rd2, acc2[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          float lo, hi;
+          upk2(acc2[k], lo, hi);
+          acc[k] = lo + hi;
+        }
+      } else if (!X2 && sqrtf(r2) <= r_max) {
 #pragma unroll
         for (int m = 0; m < MM; ++m) {
           // R_d = c z_r (s + 1/d_r) e^{-s d_r} / d_r^2 + (the same at z_v),
