@@ -272,10 +272,17 @@ int sss_sweep_gemm(int n_points, int M, const void* Bq, const void* Gq, const fl
 #define SSS_SW(TMN, THR, SMEMKB)                                                                   \
   do {                                                                                             \
     const size_t smem = (size_t)(SMEMKB) * 1024;                                                  \
-    const void* fn = (const void*)sss::k_sweep_umma<TMN, THR>;                                     \
+    const void* fn = n_points == 65536 ? (const void*)sss::k_sweep_umma<TMN, THR, 65536>          \
+                                       : (const void*)sss::k_sweep_umma<TMN, THR>;                 \
     if (int r = set_smem(fn, smem)) return r;                                                      \
     dim3 grid = g1;                                                                                \
     grid.z = (M + TMN - 1) / TMN;                                                                  \
+    if (n_points == 65536)                                                                         \
+      sss::k_sweep_umma<TMN, THR, 65536><<<grid, THR, smem, S_(stream)>>>(                         \
+          n_points, M, reinterpret_cast<const __nv_bfloat16*>(Bq),                                 \
+          reinterpret_cast<const __nv_bfloat16*>(Gq), eta, eta_lo, eta_hi, positions, normals,     \
+          cam, out);                                                                               \
+    else                                                                                           \
     sss::k_sweep_umma<TMN, THR><<<grid, THR, smem, S_(stream)>>>(                                  \
         n_points, M, reinterpret_cast<const __nv_bfloat16*>(Bq),                                   \
         reinterpret_cast<const __nv_bfloat16*>(Gq), eta, eta_lo, eta_hi, positions, normals, cam,   \

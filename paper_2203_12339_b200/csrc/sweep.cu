@@ -58,14 +58,18 @@ __device__ __forceinline__ float ft_exit_f(float eta, float ci) {
 // SWEEP_M materials per MMA (N of the UMMA): multiple of 16, <= 256.
 // THREADS = 128 or 256: warp w reads TMEM lane quarter w % 4 (a tile row per
 // lane); with 256 threads the two warps of a quarter split the columns.
-template <int SWEEP_M, int THREADS>
+// NC > 0: the point count is the compile-time constant NC (the 256^2 sweep),
+// so the per-material store offsets j * N become STG immediates (no 64-bit
+// address arithmetic per element)
+template <int SWEEP_M, int THREADS, int NC = 0>
 __global__ void __launch_bounds__(THREADS) k_sweep_umma(
-    int N, int M_total, const __nv_bfloat16* __restrict__ Bq /* (3, N, 16) */,
+    int N_rt, int M_total, const __nv_bfloat16* __restrict__ Bq /* (3, N, 16) */,
     const __nv_bfloat16* __restrict__ Gq /* (3, M_total, 16) */,
     const float* __restrict__ eta /* (M_total) */, float eta_lo, float eta_hi,
     const float* __restrict__ positions, const float* __restrict__ normals,
     const double* __restrict__ cam, float* __restrict__ out /* (3, M_total, N) */) {
   static_assert(SWEEP_M % 16 == 0 && SWEEP_M <= 256, "UMMA N");
+  const int N = NC > 0 ? NC : N_rt;
   constexpr int TMEM_COLS = SWEEP_M <= 32 ? 32 : SWEEP_M <= 64 ? 64 : SWEEP_M <= 128 ? 128 : 256;
   extern __shared__ __align__(1024) uint8_t sw_smem[];
   uint8_t* sA = sw_smem;                                   // 128 x 16 bf16 = 4 KB
@@ -175,14 +179,33 @@ __global__ void __launch_bounds__(THREADS) k_sweep_umma(
       float* o = oc + (size_t)(m0 + j0) * N + p;
       if (j0 + 32 <= nm) {  // full chunk: no per-element bounds checks
         const float4* t4 = reinterpret_cast<const float4*>(st + j0);
+        // two materials per packed FP32x2 instruction (FFMA2 / FMUL2): the
+        // cubic in t and the scale, then clamp and store per element
+        unsigned long long A0, A1, A2, A3;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(A0) : "f"(a0));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(A1) : "f"(a1));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(A2) : "f"(a2));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(A3) : "f"(a3));
+        const unsigned long long* t2 = reinterpret_cast<const unsigned long long*>(st + j0);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 t = t4[q];
-          const float tt[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float ft = fmaf(fmaf(fmaf(a3, tt[u], a2), tt[u], a1), tt[u], a0);
-            __stcs(o, fmaxf(ft * __uint_as_float(r[q * 4 + u]), 0.0f));
+        for (int q = 0; q < 16; ++q) {
+          const unsigned long long T = t2[q];
+          unsigned long long f, v;
+          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(f) : "l"(A3), "l"(T), "l"(A2));
+          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(f) : "l"(f), "l"(T), "l"(A1));
+          asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(f) : "l"(f), "l"(T), "l"(A0));
+          unsigned long long rr;
+          asm("mov.b64 %0, {%1, %2};" : "=l"(rr) : "r"(r[2 * q]), "r"(r[2 * q + 1]));
+          asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(v) : "l"(f), "l"(rr));
+          float v0, v1;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(v0), "=f"(v1) : "l"(v));
+          if (NC > 0) {
+            __stcs(o + (size_t)(2 * q) * NC, fmaxf(v0, 0.0f));
+            __stcs(o + (size_t)(2 * q + 1) * NC, fmaxf(v1, 0.0f));
+          } else {
+            __stcs(o, fmaxf(v0, 0.0f));
+            o += N;
+            __stcs(o, fmaxf(v1, 0.0f));
             o += N;
           }
         }
