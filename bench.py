@@ -262,6 +262,7 @@ def run_ours(a, cfg):
     torch.cuda.synchronize()
     k_ms = float(np.mean([x.elapsed_time(y) for x, y in kt]))
     kname = scene.transfer_kernel
+    kchoice = dict(scene.transfer_timings_us)
     # algorithmic bytes of one transfer launch (SURVEY §8d B_T + B_c), with the
     # selection of the current frame: entries whose w0 column is kept by any
     # channel (8 B each: u32 col + f32 val) + row pointers + v_k cache write +
@@ -392,7 +393,7 @@ def run_ours(a, cfg):
                          "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes, "stored_bytes_per_launch": all_bytes,
                          "touched_nnz": touched, "kernel_ms": k_ms,
-                         "kernel_choice_us": scene.transfer_timings_us},
+                         "kernel_choice_us": kchoice},
             "e2e": e2e,
             # per relight: env_project, env_union, env_irradiance, select, weights,
             # pack_x_bits, transfer, edit_finish; per edit: weights, edit_finish
