@@ -253,3 +253,63 @@ def to_device(c: PRTS1, levels: int, device="cuda"):
     if not c.is_identity_geometry_image():
         raise PRTS1Error("only single-part identity atlases (geometry images) map to the GPU layout")
     return DeviceTransfer.from_reference(c.operators, c.grid_side, levels, device=device)
+
+
+# ---------------------------------------------------------------------------
+# GPU-native blocked layout, stored beside a container
+# ---------------------------------------------------------------------------
+# The reference's loader rejects unknown chunks (container.py:222-226), so the
+# frame layout the transfer kernel streams (layout.KfrLayout: warp items,
+# TMA batches of (column, term-mask) pair words + values) goes to a sidecar
+# file <container>.kfr tied to the container's operators by a digest: loading
+# it skips the layout build, and the container itself stays reference-valid.
+
+KFR_MAGIC = "PRTSKFR1"
+_KFR_ARRAYS = ("items", "lane_len", "lane_dst", "batch_off", "stream", "partial_row",
+               "multi_info")
+
+
+def operators_digest(operators) -> str:
+    """sha256 over every operator's cols / colptr / rowidx / f32 vals."""
+    h = hashlib.sha256()
+    for op in operators:
+        for a, dt in ((op.cols, "<u4"), (op.colptr, "<i8"), (op.rowidx, "<u4"), (op.vals, "<f4")):
+            h.update(np.ascontiguousarray(a, dt).tobytes())
+    return h.hexdigest()
+
+
+def save_gpu_layout(path, layout, digest: str) -> None:
+    """Write the kfr frame layout of an operator set (digest = operators_digest
+    of the container's operators) as a sidecar .npz."""
+    meta = {"magic": KFR_MAGIC, "K": layout.K, "n": layout.n, "n_items": layout.n_items,
+            "n_partials": layout.n_partials, "stats": layout.stats, "digest": digest}
+    arrays = {k: getattr(layout, k).cpu().numpy() for k in _KFR_ARRAYS}
+    with open(path, "wb") as fh:
+        np.savez(fh, meta=np.frombuffer(json.dumps(meta).encode("utf-8"), np.uint8), **arrays)
+
+
+def load_gpu_layout(path, digest: str, device="cuda"):
+    """Read a sidecar written by save_gpu_layout; PRTS1Error if it belongs to
+    other operators (digest mismatch) or is not a kfr layout."""
+    import torch
+
+    from .layout import KFR_GROUP, KfrLayout
+
+    with np.load(path) as z:
+        meta = json.loads(bytes(z["meta"]).decode("utf-8"))
+        if meta.get("magic") != KFR_MAGIC:
+            raise PRTS1Error(f"{path}: not a kfr layout sidecar")
+        if meta.get("digest") != digest:
+            raise PRTS1Error(f"{path}: layout was built for different operators")
+        t = {k: torch.as_tensor(z[k], device=device) for k in _KFR_ARRAYS}
+    M = int(t["multi_info"].shape[0])
+    dev = torch.device(device)
+    return KfrLayout(
+        K=meta["K"], n=meta["n"], n_items=meta["n_items"], n_partials=meta["n_partials"],
+        items=t["items"], lane_len=t["lane_len"], lane_dst=t["lane_dst"],
+        batch_off=t["batch_off"], stream=t["stream"],
+        partials=torch.zeros((3 * KFR_GROUP, max(meta["n_partials"], 1)), dtype=torch.float64,
+                             device=dev),
+        partial_row=t["partial_row"], multi_info=t["multi_info"],
+        multi_count=torch.zeros(M, dtype=torch.int32, device=dev),
+        work=torch.zeros(2, dtype=torch.int32, device=dev), stats=meta["stats"])

@@ -760,3 +760,35 @@ def test_transfer_autotune_picks_a_kernel_and_keeps_parity(c1, monkeypatch):
     for _ in range(3):
         g = sc.relight()  # graph replays with the chosen kernel
     assert O.parity_error(g.radiance_unclamped, f.radiance_unclamped, TAU) <= 1e-12
+
+
+def test_prts1_gpu_layout_sidecar_drives_the_transfer(lib, tmp_path, monkeypatch):
+    """A container's kfr frame layout saved as a sidecar (prts1.save_gpu_layout)
+    and loaded into a DeviceTransfer is used by the frame as is and gives the
+    bitwise v_k of a freshly built layout."""
+    from pathlib import Path
+
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200 import prts1
+    from paper_2203_12339_b200.basis import OpticalMaterial, build_basis
+    from paper_2203_12339_b200.geometry import make_geometry_image
+    from paper_2203_12339_b200.layout import kfr_layout
+    from paper_2203_12339_b200.runtime import Scene, SHLight
+
+    monkeypatch.setenv("SSS_TRANSFER", "kfr")
+    c = prts1.load_prts1(Path(__file__).resolve().parent / "golden" / "ref16.prts")
+    geom = make_geometry_image(16, 10.0, 0.05, 8, 11)
+    mat = OpticalMaterial(sigma_s_prime=[1.2, 1.5, 1.8], sigma_a=[0.01, 0.02, 0.04])
+    light = SHLight(LT.random_sh_light(3, 5))
+    dt_a = prts1.to_device(c, levels=2)
+    basis = build_basis(dt_a.K, (4, 4))
+    sc_a = Scene(geom, dt_a, basis, mat, light)
+    sc_a.relight()
+    side = tmp_path / "ref16.prts.kfr"
+    prts1.save_gpu_layout(side, dt_a.kfr, prts1.operators_digest(c.operators))
+    dt_b = prts1.to_device(c, levels=2)
+    dt_b.kfr = prts1.load_gpu_layout(side, prts1.operators_digest(c.operators))
+    sc_b = Scene(geom, dt_b, basis, mat, light)
+    sc_b.relight()
+    assert sc_b.transfer.kfr is dt_b.kfr
+    assert torch.equal(sc_a.vk, sc_b.vk)

@@ -105,3 +105,27 @@ def test_default_mesh_hash_is_the_reference_content_hash(tmp_path):
     mesh = TriangleMesh(vertices=gi.positions.astype(np.float64),
                         normals=gi.normals.astype(np.float64), triangles=grid_triangles(16))
     assert got == mesh.content_hash()
+
+
+def test_gpu_layout_sidecar_round_trip(tmp_path):
+    """The kfr frame layout of a reference container's operators, saved as a
+    sidecar tied to the operators' digest, loads back identical; a digest of
+    other operators is rejected (CPU: the layout build runs with torch)."""
+    import torch
+
+    from paper_2203_12339_b200.layout import kfr_layout, kfr_reference_apply
+
+    c = prts1.load_prts1(GOLD / "ref16.prts")
+    dt = prts1.to_device(c, levels=2, device="cpu")
+    lay = kfr_layout(dt, chunk=64)
+    dig = prts1.operators_digest(c.operators)
+    side = tmp_path / "ref16.prts.kfr"
+    prts1.save_gpu_layout(side, lay, dig)
+    back = prts1.load_gpu_layout(side, dig, device="cpu")
+    for k in ("items", "lane_len", "lane_dst", "batch_off", "stream", "partial_row", "multi_info"):
+        assert torch.equal(getattr(back, k), getattr(lay, k)), k
+    assert back.stats == lay.stats and back.n_items == lay.n_items
+    x = torch.as_tensor(np.random.default_rng(1).standard_normal((3, dt.n)))
+    assert torch.equal(kfr_reference_apply(back, x), kfr_reference_apply(lay, x))
+    with pytest.raises(prts1.PRTS1Error):
+        prts1.load_gpu_layout(side, "0" * 64, device="cpu")
