@@ -668,7 +668,7 @@ int sss_pair_rows_exact(int levels, int side, const float* pos, const float* are
   const char* x2e = getenv("SSS_C5_X2");
   const bool x2 = !x2e || atoi(x2e) != 0;
   dim3 grid(tiles, nrt);
-  const int rpp = 512 / T2 > 0 ? (512 / T2 < 8 ? 512 / T2 : 8) : 1;
+  const int rpp = 1024 / T2 > 0 ? (1024 / T2 < 16 ? 1024 / T2 : 16) : 1;
   const size_t smem = (size_t)KT * rpp * (T2 + 1) * sizeof(double);
 #define SSS_PR(LV, KK, M_)                                                                      \
   if (levels == LV && KT == KK && MM == M_) {                                                   \

@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(256) k_pair_rows_exact(const __grid_constant__
                                                          float r_max, int rt0, int nrt,
                                                          double* __restrict__ D) {
   constexpr int T = 1 << L, T2 = T * T, LD = T2 + 1;
-  constexpr int RPP = 512 / T2 > 0 ? (512 / T2 < 8 ? 512 / T2 : 8) : 1;  // receiver rows per pass
+  constexpr int RPP = 1024 / T2 > 0 ? (1024 / T2 < 16 ? 1024 / T2 : 16) : 1;  // receiver rows per pass
   extern __shared__ double smx[];
   double* hrow = smx;  // (KT * RPP) x LD
   const int N = S * S, tpr = S / T;
