@@ -285,7 +285,7 @@ int sss_pair_block(int levels, int exact, int side, const float* pos, const floa
  * pair's fp32 R_d at the n_mat training materials is evaluated once and
  * projected on all K terms, x area, w0 Haar along sources. Pkm (K, n_mat)
  * and mat (n_mat, 4) {sigma_tr, z_r, z_v, alpha'/(4 pi)} are HOST arrays
- * (copied into the kernel's parameter bank; n_mat <= 64, K <= 16). D (K,
+ * (copied into the kernel's parameter bank; n_mat <= 64, K <= 8). D (K,
  * nrt * 4^L, N) fp64 = the step-1 rows of the block for every term
  * (tile-major rows and columns). */
 int sss_pair_rows_exact(int levels, int side, const float* pos, const float* area, int K,

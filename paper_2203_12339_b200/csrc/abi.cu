@@ -19,45 +19,7 @@
 #include "raster.cu"
 #include "seam.cu"
 
-namespace {
-thread_local std::string g_err;
-
-int fail(int code, const char* msg) {
-  g_err = msg;
-  return code;
-}
-
-int check_launch(const char* what) {
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    g_err = std::string(what) + ": " + cudaGetErrorString(e);
-    return SSS_ECUDA;
-  }
-  return SSS_OK;
-}
-
-bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
-
-int set_smem(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) {
-      g_err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
-      return SSS_ECUDA;
-    }
-  }
-  return SSS_OK;
-}
-
-int check_geom(int side, int levels) {
-  if (!pow2(side) || side < 2) return fail(SSS_EINVAL, "side must be a power of two >= 2");
-  if (levels < 1 || (1 << levels) > side || levels > 6)
-    return fail(SSS_EINVAL, "levels must lie in [1, min(6, log2 side)]");
-  return SSS_OK;
-}
-
-inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-}  // namespace
+#include "abi_util.cuh"
 
 extern "C" {
 
@@ -626,67 +588,6 @@ int sss_pair_block(int levels, int exact, int side, const float* pos, const floa
   }
 #undef SSS_PAIR_CASE
   return check_launch("k_pair_block");
-}
-
-int sss_pair_rows_exact(int levels, int side, const float* pos, const float* area, int K,
-                        const float* Pkm, const float* mat, int n_mat, float r_max, int rt0,
-                        int nrt, double* D, void* stream) {
-  if (int r = check_geom(side, levels)) return r;
-  if (levels > 3) return fail(SSS_EINVAL, "pair pass supports levels <= 3");
-  if (!pos || !area || !Pkm || !mat || !D) return fail(SSS_EINVAL, "bad pair_rows pointers");
-  if (K < 1 || K > sss::kExactMaxK) return fail(SSS_EINVAL, "K must lie in [1, 16]");
-  if (n_mat < 1 || n_mat > sss::kExactMaxM) return fail(SSS_EINVAL, "n_mat must lie in [1, 64]");
-  const int MM = n_mat <= 16 ? 16 : (n_mat <= 32 ? 32 : 64);
-  const int T = 1 << levels, T2 = T * T, tiles = (side / T) * (side / T);
-  if (rt0 < 0 || nrt <= 0 || rt0 + nrt > tiles) return fail(SSS_EINVAL, "receiver tile block out of range");
-  const int KT = K <= 4 ? 4 : (K <= 8 ? 8 : (K <= 12 ? 12 : 16));
-  // host tables -> the kernel's parameter bank (Pkm / mat are host arrays:
-  // Pkm (K, n_mat) row-major, mat (n_mat, 4) {sigma_tr, z_r, z_v, c}); the
-  // padded materials and terms have zero weight
-  sss::ExactTables tb;
-  std::memset(&tb, 0, sizeof(tb));
-  for (int k = 0; k < K; ++k)
-    for (int m = 0; m < n_mat; ++m) tb.P[k * MM + m] = Pkm[k * n_mat + m];
-  for (int m = 0; m < MM; ++m) {
-    const bool real = m < n_mat;
-    const float s = real ? mat[m * 4] : 1.0f, zr = real ? mat[m * 4 + 1] : 1.0f,
-                zv = real ? mat[m * 4 + 2] : 1.0f, c = real ? mat[m * 4 + 3] : 0.0f;
-    tb.m0[m] = make_float4(zr * zr, zv * zv, -s * 1.4426950408889634f, s);
-    tb.m1[m] = make_float4(c * zr, c * zv, 0.0f, 0.0f);
-  }
-  for (int j = 0; j < MM / 2; ++j) {  // the packed material pairs
-    const float4 a = tb.m0[2 * j], b = tb.m0[2 * j + 1], c = tb.m1[2 * j], d = tb.m1[2 * j + 1];
-    tb.pA[j] = make_float2(a.x, b.x);
-    tb.pB[j] = make_float2(a.y, b.y);
-    tb.pS[j] = make_float2(a.z, b.z);
-    tb.ps[j] = make_float2(a.w, b.w);
-    tb.pCr[j] = make_float2(c.x, d.x);
-    tb.pCv[j] = make_float2(c.y, d.y);
-    for (int k = 0; k < sss::kExactMaxK; ++k)
-      tb.pP[k * (MM / 2) + j] = make_float2(tb.P[k * MM + 2 * j], tb.P[k * MM + 2 * j + 1]);
-  }
-  const char* x2e = getenv("SSS_C5_X2");
-  const bool x2 = !x2e || atoi(x2e) != 0;
-  dim3 grid(tiles, nrt);
-  const int rpp = 1024 / T2 > 0 ? (1024 / T2 < 16 ? 1024 / T2 : 16) : 1;
-  const size_t smem = (size_t)KT * rpp * (T2 + 1) * sizeof(double);
-#define SSS_PR(LV, KK, M_)                                                                      \
-  if (levels == LV && KT == KK && MM == M_) {                                                   \
-    if (x2) {                                                                                   \
-      if (int r = set_smem((const void*)sss::k_pair_rows_exact<LV, KK, M_, true>, smem)) return r; \
-      sss::k_pair_rows_exact<LV, KK, M_, true><<<grid, 256, smem, S_(stream)>>>(                \
-          tb, pos, area, side, r_max, rt0, nrt, D);                                             \
-    } else {                                                                                    \
-      if (int r = set_smem((const void*)sss::k_pair_rows_exact<LV, KK, M_>, smem)) return r;    \
-      sss::k_pair_rows_exact<LV, KK, M_><<<grid, 256, smem, S_(stream)>>>(tb, pos, area, side,  \
-                                                                         r_max, rt0, nrt, D);   \
-    }                                                                                           \
-    return check_launch("k_pair_rows_exact");                                                   \
-  }
-  SSS_PR(3, 8, 64) SSS_PR(3, 4, 16) SSS_PR(3, 8, 32) SSS_PR(3, 4, 64) SSS_PR(3, 12, 64)
-  SSS_PR(3, 16, 64) SSS_PR(2, 4, 16) SSS_PR(2, 8, 32) SSS_PR(2, 8, 64)
-#undef SSS_PR
-  return fail(SSS_EINVAL, "pair_rows: unsupported (levels, K, n_mat)");
 }
 
 int sss_step1_select(const double* D, int n_dom, int n_rows, int n_keep, const uint32_t* tm2flat,
