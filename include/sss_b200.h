@@ -49,6 +49,16 @@ int sss_haar2d(const double* in, double* out, int batch, int side, int levels,
 int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, const uint32_t* f2t,
                     double* x_out, uint32_t* mask, double* energy, void* stream);
 
+/* The frame's form of the same selection (runtime.py:112-118: the three RGB
+ * spectra of E): additionally writes what the transfer kernels read, the
+ * packed (n_dom, 4) fp64 records {x_r, x_g, x_b, 0} (xp; the fourth component
+ * is never written) and the kept-column bitmap (bits, n_dom/32 + 1 words, bit
+ * set iff any channel kept a nonzero coefficient of the column) - the outputs
+ * of sss_pack_x_bits, without a second launch. bits MUST be zero on entry. */
+int sss_select_topn_pack(const double* v, int n_dom, int n_keep, const uint32_t* f2t,
+                         double* x_out, uint32_t* mask, double* energy, double* xp,
+                         uint32_t* bits, void* stream);
+
 /* ---- (a) light projection. SH: E = T L (ambient_irradiance_dense analogue,
  *      lighting.py:332-336) fused with the w0 Haar (transfer.w0_forward,
  *      transfer.py:140-144). T_l: (nl, N) float32 l-major; Lsh (nl, 3).

@@ -22,6 +22,7 @@ _D = C.c_double
 _SIGS = {
     "sss_haar2d": [_P, _P, _I, _I, _I, _I, _P],
     "sss_select_topn": [_P, _I, _I, _I, _P, _P, _P, _P, _P],
+    "sss_select_topn_pack": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "sss_sh_irradiance": [_P, _P, _I, _I, _I, _P, _P, _P],
     "sss_env_project": [_P, _I, _I, _P, _P, _P, _P, _P, _P],
     "sss_env_irradiance": [_P, _I, _P, _P, _P, _I, _I, _I, _P, _P, _P],

@@ -40,31 +40,50 @@ int sss_haar2d(const double* in, double* out, int batch, int side, int levels, i
   return check_launch("k_haar2d_batch");
 }
 
-int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, const uint32_t* f2t,
-                    double* x_out, uint32_t* mask, double* energy, void* stream) {
+static int select_topn_impl(const double* v, int nvec, int n_dom, int n_keep, const uint32_t* f2t,
+                            double* x_out, uint32_t* mask, double* energy, double* xp,
+                            uint32_t* bits, void* stream) {
   if (nvec < 0 || nvec > 65535 || n_dom <= 0 || n_keep < 0 || !v || !x_out)
     return fail(SSS_EINVAL, "bad select arguments");
   if (nvec == 0) return SSS_OK;
-  if (mask) {
-    cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)nvec * ((n_dom + 31) / 32) * 4, S_(stream));
-    if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
-  }
   const int chunk = (((n_dom + sss::kSelCluster - 1) / sss::kSelCluster) + 31) / 32 * 32;
   if (chunk <= 16384 && n_dom >= 32 * sss::kSelCluster) {
-    // one 8-CTA cluster per vector, slices resident in shared memory
+    // one 16-CTA cluster per vector, slices resident in shared memory; the
+    // kernel writes every mask word of its slices itself
     const size_t smem = ((sizeof(sss::ClusterSelShared) + 15) & ~size_t(15)) + chunk * sizeof(double);
     if (int r = set_smem((const void*)sss::k_select_cluster, smem)) return r;
     if (sss::kSelCluster > 8)
       cudaFuncSetAttribute((const void*)sss::k_select_cluster,
                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    sss::k_select_cluster<<<nvec * sss::kSelCluster, 1024, smem, S_(stream)>>>(
-        v, n_dom, n_keep, chunk, f2t, x_out, mask, energy);
+    launch_chain(sss::k_select_cluster, dim3(nvec * sss::kSelCluster), dim3(1024), smem, S_(stream), v,
+                 n_dom, n_keep, chunk, f2t, x_out, mask, energy, xp, bits);
     return check_launch("k_select_cluster");
+  }
+  if (mask) {
+    cudaError_t e = cudaMemsetAsync(mask, 0, (size_t)nvec * ((n_dom + 31) / 32) * 4, S_(stream));
+    if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));
   }
   const size_t smem = sizeof(sss::SelShared);
   if (int r = set_smem((const void*)sss::k_select_topn, smem)) return r;
   sss::k_select_topn<<<nvec, 1024, smem, S_(stream)>>>(v, n_dom, n_keep, f2t, x_out, mask, energy);
-  return check_launch("k_select_topn");
+  if (int r = check_launch("k_select_topn")) return r;
+  if (xp) {  // small domains: the block kernel, then the packing pass
+    sss::k_pack_x_bits<<<(n_dom + 255) / 256, 256, 0, S_(stream)>>>(
+        x_out, n_dom, reinterpret_cast<double4*>(xp), bits);
+    return check_launch("k_pack_x_bits");
+  }
+  return SSS_OK;
+}
+
+int sss_select_topn(const double* v, int nvec, int n_dom, int n_keep, const uint32_t* f2t,
+                    double* x_out, uint32_t* mask, double* energy, void* stream) {
+  return select_topn_impl(v, nvec, n_dom, n_keep, f2t, x_out, mask, energy, nullptr, nullptr, stream);
+}
+
+int sss_select_topn_pack(const double* v, int n_dom, int n_keep, const uint32_t* f2t, double* x_out,
+                         uint32_t* mask, double* energy, double* xp, uint32_t* bits, void* stream) {
+  if (!xp || !bits) return fail(SSS_EINVAL, "bad select_pack arguments");
+  return select_topn_impl(v, 3, n_dom, n_keep, f2t, x_out, mask, energy, xp, bits, stream);
 }
 
 int sss_sh_irradiance(const float* T_l, const double* Lsh, int nl, int side, int levels,
@@ -88,7 +107,8 @@ int sss_env_project(const double* faces, int env_side, int n_keep, uint32_t* idx
   const int s2 = env_side * env_side;
   const size_t smem = (size_t)12 * s2 * sizeof(double) + sizeof(sss::SelShared);
   if (int r = set_smem((const void*)sss::k_env_project, smem)) return r;
-  sss::k_env_project<<<3, 1024, smem, S_(stream)>>>(faces, env_side, n_keep, idx, val, nullptr);
+  launch_chain(sss::k_env_project, dim3(3), dim3(1024), smem, S_(stream), faces, env_side, n_keep, idx,
+               val, (double*)nullptr);
   if (int r = check_launch("k_env_project")) return r;
   if (union_idx && union_lc && n_union) {
     sss::k_env_union<<<1, 1024, 0, S_(stream)>>>(idx, val, n_keep, 6 * s2, union_idx, union_lc,
@@ -132,13 +152,16 @@ int sss_env_irradiance_sel(const float* W2, int D, const uint32_t* sel_idx, cons
   int tpb = tpb_env ? atoi(tpb_env) : (T * 4 <= side ? 4 : 1);
   if (tpb < 1 || (side / T) % tpb) tpb = 1;
   const int tiles = (side / T) * (side / T);
-  const size_t nw = (size_t)(D + 31) / 32;
-  const size_t smem = 6 * (size_t)tpb * T2 * sizeof(double) + 12 * (size_t)n_keep * sizeof(double) +
-                      3 * (size_t)n_keep * sizeof(int) + 2 * nw * sizeof(uint32_t);
-  if (int r = set_smem((const void*)sss::k_env_irradiance_multi, smem)) return r;
-  sss::k_env_irradiance_multi<<<tiles / tpb, tpb * T2 < 32 ? 32 : tpb * T2, smem, S_(stream)>>>(
-      W2, nullptr, nullptr, nullptr, n_keep, side, levels, tpb, E_out, ehat, sel_idx, sel_val, D);
-  return check_launch("k_env_irradiance_multi");
+  while (tpb & (tpb - 1)) tpb &= tpb - 1;  // a power of two (the kernel's index math shifts)
+  const size_t nk8 = ((size_t)n_keep + 7) & ~size_t(7);
+  const size_t smem = 6 * (size_t)tpb * T2 * sizeof(double) + 3 * nk8 * (sizeof(double) + sizeof(uint32_t));
+  const int threads = 3 * tpb * T2 > 768 ? 768 : 3 * tpb * T2;  // the kernel strides over (point, channel)
+  if ((double)D * side * side >= 4294967296.0)
+    return fail(SSS_EINVAL, "env_irradiance_sel: W^{w2} larger than 2^32 elements");
+  if (int r = set_smem((const void*)sss::k_env_irradiance_chan, smem)) return r;
+  launch_chain(sss::k_env_irradiance_chan, dim3(tiles / tpb), dim3(threads < 32 ? 32 : threads), smem,
+               S_(stream), W2, sel_idx, sel_val, n_keep, D, side, levels, tpb, E_out, ehat);
+  return check_launch("k_env_irradiance_chan");
 }
 
 int sss_env_transfer(const float* normals, int n_points, const double* dirs, const double* dom,
@@ -422,11 +445,11 @@ int sss_transfer_kfr(int K, int n_rows, unsigned n_items, unsigned n_partials, c
     if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
                              (int)smem) != cudaSuccess)                                          \
       return fail(SSS_ECUDA, "transfer_kfr: shared memory attribute");                          \
-    fn<<<grid, sss::kKfrWarps * 32, smem, S_(stream)>>>(                                         \
-        n_rows, K, n_items, n_partials, reinterpret_cast<const uint2*>(items), lane_len,         \
-        lane_dst, batch_off, reinterpret_cast<const unsigned char*>(stream_bytes),               \
-        reinterpret_cast<const double4*>(xp), bits, vk, partials, partial_row,                   \
-        reinterpret_cast<const uint4*>(multi_info), multi_count, work);                          \
+    launch_chain(fn, dim3(grid), dim3(sss::kKfrWarps * 32), smem, S_(stream), n_rows, K, n_items,   \
+                 n_partials, reinterpret_cast<const uint2*>(items), lane_len, lane_dst, batch_off, \
+                 reinterpret_cast<const unsigned char*>(stream_bytes),                           \
+                 reinterpret_cast<const double4*>(xp), bits, vk, partials, partial_row,          \
+                 reinterpret_cast<const uint4*>(multi_info), multi_count, work);                 \
     return check_launch("k_transfer_kfr");                                                       \
   }
   SSS_KFR(4, 2, 3) SSS_KFR(8, 2, 2)
@@ -539,9 +562,9 @@ int sss_edit_finish(int K, int side, int levels, const double* vk, const double*
   if (T2 <= 256) {
     const size_t smem = 6 * (size_t)G * T2 * sizeof(double);
     if (int r = set_smem((const void*)sss::k_edit_finish_multi, smem)) return r;
-    sss::k_edit_finish_multi<<<tiles / G, G * T2 < 64 ? 64 : G * T2, smem, S_(stream)>>>(
-        K, side, levels, G, vk, g, positions, normals, cam, material, scatter, radiance,
-        radiance_unclamped);
+    launch_chain(sss::k_edit_finish_multi, dim3(tiles / G), dim3(G * T2 < 64 ? 64 : G * T2), smem,
+                 S_(stream), K, side, levels, G, vk, g, positions, normals, cam, material, scatter,
+                 radiance, radiance_unclamped);
     return check_launch("k_edit_finish_multi");
   }
   const size_t smem = 4 * (size_t)T * T * sizeof(double);

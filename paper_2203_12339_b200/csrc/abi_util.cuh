@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "../../include/sss_b200.h"
@@ -50,5 +51,35 @@ inline int check_geom(int side, int levels) {
 }
 
 inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Launch of a kernel of the frame's chain with programmatic stream
+// serialization (see sss_common.cuh pdl_*): the kernel may start while its
+// predecessor in the stream is still running and orders its own memory
+// accesses with griddepcontrol.wait. SSS_PDL=0 turns the attribute off
+// (plain stream order). Works eagerly and under stream capture (the edge
+// becomes a programmatic dependency of the graph).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SSS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 }  // namespace sss_abi
 using namespace sss_abi;

@@ -230,6 +230,8 @@ __global__ void k_env_project(const double* __restrict__ faces, int s, int n_kee
   double* a = sm;             // D
   double* tmp = sm + D;       // D (the 6 faces transform as one batch)
   SelShared& sh = *reinterpret_cast<SelShared*>(tmp + D);
+  pdl_launch_dependents();
+  pdl_wait();
   ENV_TRACE(0);
   for (int e = threadIdx.x; e < D; e += blockDim.x) a[e] = faces[(size_t)e * 3 + c];
   __syncthreads();
@@ -527,6 +529,75 @@ __global__ void k_env_irradiance_multi(const float* __restrict__ W2,
   scatter_ehat(a, T, TPB, tile0, L, S, ehat);
 }
 
+// The frame's environment irradiance, one thread per (point, channel): channel
+// c sums W^{w2}[l, i] * L_c[l] over ITS OWN kept w2 ids in ascending order - the
+// reference's per-channel sum (lighting.py:318-336 on the compress_top_n
+// spectrum), and value-equal to the union form above, whose extra terms are
+// exact zeros. Three times the threads of the per-point form (the sums are
+// sequential, so threads are the only parallelism) for 128 instead of ~300
+// terms each, and no union to build. The kept lists are staged as 32-bit row
+// offsets (id * N < 2^32) and padded to a multiple of 8 with (row 0, L = 0),
+// whose products add exact zeros after the last real term: the loop is
+// branch-free, 8 loads in flight per thread. blockDim = 3 * TPB * 4^L.
+__global__ void __launch_bounds__(768, 2) k_env_irradiance_chan(
+    const float* __restrict__ W2, const uint32_t* __restrict__ sel_idx,
+    const double* __restrict__ sel_val, int n_keep, int D, int S, int L, int TPB,
+    double* __restrict__ E_out, double* __restrict__ ehat) {
+  extern __shared__ __align__(16) double sm[];
+  pdl_launch_dependents();
+  const int T = 1 << L, T2 = T * T, N = S * S, tpr = S / T, P = TPB * T2;
+  const int nk8 = (n_keep + 7) & ~7;
+  double* a = sm;                   // TPB * 3 * T2
+  double* tmp = a + 3 * P;          // TPB * 3 * T2
+  double* lv = tmp + 3 * P;         // 3 nk8 kept values
+  uint32_t* roff = reinterpret_cast<uint32_t*>(lv + 3 * nk8);  // 3 nk8 row offsets id * N
+  pdl_wait();
+  for (int e = threadIdx.x; e < 3 * nk8; e += blockDim.x) {
+    const int c = e / nk8, q = e % nk8;
+    const uint32_t id = q < n_keep ? sel_idx[c * n_keep + q] : 0xffffffffu;
+    const bool ok = id < (uint32_t)D;
+    roff[e] = ok ? id * (uint32_t)N : 0u;
+    lv[e] = ok ? sel_val[c * n_keep + q] : 0.0;
+  }
+  __syncthreads();
+  const int tile0 = blockIdx.x * TPB;
+  const int lB = 31 - __clz(TPB), lP = lB + 2 * L, ltpr = 31 - __clz(tpr);
+  for (int t = threadIdx.x; t < 3 * P; t += blockDim.x) {
+    // the CTA's TPB tiles are horizontally adjacent: consecutive threads walk
+    // one image row across them, so a warp's W^{w2} loads are whole lines
+    // TPB, T, S are powers of two (the launcher enforces it): shifts, not divisions
+    const int c = t >> lP, q = t & (P - 1);
+    const int rr = q >> (lB + L), cc = q & ((TPB << L) - 1);
+    const int j = cc >> L, e = (rr << L) + (cc & (T - 1));
+    const int tile = tile0 + j, tr = tile >> ltpr, tc = tile & (tpr - 1);
+    const uint32_t i = (uint32_t)((tr * T + rr) * S + tc * T + (cc & (T - 1)));
+    const uint32_t* ro = roff + c * nk8;
+    const double* lc = lv + c * nk8;
+    double acc = 0.0;
+#pragma unroll 2
+    for (int q0 = 0; q0 < nk8; q0 += 8) {
+      const uint4 r0 = *reinterpret_cast<const uint4*>(ro + q0);
+      const uint4 r1 = *reinterpret_cast<const uint4*>(ro + q0 + 4);
+      float w[8];
+      w[0] = __ldg(W2 + (r0.x + i)); w[1] = __ldg(W2 + (r0.y + i));
+      w[2] = __ldg(W2 + (r0.z + i)); w[3] = __ldg(W2 + (r0.w + i));
+      w[4] = __ldg(W2 + (r1.x + i)); w[5] = __ldg(W2 + (r1.y + i));
+      w[6] = __ldg(W2 + (r1.z + i)); w[7] = __ldg(W2 + (r1.w + i));
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        const double2 l = *reinterpret_cast<const double2*>(lc + q0 + u);
+        acc = dadd(acc, dmul((double)w[u], l.x));
+        acc = dadd(acc, dmul((double)w[u + 1], l.y));
+      }
+    }
+    a[(j * 3 + c) * T2 + e] = acc;
+    if (E_out) E_out[i * 3 + c] = acc;
+  }
+  __syncthreads();
+  batch_tile_haar_fwd(a, tmp, T, 3 * TPB);
+  scatter_ehat(a, T, TPB, tile0, L, S, ehat);
+}
+
 __global__ void k_sh_irradiance_multi(const float* __restrict__ T_l, const double* __restrict__ Lsh,
                                       int nl, int S, int L, int TPB, double* __restrict__ E_out,
                                       double* __restrict__ ehat) {
@@ -747,14 +818,29 @@ __global__ void __launch_bounds__(256) k_edit_finish_multi(
   double* summed = sm;                        // G x 3 x T2
   double* tmp = sm + (size_t)G * 3 * T2;      // same
   const int tile0 = blockIdx.x * G;
+  pdl_launch_dependents();
+  pdl_wait();
   for (int q = threadIdx.x; q < G * T2; q += blockDim.x) {
     const int row = tile0 * T2 + q;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int k = 0; k < K; ++k) {
-      const double* vo = vk + (size_t)k * 3 * N;
-      s0 += g[k] * vo[row];
-      s1 += g[K + k] * vo[N + row];
-      s2 += g[2 * K + k] * vo[2 * N + row];
+    // eight terms' v_k loads in flight at once; the sums keep their k order
+    for (int k0 = 0; k0 < K; k0 += 8) {
+      double v[8][3];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double* vo = vk + (size_t)(k0 + u) * 3 * N;
+        const bool in = k0 + u < K;
+        v[u][0] = in ? __ldcs(&vo[row]) : 0.0;
+        v[u][1] = in ? __ldcs(&vo[N + row]) : 0.0;
+        v[u][2] = in ? __ldcs(&vo[2 * N + row]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (k0 + u >= K) break;
+        s0 += g[k0 + u] * v[u][0];
+        s1 += g[K + k0 + u] * v[u][1];
+        s2 += g[2 * K + k0 + u] * v[u][2];
+      }
     }
     const int j = q / T2, e = q % T2;
     summed[(j * 3 + 0) * T2 + e] = s0;

@@ -15,6 +15,18 @@
 
 namespace sss {
 
+// Programmatic dependent launch (the frame's kernel chain, abi_util.cuh
+// launch_chain): a kernel lets its successor's CTAs be scheduled as soon as
+// all of its own have started (pdl_launch_dependents, first statement), and
+// touches global memory only after its predecessor has completed and flushed
+// (pdl_wait). Launch latency, CTA scheduling and shared-memory set-up of
+// kernel n + 1 overlap the tail of kernel n; without the launch attribute
+// both are no-ops.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // exact-order double arithmetic (no FMA contraction) so results are bitwise
 // equal to the numpy reference (_kernels_np.py, no fused multiply-add)
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }

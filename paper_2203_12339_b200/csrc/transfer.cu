@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
   constexpr int G = kKfrG;
   extern __shared__ __align__(128) unsigned char kfr_smem[];
   __shared__ uint32_t sbits[kKfrBitWords];
+  pdl_launch_dependents();
   const int nbw = (N >> 5) + 1;
-  for (int t = threadIdx.x; t < nbw; t += blockDim.x) sbits[t] = bits[t];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wb = kfr_smem + wid * SM::WARP;
   uint64_t* bar = reinterpret_cast<uint64_t*>(wb + NS * SM::SLOT);
@@ -118,6 +118,8 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
     for (int j = 0; j < NS; ++j) mbar_init(&bar[j], 1);
     fence_mbar_init();
   }
+  pdl_wait();  // x, the bitmap and the claim counters are the predecessor's
+  for (int t = threadIdx.x; t < nbw; t += blockDim.x) sbits[t] = bits[t];
   __syncthreads();
   // batches consumed by this warp: slot seq % NS, parity (seq / NS) & 1; the
   // ring runs NS - 1 batches ahead of the consumer

@@ -335,7 +335,7 @@ class Scene:
     # kernel sequences (stream-ordered, capturable)
     # ------------------------------------------------------------------
 
-    def _launch_stage1(self, stream=None, want_E=False):
+    def _launch_stage1(self, stream=None, want_E=False, before_select=None):
         sp = _lib.stream_ptr(stream)
         if want_E and self.E is None:
             self.E = torch.empty((self.n, 3), dtype=torch.float64, device="cuda")
@@ -375,8 +375,18 @@ class Scene:
                           _lib.ptr(self.env_idx), _lib.ptr(self.env_val), kk, self.side,
                           self.levels, _lib.ptr(E), _lib.ptr(self.ehat), sp)
         keep = max(1, int(round(self.e_keep * self.n)))  # runtime.py:112
-        _lib.call("sss_select_topn", _lib.ptr(self.ehat), 3, self.n, keep, _lib.ptr(self.f2t),
-                  _lib.ptr(self.x), _lib.ptr(self.mask), _lib.ptr(self.energy), sp)
+        # the selection also writes the transfer's inputs (packed x records and
+        # the kept-column bitmap): no packing launch. The bitmap is cleared
+        # first - on the forked stream when the caller gives the hook
+        self._alloc_xp()
+        if before_select is not None:
+            before_select()
+        else:
+            _lib.call("sss_zero", _lib.ptr(self.xbits), self.xbits.numel() * 4, sp)
+        _lib.call("sss_select_topn_pack", _lib.ptr(self.ehat), self.n, keep, _lib.ptr(self.f2t),
+                  _lib.ptr(self.x), _lib.ptr(self.mask), _lib.ptr(self.energy), _lib.ptr(self.xp),
+                  _lib.ptr(self.xbits), sp)
+        self._x_packed = True
 
     def _launch_weights(self, stream=None):
         dev = self.basis.device()
@@ -401,11 +411,16 @@ class Scene:
             t.flat16 = flat16_layout(t)
         return t.flat16
 
-    def _pack_x(self, sp):
-        """xp (N, 4) f64 + the kept-column bitmap (one clear word past N)."""
+    def _alloc_xp(self):
         if getattr(self, "xp", None) is None:
-            self.xp = torch.empty((self.n, 4), dtype=torch.float64, device="cuda")
+            self.xp = torch.zeros((self.n, 4), dtype=torch.float64, device="cuda")
             self.xbits = torch.zeros((self.n >> 5) + 1, dtype=torch.int32, device="cuda")
+
+    def _pack_x(self, sp):
+        """xp (N, 4) f64 + the kept-column bitmap (one clear word past N) from
+        self.x - only when x was set some other way than by the frame's
+        selection, which writes both itself (sss_select_topn_pack)."""
+        self._alloc_xp()
         _lib.call("sss_pack_x_bits", _lib.ptr(self.x), self.n, _lib.ptr(self.xp),
                   _lib.ptr(self.xbits), sp)
 
@@ -460,7 +475,9 @@ class Scene:
         """Stage 2 (+ stages 3-5 when `epilogue`): v_k = T_k x for every term
         and channel. Returns False: the transfer never fuses the epilogue."""
         sp = _lib.stream_ptr(stream)
-        self._pack_x(sp)
+        if not getattr(self, "_x_packed", False):
+            self._pack_x(sp)
+        self._x_packed = False
         if self._autotune and not torch.cuda.is_current_stream_capturing():
             self._autotune_transfer(stream)
         # flat16 accumulates with atomics into a zeroed v_k (zeroed on the side
@@ -500,6 +517,13 @@ class Scene:
         fork, join = torch.cuda.Event(), torch.cuda.Event()
         fork.record(cur)
         self._side.wait_event(fork)
+        # the kept-column bitmap is cleared on the forked stream too (the
+        # selection ORs into it), joined just before the selection
+        self._alloc_xp()
+        bits_clear = torch.cuda.Event()
+        _lib.call("sss_zero", _lib.ptr(self.xbits), self.xbits.numel() * 4,
+                  _lib.stream_ptr(self._side))
+        bits_clear.record(self._side)
         self._launch_weights(self._side)
         # the default transfer accumulates into a zeroed v_k: zero it here,
         # overlapping stage 1, instead of on the critical path
@@ -510,7 +534,7 @@ class Scene:
             _lib.call("sss_zero", _lib.ptr(self.vk), self.vk.numel() * 8, _lib.stream_ptr(self._side))
             _lib.call("sss_zero", _lib.ptr(self._wctr), 4, _lib.stream_ptr(self._side))
         join.record(self._side)
-        self._launch_stage1(cur)
+        self._launch_stage1(cur, before_select=lambda: cur.wait_event(bits_clear))
         cur.wait_event(join)
         if self._ambient_active():
             # v_k = T_k x + F_k L^{w2} (runtime.py:138-150), then stages 3-5

@@ -13,7 +13,7 @@ extern "C" int select_trace(const double* v, int nvec, int n_dom, int n_keep, co
   unsigned long long zero[32] = {0};
   cudaMemcpyToSymbol(sss::g_sel_trace, zero, sizeof(zero));
   sss::k_select_cluster<<<nvec * sss::kSelCluster, 1024, smem>>>(v, n_dom, n_keep, chunk, f2t, x,
-                                                                  mask, energy);
+                                                                  mask, energy, nullptr, nullptr);
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, sss::g_sel_trace, sizeof(zero));
   return (int)cudaGetLastError();
