@@ -335,7 +335,7 @@ class Scene:
     # kernel sequences (stream-ordered, capturable)
     # ------------------------------------------------------------------
 
-    def _launch_stage1(self, stream=None, want_E=False, before_select=None):
+    def _launch_stage1(self, stream=None, want_E=False, before_select=None, after_project=None):
         sp = _lib.stream_ptr(stream)
         if want_E and self.E is None:
             self.E = torch.empty((self.n, 3), dtype=torch.float64, device="cuda")
@@ -371,6 +371,9 @@ class Scene:
             else:  # the union is rebuilt inside every irradiance CTA: one launch less
                 _lib.call("sss_env_project", _lib.ptr(self.light_buf), s, kk,
                           _lib.ptr(self.env_idx), _lib.ptr(self.env_val), None, None, None, sp)
+                if after_project is not None:
+                    after_project()  # forked-stream work joins here, under the projection
+                    before_select = lambda: None  # noqa: E731
                 _lib.call("sss_env_irradiance_sel", _lib.ptr(self.W2), 6 * s * s,
                           _lib.ptr(self.env_idx), _lib.ptr(self.env_val), kk, self.side,
                           self.levels, _lib.ptr(E), _lib.ptr(self.ehat), sp)
@@ -534,8 +537,21 @@ class Scene:
             _lib.call("sss_zero", _lib.ptr(self.vk), self.vk.numel() * 8, _lib.stream_ptr(self._side))
             _lib.call("sss_zero", _lib.ptr(self._wctr), 4, _lib.stream_ptr(self._side))
         join.record(self._side)
-        self._launch_stage1(cur, before_select=lambda: cur.wait_event(bits_clear))
-        cur.wait_event(join)
+        # environment light + kfr: the forked work (~7 us) ends under the
+        # environment projection (~16 us), so it is joined right after that
+        # launch and irradiance -> selection -> transfer -> epilogue stay one
+        # chain of programmatic dependent launches; otherwise the bitmap clear
+        # is joined before the selection and the rest before the transfer
+        joined = []
+
+        def join_all():
+            cur.wait_event(join)
+            joined.append(True)
+
+        self._launch_stage1(cur, before_select=lambda: cur.wait_event(bits_clear),
+                            after_project=None if self._vk_zeroed else join_all)
+        if not joined:
+            cur.wait_event(join)
         if self._ambient_active():
             # v_k = T_k x + F_k L^{w2} (runtime.py:138-150), then stages 3-5
             self._launch_transfer(cur, epilogue=False)
