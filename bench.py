@@ -395,9 +395,10 @@ def run_ours(a, cfg):
                          "touched_nnz": touched, "kernel_ms": k_ms,
                          "kernel_choice_us": kchoice},
             "e2e": e2e,
-            # per relight: env_project, env_union, env_irradiance, select, weights,
-            # pack_x_bits, transfer, edit_finish; per edit: weights, edit_finish
-            "gpu_launches": 7 * a.steps + 2 * n_edit,
+            # per relight: env_project, env_irradiance, select (writes the packed x
+            # and the kept bitmap), weights, transfer, edit_finish; per edit:
+            # weights, edit_finish
+            "gpu_launches": 6 * a.steps + 2 * n_edit,
             "clocks": clk,
             "relight_ms": relight_ms, "edit_ms": edit_ms,
             "cpu_baseline": cpu,

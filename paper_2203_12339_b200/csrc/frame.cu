@@ -222,14 +222,31 @@ __device__ inline void env_faces_haar_fwd(double* a, double* tmp, int T, int B) 
   __syncthreads();
 }
 
-__global__ void k_env_project(const double* __restrict__ faces, int s, int n_keep,
-                              uint32_t* __restrict__ idx_out, double* __restrict__ val_out,
-                              double* __restrict__ energy) {
+// Selection state of k_env_project (one CTA, keys in registers).
+struct EnvSelShared {
+  unsigned hist[256];
+  int scal_b, ncand, wsum[32];
+  long long scal_need, scal_cnt, take, ties;
+  uint64_t ckey[64], thr;
+  double red[32], red2[32];
+};
+
+// grid: one CTA of 1024 threads per channel. Per-face full-pyramid Haar of the
+// 6 x s x s cubemap (lighting.py:293-305), then the exact top-n_keep by
+// magnitude (ties -> lower id) with a most-significant-digit radix descent on
+// keys held in registers (each thread owns kEnvPer consecutive ids, so the
+// ordered compaction is one block scan): three 8-bit passes, then the <= 64
+// keys left in the threshold bucket are ranked directly.
+constexpr int kEnvPer = 6;  // ids per thread: 1024 x 6 = the 6 x 32 x 32 cubemap
+__global__ void __launch_bounds__(1024) k_env_project(const double* __restrict__ faces, int s,
+                                                      int n_keep, uint32_t* __restrict__ idx_out,
+                                                      double* __restrict__ val_out,
+                                                      double* __restrict__ energy) {
   extern __shared__ __align__(16) double sm[];
   const int c = blockIdx.x, s2 = s * s, D = 6 * s2;
   double* a = sm;             // D
   double* tmp = sm + D;       // D (the 6 faces transform as one batch)
-  SelShared& sh = *reinterpret_cast<SelShared*>(tmp + D);
+  EnvSelShared& sh = *reinterpret_cast<EnvSelShared*>(tmp + D);
   pdl_launch_dependents();
   pdl_wait();
   ENV_TRACE(0);
@@ -238,51 +255,168 @@ __global__ void k_env_project(const double* __restrict__ faces, int s, int n_kee
   ENV_TRACE(1);
   env_faces_haar_fwd(a, tmp, s, 6);
   ENV_TRACE(2);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int n = min(n_keep, D);
-  SelectResult sel;
-  {
-    uint64_t t;
-    long long take, tiecnt;
-    radix_cut<false>(a, D, n, 0.0, sh, &t, &take, &tiecnt);
-    sel.key = t;
-    sel.take_eq = (int)take;
+  const int lo = min(tid * kEnvPer, D), cnt_own = min(kEnvPer, D - lo);
+  double v[kEnvPer];
+  uint64_t key[kEnvPer];
+#pragma unroll
+  for (int j = 0; j < kEnvPer; ++j) {
+    v[j] = j < cnt_own ? a[lo + j] : 0.0;
+    key[j] = mkey(v[j]);
+  }
+  uint64_t prefix = 0, pmask = 0;
+  long long need = n, ties = 0;
+  for (int p = 0; p < 8 && n > 0; ++p) {
+    const int shf = 56 - 8 * p;
+    if (tid < 256) sh.hist[tid] = 0u;
+    if (tid == 0) { sh.scal_b = 0; sh.scal_need = need; sh.scal_cnt = 0; sh.ncand = 0; }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kEnvPer; ++j) {
+      unsigned bin = 0xffffffffu;
+      if (j < cnt_own && (key[j] & pmask) == prefix) bin = (unsigned)(key[j] >> shf) & 255u;
+      if (p == 0) {  // the top digit takes a handful of values: aggregate per warp
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (bin != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(&sh.hist[bin], __popc(peers));
+      } else if (bin != 0xffffffffu) {
+        atomicAdd(&sh.hist[bin], 1u);
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {  // lane l: bins 255 - 8l .. 248 - 8l, scanned from the top
+      unsigned h[8], ssum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { h[q] = sh.hist[255 - 8 * lane - q]; ssum += h[q]; }
+      unsigned incl = ssum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      long long before = (long long)(incl - ssum);
+      if (before < need && need <= before + (long long)ssum) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (before + (long long)h[q] >= need) {
+            sh.scal_b = 255 - 8 * lane - q;
+            sh.scal_need = need - before;
+            sh.scal_cnt = h[q];
+            break;
+          }
+          before += h[q];
+        }
+      }
+    }
+    __syncthreads();
+    const int bsel = sh.scal_b;
+    need = sh.scal_need;
+    ties = sh.scal_cnt;
+    prefix |= (uint64_t)bsel << shf;
+    pmask |= (uint64_t)255u << shf;
+    if (p < 7 && ties <= 64) {
+#pragma unroll
+      for (int j = 0; j < kEnvPer; ++j)
+        if (j < cnt_own && (key[j] & pmask) == prefix) sh.ckey[atomicAdd(&sh.ncand, 1)] = key[j];
+      __syncthreads();
+      const int total = sh.ncand;
+      if (tid < total) {
+        const uint64_t kj = sh.ckey[tid];
+        long long g = 0, e = 0;
+        for (int q = 0; q < total; ++q) {
+          g += sh.ckey[q] > kj;
+          e += sh.ckey[q] == kj;
+        }
+        if (g < need && need <= g + e) {  // equal keys write equal values
+          sh.thr = kj;
+          sh.take = need - g;
+          sh.ties = e;
+        }
+      }
+      __syncthreads();
+      prefix = sh.thr;
+      need = sh.take;
+      ties = sh.ties;
+      break;
+    }
   }
   ENV_TRACE(3);
-  // compaction in index order: rank via a second scan
-  int* wsum = reinterpret_cast<int*>(sh.wsum);
-  // mark kept into tmp-as-flags then compact with a block scan
-  unsigned char* keep = (unsigned char*)tmp;  // reuse (s2 doubles >= D bytes)
-  block_apply_selection(a, D, sel, wsum, [&](int i, bool k) { keep[i] = k; });
-  ENV_TRACE(4);
-  // ordered compaction (chunked, like block_apply_selection)
-  const int nt = blockDim.x, tid = threadIdx.x;
-  const int chunk = (D + nt - 1) / nt;
-  const int lo = min(tid * chunk, D), hi = min(lo + chunk, D);
+  const uint64_t t = n > 0 ? prefix : ~0ULL;
+  const long long take = n > 0 ? need : 0;
+  const bool all_ties = take == ties;  // every key equal to the threshold is kept
+  int tie_rank = 0;
+  if (!all_ties) {  // some ties kept: the lowest ids first (block scan of the tie counts)
+    int my = 0;
+#pragma unroll
+    for (int j = 0; j < kEnvPer; ++j) my += (j < cnt_own && key[j] == t);
+    int incl = my;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane == 31) sh.wsum[wid] = incl;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < wid; ++w) base += sh.wsum[w];
+    tie_rank = base + incl - my;
+    __syncthreads();
+  }
+  unsigned kb = 0;
   int cnt = 0;
-  for (int i = lo; i < hi; ++i) cnt += keep[i];
-  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+#pragma unroll
+  for (int j = 0; j < kEnvPer; ++j) {
+    if (j >= cnt_own) break;
+    bool keep = all_ties ? key[j] >= t : key[j] > t;
+    if (!all_ties && key[j] == t) { keep = tie_rank < take; ++tie_rank; }
+    kb |= (keep ? 1u : 0u) << j;
+    cnt += keep;
+  }
+  ENV_TRACE(4);
+  // ordered compaction: exclusive block scan of the kept counts
   int incl = cnt;
+#pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  if (lane == 31) wsum[wid] = incl;
+  if (lane == 31) sh.wsum[wid] = incl;
   __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int w = 0; w < nw; ++w) { const int t = wsum[w]; wsum[w] = acc; acc += t; }
+  int pos = incl - cnt;
+  for (int w = 0; w < wid; ++w) pos += sh.wsum[w];
+#pragma unroll
+  for (int j = 0; j < kEnvPer; ++j)
+    if ((kb >> j) & 1u) {
+      idx_out[c * n_keep + pos] = (uint32_t)(lo + j);
+      val_out[c * n_keep + pos] = v[j];
+      ++pos;
+    }
+  for (int q = n + tid; q < n_keep; q += blockDim.x) {
+    idx_out[c * n_keep + q] = 0xffffffffu;
+    val_out[c * n_keep + q] = 0.0;
   }
-  __syncthreads();
-  int pos = wsum[wid] + incl - cnt;
-  for (int i = lo; i < hi; ++i)
-    if (keep[i]) { idx_out[c * n_keep + pos] = i; val_out[c * n_keep + pos] = a[i]; ++pos; }
-  for (int q = n + tid; q < n_keep; q += nt) { idx_out[c * n_keep + q] = 0xffffffffu; val_out[c * n_keep + q] = 0.0; }
   ENV_TRACE(5);
-  if (energy && tid == 0) {
+  if (energy) {
     double tot = 0.0, kept = 0.0;
-    for (int i = 0; i < D; ++i) { tot += a[i] * a[i]; if (keep[i]) kept += a[i] * a[i]; }
-    energy[c * 2 + 0] = tot;
-    energy[c * 2 + 1] = fmin(kept, tot);
+#pragma unroll
+    for (int j = 0; j < kEnvPer; ++j) {
+      tot += v[j] * v[j];
+      if ((kb >> j) & 1u) kept += v[j] * v[j];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      kept += __shfl_xor_sync(0xffffffffu, kept, o);
+    }
+    __syncthreads();
+    if (lane == 0) { sh.red[wid] = tot; sh.red2[wid] = kept; }
+    __syncthreads();
+    if (tid == 0) {
+      double T = 0.0, Kp = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { T += sh.red[w]; Kp += sh.red2[w]; }
+      energy[c * 2 + 0] = T;
+      energy[c * 2 + 1] = fmin(Kp, T);
+    }
   }
 }
 
