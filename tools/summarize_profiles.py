@@ -16,7 +16,7 @@ from collections import OrderedDict, defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-FRAME = ("k_transfer_kfr", "k_transfer_flat16", "k_transfer_flat8s", "k_env_irradiance_multi", "k_select_cluster", "k_env_project",
+FRAME = ("k_transfer_kfr", "k_transfer_flat16", "k_transfer_flat8s", "k_env_irradiance_multi", "k_env_irradiance_chan", "k_select_cluster", "k_env_project",
          "k_edit_finish_multi", "k_material_weights", "k_env_union", "k_pack_x_bits",
          "k_sh_irradiance_multi", "k_direct_single", "k_fold_apply_rows")
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
