@@ -88,6 +88,76 @@ def test_select_topn_vs_oracle(lib, n_dom, n):
         assert e[1] == pytest.approx(s.kept_energy, rel=1e-12)
 
 
+@pytest.mark.parametrize("n_dom,n_keep,extra", [(65536, 16384, 9), (65536, 16384, 40), (8192, 100, 5)])
+def test_select_partial_ties_across_cluster_ranks(lib, n_dom, n_keep, extra):
+    """A small tie group at the threshold, spread over the cluster's slices,
+    of which only some are kept: the lowest flat indices win (the gathered-
+    candidate finish of k_select_cluster with take < ties)."""
+    from paper_2203_12339_b200 import wavelets as W
+
+    rng = np.random.default_rng(n_dom + extra)
+    v = rng.permutation(np.arange(1, n_dom + 1)).astype(np.float64)
+    v *= rng.choice([-1.0, 1.0], n_dom)
+    t = float(n_dom - n_keep + 3)  # with the copies below: n_keep - 3 above, 1 + extra ties, 3 taken
+    small = np.flatnonzero(np.abs(v) < n_dom // 4)
+    pos = rng.choice(small, extra, replace=False)
+    v[pos] = t * rng.choice([-1.0, 1.0], extra)
+    vv = np.stack([v, -v, v[::-1].copy()])
+    x, mask, energy = W.select_top_n_device(torch.as_tensor(vv, device="cuda"), n_keep)
+    for c in range(3):
+        s = O.compress_top_n(vv[c], n_keep)
+        got = W.mask_to_indices(mask[c].cpu().numpy(), n_dom)
+        assert np.array_equal(got, s.indices), c
+        dense = np.zeros(n_dom)
+        dense[s.indices] = vv[c, s.indices]
+        assert np.array_equal(x[c].cpu().numpy(), dense)
+
+
+def test_select_pack_writes_the_transfer_inputs(lib):
+    """sss_select_topn_pack = sss_select_topn + sss_pack_x_bits (the packed
+    (N, 4) x records and the kept-column bitmap), bit for bit."""
+    from paper_2203_12339_b200 import _lib
+
+    n, keep = 65536, 16384
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal((3, n))
+    v[1, ::3] = 0.0  # kept zeros do not set bits
+    f2t = torch.as_tensor(rng.permutation(n).astype(np.int32), device="cuda")
+    vd = torch.as_tensor(v, device="cuda")
+    x = torch.empty((3, n), dtype=torch.float64, device="cuda")
+    mask = torch.empty((3, n // 32), dtype=torch.int32, device="cuda")
+    energy = torch.empty((3, 2), dtype=torch.float64, device="cuda")
+    xp_ref = torch.empty((n, 4), dtype=torch.float64, device="cuda")
+    bits_ref = torch.zeros(n // 32 + 1, dtype=torch.int32, device="cuda")
+    sp = _lib.stream_ptr()
+    _lib.call("sss_select_topn", _lib.ptr(vd), 3, n, keep, _lib.ptr(f2t), _lib.ptr(x), _lib.ptr(mask),
+              _lib.ptr(energy), sp)
+    _lib.call("sss_pack_x_bits", _lib.ptr(x), n, _lib.ptr(xp_ref), _lib.ptr(bits_ref), sp)
+    x2 = torch.empty_like(x)
+    mask2 = torch.empty_like(mask)
+    energy2 = torch.empty_like(energy)
+    xp = torch.zeros((n, 4), dtype=torch.float64, device="cuda")
+    bits = torch.zeros(n // 32 + 1, dtype=torch.int32, device="cuda")
+    _lib.call("sss_select_topn_pack", _lib.ptr(vd), n, keep, _lib.ptr(f2t), _lib.ptr(x2),
+              _lib.ptr(mask2), _lib.ptr(energy2), _lib.ptr(xp), _lib.ptr(bits), sp)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x2) and torch.equal(mask, mask2) and torch.equal(energy, energy2)
+    assert torch.equal(xp, xp_ref)
+    assert torch.equal(bits, bits_ref)
+    # a small domain takes the block kernel + packing pass inside the same entry point
+    m = 256
+    vs = torch.as_tensor(rng.standard_normal((3, m)), device="cuda")
+    xs = torch.empty((3, m), dtype=torch.float64, device="cuda")
+    xps = torch.zeros((m, 4), dtype=torch.float64, device="cuda")
+    bs = torch.zeros(m // 32 + 1, dtype=torch.int32, device="cuda")
+    ms = torch.empty((3, m // 32), dtype=torch.int32, device="cuda")
+    _lib.call("sss_select_topn_pack", _lib.ptr(vs), m, 64, None, _lib.ptr(xs), _lib.ptr(ms), None,
+              _lib.ptr(xps), _lib.ptr(bs), sp)
+    torch.cuda.synchronize()
+    assert torch.equal(xps[:, :3], xs.T)
+    assert int((xs != 0).any(dim=0).sum()) == sum(bin(int(w) & 0xFFFFFFFF).count("1") for w in bs.tolist())
+
+
 def test_select_all_equal_ties_lowest_index(lib):
     from paper_2203_12339_b200 import wavelets as W
 
