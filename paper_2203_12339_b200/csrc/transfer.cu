@@ -49,12 +49,16 @@ __global__ void k_pack_x_bits(const double* __restrict__ x, int N, double4* __re
   if ((threadIdx.x & 31) == 0 && i < N) bits[i >> 5] = m;
 }
 
-// one 32-byte x record through the read-only path
-__device__ __forceinline__ void gather_x(const double4* __restrict__ xp, uint32_t c, double& a,
-                                         double& b, double& d) {
-  double e;
-  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(d), "=d"(e) : "l"(xp + c));
-  (void)e;
+// one 32-byte x record through the read-only path, predicated inside the
+// instruction: the destination registers ARE the lane's x registers (a lane
+// that skips keeps its last record), so no conditional moves sit between the
+// load and its first use and the U gathers of a batch stay in flight together
+__device__ __forceinline__ void gather_x_if(const double4* __restrict__ xp, uint32_t c, bool kept,
+                                            double (&x)[4]) {
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+      "@q ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n\t}"
+      : "+d"(x[0]), "+d"(x[1]), "+d"(x[2]), "+d"(x[3])
+      : "l"(xp + c), "r"((unsigned)kept));
 }
 
 // the same through the L1-bypassing load the flat16 kernel uses
@@ -157,21 +161,21 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
     // gathered (finite) value, so an absent or unkept term's 0 * x adds
     // exactly nothing
     auto phaseA = [&](const unsigned char* slot_p, uint32_t (&w)[U], bool (&kp)[U],
-                      double (&xa)[U][3]) {
+                      double (&xa)[U][4]) {
       const uint32_t* sw = reinterpret_cast<const uint32_t*>(slot_p);
 #pragma unroll
       for (int t = 0; t < U; ++t) {
         w[t] = sw[t * 32 + lane];
         const uint32_t c = w[t] & 0xffffu;
         kp[t] = ((sbits[c >> 5] >> (c & 31u)) & (w[t] >> 16 != 0u ? 1u : 0u)) != 0u;
-        if (kp[t]) gather_x(xp, c, xa[t][0], xa[t][1], xa[t][2]);
+        gather_x_if(xp, c, kp[t], xa[t]);
       }
     };
     // phase B: the lane's values (lane-major in the step block; the term of
     // each is the next set bit of the mask), fp64 accumulation in (step,
     // term) order
     auto phaseB = [&](const unsigned char* slot_p, const uint32_t (&w)[U], const bool (&kp)[U],
-                      const double (&xa)[U][3]) {
+                      const double (&xa)[U][4]) {
       const float* sv = reinterpret_cast<const float*>(slot_p + SM::WB);
       unsigned vbase = 0;
 #pragma unroll
@@ -196,9 +200,9 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
     auto slot_of = [&](unsigned q) { return wb + (q % NS) * SM::SLOT; };
     uint32_t w[U];
     bool kp[U];
-    double xa[U][3];
+    double xa[U][4];
 #pragma unroll
-    for (int t = 0; t < U; ++t) xa[t][0] = xa[t][1] = xa[t][2] = 0.0;
+    for (int t = 0; t < U; ++t) xa[t][0] = xa[t][1] = xa[t][2] = xa[t][3] = 0.0;
     const unsigned q0 = seq;  // ring position of batch 0 of this item
 #pragma unroll
     for (int j = 0; j < NS; ++j)
