@@ -273,6 +273,15 @@ int sss_edit_finish(int K, int side, int levels, const double* vk, const double*
                     const double* material, double* scatter, float* radiance,
                     float* radiance_unclamped, void* stream);
 
+/* The same, additionally writing the API's float64 FrameResult pair rad64
+ * (2 x N x 3: radiance, then radiance_unclamped, the float32 results widened:
+ * sss_widen_frame's output) so an API frame needs no widening launch. rad64
+ * may be NULL (= sss_edit_finish). Tiles up to 16 x 16 (levels <= 4). */
+int sss_edit_finish_wide(int K, int side, int levels, const double* vk, const double* g,
+                         const float* positions, const float* normals, const double* cam,
+                         const double* material, double* scatter, float* radiance,
+                         float* radiance_unclamped, double* rad64, void* stream);
+
 /* ================= precompute (path d): pair pass + two-step compression ====
  * replaces precompute_compressed (transfer.py:350-361) for a geometry image
  * with L-level Haar (L <= 3) on w0 and w1. N = side^2; "tm" = tile-major.  */
@@ -460,8 +469,10 @@ int sss_energy_cut(const double* sqT, int nvec, int D, double fraction, const in
  *   per-call overhead of the relight / edit frames): n_h2d host->device copies
  *   from pinned staging (the new light / material / camera), an event, the
  *   frame's CUDA graph (cudaGraphExec_t), an event, the float64 widening of
- *   the radiance (as sss_widen_frame) and its device->host copy into pinned
- *   memory, the kept-energy copy. Any part may be NULL / 0. */
+ *   the radiance (as sss_widen_frame; skipped when radiance is NULL: the
+ *   graph's epilogue wrote rad64 itself, sss_edit_finish_wide) and its
+ *   device->host copy into pinned memory, the kept-energy copy. Any part may
+ *   be NULL / 0. */
 int sss_frame_replay(void* graph_exec, int n_h2d, void* const* h2d_dst, const void* const* h2d_src,
                      const unsigned long long* h2d_bytes, void* ev_start, void* ev_end,
                      const float* radiance, const float* radiance_unclamped, long long n3,

@@ -49,6 +49,7 @@ _SIGS = {
     "sss_direct_irradiance64": [_I, _P, _P, _I, _P, _P, _P, C.c_double, C.c_double, _P, _P, _P,
                                 _P],
     "sss_edit_finish": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "sss_edit_finish_wide": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_pair_block": [_I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P, _P, _I, C.c_float, _P, _P, _P],
     "sss_pair_rows_exact": [_I, _I, _P, _P, _I, _P, _P, _I, C.c_float, _I, _I, _P, _P],
     "sss_step1_select": [_P, _I, _I, _I, _P, _P, _P],

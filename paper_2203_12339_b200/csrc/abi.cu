@@ -548,6 +548,14 @@ int sss_edit_finish(int K, int side, int levels, const double* vk, const double*
                     const float* positions, const float* normals, const double* cam,
                     const double* material, double* scatter, float* radiance,
                     float* radiance_unclamped, void* stream) {
+  return sss_edit_finish_wide(K, side, levels, vk, g, positions, normals, cam, material, scatter,
+                              radiance, radiance_unclamped, nullptr, stream);
+}
+
+int sss_edit_finish_wide(int K, int side, int levels, const double* vk, const double* g,
+                         const float* positions, const float* normals, const double* cam,
+                         const double* material, double* scatter, float* radiance,
+                         float* radiance_unclamped, double* rad64, void* stream) {
   if (int r = check_geom(side, levels)) return r;
   if (K <= 0 || !vk || !g || !positions || !normals || !cam || !material || !radiance ||
       !radiance_unclamped)
@@ -564,9 +572,10 @@ int sss_edit_finish(int K, int side, int levels, const double* vk, const double*
     if (int r = set_smem((const void*)sss::k_edit_finish_multi, smem)) return r;
     launch_chain(sss::k_edit_finish_multi, dim3(tiles / G), dim3(G * T2 < 64 ? 64 : G * T2), smem,
                  S_(stream), K, side, levels, G, vk, g, positions, normals, cam, material, scatter,
-                 radiance, radiance_unclamped);
+                 radiance, radiance_unclamped, rad64);
     return check_launch("k_edit_finish_multi");
   }
+  if (rad64) return fail(SSS_EINVAL, "edit_finish_wide: tiles larger than 16 x 16 are not widened");
   const size_t smem = 4 * (size_t)T * T * sizeof(double);
   if (int r = set_smem((const void*)sss::k_edit_finish, smem)) return r;
   sss::k_edit_finish<<<tiles, 128, smem, S_(stream)>>>(
@@ -931,7 +940,9 @@ int sss_frame_replay(void* graph_exec, int n_h2d, void* const* h2d_dst, const vo
   if (ev_end && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_end), st) != cudaSuccess)
     return fail(SSS_ECUDA, "frame_replay: event record");
   if (rad64 && host_rad64) {  // the float64 FrameResult arrays, widened on the device, one D2H
-    if (int r = sss_widen_frame(radiance, radiance_unclamped, n3, rad64, stream)) return r;
+    // radiance == NULL: the graph's epilogue already wrote rad64 (sss_edit_finish_wide)
+    if (radiance)
+      if (int r = sss_widen_frame(radiance, radiance_unclamped, n3, rad64, stream)) return r;
     e = cudaMemcpyAsync(host_rad64, rad64, (size_t)(2 * n3) * sizeof(double),
                         cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return fail(SSS_ECUDA, cudaGetErrorString(e));

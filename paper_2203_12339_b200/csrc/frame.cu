@@ -882,9 +882,11 @@ __device__ void multi_tile_epilogue(double* summed, double* tmp, int T, int tile
                                     const double* __restrict__ cam,
                                     const double* __restrict__ material,
                                     double* __restrict__ scatter, float* __restrict__ radiance,
-                                    float* __restrict__ radiance_unclamped) {
+                                    float* __restrict__ radiance_unclamped,
+                                    double* __restrict__ rad64 = nullptr) {
   const int T2 = T * T, tpr = S / T;
   const double eta = material[6];
+  const size_t n3 = (size_t)3 * S * S;
   batch_tile_haar_inv(summed, tmp, T, 3 * ntiles);
   const double inv_pi = 1.0 / 3.141592653589793;
   for (int q = threadIdx.x; q < ntiles * T2; q += blockDim.x) {
@@ -902,8 +904,13 @@ __device__ void multi_tile_epilogue(double* summed, double* tmp, int T, int tile
       const double sc = summed[(j * 3 + c) * T2 + e];
       const double u = sc * f;
       if (scatter) scatter[i * 3 + c] = sc;
-      radiance_unclamped[i * 3 + c] = (float)u;
-      radiance[i * 3 + c] = (float)fmax(u, 0.0);
+      const float uf = (float)u, cf = (float)fmax(u, 0.0);
+      radiance_unclamped[i * 3 + c] = uf;
+      radiance[i * 3 + c] = cf;
+      if (rad64) {  // the API's float64 FrameResult pair (k_widen_frame's output)
+        rad64[i * 3 + c] = (double)cf;
+        rad64[n3 + i * 3 + c] = (double)uf;
+      }
     }
   }
 }
@@ -946,7 +953,7 @@ __global__ void __launch_bounds__(256) k_edit_finish_multi(
     const float* __restrict__ positions, const float* __restrict__ normals,
     const double* __restrict__ cam, const double* __restrict__ material,
     double* __restrict__ scatter, float* __restrict__ radiance,
-    float* __restrict__ radiance_unclamped) {
+    float* __restrict__ radiance_unclamped, double* __restrict__ rad64) {
   extern __shared__ double sm[];
   const int T = 1 << L, T2 = T * T, N = S * S;
   double* summed = sm;                        // G x 3 x T2
@@ -983,7 +990,7 @@ __global__ void __launch_bounds__(256) k_edit_finish_multi(
   }
   __syncthreads();
   multi_tile_epilogue(summed, tmp, T, tile0, G, S, positions, normals, cam, material, scatter,
-                      radiance, radiance_unclamped);
+                      radiance, radiance_unclamped, rad64);
 }
 
 // ---------------------------------------------------------------------------

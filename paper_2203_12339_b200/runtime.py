@@ -502,11 +502,16 @@ class Scene:
         self._transfer_core(sp, zero_vk=False)
 
     def _launch_edit(self, stream=None):
-        _lib.call("sss_edit_finish", self.K, self.side, self.levels, _lib.ptr(self.vk),
+        # with the API's float64 read-back buffer allocated the epilogue writes
+        # the widened pair too (no widening launch per API frame); a graph
+        # captured that way says so (_wide)
+        r64 = getattr(self, "_rad64", None) if self.levels <= 4 else None
+        _lib.call("sss_edit_finish_wide", self.K, self.side, self.levels, _lib.ptr(self.vk),
                   _lib.ptr(self.g), _lib.ptr(self.positions), _lib.ptr(self.normals),
                   _lib.ptr(self.cam_buf), _lib.ptr(self.material_buf), _lib.ptr(self.scatter),
-                  _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped),
+                  _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped), _lib.ptr(r64),
                   _lib.stream_ptr(stream))
+        return r64 is not None
 
     def launch_relight(self, stream=None):
         """Enqueue a full relight (no host sync). The material weights do not
@@ -575,8 +580,11 @@ class Scene:
     def capture(self):
         """Capture the relight sequence in a CUDA graph (replayed by
         ``replay``); per-frame inputs are the device buffers it reads."""
+        if getattr(self, "_pin", None) is None:
+            self._enqueue_readback_init()  # the epilogue writes the API's float64 pair
         self.launch_relight()  # warm (sets smem attributes, first-touch)
         torch.cuda.synchronize()
+        self._graph_wide = self.levels <= 4
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             self.launch_relight()
@@ -675,12 +683,14 @@ class Scene:
         if pend:
             self._pending.clear()
         n = len(pend)
+        wide = getattr(self, "_graph_wide", False)  # the graph's epilogue wrote _rad64
         dsts = (C.c_void_p * max(n, 1))(*[d.data_ptr() for d, _ in pend])
         srcs = (C.c_void_p * max(n, 1))(*[p_.data_ptr() for _, p_ in pend])
         sizes = (C.c_ulonglong * max(n, 1))(*[d.numel() * d.element_size() for d, _ in pend])
         _lib.call("sss_frame_replay", C.c_void_p(graph.raw_cuda_graph_exec()), n, dsts, srcs, sizes,
                   C.c_void_p(ev[0].cuda_event), C.c_void_p(ev[1].cuda_event),
-                  _lib.ptr(self.radiance), _lib.ptr(self.radiance_unclamped), self.n * 3,
+                  None if wide else _lib.ptr(self.radiance),
+                  None if wide else _lib.ptr(self.radiance_unclamped), self.n * 3,
                   _lib.ptr(self._rad64), C.c_void_p(blk.data_ptr()), _lib.ptr(self.energy),
                   C.c_void_p(self._pin["energy"].data_ptr()), 48, _lib.stream_ptr())
         self._blk = blk
