@@ -5,6 +5,7 @@
 D=${1:-gpurun_out/r02f}
 mkdir -p $D
 python bench.py > $D/bench.json 2> $D/bench.err
+python bench.py --steps 1000 --warmup 5 --no-cpu-baseline --no-secondary > $D/bench_1000.json 2> $D/bench_1000.err
 python bench.py --impl reference --steps 3 --warmup 1 > $D/bench_ref.json 2> $D/bench_ref.err
 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $D/launches.csv python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-secondary \
