@@ -242,8 +242,13 @@ int sss_pack_x_bits(const double* x, int n, void* xp, uint32_t* bits, void* stre
  *   `bits` needs n_rows / 32 + 1 words with the bit of column n_rows clear.
  *   col_bits 16 (n_rows <= 65536, 16 entries per lane): u16 columns, padding
  *   keeps column 0 with value 0. min_blocks = CTAs of 128 threads per SM: 4, 6,
- *   8 for 16 entries, 6, 8 for 32, 8 for 16-bit columns. Accumulates into vk
- *   with fp64 atomics (order not fixed), zeroing it first when zero_vk.
+ *   8 for 16 entries, 6, 8 for 32, 8 for 16-bit columns. vk must be zero
+ *   (zeroed here when zero_vk). word_partials != NULL (6 doubles per word of
+ *   32 lanes, ceil(n_entries / entries_per_lane / 32) words): deterministic
+ *   sums - segments inside one word are stored, the pieces of rows spanning
+ *   words are added in word order by a second small launch (span_first: per
+ *   word, the word in which the row running into it began = the last word
+ *   before it that holds a head); NULL: fp64 atomics into vk (order not fixed).
  *   work_counter (u32, nullable): warps claim `chunk` words at a time from it;
  *   it must be zero at launch (zeroed here with vk when zero_vk). */
 int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals,
@@ -252,7 +257,7 @@ int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals
                         const unsigned* warp_begin, int n_warps, int min_blocks,
                         int entries_per_lane, int col_bits, int zero_vk, const void* xp,
                         const uint32_t* bits, double* vk, uint32_t* work_counter, int chunk,
-                        void* stream);
+                        double* word_partials, const uint32_t* span_first, void* stream);
 
 /* sss_fold_apply_rows: the same v_k update as sss_fold_apply from a row-major
  *   copy of the folded operators, ELL-interleaved per 32-row group: group g =

@@ -42,7 +42,7 @@ _SIGS = {
     "sss_transfer_kfr": [_I, _I, C.c_uint, C.c_uint, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                          _P, _P, _P, _I, _I, _I, _P],
     "sss_transfer_flat16": [_I, _I, _P, _P, C.c_ulonglong, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P,
-                            _P, _P, _P, _I, _P],
+                            _P, _P, _P, _I, _P, _P, _P],
     "sss_fold_apply_rows": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_fold_apply": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "sss_direct_irradiance": [_I, _P, _P, _I, _P, _P, _P, C.c_double, C.c_double, _P, _P, _P, _P],

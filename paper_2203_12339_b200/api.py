@@ -204,6 +204,13 @@ class _Transfer:
         self.wctr = torch.zeros(1, dtype=torch.int32, device=dev)
         self.nsm = torch.cuda.get_device_properties(0).multi_processor_count
 
+    def _flat16_partials(self, ne: int, E: int) -> torch.Tensor:
+        """Per-word partial sums of the deterministic flat16 form."""
+        if getattr(self, "_f16_part", None) is None:
+            self._f16_part = torch.zeros(((ne // E + 31) // 32, 6), dtype=torch.float64,
+                                         device="cuda")
+        return self._f16_part
+
     def apply(self, x: torch.Tensor, vk: torch.Tensor, sp):
         _lib.call("sss_pack_x_bits", _lib.ptr(x), self.n, _lib.ptr(self.xp), _lib.ptr(self.xbits), sp)
         if self.kind == "kfr":
@@ -220,7 +227,8 @@ class _Transfer:
             _lib.call("sss_transfer_flat16", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
                       _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W, 8, st["E"],
                       st["col_bits"], 1, _lib.ptr(self.xp), _lib.ptr(self.xbits), _lib.ptr(vk),
-                      _lib.ptr(self.wctr), 4, sp)
+                      _lib.ptr(self.wctr), 4, _lib.ptr(self._flat16_partials(ne, st["E"])),
+                      _lib.ptr(st["span_first"]), sp)
 
 
 def pack_accelerator(accel):

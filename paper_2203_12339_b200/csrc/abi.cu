@@ -476,7 +476,7 @@ int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals
                         const unsigned* warp_begin, int n_warps, int min_blocks,
                         int entries_per_lane, int col_bits, int zero_vk, const void* xp,
                         const uint32_t* bits, double* vk, uint32_t* work_counter, int chunk,
-                        void* stream) {
+                        double* word_partials, const uint32_t* span_first, void* stream) {
   const int E = entries_per_lane;
   if ((col_bits != 16 && col_bits != 32) || (col_bits == 16 && (n_rows > 65536 || E != 16)))
     return fail(SSS_EINVAL, "transfer_flat16: col_bits 32, or 16 with n_rows <= 65536 and E 16");
@@ -500,21 +500,33 @@ int sss_transfer_flat16(int K, int n_rows, const void* pcols, const float* pvals
   const auto* x4 = reinterpret_cast<const double4*>(xp);
   const unsigned grid = n_warps / (sss::kV25Threads / 32);
   const unsigned ng = (unsigned)(n_entries / E);
+  // word_partials (2 x 3 doubles per word of 32 lanes): the deterministic form,
+  // plain stores + k_flat16_merge instead of fp64 atomics
+  const unsigned nwords = (ng + 31u) / 32u;
+  auto merge = [&]() -> int {
+    if (!word_partials) return SSS_OK;
+    if (!span_first) return fail(SSS_EINVAL, "transfer_flat16: word_partials needs span_first");
+    launch_chain(sss::k_flat16_merge, dim3((nwords + 127u) / 128u), dim3(128), 0, S_(stream), n_rows,
+                 nwords, heads, head_prefix, seg_rowk, span_first, (const double*)word_partials, vk);
+    return check_launch("k_flat16_merge");
+  };
 #define SSS_V25(MB, EE)                                                                          \
   if (min_blocks == MB && E == EE) {                                                             \
     if (int r = set_smem((const void*)sss::k_transfer_flat16<MB, EE>, smem)) return r;           \
     sss::k_transfer_flat16<MB, EE><<<grid, sss::kV25Threads, smem, S_(stream)>>>(                \
         n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk,            \
-        work_counter, chunk);                                                                    \
-    return check_launch("k_transfer_flat16");                                                    \
+        work_counter, chunk, word_partials);                                                     \
+    if (int r = check_launch("k_transfer_flat16")) return r;                                     \
+    return merge();                                                                              \
   }
   if (col_bits == 16) {
     if (min_blocks != 8) return fail(SSS_EINVAL, "transfer_flat16: 16-bit columns use min_blocks 8");
     if (int r = set_smem((const void*)sss::k_transfer_flat16<8, 16, true>, smem)) return r;
     sss::k_transfer_flat16<8, 16, true><<<grid, sss::kV25Threads, smem, S_(stream)>>>(
         n_rows, ng, c16, v16, heads, head_prefix, seg_rowk, warp_begin, x4, bits, vk,
-        work_counter, chunk);
-    return check_launch("k_transfer_flat16");
+        work_counter, chunk, word_partials);
+    if (int r = check_launch("k_transfer_flat16")) return r;
+    return merge();
   }
   SSS_V25(4, 16) SSS_V25(6, 16) SSS_V25(8, 16) SSS_V25(8, 32) SSS_V25(6, 32)
 #undef SSS_V25

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
     const uint32_t* __restrict__ H, const uint32_t* __restrict__ hpre,
     const uint32_t* __restrict__ rowk, const unsigned* __restrict__ warp_begin,
     const double4* __restrict__ xp, const uint32_t* __restrict__ bits, double* __restrict__ vk,
-    unsigned* __restrict__ work = nullptr, int chunk = 4) {
+    unsigned* __restrict__ work = nullptr, int chunk = 4, double* __restrict__ part = nullptr) {
   constexpr int G = E / 16;
   extern __shared__ uint32_t v25_bits[];
   // one word past the N columns: padding entries carry column N, never kept
@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const unsigned upto = (2u << lane) - 1u;
+  const unsigned nwords_all = warp_begin[(gridDim.x * blockDim.x) >> 5];
   auto word = [&](unsigned i) {
     V25Slot<COL16> S;
     S.h = __ldg(&H[i]);
@@ -117,7 +118,26 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
       }
     }
     const bool tail = (lane == 31) || ((S.h >> (lane + 1)) & 1u);
-    if (tail && (p0 != 0.0 || p1 != 0.0 || p2 != 0.0)) {
+    if (part) {
+      // Deterministic sums: a (row, term) segment that starts and ends inside
+      // this word is stored directly (v_k is zeroed, nobody else writes it);
+      // a segment continuing the previous word's row (no head at or before
+      // the lane) leaves its sum in the word's slot 0, one running into the
+      // next word (lane 31, next word's lane 0 is no head) in slot 1, and
+      // k_flat16_merge adds the pieces of every spanning row in word order
+      const bool cont = hm == 0u;
+      const bool open = lane == 31 && i + 1u < nwords_all && !(__ldg(&H[i + 1u]) & 1u);
+      if (tail && (cont || open)) {
+        double* q = part + ((size_t)i * 2 + (cont ? 0 : 1)) * 3;
+        q[0] = p0; q[1] = p1; q[2] = p2;
+      } else if (tail && (p0 != 0.0 || p1 != 0.0 || p2 != 0.0)) {
+        const unsigned rk = __ldg(&rowk[S.hp + __popc(hm) - 1u]);
+        double* vo = vk + (size_t)(rk & 15u) * 3 * N + (rk >> 4);
+        vo[0] = p0;
+        vo[N] = p1;
+        vo[2 * (size_t)N] = p2;
+      }
+    } else if (tail && (p0 != 0.0 || p1 != 0.0 || p2 != 0.0)) {
       const unsigned rk = __ldg(&rowk[S.hp + __popc(hm) - 1u]);
       double* vo = vk + (size_t)(rk & 15u) * 3 * N + (rk >> 4);
       atomicAdd(vo, p0);
@@ -133,7 +153,7 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
   }
   // dynamic: warps claim chunks of words from a zeroed counter (the equal
   // static ranges differ in gather count: SM busy times spread by +-10 %)
-  const unsigned nwords = warp_begin[(gridDim.x * blockDim.x) >> 5];
+  const unsigned nwords = nwords_all;
 #pragma unroll 1
   for (;;) {
     unsigned c = 0;
@@ -145,6 +165,53 @@ __global__ void __launch_bounds__(kV25Threads, MINB) k_transfer_flat16(
 #pragma unroll 1
     for (unsigned i = i0; i < i1; ++i) word(i);
   }
+}
+
+// The second pass of the deterministic form: one thread per word that CLOSES a
+// row spanning several words (it continues the previous word, and the row ends
+// in it: a head further on, or the next word starts fresh, or the stream ends). The row's pieces are the open last segment
+// of the word it began in (slot 1), the whole of every headless word in
+// between (slot 0) and this word's leading segment (slot 0), added in word
+// order - a fixed order, so v_k is bitwise reproducible.
+__global__ void k_flat16_merge(int N, unsigned nwords, const uint32_t* __restrict__ H,
+                               const uint32_t* __restrict__ hpre,
+                               const uint32_t* __restrict__ rowk,
+                               const uint32_t* __restrict__ span_first,
+                               const double* __restrict__ part, double* __restrict__ vk) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const unsigned b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0u || b >= nwords) return;
+  // every independent load first (the kernel is a chain of L2 round trips)
+  const uint32_t h = __ldg(&H[b]);
+  const uint32_t hn = b + 1u < nwords ? __ldg(&H[b + 1u]) : 1u;
+  const unsigned a = __ldg(&span_first[b]);  // the word the row began in (layout.flat16_layout)
+  const unsigned seg = __ldg(&hpre[b]) - 1u;
+  const double* qb = part + (size_t)b * 2 * 3;
+  const double b0 = qb[0], b1 = qb[1], b2 = qb[2];
+  if (h & 1u) return;  // starts fresh: nothing continues into this word
+  // a headless word whose row also runs into the next word is a through word
+  if (h == 0u && !(hn & 1u)) return;
+  const unsigned rk = __ldg(&rowk[seg]);
+  const double* q = part + ((size_t)a * 2 + 1) * 3;
+  double s0 = q[0], s1 = q[1], s2 = q[2];
+  for (unsigned w0 = a + 1u; w0 < b; w0 += 4u) {  // the through words, four loads in flight, adds in order
+    double t[4][3];
+#pragma unroll
+    for (unsigned u = 0; u < 4u; ++u) {
+      const bool in = w0 + u < b;
+      q = part + (size_t)(in ? w0 + u : b) * 2 * 3;
+      t[u][0] = in ? q[0] : 0.0; t[u][1] = in ? q[1] : 0.0; t[u][2] = in ? q[2] : 0.0;
+    }
+#pragma unroll
+    for (unsigned u = 0; u < 4u; ++u)
+      if (w0 + u < b) { s0 += t[u][0]; s1 += t[u][1]; s2 += t[u][2]; }
+  }
+  s0 += b0; s1 += b1; s2 += b2;
+  double* vo = vk + (size_t)(rk & 15u) * 3 * N + (rk >> 4);
+  vo[0] = s0;
+  vo[N] = s1;
+  vo[2 * (size_t)N] = s2;
 }
 
 }  // namespace sss

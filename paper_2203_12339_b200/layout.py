@@ -350,7 +350,14 @@ def flat16_layout(t, warps_per_sm: int = 32, col16: bool = None):
         pc = torch.where(pcols >= 32768, pcols - 65536, pcols).to(torch.int16)
     else:
         pc = pcols.to(torch.int32)
+    # for the deterministic merge: the word in which the row running into word
+    # b began = the last word before b that holds a head
+    has = (cnt > 0).to(torch.int64) * torch.arange(nw, device=dev)
+    last_head = torch.cummax(has, 0).values
+    span_first = torch.zeros(nw, dtype=torch.int64, device=dev)
+    span_first[1:] = last_head[:-1]
     stats = {"entries": pcols.numel(), "words": nw, "segments": int(s4.numel()),
-             "E": E, "col_bits": 16 if col16 else 32}
+             "E": E, "col_bits": 16 if col16 else 32,
+             "span_first": span_first.to(torch.int32).contiguous()}
     return (pc.contiguous(), pvals, pcols.numel(), heads.contiguous(), hpre.contiguous(),
             rowk.to(torch.int32).contiguous(), wbeg.to(torch.int32).contiguous(), W, stats)

@@ -198,6 +198,7 @@ class Scene:
             "kfr_chunk": int(os.environ.get("SSS_KFR_CHUNK", "256")),
             "kfr_steps": int(os.environ.get("SSS_KFR_STEPS", "4")),
             "kfr_minb": int(os.environ.get("SSS_KFR_MINB", "3")),
+            "flat16_atomics": os.environ.get("SSS_FLAT16_ATOMICS", "0") == "1",
             "env_union_kernel": os.environ.get("SSS_ENV_UNION_KERNEL", "0") == "1",
         }
         self._have_cache = False
@@ -443,10 +444,19 @@ class Scene:
         pcols, pvals, ne, heads, hpre, rowk, wbeg, W, st = lay
         if getattr(self, "_wctr", None) is None:
             self._wctr = torch.zeros(1, dtype=torch.int32, device="cuda")
+        # deterministic sums (per-word partials + an ordered merge launch) unless
+        # SSS_FLAT16_ATOMICS=1 asks for the fp64-atomics form (A/B)
+        part = None
+        if not self._knobs["flat16_atomics"]:
+            if getattr(self, "_f16_part", None) is None:
+                nwords = (ne // st["E"] + 31) // 32
+                self._f16_part = torch.zeros((nwords, 6), dtype=torch.float64, device="cuda")
+            part = self._f16_part
         _lib.call("sss_transfer_flat16", self.K, self.n, _lib.ptr(pcols), _lib.ptr(pvals), ne,
                   _lib.ptr(heads), _lib.ptr(hpre), _lib.ptr(rowk), _lib.ptr(wbeg), W, 8, st["E"],
                   st["col_bits"], int(zero_vk), _lib.ptr(self.xp), _lib.ptr(self.xbits),
-                  _lib.ptr(self.vk), _lib.ptr(self._wctr), 4, sp)
+                  _lib.ptr(self.vk), _lib.ptr(self._wctr), 4, _lib.ptr(part),
+                  _lib.ptr(st["span_first"]), sp)
 
     def _autotune_transfer(self, stream=None):
         """Time the core transfer launch of every candidate kernel on this

@@ -12,6 +12,7 @@ Bars as the rest of the suite: kept index sets identical; radiance within
 """
 
 import numpy as np
+import torch
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -79,6 +80,42 @@ def test_c2_frames_parity(lib):
             assert np.array_equal(sc.selected_indices(c), ref["spectra"][c].indices), (f, c)
         assert O.parity_error(fr.radiance_unclamped, ref["radiance_unclamped"], TAU) <= TOL, f
         assert O.parity_error(sc.scatter.cpu().numpy(), ref["scatter"], TAU) <= TOL, f
+
+
+def test_c2_flat16_sums_are_deterministic(lib, monkeypatch):
+    """The flat16 transfer (the autotuned choice at C2) in its default form:
+    per-word partial sums merged in word order - two relights are bitwise
+    equal, v_k agrees with the fp64-atomics form and with kfr to rounding, and
+    every row is written (rows spanning several 512-entry words included)."""
+    from paper_2203_12339_b200 import config as C
+    from paper_2203_12339_b200 import lighting as LT
+    from paper_2203_12339_b200.runtime import Scene, SHLight
+
+    cfg = C.C2
+    g, b, dt = _setup(cfg)
+    rng = np.random.default_rng(21)
+    L0 = LT.random_sh_light(cfg.sh_bands, 3)
+    m = _material(rng)
+    monkeypatch.setenv("SSS_TRANSFER", "flat16")
+    sc = Scene(g, dt, b, m, SHLight(L0))
+    assert sc.transfer_kernel == "flat16"
+    f1 = sc.relight()
+    v1 = sc.vk.clone()
+    assert torch.isfinite(v1).all()
+    for _ in range(4):  # two eager frames, then graph replays
+        f2 = sc.relight()
+        assert torch.equal(sc.vk, v1)
+    assert np.array_equal(f1.radiance_unclamped, f2.radiance_unclamped)
+    scale = v1.abs().max().item()
+    monkeypatch.setenv("SSS_FLAT16_ATOMICS", "1")
+    sa = Scene(g, dt, b, m, SHLight(L0))
+    sa.relight()
+    assert (sa.vk - v1).abs().max().item() <= 1e-12 * scale
+    monkeypatch.delenv("SSS_FLAT16_ATOMICS")
+    monkeypatch.setenv("SSS_TRANSFER", "kfr")
+    sk = Scene(g, dt, b, m, SHLight(L0))
+    sk.relight()
+    assert (sk.vk - v1).abs().max().item() <= 1e-12 * scale
 
 
 @pytest.fixture(scope="module")

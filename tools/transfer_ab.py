@@ -48,6 +48,8 @@ def main():
         torch.cuda.synchronize()
         st = getattr(dt, kern, None)
         stats = st.stats if hasattr(st, "stats") else (st[-1] if isinstance(st, tuple) else None)
+        if isinstance(stats, dict):  # the flat16 stats carry a device tensor (span_first)
+            stats = {k: v for k, v in stats.items() if not torch.is_tensor(v)}
         out[kern] = {"us": 1e3 * e0.elapsed_time(e1) / reps, "rel_err_vs_kfr": err, "stats": stats}
         print(json.dumps({kern: out[kern]}), flush=True)
 
