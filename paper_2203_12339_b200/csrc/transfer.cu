@@ -12,7 +12,8 @@
 // (row, column) pairs (the K terms of one row share columns), so this kernel
 // gathers x once per PAIR and applies it to all the pair's terms:
 //   * the layout (layout.py:kfr_layout) cuts every receiver row into chunks
-//     of <= 512 (column, term-mask) pairs; a warp owns 32 chunks (lane ==
+//     of a length chosen per operator (layout.kfr_auto_chunk: just under the
+//     mean work per warp) of (column, term-mask) pairs; a warp owns 32 chunks (lane ==
 //     chunk == one row, all K terms: 3K fp64 accumulators in registers, no
 //     atomics, no cross-lane reduction, deterministic order);
 //   * step s of a warp: every lane takes the s-th pair of its chunk. The
@@ -26,7 +27,7 @@
 //     conflict-free LDS per plane, and the L1 pipe is left to the x gathers;
 //   * only lanes whose column is kept (kept-column bitmap in shared memory)
 //     gather x (one 32-byte fp64 record) and touch their values;
-//   * chunks of rows longer than 512 pairs write fp64 partial sums; the last
+//   * chunks of rows longer than one chunk write fp64 partial sums; the last
 //     chunk to finish a row (atomic arrival count) sums them in chunk order.
 // Products are f32 operator value x fp64 x, accumulated in fp64 (SURVEY §8d:
 // fp32 accumulation fails the 1e-4 bar); the summation order is fixed by the

@@ -80,7 +80,22 @@ def _bitrev(mask: torch.Tensor, K: int) -> torch.Tensor:
     return r
 
 
-def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4) -> KfrLayout:
+def kfr_auto_chunk(n_pairs: int, n_warps: int, steps_per_batch: int) -> int:
+    """Chunk length for an operator of `n_pairs` (column, mask) pairs streamed
+    by `n_warps` resident warps. A warp item is 32 chunks, so the longest item
+    is `chunk` steps: measured on the C3 operator, time is flat while that
+    stays just under the mean work per warp (steps / warps: 423 at 2 CTAs/SM,
+    optimum 416; 282 at 3, optimum 272) - longer and the longest item is the
+    makespan, shorter and rows split into more partial sums than needed
+    (profiles/r02_transfer_experiments.json, chunk sweeps)."""
+    steps = n_pairs / 32.0 / 0.974  # the layouts fill ~97.4 % of the lane slots
+    U = steps_per_batch
+    c = int(0.983 * steps / max(n_warps, 1)) // U * U
+    return max(64, min(c, KFR_MAX_BATCHES * U))
+
+
+def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4,
+               n_warps: int = 0) -> KfrLayout:
     """K-fused row-chunk layout of sss_transfer_kfr (see csrc/transfer.cu).
 
     The K terms are split in groups of G = KFR_GROUP; the terms of one
@@ -101,6 +116,7 @@ def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4) 
         raise ValueError("kfr layout: K <= 16 terms and n <= 65536 rows (16-bit columns)")
     if chunk > KFR_MAX_BATCHES * steps_per_batch:
         raise ValueError(f"kfr layout: chunk <= {KFR_MAX_BATCHES} x steps_per_batch")
+    auto_chunk = chunk <= 0  # chosen below from the pair count and `n_warps`
     dev = t.rowptr.device
     U = steps_per_batch
     row, k, col, val = canonical_entries(t)
@@ -127,6 +143,8 @@ def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4) 
     rank_of_pair = torch.empty_like(po)
     rank_of_pair[po] = torch.arange(P, device=dev)
     prg, pcol, pmask = prg[po], pcol[po], pmask[po]
+    if auto_chunk:
+        chunk = kfr_auto_chunk(P, n_warps, U)
     RG = n * NG
     cnt = torch.bincount(prg, minlength=RG)
     start = torch.cumsum(cnt, 0) - cnt
@@ -232,7 +250,7 @@ def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4) 
         return torch.where(x >= (1 << 31), x - (1 << 32), x).to(torch.int32).contiguous()
 
     steps = int(S.sum())
-    stats = {"steps_per_batch": U, "groups": NG, "pairs": P, "entries": nnz, "chunks": NC,
+    stats = {"steps_per_batch": U, "chunk": chunk, "groups": NG, "pairs": P, "entries": nnz, "chunks": NC,
              "items": NI, "steps": steps, "batches": NB,
              "lane_util": round(P / max(32 * steps, 1), 4), "multi": M, "partials": n_partials,
              "bytes": total * 4 + NI * 8 + NI * 256 + (NB + 1) * 4}

@@ -195,9 +195,12 @@ class Scene:
         self._autotune = choice == "auto" and kfr_ok
         self.transfer_timings_us = {}
         self._knobs = {
-            "kfr_chunk": int(os.environ.get("SSS_KFR_CHUNK", "256")),
-            "kfr_steps": int(os.environ.get("SSS_KFR_STEPS", "4")),
-            "kfr_minb": int(os.environ.get("SSS_KFR_MINB", "3")),
+            # kfr: 8-step batches at 2 CTAs/SM, chunk length from the operator
+            # (layout.kfr_auto_chunk; 0 = auto). 4 steps / 3 CTAs / 256 was the
+            # default until the chunk sweeps (154 vs 142 us on the C3 operator)
+            "kfr_chunk": int(os.environ.get("SSS_KFR_CHUNK", "0")),
+            "kfr_steps": int(os.environ.get("SSS_KFR_STEPS", "8")),
+            "kfr_minb": int(os.environ.get("SSS_KFR_MINB", "2")),
             "flat16_atomics": os.environ.get("SSS_FLAT16_ATOMICS", "0") == "1",
             "env_union_kernel": os.environ.get("SSS_ENV_UNION_KERNEL", "0") == "1",
         }
@@ -408,8 +411,10 @@ class Scene:
         t = self.transfer
         if self.transfer_kernel == "kfr":
             if getattr(t, "kfr", None) is None:
+                nsm = torch.cuda.get_device_properties(0).multi_processor_count
                 t.kfr = kfr_layout(t, chunk=self._knobs["kfr_chunk"],
-                                   steps_per_batch=self._knobs["kfr_steps"])
+                                   steps_per_batch=self._knobs["kfr_steps"],
+                                   n_warps=nsm * self._knobs["kfr_minb"] * 8)
             return t.kfr
         if getattr(t, "flat16", None) is None:
             t.flat16 = flat16_layout(t)

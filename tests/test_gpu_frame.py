@@ -802,9 +802,11 @@ def test_env_union_fused_equals_union_kernel(c1):
 
     env = LT.Environment(side=16, seed=12)
     sc = _scene(c1, EnvLight(env.faces(21.0)))
+    sc._flush_pending()  # the constructor only stages the cubemap; upload it
     sc._launch_stage1(want_E=True)
     torch.cuda.synchronize()
     e_fused, h_fused = sc.E.clone(), sc.ehat.clone()
+    assert torch.isfinite(e_fused).all() and float(e_fused.abs().max()) > 0.0
     sc._knobs["env_union_kernel"] = True  # knobs are read once, at construction
     sc._launch_stage1(want_E=True)
     torch.cuda.synchronize()
