@@ -197,7 +197,11 @@ class _Transfer:
         self.n, self.K = n, len(operators)
         csr = csr_from_operators(operators, n, levels)
         self.kind = "kfr" if (self.K <= 16 and n <= 65536) else "flat16"
-        self.lay = kfr_layout(csr) if self.kind == "kfr" else flat16_layout(csr)
+        nsm = torch.cuda.get_device_properties(0).multi_processor_count
+        # the geometry-image runtime's kfr configuration (8-step batches, 2
+        # CTAs/SM, chunk length from the operator)
+        self.lay = (kfr_layout(csr, chunk=0, steps_per_batch=8, n_warps=nsm * 2 * 8)
+                    if self.kind == "kfr" else flat16_layout(csr))
         dev = torch.device("cuda")
         self.xp = torch.empty((n, 4), dtype=torch.float64, device=dev)
         self.xbits = torch.zeros((n >> 5) + 1, dtype=torch.int32, device=dev)
@@ -220,7 +224,7 @@ class _Transfer:
                       _lib.ptr(lay.batch_off), _lib.ptr(lay.stream), _lib.ptr(self.xp),
                       _lib.ptr(self.xbits), _lib.ptr(vk), _lib.ptr(lay.partials),
                       _lib.ptr(lay.partial_row), _lib.ptr(lay.multi_info), _lib.ptr(lay.multi_count),
-                      _lib.ptr(lay.work), lay.stats["steps_per_batch"], self.nsm * 3 * 8, 3, sp)
+                      _lib.ptr(lay.work), lay.stats["steps_per_batch"], self.nsm * 2 * 8, 2, sp)
         else:
             pcols, pvals, ne, heads, hpre, rowk, wbeg, W, st = self.lay
             _lib.call("sss_zero", _lib.ptr(self.wctr), 4, sp)
