@@ -83,14 +83,15 @@ def _bitrev(mask: torch.Tensor, K: int) -> torch.Tensor:
 def kfr_auto_chunk(n_pairs: int, n_warps: int, steps_per_batch: int) -> int:
     """Chunk length for an operator of `n_pairs` (column, mask) pairs streamed
     by `n_warps` resident warps. A warp item is 32 chunks, so the longest item
-    is `chunk` steps: measured on the C3 operator, time is flat while that
-    stays just under the mean work per warp (steps / warps: 423 at 2 CTAs/SM,
-    optimum 416; 282 at 3, optimum 272) - longer and the longest item is the
-    makespan, shorter and rows split into more partial sums than needed
+    is at most `chunk` steps: measured on the C3 operator, time is lowest while
+    that stays just under the mean work per warp (steps / warps: 423 at 2
+    CTAs/SM, optimum 376-400 with long rows cut into equal chunks; 282 at 3,
+    optimum 272) - longer and the longest item is the makespan, shorter and
+    rows split into more partial sums than needed
     (profiles/r02_transfer_experiments.json, chunk sweeps)."""
     steps = n_pairs / 32.0 / 0.974  # the layouts fill ~97.4 % of the lane slots
     U = steps_per_batch
-    c = int(0.983 * steps / max(n_warps, 1)) // U * U
+    c = int(0.93 * steps / max(n_warps, 1)) // U * U
     return max(64, min(c, KFR_MAX_BATCHES * U))
 
 
@@ -151,8 +152,12 @@ def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4,
     pos = torch.arange(P, device=dev) - start[prg]
     nch = torch.clamp((cnt + chunk - 1) // chunk, min=1)
     chbase = torch.cumsum(nch, 0) - nch
-    pchunk = chbase[prg] + pos // chunk
-    pstep = pos % chunk
+    # a (row, group) longer than `chunk` is cut into equal chunks (420 pairs at
+    # chunk 408 -> 210 + 210, not 408 + 12): shorter longest items for the
+    # same number of partial sums (142.6 -> 137.9 us on the C3 operator)
+    cs = torch.clamp((cnt + nch - 1) // nch, min=1)
+    pchunk = chbase[prg] + pos // cs[prg]
+    pstep = pos % cs[prg]
     NC = int(nch.sum())
     clen = torch.bincount(pchunk, minlength=NC)
     crg = torch.repeat_interleave(torch.arange(RG, device=dev), nch)
