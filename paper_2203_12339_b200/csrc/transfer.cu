@@ -17,10 +17,11 @@
 //     chunk == one row, all K terms: 3K fp64 accumulators in registers, no
 //     atomics, no cross-lane reduction, deterministic order);
 //   * step s of a warp: every lane takes the s-th pair of its chunk. The
-//     pairs' {col u16 | mask << 16} words of one step are stored compacted
-//     (active lanes in lane order), the f32 values term-plane by term-plane
-//     (plane k: the lanes whose mask has bit k, in lane order), so the lane
-//     offsets are __popc of warp ballots: no per-step headers;
+//     pairs' {col u16 | mask << 16 | value offset << 20} words of one step are
+//     32 dense words (0 where the lane's chunk has ended), the f32 values of a
+//     batch of U steps follow in (step, lane, term) order and every word
+//     carries its lane's offset in that block: no per-step headers, no
+//     running base between the steps of a batch;
 //   * the warp's stream (words + values) is staged through shared memory by
 //     TMA bulk copies (cp.async.bulk, mbarrier transaction counts), two
 //     batches of U steps in flight per warp: reading it costs one
@@ -98,7 +99,7 @@ inline size_t kfr_smem_bytes(int N, size_t warp_bytes) {
 }
 
 // Pair word: col (bits 0-15) | term mask within the group (16-19) | offset of
-// the lane's first value in the step's value block (20-26); 0 = no pair.
+// the lane's first value in the batch's value block (20-31); 0 = no pair.
 template <int U, int NS, int MINB>
 __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
     int N, int Kr, unsigned n_items, unsigned n_partials, const uint2* __restrict__ items,
@@ -178,11 +179,10 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
     auto phaseB = [&](const unsigned char* slot_p, const uint32_t (&w)[U], const bool (&kp)[U],
                       const double (&xa)[U][4]) {
       const float* sv = reinterpret_cast<const float*>(slot_p + SM::WB);
-      unsigned vbase = 0;
 #pragma unroll
       for (int t = 0; t < U; ++t) {
         const uint32_t m = (w[t] >> 16) & 0xfu;
-        const float* sl = sv + vbase + ((w[t] >> 20) & 0x7fu);
+        const float* sl = sv + (w[t] >> 20);  // offset in the batch's value block
         const uint32_t mk = kp[t] ? m : 0u;
         float vf[G];  // one predicated load per present term
 #pragma unroll
@@ -195,7 +195,6 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
           acc[k][1] = fma(v, xa[t][1], acc[k][1]);
           acc[k][2] = fma(v, xa[t][2], acc[k][2]);
         }
-        vbase += __reduce_add_sync(0xffffffffu, __popc(m));
       }
     };
     auto slot_of = [&](unsigned q) { return wb + (q % NS) * SM::SLOT; };

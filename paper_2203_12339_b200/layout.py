@@ -107,7 +107,7 @@ def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4,
     chunks, one per lane; step s of an item holds the s-th pair of every
     lane: 32 dense words {col | mask << 16 | offset << 20} (0 where the lane's
     chunk has ended) and the lanes' values lane-major (offset = the lane's
-    first value in the step). Chunks are grouped by (row level class, length
+    first value in the batch's value block). Chunks are grouped by (row level class, length
     bucket, row, group) so an item's lanes have similar lengths and
     neighbouring rows; items are ordered longest first (dynamic claiming)."""
     G = KFR_GROUP
@@ -225,13 +225,16 @@ def kfr_layout(t, chunk: int = 256, bucket: int = 16, steps_per_batch: int = 4,
     # first value of every pair, of every step and of every batch (global order)
     pfirst = torch.full((P,), nnz, dtype=torch.int64, device=dev).scatter_reduce_(
         0, ent_pair, vpos, "amin")
-    step_first = torch.searchsorted(vkey_sorted, (item_p << 30) | (pstep << 14))
-    poff = pfirst - step_first
-    if P and int(poff.max()) >= 128:
-        raise AssertionError("kfr layout: step value offset overflow")
     bitem = torch.repeat_interleave(torch.arange(NI, device=dev), nbat)
     bstep = (torch.arange(NB, device=dev) - bbase[bitem]) * U
     bv0 = torch.searchsorted(vkey_sorted, (bitem << 30) | (bstep << 14))
+    # the pair's first value, counted from the start of its BATCH's value block
+    # (<= U * 32 * G values: 12 bits at 8 steps): no running per-step base in
+    # the kernel, so the value loads of a batch's steps do not wait on one
+    # another
+    poff = pfirst - bv0[pbatch]
+    if P and int(poff.max()) >= 4096:
+        raise AssertionError("kfr layout: batch value offset overflow")
     bv1 = torch.cat([bv0[1:], torch.tensor([nnz], device=dev)]) if NB else bv0
     bwords = (U * 32 * 4) // 4
     bsize = bwords + ((bv1 - bv0) + 3) // 4 * 4  # in 4-byte units, 16-byte multiples
@@ -292,9 +295,8 @@ def kfr_reference_apply(lay: KfrLayout, x: torch.Tensor) -> torch.Tensor:
             b = b0 + s // U
             base = int(boff[b]) // 4
             w = words[base + (s % U) * 32: base + (s % U) * 32 + 32]
-            if s % U == 0:
-                vbase = base + U * 32
-            col, mask, off = w & 0xFFFF, (w >> 16) & 0xF, (w >> 20) & 0x7F
+            vbase = base + U * 32  # offsets count from the batch's value block
+            col, mask, off = w & 0xFFFF, (w >> 16) & 0xF, (w >> 20) & 0xFFF
             xs = x[:, col].T  # (32, 3)
             for ln in range(32):
                 a = vbase + int(off[ln])
@@ -302,7 +304,6 @@ def kfr_reference_apply(lay: KfrLayout, x: torch.Tensor) -> torch.Tensor:
                     if (int(mask[ln]) >> k) & 1:
                         acc[ln, k] += vals[a] * xs[ln]
                         a += 1
-            vbase += int(sum(bin(int(m)).count("1") for m in mask))
         for ln in range(32):
             dd = int(dst[i * 32 + ln])
             if dd == 0xFFFFFFFF:
