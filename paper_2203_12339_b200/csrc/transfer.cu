@@ -169,7 +169,9 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
       for (int t = 0; t < U; ++t) {
         w[t] = sw[t * 32 + lane];
         const uint32_t c = w[t] & 0xffffu;
-        kp[t] = ((sbits[c >> 5] >> (c & 31u)) & (w[t] >> 16 != 0u ? 1u : 0u)) != 0u;
+        // an empty slot (word 0: column 0, mask 0) may pass the test and gather
+        // x[0]; its mask contributes no values, so nothing is added
+        kp[t] = ((sbits[c >> 5] >> (c & 31u)) & 1u) != 0u;
         gather_x_if(xp, c, kp[t], xa[t]);
       }
     };
