@@ -241,30 +241,36 @@ __global__ void __launch_bounds__(kKfrWarps * 32, MINB) k_transfer_kfr(
       const unsigned old = atomicAdd(&mcount[m], 1u);
       if (old == mi.z - 1u) {
         __threadfence();
-        // fixed order: i ascending per component; the loads of 8 chunks x 3
-        // channels are issued together (the adds stay in order)
+        // fixed order: i ascending per component. All G terms' partial sums of
+        // four chunks are loaded together (one round trip for the usual rows
+        // of <= 4 chunks instead of one per term; the adds stay in order)
+        double sum[G][3];
+#pragma unroll
+        for (int k = 0; k < G; ++k) sum[k][0] = sum[k][1] = sum[k][2] = 0.0;
 #pragma unroll 1
-        for (int k = 0; k < G; ++k) {
-          if (mi.w * G + k >= (unsigned)Kr) break;
-          double sum[3] = {0.0, 0.0, 0.0};
-#pragma unroll 1
-          for (unsigned i0 = 0; i0 < mi.z; i0 += 8) {
-            double q[3][8];
+        for (unsigned i0 = 0; i0 < mi.z; i0 += 4) {
+          double q[G][3][4];
+#pragma unroll
+          for (int k = 0; k < G; ++k)
 #pragma unroll
             for (int c = 0; c < 3; ++c)
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                q[c][i] = (i0 + i < mi.z)
-                              ? __ldcg(&part[(size_t)(k * 3 + c) * n_partials + mi.y + i0 + i]) : 0.0;
+              for (int i = 0; i < 4; ++i)
+                q[k][c][i] = (i0 + i < mi.z)
+                                 ? __ldcg(&part[(size_t)(k * 3 + c) * n_partials + mi.y + i0 + i]) : 0.0;
+#pragma unroll
+          for (int k = 0; k < G; ++k)
 #pragma unroll
             for (int c = 0; c < 3; ++c)
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (i0 + i < mi.z) sum[c] += q[c][i];
-          }
-#pragma unroll
-          for (int c = 0; c < 3; ++c) vk[((size_t)(mi.w * G + k) * 3 + c) * N + mi.x] = sum[c];
+              for (int i = 0; i < 4; ++i)
+                if (i0 + i < mi.z) sum[k][c] += q[k][c][i];
         }
+#pragma unroll
+        for (int k = 0; k < G; ++k)
+          if (mi.w * G + k < (unsigned)Kr)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) vk[((size_t)(mi.w * G + k) * 3 + c) * N + mi.x] = sum[k][c];
         mcount[m] = 0u;  // ready for the next frame
       }
     }
